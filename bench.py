@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark of the TOAST hot path on B200 (BASELINE.json metric: candidate
+cost-evals/sec; config M2 GPT-24, mesh {data:8, model:4}).
+
+One step = one toast_rollout_batch call: N rollouts from the unsharded root,
+each drawn with Philox (H8) and then fully costed (H1-H7) inside the same
+kernel — all of SURVEY §8(a).  Inputs (N x 64 B prefixes) are resident in HBM
+when the timed region starts; L2 is flushed (256 MiB write) between timed
+steps and each step is timed with CUDA events on the launching stream.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n ROLLOUTS] [--config gpt24]
+    python bench.py --impl reference ...      # the CPU oracle on this host
+
+Multi-GPU (torchrun): every rank runs N rollouts of its own id range (weak
+scaling; no collective on the data path); the step time is the max over
+ranks; value = all ranks' rollouts / that time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate cost-evals/sec"
+UNIT = "evals/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--n", type=int, default=1 << 18, help="rollouts per step per GPU")
+    p.add_argument("--config", default="gpt24")
+    p.add_argument("--impl", default="toast", choices=["toast", "reference"])
+    p.add_argument("--seed", type=int, default=2024)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--search", action="store_true", help="also time toast_search (time-to-best)")
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------------- dist
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) > 8:
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- cpu baseline
+def cpu_baseline(cfg, seconds: float, n_first: int = 64):
+    """The oracle as it stands (oracle/), rollouts from the empty prefix on all
+    host cores, on a bounded sample sized to take `seconds`."""
+    import numpy as np
+    from oracle.oracle import Oracle
+    cores = os.cpu_count() or 1
+    o = Oracle(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth)
+    n, done, t_used, idb = n_first, 0, 0.0, 0
+    while t_used < seconds:
+        pre = np.zeros((n, 32), np.uint16)
+        t = time.perf_counter()
+        o.rollout(pre, seed=7, id_base=idb, threads=cores)
+        dt = time.perf_counter() - t
+        done += n
+        idb += n
+        t_used += dt
+        rate = n / max(dt, 1e-9)
+        n = int(min(max(n * 2, rate * (seconds - t_used) * 0.9), 1 << 22)) if t_used < seconds else n
+        if n <= 0:
+            break
+    return {"value": done / t_used, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done} rollouts+evals of {cfg.name} from the empty prefix in {t_used:.1f} s"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle timed on this host (rank 0 only)."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.oracle import Oracle
+    cores = os.cpu_count() or 1
+    o = Oracle(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth)
+    # size one step at ~2 s of CPU work
+    t = time.perf_counter()
+    o.rollout(np.zeros((cores * 4, 32), np.uint16), seed=1, id_base=0, threads=cores)
+    rate = cores * 4 / max(time.perf_counter() - t, 1e-9)
+    n = max(cores, int(rate * 2.0))
+    pre = np.zeros((n, 32), np.uint16)
+    for w in range(args.warmup):
+        o.rollout(pre[: max(cores, n // 8)], seed=2, id_base=w * n, threads=cores)
+    times = []
+    for s in range(args.steps):
+        t = time.perf_counter()
+        o.rollout(pre, seed=args.seed, id_base=s * n, threads=cores)
+        times.append(time.perf_counter() - t)
+    ms = 1000.0 * statistics.mean(times)
+    value = n / (ms / 1000.0)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": cfg.name, "rollouts_per_step": n, "mesh": [list(a) for a in cfg.axes],
+                       "description": cfg.description},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} rollouts+evals of {cfg.name} per step, {args.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- main arm
+def algorithmic_ops_per_eval(dump: dict, n_axes: int) -> int:
+    """one check per loop (H2), rank x axes transitions
+    per use edge (H4), three scan/score steps per op (H5)."""
+    return int(dump["n_loops"]) + int(dump["n_edges"]) * n_axes + 3 * int(dump["n_ops"])
+
+
+def run_toast(args, cfg, rank, world, local):
+    import numpy as np
+    import torch
+    from paper_2508_15010_b200 import toast as T
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    t = time.perf_counter()
+    a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
+                         cuda_device=local)
+    nda_s = time.perf_counter() - t
+    dump = a.dump()
+    N = args.n
+    stream = torch.cuda.current_stream(dev)
+    pre = torch.zeros((N, 32), dtype=torch.int16, device=dev)
+    seqs = torch.empty_like(pre)
+    out = torch.empty((N, 256), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    base = rank * (1 << 40)
+
+    # warm-up
+    for w in range(args.warmup):
+        T.rollout_batch(a, pre, args.seed, base + (1 << 36) + w * N, seqs, out, stream=stream)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    for s in range(args.steps):
+        flush.zero_()                                     # L2 flush between timed steps
+        ev[s][0].record(stream)
+        T.rollout_batch(a, pre, args.seed, base + s * N, seqs, out, stream=stream)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    ms_local = statistics.mean(step_ms)
+    ms = allreduce_max(ms_local, world)
+    value = N * world / (ms / 1000.0)
+
+    # sanity: every record valid
+    st = T.as_costs(out[:4096])
+    assert (st["status"] == 0).all()
+
+    # e2e through the public API with host (pinned) buffers: H2D + kernel + D2H
+    h_pre = torch.zeros((N, 32), dtype=torch.int16).pin_memory()
+    h_seqs = torch.empty_like(h_pre).pin_memory()
+    h_out = torch.empty((N, 256), dtype=torch.uint8).pin_memory()
+    T.rollout_batch(a, h_pre, args.seed, base, h_seqs, h_out, stream=stream)   # warm (scratch alloc)
+    e2e_ms = []
+    for s in range(max(3, min(args.steps, 10))):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        T.rollout_batch(a, h_pre, args.seed, base + s * N, h_seqs, h_out, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e = allreduce_max(statistics.mean(e2e_ms), world)
+
+    line = None
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        n_axes = len(cfg.axes)
+        ops = algorithmic_ops_per_eval(dump, n_axes)
+        achieved = ops * (N / (ms_local / 1000.0)) / 1e9          # Gop/s on this GPU
+        peak_alu = 148 * 128 * sm_max * 1e6 / 1e9                  # INT32 lanes x clock (Gop/s)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": cfg.name, "rollouts_per_step_per_gpu": N, "mesh": [list(x) for x in cfg.axes],
+                       "ops": dump["n_ops"], "loops": dump["n_loops"], "actions": len(dump["actions"]) + 1,
+                       "l2": "flushed (256 MiB write) between timed steps", "description": cfg.description},
+            "gpu_launches": args.steps,
+            "wall_s_timed_region": wall,
+            "nda_s": nda_s,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_alu, "unit": "Gop/s",
+                         "frac": achieved / peak_alu, "traffic": None,
+                         "note": f"{ops} algorithmic int ops/eval (DESIGN.md Roofline); peak = 148 SMs x 128 INT32 "
+                                 f"lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
+            "clocks": clk,
+            "e2e": {"value": N * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": N * 64,
+                    "d2h_bytes_per_step": N * (64 + 256)},
+        }
+    if args.search and rank == 0:
+        r = T.search(a, T.SearchOptions(seed=args.seed, max_evals=2_000_000, leaves_per_round=64,
+                                        rollouts_per_leaf=256, patience=3), stream=stream)
+        line["search"] = {"best_score": float(r["best"]["score"]), "evals": int(r["evals"]),
+                          "rounds": int(r["rounds"]), "wall_s": float(r["wall_s"])}
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_init(args)
+    from workloads import configs
+    cfg = configs.get(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+    else:
+        run_toast(args, cfg, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

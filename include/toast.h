@@ -1,0 +1,210 @@
+/* =============================================================================
+ * toast.h — C ABI of the B200-native TOAST hot path (libtoast.so)
+ *
+ * What it computes: batched evaluation of MCTS rollouts over the sharding-
+ * decision space of arXiv 2508.15010 ("TOAST"), /root/reference/PAPER.md
+ * (cited as P:<line>).  For each candidate action sequence it materialises the
+ * sharding, derives local FLOPs, inserts and costs the
+ * implied collectives, runs the live-range sweep for peak memory
+ * and returns runtime and score C(s) = RT(s) + MP(s).
+ * The exact definitions are SURVEY.md §8(c) C0-C16 and DESIGN.md.
+ *
+ * Conventions (all calls):
+ *   - Every call returns toast_status (0 = TOAST_OK) and never throws across
+ *     the ABI; toast_last_error() returns a thread-local message valid until
+ *     the next call on that thread.
+ *   - Handles (toast_graph, toast_analysis, toast_search_state) are owned by
+ *     the library and freed with the matching toast_free_* call.  Caller
+ *     buffers are never freed or retained.
+ *   - Candidate buffers (seqs, out, prefixes, out_seqs) may be host or device
+ *     pointers.  Device pointers: the call is asynchronous on `cuda_stream`
+ *     (a cudaStream_t, NULL = legacy default stream); the caller synchronises.
+ *     Host pointers (pageable or pinned): the library copies through device
+ *     scratch on `cuda_stream` and returns after the results are in host
+ *     memory.  All buffers must use the same kind of memory.
+ *   - Candidate-level problems never fail a call; they are reported in
+ *     toast_cost.status with every other field zero.
+ *   - A toast_analysis is immutable after toast_nda and safe for concurrent
+ *     calls on different streams (host-pointer calls serialise on a mutex).
+ * ============================================================================= */
+#ifndef TOAST_H
+#define TOAST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TOAST_OK = 0,
+  TOAST_E_INVALID_ARG = 1,  /* NULL pointer, negative size, bad option value */
+  TOAST_E_PARSE = 2,        /* syntax error; message holds "line:col: ..." */
+  TOAST_E_SHAPE = 3,        /* shape/attribute mismatch; message names the binding */
+  TOAST_E_UNDEFINED = 4,    /* use before definition */
+  TOAST_E_DUPLICATE = 5,    /* a name bound twice */
+  TOAST_E_MESH = 6,         /* duplicate axis name, size < 2, 0 or > 4 axes, bw <= 0 */
+  TOAST_E_MACHINE = 7,      /* flops_per_sec <= 0, penalty_c < 0 */
+  TOAST_E_DEGENERATE = 8,   /* baseline runtime 0: no contraction op */
+  TOAST_E_LIMIT = 9,        /* > 8 SetGroups in a super-color, > 1023 actions, > 64 SetGroups,
+                               > 8 loops or operands per op, rank > 8, > 2^31 loops */
+  TOAST_E_CUDA = 10,        /* CUDA runtime error, or no device attached to the graph */
+  TOAST_E_NCCL = 11,        /* reserved: collectives run in the caller (torch.distributed) */
+  TOAST_E_OOM = 12          /* host or device allocation failed */
+} toast_status;
+
+/* candidate status bits (toast_cost.status) */
+#define TOAST_ST_BAD_ACTION_ID 1u        /* an id >= number of actions */
+#define TOAST_ST_DUP_COLOR_AXIS 2u       /* the same (super-color, axis) twice */
+#define TOAST_ST_RES_MISMATCH 4u         /* a SetGroup bit disagrees with an earlier action's */
+#define TOAST_ST_NONZERO_AFTER_STOP 8u   /* a nonzero entry after the first 0 (STOP) */
+
+/* collective kinds, index of toast_cost.payload[axis][kind] */
+#define TOAST_AG 0
+#define TOAST_RS 1
+#define TOAST_AR 2
+#define TOAST_A2A 3
+
+/* One mesh axis.  Mesh order = array order.  bytes_per_sec is
+   the link bandwidth used by the ring cost model. */
+typedef struct {
+  const char* name;
+  int32_t size;          /* >= 2 */
+  double bytes_per_sec;  /* > 0 */
+} toast_axis;
+
+/* Machine characteristics: FLOP rate for matmul-class ops,
+   per-device memory DM and penalty constant C of MP(s). */
+typedef struct {
+  double flops_per_sec;
+  uint64_t device_memory_bytes;
+  double penalty_c;
+} toast_machine;
+
+/* NDA options: prune super-colors with fewer than min_unique_dims value
+   dims (default 10); maximum trajectory depth (default 30). */
+typedef struct {
+  int32_t min_unique_dims;
+  int32_t max_depth;
+} toast_nda_opts;
+
+typedef struct toast_graph toast_graph;        /* opaque, library-owned */
+typedef struct toast_analysis toast_analysis;  /* opaque, library-owned, immutable */
+
+/* 256-byte cost record, one per candidate (16-byte aligned). */
+typedef struct {
+  double runtime_s;        /* C13: flops/F + sum over axes of ring collective time */
+  double score;            /* RT + MP */
+  uint64_t peak_bytes;     /* C12: max over program points of live device-local bytes */
+  uint64_t flops;          /* C10: low 64 bits of the local matmul-class FLOP total */
+  uint64_t state_key;      /* C14: order-independent hash of the materialised masks */
+  uint32_t status;         /* TOAST_ST_* bits; 0 = ok */
+  uint32_t n_collectives;  /* sum of count[][] */
+  uint64_t payload[4][4];  /* C11 bytes per [axis][AG, RS, AR, A2A] */
+  uint16_t count[4][4];    /* number of collectives per [axis][kind] */
+  uint64_t flops_hi;       /* high 64 bits of the FLOP total */
+  uint8_t pad[40];
+} toast_cost;
+
+/* action id -> (super-color, resolution bits r, axis index, #value dims). id 0 = STOP. */
+typedef struct {
+  int32_t super_color, resolution, axis, n_value_dims;
+} toast_action_info;
+
+/* ---------------------------------------------------------------------------
+ * toast_load_graph — parse the text IR (SPEC grammar S:92-104
+ * extended with dot_general/conv/gather/... ) and bind it to a mesh and
+ * machine.  `ir_text` need not be NUL-terminated (`len` bytes are read).
+ * `cuda_device` >= 0 selects the device the tables are uploaded to by
+ * toast_nda; -1 builds a host-only graph (analysis and dumps only; eval calls
+ * then fail with TOAST_E_CUDA).  On error *out is NULL.
+ * ------------------------------------------------------------------------- */
+toast_status toast_load_graph(const char* ir_text, size_t len, const toast_axis* axes, int32_t n_axes,
+                              const toast_machine* m, int32_t cuda_device, toast_graph** out);
+
+/* toast_nda — H0 (once per graph): loop table from the NDA rules (Fig. 3,
+ * P:443-558), I∪M components, conflicts,
+ * compatibility sets (§3.5), cross-layer SetGroups (§3.6),
+ * argument groups / super-colors (§4.4), the action table
+ * (§4.2) and the baseline cost; uploads the device tables.
+ * `g` stays owned by the caller and may be freed after this call. */
+toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_analysis** out);
+
+/* number of actions including STOP (id 0) */
+toast_status toast_num_actions(const toast_analysis* a, int32_t* n);
+/* fills up to cap entries (index = action id); *n = number of actions */
+toast_status toast_query_actions(const toast_analysis* a, toast_action_info* out, int32_t cap, int32_t* n);
+/* the empty sequence's record (RT = 1) */
+toast_status toast_query_baseline(const toast_analysis* a, toast_cost* out);
+/* JSON dump of the H0 tables (loops, conflicts, sets, groups, super-colors,
+ * actions, baseline).  *needed = bytes incl. NUL; writes only if cap >= *needed. */
+toast_status toast_dump_analysis(const toast_analysis* a, char* buf, size_t cap, size_t* needed);
+
+/* toast_eval_batch — H1-H7 for n candidates.  seqs: uint16[n][32] action ids,
+ * 0 = STOP; out: toast_cost[n]. */
+toast_status toast_eval_batch(const toast_analysis* a, const uint16_t* seqs, int64_t n, toast_cost* out,
+                              void* cuda_stream);
+
+/* toast_rollout_batch — H8: from each prefix (uint16[n][32]),
+ * extend with Philox4x32-10 draws (key = seed, counter = (id_base + i, depth))
+ * until STOP (p = depth/max_depth), no legal action, or
+ * max_depth; writes the sequence to out_seqs[n][32] and its cost to out[n].
+ * A prefix with an invalid id or nonzero after STOP is returned unextended. */
+toast_status toast_rollout_batch(const toast_analysis* a, const uint16_t* prefixes, int64_t n, uint64_t seed,
+                                 uint64_t id_base, uint16_t* out_seqs, toast_cost* out, void* cuda_stream);
+
+/* per-loop axis masks of one sequence (debug / tests; NEXT-1 lowering).
+ * masks: uint8[cap]; *n = number of loops. seq is a host pointer. */
+toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], uint8_t* masks, int64_t cap,
+                               int64_t* n);
+
+/* ---------------------------------------------------------------------------
+ * Search (C16).  Single GPU: toast_search.  Root-parallel
+ * multi-GPU: the caller drives begin / round / (all_gather of the export
+ * bytes across ranks) / import / end, e.g. with torch.distributed (NCCL).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t seed;
+  int64_t max_evals;        /* 0 = unlimited */
+  double time_limit_s;      /* 0 = unlimited */
+  int32_t leaves_per_round; /* L */
+  int32_t rollouts_per_leaf;/* R */
+  int32_t patience;         /* stop after this many non-improving rounds (1) */
+  int32_t pad0;
+  double uct_c;             /* UCT exploration constant (sqrt 2) */
+  double target_score;      /* stop once best <= target; NaN = disabled */
+  void* cuda_stream;
+} toast_search_opts;
+
+typedef struct {
+  uint16_t best_seq[32];
+  toast_cost best;
+  int64_t evals;
+  int32_t rounds, hit_target;
+  double wall_s, time_to_target_s; /* time_to_target_s < 0 if never reached */
+} toast_search_result;
+
+typedef struct toast_search_state toast_search_state;
+
+toast_status toast_search(const toast_analysis* a, const toast_search_opts* o, toast_search_result* out);
+
+/* bytes one rank contributes to the per-round all_gather */
+size_t toast_search_export_bytes(const toast_analysis* a);
+toast_status toast_search_begin(const toast_analysis* a, const toast_search_opts* o, int32_t rank, int32_t world,
+                                toast_search_state** out);
+/* runs one round; writes this rank's export record to `export_buf` (host memory) */
+toast_status toast_search_round(toast_search_state* s, void* export_buf);
+/* imports world records ([world][export_bytes], host memory); *stop = 1 when all ranks must stop */
+toast_status toast_search_import(toast_search_state* s, const void* gathered, int32_t* stop);
+toast_status toast_search_end(toast_search_state* s, toast_search_result* out);
+
+const char* toast_last_error(void);
+void toast_free_graph(toast_graph* g);
+void toast_free_analysis(toast_analysis* a);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOAST_H */

@@ -1134,6 +1134,7 @@ struct Oracle {
     // C11: collectives per use edge (Fig. 2c; Fig. 5b)
     std::vector<u64> temp_total(M.ops.size(), 0);
     int nA = (int)axes.size();
+    u64 ncount[4][4] = {{0}};   // true counts; the record keeps them saturated to 16 bits
     for (size_t t = 0; t < M.ops.size(); t++) {
       const Op& op = M.ops[t];
       std::vector<std::pair<int, std::vector<int>>> done;   // (value, U) already costed at this op
@@ -1159,10 +1160,10 @@ struct Oracle {
             int j_other = -1;
             for (size_t j = 0; j < U.size(); j++) if (j != i && (U[j] & (1 << A))) j_other = (int)j;
             if (j_other >= 0) {
-              out.payload[A][K_A2A] += size; out.count[A][K_A2A]++;
+              out.payload[A][K_A2A] += size; ncount[A][K_A2A]++;
               cur[i] &= ~(1 << A); cur[j_other] |= 1 << A;
             } else {
-              out.payload[A][K_AG] += size; out.count[A][K_AG]++;
+              out.payload[A][K_AG] += size; ncount[A][K_AG]++;
               cur[i] &= ~(1 << A); size *= (u64)axes[A].size;
             }
           }
@@ -1174,10 +1175,10 @@ struct Oracle {
           for (size_t j = 0; j < U.size(); j++) if (U[j] & (1 << A)) j_u = (int)j;
           if (j_u >= 0) {
             size /= (u64)axes[A].size;
-            out.payload[A][K_RS] += size; out.count[A][K_RS]++;
+            out.payload[A][K_RS] += size; ncount[A][K_RS]++;
             cur[j_u] |= 1 << A;
           } else {
-            out.payload[A][K_AR] += size; out.count[A][K_AR]++;
+            out.payload[A][K_AR] += size; ncount[A][K_AR]++;
           }
         }
         // phase 3: free local slices (no payload)
@@ -1219,9 +1220,13 @@ struct Oracle {
     out.flops = flo;
     out.flops_hi = fhi;
     out.state_key = key;
-    u32 nc = 0;
-    for (int A = 0; A < 4; A++) for (int k = 0; k < 4; k++) nc += out.count[A][k];
-    out.n_collectives = nc;
+    u64 nc = 0;
+    for (int A = 0; A < 4; A++)
+      for (int k = 0; k < 4; k++) {
+        nc += ncount[A][k];
+        out.count[A][k] = (u16)(ncount[A][k] > 65535 ? 65535 : ncount[A][k]);
+      }
+    out.n_collectives = (u32)nc;
     if (t0 > 0.0) {
       double RT = t / t0;
       double MP = (u64)peak > DM ? (C * (double)((u64)peak - DM)) / (double)peak0 : 0.0;

@@ -1,0 +1,65 @@
+"""Build libtoast.so in-tree (paper_2508_15010_b200/lib/) for sm_100a.
+
+    python -m paper_2508_15010_b200.build [--force]
+
+Kernels: nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false.
+Host code: g++ -O2 -ffp-contract=off (the search's UCT arithmetic and the
+baseline score are plain IEEE double, evaluated in a fixed order).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
+LIB = os.path.join(HERE, "lib", "libtoast.so")
+INC = os.path.join(os.path.dirname(HERE), "include")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+
+GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU_FLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                      f"-I{INC}", f"-I{SRC}"]
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", f"-I{CUDA}/include", f"-I{INC}", f"-I{SRC}"]
+
+SOURCES = ["ir.cpp", "analysis.cpp", "search.cpp", "abi.cpp", "kernels.cu"]
+HEADERS = ["toast_internal.h"]
+
+
+def _newer(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    hdrs = [os.path.join(SRC, h) for h in HEADERS] + [os.path.join(INC, "toast.h")]
+    objs = []
+    for s in SOURCES:
+        src = os.path.join(SRC, s)
+        obj = os.path.join(OBJ, s + ".o")
+        objs.append(obj)
+        if force or _newer(obj, [src] + hdrs):
+            if s.endswith(".cu"):
+                cmd = [NVCC] + CU_FLAGS + ["-c", src, "-o", obj]
+            else:
+                cmd = ["g++"] + CXX_FLAGS + ["-c", src, "-o", obj]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.check_call(cmd)
+    if force or _newer(LIB, objs):
+        cmd = [NVCC] + GENCODE + ["-shared", "-o", LIB] + objs + ["-Xcompiler", "-fPIC", "-lpthread"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

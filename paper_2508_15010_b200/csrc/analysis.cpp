@@ -1,0 +1,751 @@
+// H0: the once-per-graph analysis of libtoast, written for
+// graphs of 10^4-10^5 loops: CSR edge lists, union-find, per-component
+// bitset reachability for the "box" test, parity union-find for the
+// compatibility closure.  Produces the packed device tables of
+// toast_internal.h.  Definitions: SURVEY §8(c) C1-C8 / DESIGN.md.
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <map>
+#include <numeric>
+
+#include "toast_internal.h"
+
+namespace toast {
+namespace {
+
+// ---------------------------------------------------------------- hashing (C6/C14)
+inline uint64_t splitmix_fin(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+inline uint64_t hc(uint64_t h, uint64_t x) { return splitmix_fin(h ^ (x + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2))); }
+uint64_t hfold(const uint64_t* xs, size_t n) {
+  uint64_t h = 0;
+  for (size_t i = 0; i < n; ++i) h = hc(h, xs[i]);
+  return h;
+}
+uint64_t hfold(std::vector<uint64_t> v, bool sort_first) {
+  if (sort_first) std::sort(v.begin(), v.end());
+  return hfold(v.data(), v.size());
+}
+uint64_t fnv(const std::string& s) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (unsigned char c : s) h = (h ^ c) * 0x100000001b3ULL;
+  return h;
+}
+
+struct DSU {
+  std::vector<int32_t> par;
+  explicit DSU(size_t n) : par(n) { std::iota(par.begin(), par.end(), 0); }
+  int32_t root(int32_t x) {
+    while (par[x] != x) { par[x] = par[par[x]]; x = par[x]; }
+    return x;
+  }
+  void join(int32_t a, int32_t b) {
+    a = root(a); b = root(b);
+    if (a == b) return;
+    if (b < a) std::swap(a, b);
+    par[b] = a;   // root = smallest member
+  }
+};
+
+// per-op loop structure (C1 table, written directly per op kind)
+struct OpLoops {
+  std::vector<int64_t> ext;
+  std::vector<uint8_t> type;
+  std::vector<uint8_t> res_role;                // per result dim
+  std::vector<std::vector<uint8_t>> use_role;   // per operand, per dim
+};
+
+OpLoops loops_of(const toast_graph* g, const GOp& op) {
+  OpLoops L;
+  auto S = [&](int k) -> const std::vector<int64_t>& { return g->values[op.operands[k]].shape; };
+  const std::vector<int64_t> none;
+  const std::vector<int64_t>& R = op.result >= 0 ? g->values[op.result].shape : none;
+  auto add = [&](int64_t e, uint8_t t) { L.ext.push_back(e); L.type.push_back(t); };
+  auto ident_roles = [](size_t n) { std::vector<uint8_t> v(n); for (size_t i = 0; i < n; ++i) v[i] = (uint8_t)i; return v; };
+  switch (op.kind) {
+    case OK_PARAM:
+      for (int64_t e : R) add(e, T_P);
+      L.res_role = ident_roles(R.size());
+      break;
+    case OK_RET:
+      for (int64_t e : S(0)) add(e, T_P);
+      L.use_role.push_back(ident_roles(S(0).size()));
+      break;
+    case OK_UNARY: case OK_BINARY:
+      for (int64_t e : R) add(e, T_P);
+      L.res_role = ident_roles(R.size());
+      for (size_t k = 0; k < op.operands.size(); ++k) L.use_role.push_back(ident_roles(R.size()));
+      break;
+    case OK_TRANSPOSE:
+      for (int64_t e : S(0)) add(e, T_P);
+      L.use_role.push_back(ident_roles(S(0).size()));
+      for (int64_t p : op.ia) L.res_role.push_back((uint8_t)p);
+      break;
+    case OK_REDUCE:
+      for (size_t i = 0; i < S(0).size(); ++i) {
+        add(S(0)[i], op.ia[i] ? T_R : T_P);
+        if (!op.ia[i]) L.res_role.push_back((uint8_t)i);
+      }
+      L.use_role.push_back(ident_roles(S(0).size()));
+      break;
+    case OK_BROADCAST: {
+      for (int64_t e : R) add(e, T_P);
+      L.res_role = ident_roles(R.size());
+      std::vector<uint8_t> u;
+      for (size_t i = 0; i < S(0).size(); ++i) u.push_back((uint8_t)((int64_t)i < op.ia[0] ? i : i + 1));
+      L.use_role.push_back(u);
+      break;
+    }
+    case OK_MATMUL:
+      add(R[0], T_P); add(R[1], T_P); add(S(0)[1], T_R);
+      L.res_role = {0, 1};
+      L.use_role = {{0, 2}, {2, 1}};
+      break;
+    case OK_DOT: {
+      int64_t nb = op.ia[0], nc = op.ia[1];
+      const int64_t* lb = &op.ia[2];
+      const int64_t* rb = lb + nb;
+      const int64_t* lc = rb + nb;
+      const int64_t* rc = lc + nc;
+      const auto& A = S(0); const auto& B = S(1);
+      std::vector<int> ra(A.size(), -1), rbv(B.size(), -1);
+      int role = 0;
+      for (int64_t t = 0; t < nb; ++t) { add(A[lb[t]], T_P); ra[lb[t]] = role; rbv[rb[t]] = role; ++role; }
+      std::vector<char> ua(A.size(), 0), ub(B.size(), 0);
+      for (int64_t t = 0; t < nb; ++t) { ua[lb[t]] = 1; ub[rb[t]] = 1; }
+      for (int64_t t = 0; t < nc; ++t) { ua[lc[t]] = 1; ub[rc[t]] = 1; }
+      for (size_t i = 0; i < A.size(); ++i) if (!ua[i]) { add(A[i], T_P); ra[i] = role++; }
+      for (size_t i = 0; i < B.size(); ++i) if (!ub[i]) { add(B[i], T_P); rbv[i] = role++; }
+      int nres = role;
+      for (int64_t t = 0; t < nc; ++t) { add(A[lc[t]], T_R); ra[lc[t]] = role; rbv[rc[t]] = role; ++role; }
+      L.res_role = ident_roles(nres);
+      std::vector<uint8_t> ua8, ub8;
+      for (int x : ra) ua8.push_back((uint8_t)x);
+      for (int x : rbv) ub8.push_back((uint8_t)x);
+      L.use_role = {ua8, ub8};
+      break;
+    }
+    case OK_CONV:     // roles N Ho Wo Co | Ci | KH KW
+      add(R[0], T_P); add(R[1], T_X); add(R[2], T_X); add(R[3], T_P); add(S(0)[3], T_R); add(S(1)[0], T_X); add(S(1)[1], T_X);
+      L.res_role = {0, 1, 2, 3};
+      L.use_role = {{0, 1, 2, 4}, {5, 6, 4, 3}};
+      break;
+    case OK_CONV_BI:  // roles N H W Ci | Co | KH KW
+      add(R[0], T_P); add(R[1], T_X); add(R[2], T_X); add(R[3], T_P); add(S(0)[3], T_R); add(S(1)[0], T_X); add(S(1)[1], T_X);
+      L.res_role = {0, 1, 2, 3};
+      L.use_role = {{0, 1, 2, 4}, {5, 6, 3, 4}};
+      break;
+    case OK_CONV_BF:  // roles KH KW Ci Co | N | H W
+      add(R[0], T_X); add(R[1], T_X); add(R[2], T_P); add(R[3], T_P); add(S(0)[0], T_R); add(S(0)[1], T_X); add(S(0)[2], T_X);
+      L.res_role = {0, 1, 2, 3};
+      L.use_role = {{4, 5, 6, 2}, {4, 5, 6, 3}};
+      break;
+    case OK_RESAMPLE:
+      add(R[0], T_P); add(R[1], T_X); add(R[2], T_X); add(R[3], T_P);
+      L.res_role = {0, 1, 2, 3};
+      L.use_role = {{0, 1, 2, 3}};
+      break;
+    case OK_CONCAT: case OK_SLICE: case OK_PAD:
+      for (size_t i = 0; i < R.size(); ++i) add(R[i], (int64_t)i == op.ia[0] ? T_X : T_P);
+      L.res_role = ident_roles(R.size());
+      for (size_t k = 0; k < op.operands.size(); ++k) L.use_role.push_back(ident_roles(R.size()));
+      break;
+    case OK_GATHER: {   // roles e.. f | n(X)
+      size_t ke = S(1).size();
+      for (size_t t = 0; t <= ke; ++t) add(R[t], T_P);
+      add(S(0)[0], T_X);
+      L.res_role = ident_roles(ke + 1);
+      L.use_role = {{(uint8_t)(ke + 1), (uint8_t)ke}, ident_roles(ke)};
+      break;
+    }
+    case OK_SEGSUM: {   // roles e..(R) f | n(X)
+      size_t ke = S(1).size();
+      for (size_t t = 0; t < ke; ++t) add(S(0)[t], T_R);
+      add(R[1], T_P);
+      add(R[0], T_X);
+      L.res_role = {(uint8_t)(ke + 1), (uint8_t)ke};
+      L.use_role = {ident_roles(ke + 1), ident_roles(ke)};
+      break;
+    }
+  }
+  return L;
+}
+
+inline bool is_matmul_class(OpKind k) { return k == OK_MATMUL || k == OK_DOT || k == OK_CONV || k == OK_CONV_BI || k == OK_CONV_BF; }
+
+}  // namespace
+
+toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast_analysis* a, std::string& err) {
+  const int32_t n_ops = (int32_t)g->ops.size();
+  const int n_axes = (int)g->axis_size.size();
+  a->n_ops = n_ops;
+  a->axis_size = g->axis_size;
+
+  // ------------------------------------------------------------ C1 loops
+  std::vector<OpLoops> OL(n_ops);
+  std::vector<int64_t> lbeg(n_ops + 1, 0);
+  for (int32_t t = 0; t < n_ops; ++t) {
+    OL[t] = loops_of(g, g->ops[t]);
+    if (OL[t].ext.size() > (size_t)MAX_LOOPS_PER_OP) { err = "op '" + g->ops[t].binding + "' has more than 8 loops"; return TOAST_E_LIMIT; }
+    if (g->ops[t].operands.size() > (size_t)MAX_USES_PER_OP) { err = "op '" + g->ops[t].binding + "' has more than 8 operands"; return TOAST_E_LIMIT; }
+    lbeg[t + 1] = lbeg[t] + (int64_t)OL[t].ext.size();
+  }
+  const int64_t NL = lbeg[n_ops];
+  if (NL >= (int64_t)1 << 31) { err = "too many loops"; return TOAST_E_LIMIT; }
+  a->n_loops = NL;
+  a->loop_op.resize(NL); a->loop_role.resize(NL); a->loop_type.resize(NL); a->loop_ext.resize(NL);
+  for (int32_t t = 0; t < n_ops; ++t)
+    for (size_t r = 0; r < OL[t].ext.size(); ++r) {
+      int64_t l = lbeg[t] + (int64_t)r;
+      a->loop_op[l] = t; a->loop_role[l] = (int32_t)r; a->loop_type[l] = OL[t].type[r]; a->loop_ext[l] = OL[t].ext[r];
+    }
+  auto def_loop = [&](int32_t v, int i) { int32_t o2 = g->values[v].def_op; return (int32_t)(lbeg[o2] + OL[o2].res_role[i]); };
+  auto use_loop = [&](int32_t t, int k, int i) { return (int32_t)(lbeg[t] + OL[t].use_role[k][i]); };
+
+  // M edges over loops (deduplicated), CSR out-adjacency
+  std::vector<uint64_t> ekeys;
+  for (int32_t t = 0; t < n_ops; ++t)
+    for (size_t k = 0; k < g->ops[t].operands.size(); ++k) {
+      int32_t v = g->ops[t].operands[k];
+      for (size_t i = 0; i < g->values[v].shape.size(); ++i)
+        ekeys.push_back(((uint64_t)(uint32_t)def_loop(v, (int)i) << 32) | (uint32_t)use_loop(t, (int)k, (int)i));
+    }
+  std::sort(ekeys.begin(), ekeys.end());
+  ekeys.erase(std::unique(ekeys.begin(), ekeys.end()), ekeys.end());
+  a->n_edges = (int64_t)ekeys.size();
+  std::vector<int64_t> out_off(NL + 1, 0);
+  std::vector<int32_t> out_dst(ekeys.size());
+  for (uint64_t e : ekeys) out_off[(e >> 32) + 1]++;
+  for (int64_t l = 0; l < NL; ++l) out_off[l + 1] += out_off[l];
+  for (size_t i = 0; i < ekeys.size(); ++i) out_dst[i] = (int32_t)(uint32_t)ekeys[i];   // sorted by src then dst
+
+  // ------------------------------------------------------------ C2 components
+  DSU cd(NL);
+  for (uint64_t e : ekeys) cd.join((int32_t)(e >> 32), (int32_t)(uint32_t)e);
+  a->loop_comp.resize(NL);
+  for (int64_t l = 0; l < NL; ++l) a->loop_comp[l] = cd.root((int32_t)l);
+
+  // ------------------------------------------------------------ C3 conflicts
+  std::map<std::pair<int32_t, int32_t>, int32_t> conf_index;
+  for (int32_t t = 0; t < n_ops; ++t) {
+    const int nl = (int)OL[t].ext.size();
+    uint64_t pairbits = 0;   // bit (u*8+v) for u<v roles that co-occur
+    auto site = [&](const std::vector<uint8_t>& roles) {
+      for (size_t x = 0; x < roles.size(); ++x)
+        for (size_t y = x + 1; y < roles.size(); ++y) {
+          int u = std::min(roles[x], roles[y]), v = std::max(roles[x], roles[y]);
+          if (u != v) pairbits |= 1ULL << (u * 8 + v);
+        }
+    };
+    if (g->ops[t].result >= 0) site(OL[t].res_role);
+    for (auto& ur : OL[t].use_role) site(ur);
+    for (int u = 0; u < nl; ++u)
+      for (int v = u + 1; v < nl; ++v) {
+        if (!(pairbits >> (u * 8 + v) & 1)) continue;
+        if (OL[t].type[u] == T_X || OL[t].type[v] == T_X) continue;
+        int32_t lu = (int32_t)(lbeg[t] + u), lv = (int32_t)(lbeg[t] + v);
+        if (a->loop_comp[lu] != a->loop_comp[lv]) continue;
+        conf_index[{lu, lv}] = (int32_t)a->conflicts.size();
+        a->conflicts.push_back({t, lu, lv, -1, -1});
+      }
+  }
+  const int32_t NC = (int32_t)a->conflicts.size();
+
+  // ------------------------------------------------------------ C4 boxes
+  // reachability bitsets over conflict endpoints, computed in reverse loop order
+  // (every M edge goes from a lower to a higher loop id)
+  std::vector<int32_t> ep_index(NL, -1);
+  int32_t NE = 0;
+  for (auto& c : a->conflicts) {
+    if (ep_index[c.u] < 0) ep_index[c.u] = NE++;
+    if (ep_index[c.v] < 0) ep_index[c.v] = NE++;
+  }
+  const size_t W = (size_t)(NE + 63) / 64;
+  std::vector<char> comp_has_ep(NL, 0);
+  for (auto& c : a->conflicts) comp_has_ep[a->loop_comp[c.u]] = 1;
+  std::vector<int64_t> reach_off(NL, -1);
+  int64_t nreach = 0;
+  for (int64_t l = 0; l < NL; ++l) if (comp_has_ep[a->loop_comp[l]]) reach_off[l] = nreach++;
+  std::vector<uint64_t> reach((size_t)nreach * W, 0);
+  if (NC > 0) {
+    for (int64_t l = NL - 1; l >= 0; --l) {
+      if (reach_off[l] < 0) continue;
+      uint64_t* dst = &reach[(size_t)reach_off[l] * W];
+      for (int64_t e = out_off[l]; e < out_off[l + 1]; ++e) {
+        int32_t m = out_dst[e];
+        const uint64_t* src = &reach[(size_t)reach_off[m] * W];
+        for (size_t w = 0; w < W; ++w) dst[w] |= src[w];
+        if (ep_index[m] >= 0) dst[ep_index[m] >> 6] |= 1ULL << (ep_index[m] & 63);
+      }
+    }
+  }
+  auto reaches = [&](int32_t from, int32_t to) {
+    int32_t e = ep_index[to];
+    return (reach[(size_t)reach_off[from] * W + (e >> 6)] >> (e & 63)) & 1;
+  };
+  struct BoxRec { int32_t c1, c2, N, O, L, R, parity; };
+  std::vector<BoxRec> boxes;
+  for (int32_t ci = 0; ci < NC; ++ci) {
+    const auto c1 = a->conflicts[ci];
+    std::vector<BoxRec> mine;
+    for (int lab = 0; lab < 2; ++lab) {
+      int32_t N = lab ? c1.v : c1.u, O = lab ? c1.u : c1.v;
+      for (int64_t e1 = out_off[N]; e1 < out_off[N + 1]; ++e1)
+        for (int64_t e2 = out_off[O]; e2 < out_off[O + 1]; ++e2) {
+          int32_t L = out_dst[e1], R = out_dst[e2];
+          if (L == R || a->loop_op[L] != a->loop_op[R]) continue;
+          auto it = conf_index.find({std::min(L, R), std::max(L, R)});
+          if (it == conf_index.end()) continue;
+          if (reaches(N, R) || reaches(O, L)) continue;
+          const auto& c2 = a->conflicts[it->second];
+          mine.push_back({ci, it->second, N, O, L, R, (int32_t)((N == c1.u) ^ (L == c2.u))});
+        }
+    }
+    std::stable_sort(mine.begin(), mine.end(), [](const BoxRec& x, const BoxRec& y) { return x.c2 < y.c2; });
+    for (size_t i = 0; i < mine.size(); ++i)
+      if (i == 0 || mine[i].c2 != mine[i - 1].c2) boxes.push_back(mine[i]);
+  }
+  a->n_boxes = (int64_t)boxes.size();
+
+  // ------------------------------------------------------------ C5 compatibility sets
+  std::vector<int32_t> pp(NC);
+  std::vector<uint8_t> px(NC, 0);   // parity to parent
+  std::iota(pp.begin(), pp.end(), 0);
+  auto pfind = [&](int32_t x, uint8_t& par) {
+    // iterative: collect path, then compress
+    std::vector<int32_t> path;
+    while (pp[x] != x) { path.push_back(x); x = pp[x]; }
+    uint8_t acc = 0;
+    for (size_t i = path.size(); i-- > 0;) {
+      int32_t y = path[i];
+      acc ^= px[y];
+      px[y] = acc;
+      pp[y] = x;
+    }
+    par = path.empty() ? 0 : px[path[0]];
+    return x;
+  };
+  std::vector<char> box_ok(boxes.size(), 0);
+  for (size_t b = 0; b < boxes.size(); ++b) {
+    uint8_t p1, p2;
+    int32_t r1 = pfind(boxes[b].c1, p1), r2 = pfind(boxes[b].c2, p2);
+    if (r1 == r2) {
+      if ((p1 ^ p2) != boxes[b].parity) { a->dropped_boxes++; continue; }
+      box_ok[b] = 1;
+      continue;
+    }
+    pp[r2] = r1;
+    px[r2] = (uint8_t)(p1 ^ p2 ^ boxes[b].parity);
+    box_ok[b] = 1;
+  }
+  std::vector<int32_t> root_first(NC, -1);   // root -> smallest conflict
+  std::vector<uint8_t> cpar(NC);
+  std::vector<int32_t> croot(NC);
+  for (int32_t i = 0; i < NC; ++i) {
+    croot[i] = pfind(i, cpar[i]);
+    if (root_first[croot[i]] < 0) root_first[croot[i]] = i;
+  }
+  std::vector<int32_t> set_of_root(NC, -1);
+  int32_t n_sets = 0;
+  for (int32_t i = 0; i < NC; ++i)
+    if (root_first[croot[i]] == i) set_of_root[croot[i]] = n_sets++;
+  for (int32_t i = 0; i < NC; ++i) {
+    auto& c = a->conflicts[i];
+    int32_t first = root_first[croot[i]];
+    c.set = set_of_root[croot[i]];
+    c.side0 = (cpar[i] ^ cpar[first]) ? c.v : c.u;
+  }
+
+  // ------------------------------------------------------------ C6 SetGroups (3-round WL)
+  a->set_sig.assign(n_sets, 0);
+  {
+    std::vector<std::vector<int32_t>> set_conf(n_sets);
+    for (int32_t i = 0; i < NC; ++i) set_conf[a->conflicts[i].set].push_back(i);
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> set_medges(n_sets);
+    for (size_t b = 0; b < boxes.size(); ++b) {
+      if (!box_ok[b]) continue;
+      auto& E = set_medges[a->conflicts[boxes[b].c1].set];
+      E.push_back({boxes[b].N, boxes[b].L});
+      E.push_back({boxes[b].O, boxes[b].R});
+    }
+    for (int32_t s = 0; s < n_sets; ++s) {
+      std::map<int32_t, int> side;   // node -> side mask
+      std::vector<std::pair<int32_t, int32_t>> cedges;
+      for (int32_t i : set_conf[s]) {
+        const auto& c = a->conflicts[i];
+        int32_t s1 = c.side0 == c.u ? c.v : c.u;
+        side[c.side0] |= 1;
+        side[s1] |= 2;
+        cedges.push_back({c.u, c.v});
+      }
+      auto& me = set_medges[s];
+      std::sort(me.begin(), me.end());
+      me.erase(std::unique(me.begin(), me.end()), me.end());
+      std::sort(cedges.begin(), cedges.end());
+      cedges.erase(std::unique(cedges.begin(), cedges.end()), cedges.end());
+      std::vector<int32_t> nodes;
+      for (auto& kv : side) nodes.push_back(kv.first);
+      std::map<int32_t, size_t> pos;
+      for (size_t i = 0; i < nodes.size(); ++i) pos[nodes[i]] = i;
+      std::vector<uint64_t> lab(nodes.size());
+      for (size_t i = 0; i < nodes.size(); ++i) {
+        int32_t l = nodes[i];
+        uint64_t x[4] = {fnv(g->ops[a->loop_op[l]].name), (uint64_t)a->loop_role[l], (uint64_t)a->loop_type[l],
+                         (uint64_t)side[l]};
+        lab[i] = hfold(x, 4);
+      }
+      for (int round = 0; round < 3; ++round) {
+        std::vector<std::vector<uint64_t>> outs(nodes.size()), ins(nodes.size()), cfs(nodes.size());
+        for (auto& e : me) { outs[pos[e.first]].push_back(lab[pos[e.second]]); ins[pos[e.second]].push_back(lab[pos[e.first]]); }
+        for (auto& e : cedges) { cfs[pos[e.first]].push_back(lab[pos[e.second]]); cfs[pos[e.second]].push_back(lab[pos[e.first]]); }
+        std::vector<uint64_t> nl(nodes.size());
+        for (size_t i = 0; i < nodes.size(); ++i) {
+          uint64_t x[4] = {lab[i], hfold(outs[i], true), hfold(ins[i], true), hfold(cfs[i], true)};
+          nl[i] = hfold(x, 4);
+        }
+        lab.swap(nl);
+      }
+      a->set_sig[s] = hfold(lab, true);
+    }
+    std::map<uint64_t, int32_t> gid;
+    a->set_group.assign(n_sets, -1);
+    for (int32_t s = 0; s < n_sets; ++s) {
+      auto it = gid.find(a->set_sig[s]);
+      if (it == gid.end()) it = gid.emplace(a->set_sig[s], a->n_groups++).first;
+      a->set_group[s] = it->second;
+    }
+  }
+  if (a->n_groups > MAX_GROUPS) { err = "more than 64 SetGroups"; return TOAST_E_LIMIT; }
+
+  // ------------------------------------------------------------ C7 argument groups, super-colors
+  {
+    std::map<std::vector<int64_t>, std::vector<int32_t>> groups;
+    for (int32_t p = 0; p < g->n_params; ++p) {
+      int32_t v = g->ops[p].result;
+      const auto& shp = g->values[v].shape;
+      std::vector<std::vector<std::array<int64_t, 4>>> per(shp.size());
+      for (int32_t t = 0; t < n_ops; ++t)
+        for (size_t k = 0; k < g->ops[t].operands.size(); ++k)
+          if (g->ops[t].operands[k] == v)
+            for (size_t i = 0; i < shp.size(); ++i) {
+              int32_t l = use_loop(t, (int)k, (int)i);
+              per[i].push_back({(int64_t)fnv(g->ops[t].name), (int64_t)k, (int64_t)a->loop_role[l], (int64_t)a->loop_type[l]});
+            }
+      std::vector<int64_t> key = {g->values[v].dtype_code, (int64_t)shp.size()};
+      key.insert(key.end(), shp.begin(), shp.end());
+      for (auto& d : per) {
+        std::sort(d.begin(), d.end());
+        key.push_back((int64_t)d.size());
+        for (auto& q : d) key.insert(key.end(), q.begin(), q.end());
+      }
+      groups[key].push_back(v);
+    }
+    DSU sd(NL);
+    for (int64_t l = 0; l < NL; ++l) sd.join((int32_t)l, a->loop_comp[l]);
+    for (auto& kv : groups) {
+      const auto& mem = kv.second;
+      for (size_t j = 1; j < mem.size(); ++j)
+        for (size_t i = 0; i < g->values[mem[0]].shape.size(); ++i) sd.join(def_loop(mem[0], (int)i), def_loop(mem[j], (int)i));
+    }
+    std::vector<int32_t> sc_of_root(NL, -1);
+    a->loop_scolor.resize(NL);
+    for (int64_t l = 0; l < NL; ++l) {
+      int32_t r = sd.root((int32_t)l);
+      if (sc_of_root[r] < 0) { sc_of_root[r] = (int32_t)a->sc_min_loop.size(); a->sc_min_loop.push_back((int32_t)l); }
+      a->loop_scolor[l] = sc_of_root[r];
+    }
+  }
+  const int32_t NSC = (int32_t)a->sc_min_loop.size();
+  a->sc_value_dims.assign(NSC, 0);
+  for (size_t v = 0; v < g->values.size(); ++v)
+    for (size_t i = 0; i < g->values[v].shape.size(); ++i) a->sc_value_dims[a->loop_scolor[def_loop((int32_t)v, (int)i)]]++;
+  a->sc_groups.assign(NSC, {});
+  for (auto& c : a->conflicts) a->sc_groups[a->loop_scolor[c.u]].push_back(a->set_group[c.set]);
+  for (auto& sg : a->sc_groups) { std::sort(sg.begin(), sg.end()); sg.erase(std::unique(sg.begin(), sg.end()), sg.end()); }
+
+  // ------------------------------------------------------------ C8 action table
+  a->actions.clear();
+  a->actions.push_back({-1, 0, -1, 0});
+  std::vector<int32_t> acolor_of_sc(NSC, -1), sc_of_acolor;
+  for (int32_t c = 0; c < NSC; ++c) {
+    if (a->sc_value_dims[c] < o->min_unique_dims) continue;
+    if (a->sc_groups[c].size() > 8) { err = "more than 8 SetGroups in one super-color"; return TOAST_E_LIMIT; }
+    acolor_of_sc[c] = (int32_t)sc_of_acolor.size();
+    sc_of_acolor.push_back(c);
+    for (int32_t r = 0; r < (1 << a->sc_groups[c].size()); ++r)
+      for (int ax = 0; ax < n_axes; ++ax) a->actions.push_back({c, r, ax, (int32_t)a->sc_value_dims[c]});
+  }
+  if (a->actions.size() > (size_t)MAX_ACTIONS) { err = "more than 1023 actions"; return TOAST_E_LIMIT; }
+
+  // ------------------------------------------------------------ packed tables
+  const int32_t NA = (int32_t)a->actions.size();
+  const int32_t nwords = (NA + 31) / 32;
+  // deselection ids: need0 = groups where the loop is a side-1 endpoint (deselected when bit = 0),
+  //                  need1 = groups where it is a side-0 endpoint (deselected when bit = 1)
+  std::map<int32_t, std::pair<uint64_t, uint64_t>> dsel;
+  for (auto& c : a->conflicts) {
+    uint64_t gb = 1ULL << a->set_group[c.set];
+    int32_t s1 = c.side0 == c.u ? c.v : c.u;
+    dsel[s1].first |= gb;
+    dsel[c.side0].second |= gb;
+  }
+  a->h_desel.assign(2, 0);   // id 0 = none
+  std::map<int32_t, uint32_t> dsel_id;
+  for (auto& kv : dsel) {
+    dsel_id[kv.first] = (uint32_t)(a->h_desel.size() / 2);
+    a->h_desel.push_back(kv.second.first);
+    a->h_desel.push_back(kv.second.second);
+  }
+  if (a->h_desel.size() / 2 >= 65536) { err = "too many conflict endpoints"; return TOAST_E_LIMIT; }
+  a->h_loops.resize(NL);
+  for (int64_t l = 0; l < NL; ++l) {
+    uint32_t ac = acolor_of_sc[a->loop_scolor[l]] >= 0 ? (uint32_t)acolor_of_sc[a->loop_scolor[l]] : NO_ACOLOR;
+    if (a->loop_type[l] == T_X) ac = NO_ACOLOR;
+    uint32_t div = 0;
+    for (int S = 0; S < 16; ++S) {
+      int64_t prod = 1;
+      bool valid = true;
+      for (int A = 0; A < 4; ++A) if (S >> A & 1) { if (A >= n_axes) valid = false; else prod *= g->axis_size[A]; }
+      if (valid && a->loop_ext[l] % prod == 0) div |= 1u << S;
+    }
+    auto it = dsel_id.find((int32_t)l);
+    uint64_t did = it == dsel_id.end() ? 0 : it->second;
+    a->h_loops[l] = (uint64_t)ac | ((uint64_t)a->loop_type[l] << 10) | ((uint64_t)div << 12) | (did << 28);
+  }
+  // last uses and deaths (C12)
+  std::vector<int32_t> last_use(g->values.size());
+  for (size_t v = 0; v < g->values.size(); ++v) last_use[v] = g->values[v].def_op;
+  for (int32_t t = 0; t < n_ops; ++t)
+    for (int32_t v : g->ops[t].operands) last_use[v] = std::max(last_use[v], t);
+  std::vector<std::vector<int32_t>> deaths(n_ops);
+  for (size_t v = 0; v < g->values.size(); ++v) deaths[last_use[v]].push_back(g->values[v].def_op);
+  a->h_ops.resize(n_ops);
+  a->h_gflops.assign(n_ops, 0);
+  a->h_uses.clear();
+  a->h_deaths.clear();
+  for (int32_t t = 0; t < n_ops; ++t) {
+    const GOp& op = g->ops[t];
+    DOp d{};
+    d.loop_begin = (uint32_t)lbeg[t];
+    d.n_loops = (uint8_t)OL[t].ext.size();
+    d.rank = op.result >= 0 ? (uint8_t)g->values[op.result].shape.size() : 0;
+    for (size_t r = 0; r < OL[t].type.size(); ++r) if (OL[t].type[r] == T_R) d.rmask |= (uint8_t)(1u << r);
+    d.flags = (is_matmul_class(op.kind) ? 1 : 0) | (op.kind == OK_RET ? 2 : 0);
+    for (size_t i = 0; i < OL[t].res_role.size(); ++i) d.res_roles |= (uint32_t)OL[t].res_role[i] << (4 * i);
+    d.use_begin = (uint32_t)a->h_uses.size();
+    d.n_uses = (uint8_t)op.operands.size();
+    for (size_t k = 0; k < op.operands.size(); ++k) {
+      DUse u{};
+      u.def_op = (uint32_t)g->values[op.operands[k]].def_op;
+      for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) u.use_roles |= (uint32_t)OL[t].use_role[k][i] << (4 * i);
+      a->h_uses.push_back(u);
+    }
+    d.death_begin = (uint32_t)a->h_deaths.size();
+    d.n_death = (uint16_t)deaths[t].size();
+    if (deaths[t].size() > 65535) { err = "too many values die at one op"; return TOAST_E_LIMIT; }
+    for (int32_t v : deaths[t]) a->h_deaths.push_back((uint32_t)v);
+    if (op.result >= 0) {
+      uint64_t b = (uint64_t)g->values[op.result].elem_bytes;
+      for (int64_t e : g->values[op.result].shape) b *= (uint64_t)e;
+      d.gbytes = b;
+    }
+    if (d.flags & 1) {
+      uint64_t f = 2;
+      for (int64_t e : OL[t].ext) f *= (uint64_t)e;
+      a->h_gflops[t] = f;
+    }
+    a->h_ops[t] = d;
+  }
+  // actions and per-acolor groups
+  a->h_actions.assign(NA, 0);
+  for (int32_t i = 1; i < NA; ++i) {
+    const auto& ai = a->actions[i];
+    a->h_actions[i] = (uint32_t)acolor_of_sc[ai.super_color] | ((uint32_t)ai.resolution << 10) | ((uint32_t)ai.axis << 18);
+  }
+  a->h_acol_groups.assign(sc_of_acolor.size(), 0);
+  for (size_t ac = 0; ac < sc_of_acolor.size(); ++ac) {
+    const auto& gs = a->sc_groups[sc_of_acolor[ac]];
+    uint64_t w = 0;
+    for (int t = 0; t < 8; ++t) w |= (uint64_t)(t < (int)gs.size() ? gs[t] : 0xFF) << (8 * t);
+    a->h_acol_groups[ac] = w;
+  }
+  // kill masks (C15): chosen a kills b iff same (color, axis) or a shared group's bit disagrees
+  a->h_kill.assign((size_t)NA * nwords, 0);
+  for (int32_t x = 1; x < NA; ++x) {
+    const auto& ax = a->actions[x];
+    const auto& gx = a->sc_groups[ax.super_color];
+    for (int32_t y = 1; y < NA; ++y) {
+      const auto& ay = a->actions[y];
+      bool kill = ax.super_color == ay.super_color && ax.axis == ay.axis;
+      if (!kill) {
+        const auto& gy = a->sc_groups[ay.super_color];
+        for (size_t i = 0; i < gx.size() && !kill; ++i)
+          for (size_t j = 0; j < gy.size(); ++j)
+            if (gx[i] == gy[j] && (((ax.resolution >> i) ^ (ay.resolution >> j)) & 1)) { kill = true; break; }
+      }
+      if (kill) a->h_kill[(size_t)x * nwords + (y >> 5)] |= 1u << (y & 31);
+    }
+  }
+
+  // ------------------------------------------------------------ baseline (empty sequence)
+  {
+    unsigned __int128 fl = 0;
+    for (int32_t t = 0; t < n_ops; ++t) fl += a->h_gflops[t];
+    int64_t L = 0, peak = 0;
+    for (int32_t t = 0; t < n_ops; ++t) {
+      int64_t res = (int64_t)a->h_ops[t].gbytes;
+      peak = std::max(peak, L + res);
+      int64_t dy = 0;
+      for (int32_t v : deaths[t]) dy += (int64_t)a->h_ops[v].gbytes;
+      L += res - dy;
+    }
+    uint64_t lo = (uint64_t)fl, hi = (uint64_t)(fl >> 64);
+    volatile double fhi = (double)hi;
+    double fd = fhi * 18446744073709551616.0;
+    fd = fd + (double)lo;
+    double t0 = fd / g->machine.flops_per_sec;
+    if (!(t0 > 0.0)) { err = "baseline runtime is 0: the program has no contraction op"; return TOAST_E_DEGENERATE; }
+    a->t0 = t0;
+    a->peak0 = (uint64_t)peak;
+    memset(&a->baseline, 0, sizeof(a->baseline));
+    a->baseline.runtime_s = t0;
+    a->baseline.peak_bytes = (uint64_t)peak;
+    a->baseline.flops = lo;
+    a->baseline.flops_hi = hi;
+    double MP = (uint64_t)peak > g->machine.device_memory_bytes
+                    ? (g->machine.penalty_c * (double)((uint64_t)peak - g->machine.device_memory_bytes)) / (double)peak
+                    : 0.0;
+    a->baseline.score = t0 / t0 + MP;
+  }
+
+  // ------------------------------------------------------------ constants
+  DeviceTables& T = a->dt;
+  T.n_ops = n_ops;
+  T.n_loops = (int32_t)NL;
+  T.n_actions = NA;
+  T.n_acolors = (int32_t)sc_of_acolor.size();
+  T.n_words = nwords;
+  T.n_axes = n_axes;
+  T.max_depth = o->max_depth;
+  for (int A = 0; A < 4; ++A) {
+    T.sizes[A] = A < n_axes ? g->axis_size[A] : 1;
+    T.bw[A] = A < n_axes ? g->axis_bw[A] : 1.0;
+  }
+  T.F = g->machine.flops_per_sec;
+  T.C = g->machine.penalty_c;
+  T.DM = g->machine.device_memory_bytes;
+  T.t0 = a->t0;
+  T.peak0 = a->peak0;
+  for (int S = 0; S < 16; ++S) {
+    uint64_t d = 1;
+    for (int A = 0; A < n_axes; ++A) if (S >> A & 1) d *= (uint64_t)g->axis_size[A];
+    uint32_t sh = 0;
+    while (!(d & 1)) { d >>= 1; ++sh; }
+    uint64_t inv = d;                 // Newton iteration for the inverse of an odd d mod 2^64
+    for (int it = 0; it < 6; ++it) inv *= 2 - d * inv;
+    T.shift[S] = sh;
+    T.inv[S] = inv;
+  }
+  return TOAST_OK;
+}
+
+// ---------------------------------------------------------------- host materialisation (debug)
+void host_materialize(const toast_analysis* a, const uint16_t* seq, uint8_t* masks) {
+  const DeviceTables& T = a->dt;
+  std::vector<uint32_t> lists(T.n_acolors, 0);
+  uint64_t fixed = 0, ones = 0;
+  int n = 0;
+  while (n < 32 && seq[n]) ++n;
+  for (int j = 0; j < n; ++j) {
+    uint32_t w = a->h_actions[seq[j]];
+    uint32_t ac = w & 0x3FF, r = (w >> 10) & 0xFF, ax = (w >> 18) & 3;
+    int rank = 0;
+    while ((lists[ac] >> (8 * rank)) & 0x80) ++rank;
+    lists[ac] |= (0x80u | (ax << 5) | (uint32_t)j) << (8 * rank);
+    uint64_t gw = a->h_acol_groups[ac];
+    for (int t = 0; t < 8; ++t) {
+      uint32_t gid = (gw >> (8 * t)) & 0xFF;
+      if (gid == 0xFF) break;
+      fixed |= 1ULL << gid;
+      if ((r >> t) & 1) ones |= 1ULL << gid;
+    }
+  }
+  memset(masks, 0, (size_t)T.n_loops);
+  for (int32_t t = 0; t < T.n_ops; ++t) {
+    const DOp& op = a->h_ops[t];
+    uint32_t l8[8] = {0};
+    uint32_t div[8] = {0};
+    for (int r = 0; r < op.n_loops; ++r) {
+      uint64_t L = a->h_loops[op.loop_begin + r];
+      uint32_t ac = L & 0x3FF;
+      div[r] = (L >> 12) & 0xFFFF;
+      if (ac == NO_ACOLOR) continue;
+      uint32_t did = (L >> 28) & 0xFFFF;
+      if (did && ((((fixed & ~ones) & a->h_desel[2 * did]) | (ones & a->h_desel[2 * did + 1])) != 0)) continue;
+      l8[r] = lists[ac];
+    }
+    uint32_t opmask = 0, mk[8] = {0};
+    while (true) {
+      int best = -1;
+      uint32_t bj = 99;
+      for (int r = 0; r < op.n_loops; ++r)
+        if ((l8[r] & 0x80) && (l8[r] & 31) < bj) { bj = l8[r] & 31; best = r; }
+      if (best < 0) break;
+      uint32_t A = (l8[best] >> 5) & 3;
+      if (!(opmask >> A & 1) && ((div[best] >> (mk[best] | (1u << A))) & 1)) { mk[best] |= 1u << A; opmask |= 1u << A; }
+      l8[best] >>= 8;
+    }
+    for (int r = 0; r < op.n_loops; ++r) masks[op.loop_begin + r] = (uint8_t)mk[r];
+  }
+}
+
+// ---------------------------------------------------------------- JSON dump (same schema as the oracle's)
+std::string dump_json(const toast_analysis* a) {
+  std::string s;
+  s.reserve(64 * (size_t)a->n_loops + 4096);
+  auto I = [](int64_t x) { return std::to_string(x); };
+  s += "{\"n_ops\":" + I(a->n_ops) + ",\"n_loops\":" + I(a->n_loops) + ",\"n_edges\":" + I(a->n_edges) + ",\"loops\":[";
+  for (int64_t l = 0; l < a->n_loops; ++l) {
+    if (l) s += ',';
+    s += '[' + I(a->loop_op[l]) + ',' + I(a->loop_role[l]) + ',' + I(a->loop_ext[l]) + ',' + I(a->loop_type[l]) + ',' +
+         I(a->loop_comp[l]) + ',' + I(a->loop_scolor[l]) + ']';
+  }
+  s += "],\"conflicts\":[";
+  for (size_t i = 0; i < a->conflicts.size(); ++i) {
+    const auto& c = a->conflicts[i];
+    if (i) s += ',';
+    s += '[' + I(c.op) + ',' + I(c.u) + ',' + I(c.v) + ',' + I(c.set) + ',' + I(c.side0) + ']';
+  }
+  s += "],\"n_boxes\":" + I(a->n_boxes) + ",\"dropped_boxes\":" + I(a->dropped_boxes) + ",\"set_group\":[";
+  for (size_t i = 0; i < a->set_group.size(); ++i) { if (i) s += ','; s += I(a->set_group[i]); }
+  s += "],\"set_sig\":[";
+  for (size_t i = 0; i < a->set_sig.size(); ++i) {
+    if (i) s += ',';
+    char b[32];
+    snprintf(b, sizeof b, "\"%016llx\"", (unsigned long long)a->set_sig[i]);
+    s += b;
+  }
+  s += "],\"n_groups\":" + I(a->n_groups) + ",\"scolors\":[";
+  for (size_t c = 0; c < a->sc_min_loop.size(); ++c) {
+    if (c) s += ',';
+    s += '[' + I(a->sc_min_loop[c]) + ',' + I(a->sc_value_dims[c]) + ",[";
+    for (size_t j = 0; j < a->sc_groups[c].size(); ++j) { if (j) s += ','; s += I(a->sc_groups[c][j]); }
+    s += "]]";
+  }
+  s += "],\"actions\":[";
+  for (size_t i = 1; i < a->actions.size(); ++i) {
+    if (i > 1) s += ',';
+    s += '[' + I(a->actions[i].super_color) + ',' + I(a->actions[i].resolution) + ',' + I(a->actions[i].axis) + ']';
+  }
+  char b[160];
+  snprintf(b, sizeof b, "],\"baseline\":{\"runtime\":%.17g,\"peak\":%llu,\"flops\":%llu}}", a->t0,
+           (unsigned long long)a->peak0, (unsigned long long)a->baseline.flops);
+  s += b;
+  return s;
+}
+
+}  // namespace toast

@@ -1,0 +1,286 @@
+// Host MCTS around the K1/K2 kernels.
+// One tree per rank rooted at the unsharded module.  A round
+// selects L leaves by UCT with virtual loss, expands the lowest untried legal
+// action of each, evaluates each leaf's own state exactly (K1) plus R Philox
+// rollouts from it (K2, "generating many trajectories"), backs up
+// reward = -score, and stops when a round fails to improve the best
+// (patience configurable) or the budget is spent.
+// Root-parallel ranks exchange one fixed-size record per round; the caller
+// all-gathers the records (torch.distributed / NCCL) and imports them.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "toast_internal.h"
+
+namespace toast {
+
+struct SNode {
+  std::vector<uint16_t> prefix;
+  std::vector<int32_t> untried;
+  std::vector<SNode*> children;
+  SNode* parent = nullptr;
+  double W = 0.0;
+  int64_t N = 0;
+};
+
+// per-round exchange record (fixed size, host memory)
+struct ExportRec {
+  double best_score;
+  uint64_t best_key;
+  uint16_t best_seq[32];
+  int64_t evals;          // evaluations done by this rank so far
+  double elapsed_s;       // this rank's wall clock since begin
+  int32_t rank;
+  int32_t pad;
+  toast_cost best;        // full record of the rank's best
+};
+
+}  // namespace toast
+
+struct toast_search_state {
+  const toast_analysis* a = nullptr;
+  toast_search_opts o{};
+  int32_t rank = 0, world = 1;
+  uint64_t seed = 0;
+  toast::SNode* root = nullptr;
+  // local incumbent (reset to the global one after each import) and global incumbent
+  toast_cost best{};
+  uint16_t best_seq[32] = {0};
+  toast_cost gbest{};
+  uint16_t gbest_seq[32] = {0};
+  int64_t evals = 1;           // this rank (the root eval counts once)
+  int64_t global_evals = 1;
+  int64_t rollouts_done = 0;
+  int32_t rounds = 0, nonimprove = 0, hit_target = 0, done = 0;
+  double time_to_target = -1.0;
+  std::chrono::steady_clock::time_point t_start;
+  // buffers
+  std::vector<uint16_t> h_lpre, h_pre, h_outs;
+  std::vector<toast_cost> h_lcost, h_cost;
+  void* d_buf = nullptr;
+  size_t d_bytes = 0;
+  ~toast_search_state();
+};
+
+namespace toast {
+namespace {
+
+void free_tree(SNode* n) {
+  if (!n) return;
+  std::vector<SNode*> st{n};
+  while (!st.empty()) {
+    SNode* x = st.back();
+    st.pop_back();
+    for (SNode* c : x->children) st.push_back(c);
+    delete x;
+  }
+}
+
+std::vector<int32_t> legal_after(const toast_analysis* a, const std::vector<uint16_t>& prefix) {
+  std::vector<int32_t> out;
+  if ((int)prefix.size() >= a->dt.max_depth) return out;
+  const int nw = a->dt.n_words;
+  std::vector<uint32_t> legal(nw, 0xffffffffu);
+  legal[0] &= ~1u;
+  for (uint16_t p : prefix)
+    for (int w = 0; w < nw; ++w) legal[w] &= ~a->h_kill[(size_t)p * nw + w];
+  for (int32_t x = 1; x < a->dt.n_actions; ++x)
+    if ((legal[x >> 5] >> (x & 31)) & 1) out.push_back(x);
+  return out;
+}
+
+bool better(const toast_cost& x, const uint16_t* sx, const toast_cost& y, const uint16_t* sy) {
+  if (x.score != y.score) return x.score < y.score;
+  if (x.state_key != y.state_key) return x.state_key < y.state_key;
+  for (int i = 0; i < 32; ++i) if (sx[i] != sy[i]) return sx[i] < sy[i];
+  return false;
+}
+
+double elapsed(const toast_search_state* s) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - s->t_start).count();
+}
+
+}  // namespace
+
+toast_status search_begin(const toast_analysis* a, const toast_search_opts* o, int32_t rank, int32_t world,
+                          toast_search_state** out, std::string& err) {
+  if (o->leaves_per_round < 1 || o->rollouts_per_leaf < 0 || o->patience < 1 || world < 1 || rank < 0 || rank >= world) {
+    err = "bad search options";
+    return TOAST_E_INVALID_ARG;
+  }
+  auto s = std::make_unique<toast_search_state>();
+  s->a = a;
+  s->o = *o;
+  s->rank = rank;
+  s->world = world;
+  s->seed = o->seed + (uint64_t)rank;
+  s->t_start = std::chrono::steady_clock::now();
+  s->root = new SNode();
+  s->root->untried = legal_after(a, s->root->prefix);
+  s->best = a->baseline;              // the unsharded root is the first incumbent
+  memset(s->best_seq, 0, sizeof s->best_seq);
+  s->gbest = s->best;
+  memset(s->gbest_seq, 0, sizeof s->gbest_seq);
+  const int64_t L = o->leaves_per_round, R = o->rollouts_per_leaf;
+  s->h_lpre.assign((size_t)L * 32, 0);
+  s->h_pre.assign((size_t)L * R * 32, 0);
+  s->h_outs.assign((size_t)L * R * 32, 0);
+  s->h_lcost.resize((size_t)L);
+  s->h_cost.resize((size_t)L * R);
+  s->d_bytes = (size_t)L * 64 + (size_t)L * sizeof(toast_cost) + (size_t)L * R * (64 + 64 + sizeof(toast_cost));
+  cudaError_t e = cudaMalloc(&s->d_buf, s->d_bytes);
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_OOM; }
+  *out = s.release();
+  return TOAST_OK;
+}
+
+toast_status search_round(toast_search_state* s, void* export_buf, std::string& err) {
+  const toast_analysis* a = s->a;
+  const int L = s->o.leaves_per_round, R = s->o.rollouts_per_leaf;
+  std::vector<SNode*> leaves;
+  for (int l = 0; l < L; ++l) {
+    SNode* node = s->root;
+    while (true) {
+      if (!node->untried.empty()) {
+        SNode* ch = new SNode();
+        ch->prefix = node->prefix;
+        ch->prefix.push_back((uint16_t)node->untried.front());
+        node->untried.erase(node->untried.begin());
+        ch->parent = node;
+        ch->untried = legal_after(a, ch->prefix);
+        node->children.push_back(ch);
+        node = ch;
+        break;
+      }
+      if (node->children.empty()) break;
+      SNode* bc = nullptr;
+      double bv = 0;
+      for (SNode* ch : node->children) {
+        double v = ch->W / (double)ch->N + s->o.uct_c * std::sqrt(std::log((double)node->N) / (double)ch->N);
+        if (!bc || v > bv) { bc = ch; bv = v; }
+      }
+      node = bc;
+    }
+    for (SNode* x = node; x; x = x->parent) { x->N += 1; x->W -= 1.0; }   // virtual loss
+    leaves.push_back(node);
+  }
+  // device batch: L exact leaf evals + L*R rollouts
+  std::fill(s->h_lpre.begin(), s->h_lpre.end(), 0);
+  std::fill(s->h_pre.begin(), s->h_pre.end(), 0);
+  for (int l = 0; l < L; ++l) {
+    const auto& p = leaves[l]->prefix;
+    for (size_t i = 0; i < p.size(); ++i) s->h_lpre[(size_t)l * 32 + i] = p[i];
+    for (int j = 0; j < R; ++j)
+      for (size_t i = 0; i < p.size(); ++i) s->h_pre[((size_t)l * R + j) * 32 + i] = p[i];
+  }
+  char* d = reinterpret_cast<char*>(s->d_buf);
+  uint16_t* d_lpre = reinterpret_cast<uint16_t*>(d);
+  toast_cost* d_lcost = reinterpret_cast<toast_cost*>(d + (size_t)L * 64);
+  uint16_t* d_pre = reinterpret_cast<uint16_t*>(d + (size_t)L * (64 + sizeof(toast_cost)));
+  uint16_t* d_outs = d_pre + (size_t)L * R * 32;
+  toast_cost* d_cost = reinterpret_cast<toast_cost*>(d_outs + (size_t)L * R * 32);
+  cudaStream_t st = (cudaStream_t)s->o.cuda_stream;
+  auto ck = [&](cudaError_t e) { if (e != cudaSuccess) { err = cudaGetErrorString(e); return false; } return true; };
+  if (!ck(cudaMemcpyAsync(d_lpre, s->h_lpre.data(), (size_t)L * 64, cudaMemcpyHostToDevice, st))) return TOAST_E_CUDA;
+  if (R > 0 && !ck(cudaMemcpyAsync(d_pre, s->h_pre.data(), (size_t)L * R * 64, cudaMemcpyHostToDevice, st))) return TOAST_E_CUDA;
+  toast_status ts = launch_eval(a, d_lpre, L, d_lcost, st, err);
+  if (ts) return ts;
+  if (R > 0) {
+    ts = launch_rollout(a, d_pre, (int64_t)L * R, s->seed, (uint64_t)s->rollouts_done, d_outs, d_cost, st, err);
+    if (ts) return ts;
+  }
+  if (!ck(cudaMemcpyAsync(s->h_lcost.data(), d_lcost, (size_t)L * sizeof(toast_cost), cudaMemcpyDeviceToHost, st))) return TOAST_E_CUDA;
+  if (R > 0) {
+    if (!ck(cudaMemcpyAsync(s->h_cost.data(), d_cost, (size_t)L * R * sizeof(toast_cost), cudaMemcpyDeviceToHost, st))) return TOAST_E_CUDA;
+    if (!ck(cudaMemcpyAsync(s->h_outs.data(), d_outs, (size_t)L * R * 64, cudaMemcpyDeviceToHost, st))) return TOAST_E_CUDA;
+  }
+  if (!ck(cudaStreamSynchronize(st))) return TOAST_E_CUDA;
+  s->rollouts_done += (int64_t)L * R;
+  for (SNode* lf : leaves) for (SNode* x = lf; x; x = x->parent) { x->N -= 1; x->W += 1.0; }
+  auto consider = [&](const toast_cost& c, const uint16_t* sq, SNode* leaf) {
+    double reward = -c.score;
+    for (SNode* x = leaf; x; x = x->parent) { x->N += 1; x->W += reward; }
+    if (c.status == 0 && better(c, sq, s->best, s->best_seq)) {
+      s->best = c;
+      memcpy(s->best_seq, sq, 64);
+    }
+  };
+  for (int l = 0; l < L; ++l) {
+    consider(s->h_lcost[l], &s->h_lpre[(size_t)l * 32], leaves[l]);
+    for (int j = 0; j < R; ++j) consider(s->h_cost[(size_t)l * R + j], &s->h_outs[((size_t)l * R + j) * 32], leaves[l]);
+  }
+  s->evals += (int64_t)L * (R + 1);
+  s->rounds++;
+  ExportRec* ex = reinterpret_cast<ExportRec*>(export_buf);
+  memset(ex, 0, sizeof(ExportRec));
+  ex->best_score = s->best.score;
+  ex->best_key = s->best.state_key;
+  memcpy(ex->best_seq, s->best_seq, 64);
+  ex->evals = s->evals;
+  ex->elapsed_s = elapsed(s);
+  ex->rank = s->rank;
+  ex->best = s->best;
+  return TOAST_OK;
+}
+
+toast_status search_import(toast_search_state* s, const void* gathered, int32_t* stop, std::string& err) {
+  (void)err;
+  const ExportRec* r = reinterpret_cast<const ExportRec*>(gathered);
+  int gb = 0;
+  int64_t tot = 0;
+  for (int i = 0; i < s->world; ++i) {
+    tot += r[i].evals;
+    if (i && better(r[i].best, r[i].best_seq, r[gb].best, r[gb].best_seq)) gb = i;
+  }
+  // the global incumbent before this round is identical on every rank
+  bool improved = better(r[gb].best, r[gb].best_seq, s->gbest, s->gbest_seq);
+  if (improved) {
+    s->gbest = r[gb].best;
+    memcpy(s->gbest_seq, r[gb].best_seq, 64);
+  }
+  s->best = s->gbest;
+  memcpy(s->best_seq, s->gbest_seq, 64);
+  s->global_evals = tot;
+  const double el = r[0].elapsed_s;   // rank 0's clock decides time limits on every rank
+  if (s->time_to_target < 0 && !std::isnan(s->o.target_score) && s->best.score <= s->o.target_score) {
+    s->time_to_target = el;
+    s->hit_target = 1;
+  }
+  if (improved) s->nonimprove = 0;
+  else s->nonimprove++;
+  int st = 0;
+  if (s->nonimprove >= s->o.patience) st = 1;
+  if (s->o.max_evals > 0 && tot >= s->o.max_evals) st = 1;
+  if (s->o.time_limit_s > 0 && el >= s->o.time_limit_s) st = 1;
+  if (s->hit_target) st = 1;
+  s->done = st;
+  *stop = st;
+  return TOAST_OK;
+}
+
+void search_result(const toast_search_state* s, toast_search_result* out) {
+  memset(out, 0, sizeof(*out));
+  memcpy(out->best_seq, s->best_seq, 64);
+  out->best = s->best;
+  out->evals = s->global_evals;
+  out->rounds = s->rounds;
+  out->hit_target = s->hit_target;
+  out->wall_s = elapsed(s);
+  out->time_to_target_s = s->time_to_target;
+}
+
+size_t search_export_bytes() { return sizeof(ExportRec); }
+
+void search_free(toast_search_state* s) { delete s; }
+
+}  // namespace toast
+
+toast_search_state::~toast_search_state() {
+  toast::free_tree(root);
+  if (d_buf) cudaFree(d_buf);
+}

@@ -1,0 +1,170 @@
+// Internal structures of libtoast: host-side graph/analysis and the packed
+// device tables the sm_100a kernels read.
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/toast.h"
+
+namespace toast {
+
+// ----------------------------------------------------------------- op kinds
+enum OpKind : uint8_t {
+  OK_PARAM, OK_RET, OK_UNARY, OK_BINARY, OK_TRANSPOSE, OK_REDUCE, OK_BROADCAST, OK_MATMUL, OK_DOT,
+  OK_CONV, OK_CONV_BI, OK_CONV_BF, OK_RESAMPLE, OK_CONCAT, OK_SLICE, OK_PAD, OK_GATHER, OK_SEGSUM
+};
+
+enum LoopType : uint8_t { T_P = 0, T_R = 1, T_X = 2 };
+
+struct GValue {
+  int32_t dtype_code;          // index into the dtype table (f32, bf16, f16, i32, f64, i64)
+  int32_t elem_bytes;
+  std::vector<int64_t> shape;
+  int32_t def_op;
+  std::string name;
+};
+
+struct GOp {
+  OpKind kind;
+  std::string name;            // IR spelling (hash input for C6/C7)
+  std::vector<int64_t> ia;     // integer attributes (meaning per kind)
+  std::vector<int32_t> operands;
+  int32_t result = -1;
+  std::string binding;
+};
+
+}  // namespace toast
+
+struct toast_graph {
+  std::vector<toast::GValue> values;
+  std::vector<toast::GOp> ops;   // params, body, rets
+  int32_t n_params = 0;
+  std::vector<std::string> axis_names;
+  std::vector<int32_t> axis_size;
+  std::vector<double> axis_bw;
+  toast_machine machine;
+  int32_t device = -1;
+};
+
+namespace toast {
+
+// ------------------------------------------------------------ device tables
+// one op, 32 bytes
+struct DOp {
+  uint32_t loop_begin;   // global id of the op's role-0 loop
+  uint8_t n_loops;
+  uint8_t rank;          // result rank (0 for ret)
+  uint8_t rmask;         // bit r set <=> role r is a reduction (R) loop
+  uint8_t flags;         // bit0 matmul-class, bit1 ret
+  uint32_t res_roles;    // 4 bits per result dim: role of dim i
+  uint32_t use_begin;    // first entry in uses[]
+  uint32_t death_begin;  // first entry in deaths[]
+  uint16_t n_death;
+  uint8_t n_uses;
+  uint8_t pad;
+  uint64_t gbytes;       // global bytes of the result (0 for ret)
+};
+static_assert(sizeof(DOp) == 32, "DOp is 32 B");
+
+// one use (op t, operand k), 8 bytes
+struct DUse {
+  uint32_t def_op;       // value id == defining op
+  uint32_t use_roles;    // 4 bits per dim: role in op t of operand dim i
+};
+
+// packed loop word (uint64):
+//   [0,10)  acolor (0x3FF = no action can touch this loop)
+//   [10,12) type
+//   [12,28) div_ok: bit S <=> extent % prod(sizes of axis subset S) == 0
+//   [28,44) deselection id (0 = never deselected)
+constexpr uint32_t NO_ACOLOR = 0x3FF;
+
+constexpr int MAX_LOOPS_PER_OP = 8;
+constexpr int MAX_USES_PER_OP = 8;
+constexpr int MAX_RANK = 8;
+constexpr int MAX_ACTIONS = 1024;
+constexpr int MAX_GROUPS = 64;
+
+struct DeviceTables {
+  // device pointers
+  const DOp* ops = nullptr;
+  const uint64_t* gflops = nullptr;      // per op (0 unless matmul-class)
+  const uint64_t* loops = nullptr;
+  const DUse* uses = nullptr;
+  const uint32_t* deaths = nullptr;
+  const uint64_t* desel = nullptr;       // [id][2] = need0, need1
+  const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
+  const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids
+  const uint32_t* kill = nullptr;        // [n_actions][n_words]
+  // constants
+  int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, pad;
+  int32_t sizes[4];
+  double bw[4];
+  double F, C, t0;
+  uint64_t DM, peak0;
+  uint64_t inv[16];     // exact division by prod(subset): (x >> shift) * inv
+  uint32_t shift[16];
+};
+
+}  // namespace toast
+
+struct toast_analysis {
+  // host-side results (also used for the JSON dump)
+  int32_t n_ops = 0;
+  int64_t n_loops = 0, n_edges = 0;
+  std::vector<int32_t> loop_op, loop_role, loop_type, loop_comp, loop_scolor;
+  std::vector<int64_t> loop_ext;
+  struct Conf { int32_t op, u, v, set, side0; };
+  std::vector<Conf> conflicts;
+  int64_t n_boxes = 0, dropped_boxes = 0;
+  std::vector<int32_t> set_group;
+  std::vector<uint64_t> set_sig;
+  int32_t n_groups = 0;
+  std::vector<int32_t> sc_min_loop;
+  std::vector<int64_t> sc_value_dims;
+  std::vector<std::vector<int32_t>> sc_groups;
+  std::vector<toast_action_info> actions;   // [0] = STOP
+  toast_cost baseline;
+  double t0 = 0;
+  uint64_t peak0 = 0;
+
+  // host copies of the packed tables (kept for toast_materialize and tests)
+  std::vector<toast::DOp> h_ops;
+  std::vector<uint64_t> h_gflops, h_loops, h_desel, h_acol_groups;
+  std::vector<toast::DUse> h_uses;
+  std::vector<uint32_t> h_deaths, h_actions, h_kill;
+  std::vector<int32_t> axis_size;
+
+  toast::DeviceTables dt;       // device pointers valid iff device >= 0
+  int32_t device = -1;
+  std::vector<void*> dev_allocs;
+
+  // scratch for host-pointer calls
+  std::mutex scratch_mu;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int32_t smem_per_warp = 0;
+  int32_t eval_blocks = 0, rollout_blocks = 0;
+};
+
+namespace toast {
+// ir.cpp
+toast_status parse_ir(const char* text, size_t len, toast_graph* g, std::string& err);
+// analysis.cpp
+toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast_analysis* a, std::string& err);
+std::string dump_json(const toast_analysis* a);
+void host_materialize(const toast_analysis* a, const uint16_t* seq, uint8_t* masks);
+// kernels.cu
+toast_status upload_tables(toast_analysis* a, std::string& err);
+void free_tables(toast_analysis* a);
+toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, toast_cost* d_out, void* stream,
+                         std::string& err);
+toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
+                            uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err);
+toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h_in, int64_t n, uint64_t seed,
+                              uint64_t id_base, uint16_t* h_seqs, toast_cost* h_out, void* stream, std::string& err);
+bool is_device_pointer(const void* p);
+}  // namespace toast

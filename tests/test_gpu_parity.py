@@ -1,0 +1,238 @@
+"""GPU parity: libtoast's sm_100a kernels vs the CPU oracle, element by element.
+
+Bar (BASELINE north star): shardings, collective choice, byte
+counts, peak memory, FLOPs and state keys bit-exact; runtime/score within
+1e-6 relative — asserted here as bit-exact, which is stricter (both sides
+evaluate the same IEEE double expression in the same order without FMA).
+Inputs: oracle rollouts (C15 policy), uniform random ids (status paths),
+hand-built 30-action sequences, and the bench's full-size launch.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+from workloads import candidates, configs
+
+pytestmark = pytest.mark.gpu
+
+FIELDS_INT = ("peak_bytes", "flops", "flops_hi", "state_key", "status", "n_collectives")
+
+
+def _T():
+    from paper_2508_15010_b200 import toast as T
+    return T
+
+
+_cache = {}
+
+
+def setup(name, **over):
+    key = (name, tuple(sorted(over.items())))
+    if key not in _cache:
+        T = _T()
+        c = configs.get(name)
+        dm = over.get("dm", c.dm)
+        a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0)
+        o = Oracle(c.ir, c.axes, c.flops_per_sec, dm, c.penalty_c, c.min_dims, c.max_depth)
+        _cache[key] = (a, o)
+    return _cache[key]
+
+
+def gpu_eval(a, seqs: np.ndarray) -> np.ndarray:
+    import torch
+    T = _T()
+    d_seqs = torch.from_numpy(np.ascontiguousarray(seqs).view(np.int16)).cuda()
+    d_out = torch.empty((len(seqs), 256), dtype=torch.uint8, device="cuda")
+    T.eval_batch(a, d_seqs, d_out)
+    torch.cuda.synchronize()
+    return T.as_costs(d_out)
+
+
+def gpu_rollout(a, prefixes: np.ndarray, seed: int, id_base: int):
+    import torch
+    T = _T()
+    d_pre = torch.from_numpy(np.ascontiguousarray(prefixes).view(np.int16)).cuda()
+    d_seq = torch.empty_like(d_pre)
+    d_out = torch.empty((len(prefixes), 256), dtype=torch.uint8, device="cuda")
+    T.rollout_batch(a, d_pre, seed, id_base, d_seq, d_out)
+    torch.cuda.synchronize()
+    return d_seq.cpu().numpy().view(np.uint16), T.as_costs(d_out)
+
+
+def assert_same(g: np.ndarray, o: np.ndarray, ctx=""):
+    assert len(g) == len(o)
+    for f in FIELDS_INT:
+        bad = np.nonzero(g[f] != o[f])[0]
+        assert len(bad) == 0, (ctx, f, bad[:5], g[f][bad[:5]], o[f][bad[:5]])
+    for f in ("payload", "count"):
+        bad = np.nonzero((g[f] != o[f]).reshape(len(g), -1).any(1))[0]
+        assert len(bad) == 0, (ctx, f, bad[:5])
+    for f in ("runtime_s", "score"):
+        # the north-star tolerance (1e-6 relative) ...
+        rel = np.abs(g[f] - o[f]) / np.maximum(np.abs(o[f]), 1e-300)
+        assert (rel <= 1e-6).all(), (ctx, f, rel.max())
+        # ... and, stricter, bit equality
+        bad = np.nonzero(g[f].view(np.uint64) != o[f].view(np.uint64))[0]
+        assert len(bad) == 0, (ctx, f, bad[:5], g[f][bad[:5]], o[f][bad[:5]])
+
+
+ALL = ["mlp_c", "attn_toy", "gpt2", "gpt24", "gns16", "unet"]
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_eval_parity_on_oracle_rollouts(name):
+    a, o = setup(name)
+    n = 3000 if name in ("mlp_c", "attn_toy", "gpt2") else 300
+    seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=1234, threads=8)
+    assert_same(gpu_eval(a, seqs), oc, name)
+
+
+@pytest.mark.parametrize("name", ["mlp_c", "gpt2", "unet"])
+def test_eval_parity_uniform_ids_and_status(name):
+    """Raw random ids: exercises BAD_ACTION_ID, DUP, RES_MISMATCH, NONZERO_AFTER_STOP
+    next to valid sequences (ragged lengths 0..30)."""
+    a, o = setup(name)
+    seqs = candidates.uniform(2000 if name != "unet" else 400, o.n_actions + 2, seed=7, bad_frac=0.05)
+    oc = o.eval(seqs, threads=8)
+    assert set(np.unique(oc["status"])) >= {0}
+    assert len(np.unique(oc["status"])) >= 3
+    assert_same(gpu_eval(a, seqs), oc, name)
+
+
+def _legal_long(o: Oracle, n: int, seed: int, length: int = 30) -> np.ndarray:
+    """Sequences that keep choosing legal actions (C15 kill rule restated) with
+    STOP disabled, up to `length` actions — the worst-case batch."""
+    d = o.dump()
+    acts = d["actions"]
+    groups = [sc[2] for sc in d["scolors"]]
+    rng = np.random.default_rng(seed)
+
+    def kills(x, y):
+        cx, rx, ax = acts[x - 1]
+        cy, ry, ay = acts[y - 1]
+        if cx == cy and ax == ay:
+            return True
+        for i, gx in enumerate(groups[cx]):
+            for j, gy in enumerate(groups[cy]):
+                if gx == gy and ((rx >> i) ^ (ry >> j)) & 1:
+                    return True
+        return False
+
+    out = np.zeros((n, 32), np.uint16)
+    for r in range(n):
+        legal = list(range(1, len(acts) + 1))
+        k = 0
+        while legal and k < length:
+            a = legal[rng.integers(len(legal))]
+            out[r, k] = a
+            k += 1
+            legal = [b for b in legal if not kills(a, b)]
+    return out
+
+
+@pytest.mark.parametrize("name", ["unet", "gpt24", "mlp_c"])
+def test_eval_parity_worst_case_long_sequences(name):
+    a, o = setup(name)
+    seqs = _legal_long(o, 200, seed=3)
+    oc = o.eval(seqs, threads=8)
+    assert (oc["status"] == 0).all()
+    assert_same(gpu_eval(a, seqs), oc, name)
+
+
+def test_eval_host_pointer_path_and_edges():
+    """Host (numpy) buffers go through device scratch; n = 0 and n = 1 work."""
+    T = _T()
+    a, o = setup("gpt2")
+    seqs, oc = o.rollout(np.zeros((257, 32), np.uint16), seed=9)
+    out = np.zeros(257, dtype=T.COST_DTYPE)
+    T.eval_batch(a, seqs, out)
+    assert_same(out, oc, "host")
+    one = np.zeros(1, dtype=T.COST_DTYPE)
+    T.eval_batch(a, seqs[:1], one)
+    assert_same(one, oc[:1], "n=1")
+    T.eval_batch(a, seqs[:0], one[:0], n=0)
+
+
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt24", "unet", "gns16"])
+def test_rollout_parity(name):
+    """K2 vs C15: same (seed, id) -> same sequence and same cost record."""
+    a, o = setup(name)
+    n = 2000 if name in ("mlp_c", "attn_toy", "gpt2") else 200
+    pre = np.zeros((n, 32), np.uint16)
+    # half the rows start from a (legal) prefix drawn by the oracle
+    s0, _ = o.rollout(np.zeros((n // 2, 32), np.uint16), seed=77)
+    for i in range(n // 2):
+        L = int((s0[i] != 0).sum())
+        k = i % (L + 1)
+        pre[i, :k] = s0[i, :k]
+    seed, id_base = 0xDEADBEEF12345, (1 << 33) + 17
+    os_, oc = o.rollout(pre, seed=seed, id_base=id_base, threads=8)
+    gs, gc = gpu_rollout(a, pre, seed, id_base)
+    assert np.array_equal(gs, os_)
+    assert_same(gc, oc, name)
+
+
+def test_rollout_bad_prefix_is_not_extended():
+    a, o = setup("mlp_c")
+    pre = np.zeros((3, 32), np.uint16)
+    pre[0, 0] = 999      # bad id
+    pre[1, [0, 2]] = 1   # nonzero after STOP
+    pre[2, 0] = 1
+    os_, oc = o.rollout(pre, seed=1)
+    gs, gc = gpu_rollout(a, pre, 1, 0)
+    assert np.array_equal(gs, os_) and np.array_equal(gs[:2], pre[:2])
+    assert_same(gc, oc)
+
+
+def test_full_size_bench_launch_sampled():
+    """GPT-24 at BASELINE size in bench.py's launch configuration (2^16 rollouts
+    from the empty prefix): a sample of outputs is recomputed one by one by the
+    oracle (sequence and record)."""
+    a, o = setup("gpt24")
+    n = 1 << 16
+    seed, id_base = 2024, 0
+    gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), seed, id_base)
+    assert (gc["status"] == 0).all()
+    idx = np.random.default_rng(0).choice(n, size=48, replace=False)
+    for i in idx:
+        s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=seed, id_base=id_base + int(i))
+        assert np.array_equal(gs[i], s1[0])
+        assert_same(gc[i:i + 1], c1, f"row {i}")
+    # properties that hold at any size
+    t0, p0, _ = o.baseline()
+    assert (gc["peak_bytes"] <= p0).all()
+    assert (gc["score"] > 0).all()
+
+
+@pytest.mark.slow
+def test_llama80_sampled():
+    a, o = setup("llama80")
+    n = 4096
+    gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), 5, 0)
+    for i in np.random.default_rng(1).choice(n, size=8, replace=False):
+        s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=5, id_base=int(i))
+        assert np.array_equal(gs[i], s1[0])
+        assert_same(gc[i:i + 1], c1)
+
+
+@pytest.mark.parametrize("name,dm", [("mlp_c", None), ("attn_toy", 700), ("gpt2", None)])
+def test_search_trace_parity(name, dm):
+    """C16 implemented twice (oracle on CPU, library on host+GPU): same seed ->
+    same rounds, evaluation count and best state."""
+    T = _T()
+    a, o = setup(name, dm=dm) if dm else setup(name)
+    opts = T.SearchOptions(seed=3, max_evals=3000, leaves_per_round=4, rollouts_per_leaf=8, patience=3)
+    r = T.search(a, opts)
+    ro, _ = o.search(seed=3, max_evals=3000, L=4, R=8, patience=3)
+    assert int(r["rounds"]) == int(ro["rounds"])
+    assert int(r["evals"]) == int(ro["evals"])
+    assert np.array_equal(r["best_seq"], ro["best_seq"])
+    assert r["best"]["score"] == ro["best"]["score"]
+
+
+def test_search_mlp_c_finds_bruteforce_optimum():
+    T = _T()
+    a, o = setup("mlp_c")
+    _, best, bc = o.bruteforce()
+    r = T.search(a, T.SearchOptions(seed=0, max_evals=20000, leaves_per_round=8, rollouts_per_leaf=32, patience=4))
+    assert r["best"]["score"] == bc["score"]

@@ -1,0 +1,142 @@
+"""CPU-side checks of libtoast: the C ABI loads and exports every symbol
+include/toast.h declares, the H0 analysis equals the oracle's exactly, the
+host-side materialisation agrees, and errors come back as status codes."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+from workloads import configs, models
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_2508_15010_b200 import toast as T
+    return T
+
+
+def test_exports_every_header_symbol():
+    T = _lib()
+    hdr = open(os.path.join(ROOT, "include", "toast.h")).read()
+    declared = set(re.findall(r"^(?:toast_status|size_t|const char\*|void)\s+(toast_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 18
+    import ctypes
+    lib = ctypes.CDLL(T.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), name
+    assert declared == set(T.EXPORTED)
+
+
+def _both(name):
+    T = _lib()
+    c = configs.get(name)
+    a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=-1)
+    o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth)
+    return a, o, c
+
+
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt24", "gns16", "unet"])
+def test_h0_analysis_equals_oracle(name):
+    """H0 parity: loop table, components, super-colors, conflicts, sets, sides,
+    WL signatures, groups, action table and baseline are identical."""
+    a, o, _ = _both(name)
+    da, do = a.dump(), o.dump()
+    assert da.keys() == do.keys()
+    for k in do:
+        assert da[k] == do[k], k
+
+
+@pytest.mark.slow
+def test_h0_analysis_equals_oracle_llama80():
+    a, o, _ = _both("llama80")
+    assert a.dump() == o.dump()
+
+
+def test_h0_random_programs():
+    T = _lib()
+    for seed in range(30):
+        ir = models.random_program(seed, n_ops=16)
+        axes = [("a", 2, 1e10), ("b", 4, 1e11)]
+        a = T.build_analysis(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cuda_device=-1)
+        o = Oracle(ir, axes, 1e12, 1 << 40, 100.0, 1, 30)
+        assert a.dump() == o.dump(), ir
+
+
+@pytest.mark.parametrize("name", ["mlp_c", "gpt2", "unet"])
+def test_host_materialize_equals_oracle(name):
+    T = _lib()
+    a, o, _ = _both(name)
+    seqs, _c = o.rollout(np.zeros((200, 32), np.uint16), seed=5)
+    for s in seqs:
+        lst = [int(x) for x in s if x]
+        assert np.array_equal(T.materialize(a, lst), o.materialize(lst))
+
+
+def test_baseline_record_equals_oracle_empty_eval():
+    T = _lib()
+    for name in ("mlp_c", "gpt2", "gns16"):
+        a, o, _ = _both(name)
+        b = a.baseline()
+        e = o.eval(np.zeros((1, 32), np.uint16))[0]
+        for f in ("runtime_s", "score", "peak_bytes", "flops", "flops_hi", "state_key", "status", "n_collectives"):
+            assert b[f] == e[f], f
+
+
+@pytest.mark.parametrize("src,code", [
+    ("def f(x: f32[2,3], y: f32[4,5]) {\n  z = matmul(x, y)\n  return z\n}\n", "TOAST_E_SHAPE"),
+    ("def f(x: f32[2,2]) {\n  z = matmul(x, q)\n  return z\n}\n", "TOAST_E_UNDEFINED"),
+    ("def f(x: f32[2,2]) {\n  z = matmul(x, x)\n  z = matmul(x, x)\n  return z\n}\n", "TOAST_E_DUPLICATE"),
+    ("def f(x: f32[2,2]) {\n  z = matmul(x x)\n  return z\n}\n", "TOAST_E_PARSE"),
+    ("def f(x: f32[2,2]) {\n  z = frobnicate(x)\n  return z\n}\n", "TOAST_E_PARSE"),
+])
+def test_parse_errors(src, code):
+    T = _lib()
+    with pytest.raises(T.ToastError) as e:
+        T.load_graph(src, [("a", 2, 1e10)], 1e12, 1 << 40, cuda_device=-1)
+    assert e.value.code == code
+
+
+def test_parse_error_location_and_binding_name():
+    T = _lib()
+    with pytest.raises(T.ToastError) as e:
+        T.load_graph("def f(x: f32[2,2]) {\n  z = matmul(x x)\n  return z\n}\n", [("a", 2, 1e10)], 1e12, 1, cuda_device=-1)
+    assert "2:" in str(e.value)
+    with pytest.raises(T.ToastError) as e:
+        T.load_graph("def f(x: f32[2,3], y: f32[4,5]) {\n  zz = matmul(x, y)\n  return zz\n}\n", [("a", 2, 1e10)], 1e12, 1,
+                     cuda_device=-1)
+    assert "'zz'" in str(e.value)
+
+
+def test_mesh_machine_degenerate_limit_errors():
+    T = _lib()
+    ir = open(os.path.join(ROOT, "tests", "golden", "mlp_c.ir")).read()
+    for axes in ([("a", 1, 1e10)], [("a", 2, 1e10), ("a", 2, 1e10)], [("a", 2, 0.0)], [("a", 2, 1.0)] * 0,
+                 [(f"a{i}", 2, 1.0) for i in range(5)]):
+        with pytest.raises(T.ToastError) as e:
+            T.load_graph(ir, axes, 1e12, 1, cuda_device=-1)
+        assert e.value.code == "TOAST_E_MESH"
+    with pytest.raises(T.ToastError) as e:
+        T.load_graph(ir, [("a", 2, 1e10)], 0.0, 1, cuda_device=-1)
+    assert e.value.code == "TOAST_E_MACHINE"
+    g = T.load_graph("def id(x: f32[4,8]) {\n  y = relu(x)\n  return y\n}\n", [("a", 2, 1e10)], 1e12, 1, cuda_device=-1)
+    with pytest.raises(T.ToastError) as e:
+        T.nda(g, 1, 30)
+    assert e.value.code == "TOAST_E_DEGENERATE"
+    g = T.load_graph(ir, [("a", 2, 1e10)], 1e12, 1, cuda_device=-1)
+    with pytest.raises(T.ToastError) as e:
+        T.nda(g, 1, 33)
+    assert e.value.code == "TOAST_E_INVALID_ARG"
+
+
+def test_no_cpu_fallback_without_device():
+    """A host-only analysis refuses to evaluate: there is no CPU path."""
+    T = _lib()
+    a, _, _ = _both("mlp_c")
+    seqs = np.zeros((4, 32), np.uint16)
+    out = np.zeros(4, dtype=T.COST_DTYPE)
+    with pytest.raises(T.ToastError) as e:
+        T.eval_batch(a, seqs, out)
+    assert e.value.code == "TOAST_E_CUDA"
