@@ -32,7 +32,7 @@ toast_status ret(toast_status st, const std::string& msg) {
   g_err = st == TOAST_OK ? std::string() : msg;
   return st;
 }
-bool has_device(const toast_analysis* a) { return a && a->device >= 0 && a->dt.ops != nullptr; }
+bool has_device(const toast_analysis* a) { return a && a->device >= 0 && a->dt.stream != nullptr; }
 }  // namespace
 
 extern "C" {
@@ -209,9 +209,12 @@ toast_status toast_search(const toast_analysis* a, const toast_search_opts* o, t
   int32_t stop = 0;
   while (!stop) {
     st = toast_search_round(s, &buf[0]);
-    if (st) { toast_search_end(s, nullptr); return st; }
-    st = toast_search_import(s, buf.data(), &stop);
-    if (st) { toast_search_end(s, nullptr); return st; }
+    if (!st) st = toast_search_import(s, buf.data(), &stop);
+    if (st) {
+      std::string keep = g_err;
+      toast::search_free(s);
+      return fail(st, keep);
+    }
   }
   return toast_search_end(s, out);
 }

@@ -591,6 +591,110 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     }
   }
 
+  // ------------------------------------------------------------ device stream
+  {
+    // deselection classes: distinct (need0, need1) pairs; class 0 = never deselected
+    std::map<std::pair<uint64_t, uint64_t>, uint32_t> cls_id;
+    a->h_desel_cls.assign(2, 0);
+    std::vector<uint32_t> loop_cls(NL, 0);
+    for (auto& kv : dsel) {
+      auto it = cls_id.find(kv.second);
+      if (it == cls_id.end()) {
+        it = cls_id.emplace(kv.second, (uint32_t)(a->h_desel_cls.size() / 2)).first;
+        a->h_desel_cls.push_back(kv.second.first);
+        a->h_desel_cls.push_back(kv.second.second);
+      }
+      loop_cls[kv.first] = it->second;
+    }
+    if (a->h_desel_cls.size() / 2 > 255) { err = "more than 255 deselection classes"; return TOAST_E_LIMIT; }
+    // op signatures: the per-role words that decide materialisation (C9)
+    std::map<std::vector<uint64_t>, uint32_t> sig_id;
+    std::vector<std::vector<uint64_t>> sig_words;
+    a->op_sig.assign(n_ops, 0);
+    for (int32_t t = 0; t < n_ops; ++t) {
+      std::vector<uint64_t> w;
+      for (int64_t l = lbeg[t]; l < lbeg[t + 1]; ++l) {
+        uint64_t ac = a->h_loops[l] & 0x3FF;
+        if (ac == NO_ACOLOR) w.push_back(NO_ACOLOR);
+        else w.push_back(ac | (((a->h_loops[l] >> 12) & 0xFFFF) << 10) | ((uint64_t)loop_cls[l] << 26));
+      }
+      while (!w.empty() && w.back() == NO_ACOLOR) w.pop_back();
+      auto it = sig_id.find(w);
+      if (it == sig_id.end()) {
+        it = sig_id.emplace(w, (uint32_t)sig_words.size()).first;
+        sig_words.push_back(w);
+      }
+      a->op_sig[t] = it->second;
+    }
+    if (sig_words.size() > 65535) { err = "more than 65535 op signatures"; return TOAST_E_LIMIT; }
+    a->h_sig_roles.assign(sig_words.size() * 8, NO_ACOLOR);
+    a->h_sig_nroles.assign(sig_words.size(), 0);
+    for (size_t q = 0; q < sig_words.size(); ++q) {
+      a->h_sig_nroles[q] = (uint8_t)sig_words[q].size();
+      for (size_t r = 0; r < sig_words[q].size(); ++r) a->h_sig_roles[q * 8 + r] = sig_words[q][r];
+    }
+    // the stream
+    auto push = [&](const void* rec, size_t bytes) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(rec);
+      a->h_stream.insert(a->h_stream.end(), w, w + bytes / 4);
+    };
+    auto dimof_def = [&](int32_t v) {
+      uint64_t m = ~0ULL;
+      for (size_t i = 0; i < OL[v].res_role.size(); ++i) {
+        uint64_t r = OL[v].res_role[i];
+        m = (m & ~(0xFULL << (4 * r))) | ((uint64_t)i << (4 * r));
+      }
+      return m;
+    };
+    a->h_stream.clear();
+    for (int32_t t = 0; t < n_ops; ++t) {
+      const GOp& op = g->ops[t];
+      KHead h{};
+      h.lb = (uint32_t)lbeg[t];
+      h.sig = (uint16_t)a->op_sig[t];
+      h.rmask = a->h_ops[t].rmask;
+      h.flags = a->h_ops[t].flags;
+      h.n_uses = (uint8_t)op.operands.size();
+      h.n_death = (uint8_t)deaths[t].size();
+      if (deaths[t].size() > 255) { err = "too many values die at one op"; return TOAST_E_LIMIT; }
+      h.gbytes = a->h_ops[t].gbytes;
+      h.gflops = a->h_gflops[t];
+      push(&h, sizeof h);
+      std::vector<int> order(op.operands.size());
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return g->values[op.operands[x]].def_op < g->values[op.operands[y]].def_op;
+      });
+      for (size_t q = 0; q < order.size(); ++q) {
+        int k = order[q];
+        int32_t v = g->values[op.operands[k]].def_op;
+        KUse u{};
+        u.def_sig = (uint16_t)a->op_sig[v];
+        u.def_rmask = a->h_ops[v].rmask;
+        bool first = q == 0 || g->values[op.operands[order[q - 1]]].def_op != v;
+        bool last = q + 1 == order.size() || g->values[op.operands[order[q + 1]]].def_op != v;
+        u.flags = (uint8_t)((first ? 1 : 0) | (last ? 2 : 0));
+        u.value = (uint32_t)v;
+        u.def_dimof = dimof_def(v);
+        uint64_t um = ~0ULL;
+        for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
+          uint64_t r = OL[t].use_role[k][i];
+          um = (um & ~(0xFULL << (4 * r))) | ((uint64_t)i << (4 * r));
+        }
+        u.use_dimof = um;
+        u.def_gbytes = a->h_ops[v].gbytes;
+        push(&u, sizeof u);
+      }
+      for (int32_t v : deaths[t]) {
+        KDeath d{};
+        d.sig = (uint16_t)a->op_sig[v];
+        d.rmask = a->h_ops[v].rmask;
+        d.gbytes = a->h_ops[v].gbytes;
+        push(&d, sizeof d);
+      }
+    }
+  }
+
   // ------------------------------------------------------------ baseline (empty sequence)
   {
     unsigned __int128 fl = 0;
@@ -631,6 +735,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
   T.n_words = nwords;
   T.n_axes = n_axes;
   T.max_depth = o->max_depth;
+  T.n_sigs = (int32_t)a->h_sig_nroles.size();
   for (int A = 0; A < 4; ++A) {
     T.sizes[A] = A < n_axes ? g->axis_size[A] : 1;
     T.bw[A] = A < n_axes ? g->axis_bw[A] : 1.0;

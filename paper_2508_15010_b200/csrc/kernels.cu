@@ -1,17 +1,26 @@
 // sm_100a kernels of libtoast.
 //
-// K1 toast_eval_kernel   — one warp per candidate; lane i of the warp owns
-//   op (base + i) of a 32-op window that slides over the program in order
-//   (H1 decode, H2 materialise, H3 FLOPs, H4 collectives, H5 liveness as a
-//   warp inclusive scan + max, H6 score, H7 key).  No tensor cores: there is
-//   no dense contraction on this path (SURVEY §8(d) "Roofline").
-// K2 toast_rollout_kernel — one warp per rollout: Philox4x32-10 draws, the
-//   legal-action bitset distributed one 32-bit word per lane (ballot/popc
-//   selection), then the K1 device path on the finished sequence (H8).
+// Mapping: one WARP evaluates 32 CANDIDATES, one per lane, and the 32 lanes
+// walk the op stream in lockstep.  Every table read is therefore warp-uniform
+// (a broadcast from L1), there is no divergence by op kind, and the liveness
+// sweep (H5) is a plain per-lane running sum/max.
 //
-// Every quantity is an integer until the fixed double epilogue, which uses
-// explicit _rn intrinsics (never contracted into FMA) so the score is
-// bit-identical to the CPU oracle's.
+// Per candidate (per lane):
+//   H1 decode        the 32 action ids -> per-action-color event lists
+//                    (shared memory, [acolor][lane]) and the fixed SetGroup bits;
+//   H2 materialise   once per op SIGNATURE (ops whose loops have the same
+//                    action colors / divisibility / deselection class get the
+//                    same axes): an axis->role map, 16 bits, kept in shared
+//                    memory [sig][lane] (GPT-24: 44 signatures for 6,579 ops);
+//   sweep            per op: state key (C14), local FLOPs (C10), result bytes,
+//                    per use edge the def/use axis->dim maps -> AG/A2A/RS/AR
+//                    payloads and temporaries (C11), dying bytes, and the
+//                    running live/peak bytes (C12);
+//   H6               the fixed-order double epilogue (explicit _rn intrinsics,
+//                    never contracted) -> bit-identical to the CPU oracle.
+// K2 (rollouts): per lane, Philox4x32-10 draws over a per-lane legal bitset
+// (shared memory), then the same device path.
+// No tensor cores: there is no dense contraction on this path.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,406 +36,365 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+__host__ __device__ inline int smem_a_bytes(int n_sigs) { return ((n_sigs * 64) + 15) & ~15; }
+__host__ __device__ inline int smem_b_bytes(int n_ac, int n_words, int n_axes) {
+  int b1 = n_ac * 128 + 2048 + n_words * 128;
+  int b2 = n_axes * 4 * (256 + 128);
+  return ((b1 > b2 ? b1 : b2) + 15) & ~15;
+}
+__host__ __device__ inline int smem_warp_bytes(int n_sigs, int n_ac, int n_words, int n_axes) {
+  return smem_a_bytes(n_sigs) + smem_b_bytes(n_ac, n_words, n_axes);
+}
+
+struct Smem {
+  uint16_t* a2r;            // [n_sigs][32]  axis -> role map of each signature (nibble A; 0xF = none)
+  uint32_t* acol;           // [n_acolors][32] up to 4 events (valid | axis << 5 | position) per action color
+  uint32_t* seq;            // [16][32] the candidate's 32 ids as 16 words
+  uint32_t* legal;          // [n_words][32] rollout legal bitset
+  unsigned long long* pay;  // [n_axes*4][32] payload bytes per (axis, kind)   (overlays acol/seq/legal)
+  uint32_t* cnt;            // [n_axes*4][32] collective counts
+};
+
+__device__ __forceinline__ Smem warp_smem(const DeviceTables& T) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  const int sa = smem_a_bytes(T.n_sigs);
+  const int per = sa + smem_b_bytes(T.n_acolors, T.n_words, T.n_axes);
+  unsigned char* base = smem + (size_t)warp * per;
+  Smem s;
+  s.a2r = reinterpret_cast<uint16_t*>(base);
+  unsigned char* b = base + sa;
+  s.acol = reinterpret_cast<uint32_t*>(b);
+  s.seq = reinterpret_cast<uint32_t*>(b + T.n_acolors * 128);
+  s.legal = reinterpret_cast<uint32_t*>(b + T.n_acolors * 128 + 2048);
+  s.pay = reinterpret_cast<unsigned long long*>(b);
+  s.cnt = reinterpret_cast<uint32_t*>(b + T.n_axes * 4 * 256);
+  return s;
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
   return z ^ (z >> 31);
 }
 
-// exact division by the product of the axis sizes in subset S (the divisor
-// always divides x exactly on this path): (x >> twos) * odd^-1 mod 2^64
+// exact division by the product of the sizes of axis subset S (always exact
+// on this path): (x >> twos(d)) * odd(d)^-1 mod 2^64
 __device__ __forceinline__ uint64_t exdiv(const DeviceTables& T, uint64_t x, uint32_t S) {
   return (x >> T.shift[S]) * T.inv[S];
 }
 
-__device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
-  uint32_t lo = __reduce_or_sync(FULL, (uint32_t)v);
-  uint32_t hi = __reduce_or_sync(FULL, (uint32_t)(v >> 32));
-  return ((uint64_t)hi << 32) | lo;
+__device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+// ---------------------------------------------------------------- H1 decode (C9)
+__device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
+                                           uint64_t& ones) {
+  for (int c = 0; c < T.n_acolors; ++c) S.acol[c * 32 + lane] = 0u;
+  uint32_t status = 0;
+  bool stopped = false;
+  uint64_t fx = 0, on = 0;
+  for (int j = 0; j < 32; ++j) {
+    uint32_t id = (S.seq[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+    if (stopped) {
+      if (id) status |= TOAST_ST_NONZERO_AFTER_STOP;
+      continue;
+    }
+    if (id == 0) { stopped = true; continue; }
+    if ((int)id >= T.n_actions) { status |= TOAST_ST_BAD_ACTION_ID; continue; }
+    uint32_t aw = __ldg(T.actions + id);
+    uint32_t ac = aw & 0x3FF, rr = (aw >> 10) & 0xFF, ax = (aw >> 18) & 3;
+    uint32_t list = S.acol[ac * 32 + lane];
+    uint32_t nent = 0;
+    bool dup = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t e = (list >> (8 * q)) & 0xFF;
+      if (e & 0x80) { ++nent; dup |= ((e >> 5) & 3) == ax; }
+    }
+    if (dup) status |= TOAST_ST_DUP_COLOR_AXIS;
+    else if (nent < 4) S.acol[ac * 32 + lane] = list | ((0x80u | (ax << 5) | (uint32_t)j) << (8 * nent));
+    uint64_t gw = __ldg(T.acol_groups + ac);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      uint32_t gid = (uint32_t)(gw >> (8 * t)) & 0xFF;
+      if (gid == 0xFF) continue;
+      uint64_t g = 1ULL << gid;
+      uint64_t bit = (rr >> t) & 1;
+      if ((fx & g) && (((on >> gid) & 1) != bit)) status |= TOAST_ST_RES_MISMATCH;
+      if (!(fx & g)) { fx |= g; if (bit) on |= g; }
+    }
+  }
+  fixed0 = fx & ~on;
+  ones = on;
+  return status;
 }
 
-struct Mat {
-  uint32_t masks;   // 4 bits per role
-  uint32_t opmask;  // OR of all masks
-};
-
-struct OpRec {
-  uint32_t loop_begin, res_roles, use_begin, death_begin;
-  uint32_t n_loops, rank, rmask, flags, n_death, n_uses;
-  uint64_t gbytes;
-};
-
-__device__ __forceinline__ OpRec load_op(const DeviceTables& T, uint32_t t) {
-  const uint4* p = reinterpret_cast<const uint4*>(T.ops + t);
-  uint4 a = __ldg(p), b = __ldg(p + 1);
-  OpRec r;
-  r.loop_begin = a.x;
-  r.n_loops = a.y & 0xFF;
-  r.rank = (a.y >> 8) & 0xFF;
-  r.rmask = (a.y >> 16) & 0xFF;
-  r.flags = a.y >> 24;
-  r.res_roles = a.z;
-  r.use_begin = a.w;
-  r.death_begin = b.x;
-  r.n_death = b.y & 0xFFFF;
-  r.n_uses = (b.y >> 16) & 0xFF;
-  r.gbytes = ((uint64_t)b.w << 32) | b.z;
-  return r;
-}
-
-// H2 (C9): per-op materialisation.  Events (action position j, role) are
-// merged in action order, roles in role order; an axis shards at most one
-// loop of the op; divisibility via the loop's div_ok subset mask.
-__device__ __forceinline__ Mat materialize(const DeviceTables& T, const uint32_t* __restrict__ acol, uint32_t lb,
-                                           uint32_t nl, uint64_t fixed0, uint64_t ones) {
-  uint32_t list[MAX_LOOPS_PER_OP], div[MAX_LOOPS_PER_OP];
+// ---------------------------------------------------------------- H2 materialise one signature (C9)
+// events (action position j, role) in action order, roles in role order; an
+// axis shards at most one loop of the op; divisibility by div_ok.
+__device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, int s,
+                                                    uint64_t fixed0, uint64_t ones) {
+  const int nr = __ldg(T.sig_nroles + s);
+  uint32_t li[MAX_LOOPS_PER_OP], dv[MAX_LOOPS_PER_OP];
   uint32_t any = 0;
 #pragma unroll
   for (int r = 0; r < MAX_LOOPS_PER_OP; ++r) {
-    list[r] = 0;
-    div[r] = 0;
-    if (r < (int)nl) {
-      uint64_t L = __ldg(T.loops + lb + r);
-      uint32_t ac = (uint32_t)L & 0x3FF;
-      div[r] = (uint32_t)(L >> 12) & 0xFFFF;
+    li[r] = 0;
+    dv[r] = 0;
+    if (r < nr) {
+      uint64_t rw = __ldg(T.sig_roles + (size_t)s * 8 + r);
+      uint32_t ac = (uint32_t)rw & 0x3FF;
       if (ac != NO_ACOLOR) {
-        uint32_t li = acol[ac];
-        uint32_t did = (uint32_t)(L >> 28) & 0xFFFF;
-        if (li && did) {
-          uint64_t n0 = __ldg(T.desel + 2 * did), n1 = __ldg(T.desel + 2 * did + 1);
-          if ((fixed0 & n0) | (ones & n1)) li = 0;
+        uint32_t l = S.acol[ac * 32 + lane];
+        uint32_t cls = (uint32_t)(rw >> 26) & 0xFF;
+        if (l && cls) {
+          uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
+          if ((fixed0 & n0) | (ones & n1)) l = 0;
         }
-        list[r] = li;
-        any |= li;
+        li[r] = l;
+        dv[r] = (uint32_t)(rw >> 10) & 0xFFFF;
+        any |= l;
       }
     }
   }
-  Mat m{0, 0};
-  if (!any) return m;
+  uint32_t a2r = 0xFFFFu;
+  if (!any) return a2r;
+  uint32_t masks = 0, opmask = 0;
   while (true) {
     int best = -1;
     uint32_t bj = 64;
 #pragma unroll
     for (int r = 0; r < MAX_LOOPS_PER_OP; ++r) {
-      uint32_t e = list[r];
+      uint32_t e = li[r];
       if ((e & 0x80) && (e & 31) < bj) { bj = e & 31; best = r; }
     }
     if (best < 0) break;
-    uint32_t e = 0, dv = 0;
+    uint32_t e = 0, d = 0;
 #pragma unroll
     for (int r = 0; r < MAX_LOOPS_PER_OP; ++r)
-      if (r == best) { e = list[r]; dv = div[r]; list[r] = e >> 8; }
-    uint32_t A = (e >> 5) & 3;
-    uint32_t cur = (m.masks >> (4 * best)) & 15;
-    if (!((m.opmask >> A) & 1) && ((dv >> (cur | (1u << A))) & 1)) {
-      m.masks |= (1u << A) << (4 * best);
-      m.opmask |= 1u << A;
+      if (r == best) { e = li[r]; d = dv[r]; li[r] = e >> 8; }
+    const uint32_t A = (e >> 5) & 3;
+    const uint32_t cur = (masks >> (4 * best)) & 15;
+    if (!((opmask >> A) & 1) && ((d >> (cur | (1u << A))) & 1)) {
+      masks |= (1u << A) << (4 * best);
+      opmask |= 1u << A;
+      a2r = (a2r & ~(0xFu << (4 * A))) | ((uint32_t)best << (4 * A));
     }
   }
-  return m;
+  return a2r;
 }
 
-// per-dim masks (4 bits each) of a site given its role map
-__device__ __forceinline__ uint32_t site_masks(uint32_t masks, uint32_t roles, uint32_t rank) {
-  uint32_t out = 0;
-#pragma unroll
-  for (int i = 0; i < MAX_RANK; ++i)
-    if (i < (int)rank) out |= ((masks >> (4 * ((roles >> (4 * i)) & 15))) & 15) << (4 * i);
-  return out;
-}
-__device__ __forceinline__ uint32_t dims_or(uint32_t dm) {
-  dm |= dm >> 16;
-  dm |= dm >> 8;
-  dm |= dm >> 4;
-  return dm & 15;
-}
-__device__ __forceinline__ uint32_t roles_or(uint32_t masks, uint32_t rmask) {
-  uint32_t out = 0;
-#pragma unroll
-  for (int r = 0; r < MAX_LOOPS_PER_OP; ++r)
-    if ((rmask >> r) & 1) out |= (masks >> (4 * r)) & 15;
-  return out;
-}
-// dim holding axis A in a packed site (-1 if none)
-__device__ __forceinline__ int dim_of(uint32_t dm, uint32_t A) {
-  uint32_t sel = dm & (0x11111111u << A);
-  return sel ? (__ffs(sel) - 1) >> 2 : -1;
-}
-
-struct Acc {   // per-warp shared accumulators
-  unsigned long long payload[16];
-  unsigned int count[16];
-};
-
-// one candidate per warp; `sid` = this lane's action id (seq[lane])
-__device__ void eval_warp(const DeviceTables& T, uint32_t sid, uint32_t* __restrict__ acol, Acc* __restrict__ acc,
-                          unsigned long long* __restrict__ rec, toast_cost* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  // ---------------- H1 decode (C9)
-  unsigned zb = __ballot_sync(FULL, sid == 0);
-  int stop = zb ? __ffs(zb) - 1 : 32;
-  bool active = lane < stop;
-  uint32_t status = 0;
-  if (__ballot_sync(FULL, lane > stop && sid != 0)) status |= TOAST_ST_NONZERO_AFTER_STOP;
-  bool bad = active && (int)sid >= T.n_actions;
-  if (__ballot_sync(FULL, bad)) status |= TOAST_ST_BAD_ACTION_ID;
-  bool ok = active && !bad;
-  uint32_t aw = ok ? __ldg(T.actions + sid) : 0u;
-  uint32_t ac = aw & 0x3FF, rr = (aw >> 10) & 0xFF, ax = (aw >> 18) & 3;
-  unsigned same = __match_any_sync(FULL, ok ? ((ac << 2) | ax) : (0x80000000u | (uint32_t)lane));
-  if (__ballot_sync(FULL, ok && __popc(same) > 1)) status |= TOAST_ST_DUP_COLOR_AXIS;
-  uint64_t fx = 0, on = 0;
-  if (ok) {
-    uint64_t gw = __ldg(T.acol_groups + ac);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      uint32_t gid = (uint32_t)(gw >> (8 * t)) & 0xFF;
-      if (gid != 0xFF) {
-        fx |= 1ULL << gid;
-        if ((rr >> t) & 1) on |= 1ULL << gid;
-      }
-    }
-  }
-  uint64_t zr = warp_or64(fx & ~on);
-  on = warp_or64(on);
-  if (on & zr) status |= TOAST_ST_RES_MISMATCH;
-  if (status) {
-    if (lane == 0) {
-      memset(rec, 0, 256);
-      reinterpret_cast<uint32_t*>(rec)[10] = status;
-    }
-    __syncwarp();
-    reinterpret_cast<unsigned long long*>(out)[lane] = rec[lane];
-    __syncwarp();
-    return;
-  }
-  unsigned samec = __match_any_sync(FULL, ok ? ac : (0x80000000u | (uint32_t)lane));
-  int rank_in_color = __popc(samec & ((1u << lane) - 1u));
-  if (ok) atomicOr(acol + ac, (0x80u | (ax << 5) | (uint32_t)lane) << (8 * rank_in_color));
-  if (lane < 16) { acc->payload[lane] = 0ULL; acc->count[lane] = 0u; }
+// ---------------------------------------------------------------- the per-lane evaluation
+// S.seq holds the lane's candidate; `valid` lanes write `out`.
+__device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, int lane, bool valid,
+                                          toast_cost* __restrict__ out) {
+  uint64_t fixed0, ones;
+  const uint32_t status = decode(T, S, lane, fixed0, ones);
+  for (int s = 0; s < T.n_sigs; ++s) S.a2r[s * 32 + lane] = (uint16_t)materialize_sig(T, S, lane, s, fixed0, ones);
   __syncwarp();
+  const int nq = T.n_axes * 4;
+  for (int q = 0; q < nq; ++q) { S.pay[q * 32 + lane] = 0ULL; S.cnt[q * 32 + lane] = 0u; }
 
-  // ---------------- sweep over ops, 32 at a time
   uint64_t key = 0, flo = 0, fhi = 0;
-  long long carry = 0, peak = 0;
-  for (int base = 0; base < T.n_ops; base += 32) {
-    const int t = base + lane;
-    long long delta = 0, inop = 0;
-    const bool live = t < T.n_ops;
-    if (live) {
-      OpRec op = load_op(T, (uint32_t)t);
-      Mat me = materialize(T, acol, op.loop_begin, op.n_loops, zr, on);
-      // H7 key (C14)
-      if (me.masks) {
+  long long L = 0, peak = 0;
+  const uint4* p = T.stream;
+  for (int t = 0; t < T.n_ops; ++t) {
+    const uint4 h0 = __ldg(p), h1 = __ldg(p + 1);
+    const uint32_t lb = h0.x, sig = h0.y & 0xFFFF, rmask = (h0.y >> 16) & 0xFF, flags = h0.y >> 24;
+    const uint32_t n_uses = h0.z & 0xFF, n_death = (h0.z >> 8) & 0xFF;
+    const uint32_t a2r = S.a2r[sig * 32 + lane];
+    // axes of this op, axes of its result dims, state key (C14)
+    uint32_t opmask = 0, present = 0;
 #pragma unroll
-        for (int r = 0; r < MAX_LOOPS_PER_OP; ++r) {
-          uint32_t mk = (me.masks >> (4 * r)) & 15;
-          if (mk) key += mix64(((uint64_t)(op.loop_begin + r) << 8) | mk);
+    for (int A = 0; A < 4; ++A) {
+      const uint32_t r = (a2r >> (4 * A)) & 15;
+      if (r != 15) {
+        opmask |= 1u << A;
+        if (!((rmask >> r) & 1)) present |= 1u << A;
+        bool first = true;
+        uint32_t m = 1u << A;
+#pragma unroll
+        for (int B = 0; B < 4; ++B) {
+          const uint32_t rb = (a2r >> (4 * B)) & 15;
+          if (B < A && rb == r) first = false;
+          if (B > A && rb == r) m |= 1u << B;
+        }
+        if (first) key += mix64(((uint64_t)(lb + r) << 8) | m);
+      }
+    }
+    if (flags & 1) {   // H3 local FLOPs, matmul-class ops only
+      const uint64_t f = exdiv(T, u64of(h1.z, h1.w), opmask);
+      flo += f;
+      fhi += (flo < f) ? 1 : 0;
+    }
+    const long long res = (flags & 2) ? 0 : (long long)exdiv(T, u64of(h1.x, h1.y), present);
+    // H4: use edges (C11)
+    long long temp = 0, gmax = 0;
+    const uint4* q = p + 2;
+    const uint4* gq = q;
+    for (uint32_t k = 0; k < n_uses; ++k, q += 2) {
+      const uint4 u0 = __ldg(q), u1 = __ldg(q + 1);
+      const uint32_t def_sig = u0.x & 0xFFFF, def_rmask = (u0.x >> 16) & 0xFF, uflags = u0.x >> 24;
+      const uint64_t def_dimof = u64of(u0.z, u0.w), use_dimof = u64of(u1.x, u1.y), dgb = u64of(u1.z, u1.w);
+      if (uflags & 1) { gmax = 0; gq = q; }
+      const uint32_t da = S.a2r[def_sig * 32 + lane];
+      uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
+#pragma unroll
+      for (int A = 0; A < 4; ++A) {
+        const uint32_t rd = (da >> (4 * A)) & 15, ru = (a2r >> (4 * A)) & 15;
+        const uint32_t dd = (uint32_t)(def_dimof >> (4 * rd)) & 15, du = (uint32_t)(use_dimof >> (4 * ru)) & 15;
+        dimD |= dd << (4 * A);
+        dimU |= du << (4 * A);
+        P |= ((def_rmask >> rd) & 1) << A;
+        presD |= (dd != 15 ? 1u : 0u) << A;
+        presU |= (du != 15 ? 1u : 0u) << A;
+      }
+      bool dup = false;
+      if (!(uflags & 1)) {   // same value used again at this op: cost it once per distinct layout
+        for (const uint4* q2 = gq; q2 < q; q2 += 2) {
+          const uint4 w1 = __ldg(q2 + 1);
+          const uint64_t ud2 = u64of(w1.x, w1.y);
+          uint32_t dimU2 = 0;
+#pragma unroll
+          for (int A = 0; A < 4; ++A) dimU2 |= ((uint32_t)(ud2 >> (4 * ((a2r >> (4 * A)) & 15))) & 15) << (4 * A);
+          dup |= dimU2 == dimU;
         }
       }
-      // H3 FLOPs (C10)
-      if (op.flags & 1) {
-        uint64_t f = exdiv(T, __ldg(T.gflops + t), me.opmask);
-        flo += f;
-        fhi += (flo < f) ? 1 : 0;
-      }
-      long long res = 0;
-      if (!(op.flags & 2)) res = (long long)exdiv(T, op.gbytes, dims_or(site_masks(me.masks, op.res_roles, op.rank)));
-      // H4 collectives per use edge (C11)
-      uint32_t Uk[MAX_USES_PER_OP], vk[MAX_USES_PER_OP];
-      long long gk[MAX_USES_PER_OP];
-      long long temp_total = 0;
-#pragma unroll
-      for (int k = 0; k < MAX_USES_PER_OP; ++k) {
-        Uk[k] = 0; vk[k] = 0xFFFFFFFFu; gk[k] = 0;
-        if (k < (int)op.n_uses) {
-          uint2 uw = __ldg(reinterpret_cast<const uint2*>(T.uses + op.use_begin + k));
-          uint32_t v = uw.x;
-          OpRec dop = load_op(T, v);
-          uint32_t U = site_masks(me.masks, uw.y, dop.rank);
-          Uk[k] = U;
-          vk[k] = v;
-          bool dup = false;
-#pragma unroll
-          for (int k2 = 0; k2 < k; ++k2) dup |= (vk[k2] == v && Uk[k2] == U);
-          if (!dup) {
-            Mat dm = materialize(T, acol, dop.loop_begin, dop.n_loops, zr, on);
-            uint32_t D = site_masks(dm.masks, dop.res_roles, dop.rank);
-            uint32_t P = roles_or(dm.masks, dop.rmask);
-            if (D != U || P != 0) {
-              uint32_t Dp = dims_or(D), Up = dims_or(U);
-              uint64_t size = exdiv(T, dop.gbytes, Dp);
-              for (int A = 0; A < T.n_axes; ++A) {          // phase 1: AG / A2A
-                int dD = dim_of(D, A);
-                if (dD < 0) continue;
-                int dU = dim_of(U, A);
-                if (dD == dU) continue;
-                if (dU >= 0) {
-                  atomicAdd(&acc->payload[A * 4 + TOAST_A2A], (unsigned long long)size);
-                  atomicAdd(&acc->count[A * 4 + TOAST_A2A], 1u);
-                } else {
-                  atomicAdd(&acc->payload[A * 4 + TOAST_AG], (unsigned long long)size);
-                  atomicAdd(&acc->count[A * 4 + TOAST_AG], 1u);
-                  size *= (uint64_t)T.sizes[A];
-                }
-              }
-              for (int A = 0; A < T.n_axes; ++A) {          // phase 2: RS / AR
-                if (!((P >> A) & 1)) continue;
-                if (dim_of(U, A) >= 0) {
-                  size = exdiv(T, size, 1u << A);
-                  atomicAdd(&acc->payload[A * 4 + TOAST_RS], (unsigned long long)size);
-                  atomicAdd(&acc->count[A * 4 + TOAST_RS], 1u);
-                } else {
-                  atomicAdd(&acc->payload[A * 4 + TOAST_AR], (unsigned long long)size);
-                  atomicAdd(&acc->count[A * 4 + TOAST_AR], 1u);
-                }
-              }
-              gk[k] = (long long)exdiv(T, dop.gbytes, Up) - (long long)exdiv(T, dop.gbytes, Dp);
-            }
+      if (!dup && (dimD != dimU || P)) {
+        uint64_t size = exdiv(T, dgb, presD);
+        for (int A = 0; A < T.n_axes; ++A) {          // phase 1: all_gather / all_to_all
+          const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+          if (dd == 15 || dd == du) continue;
+          if (du != 15) {
+            S.pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
+            S.cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
+          } else {
+            S.pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
+            S.cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
+            size *= (uint64_t)T.sizes[A];
           }
         }
-      }
-      // temporaries: per distinct operand value, the largest growth (C11/C12)
-#pragma unroll
-      for (int k = 0; k < MAX_USES_PER_OP; ++k) {
-        if (k < (int)op.n_uses) {
-          bool first = true;
-#pragma unroll
-          for (int k2 = 0; k2 < k; ++k2) first &= (vk[k2] != vk[k]);
-          if (first) {
-            long long mx = 0;
-#pragma unroll
-            for (int k2 = k; k2 < MAX_USES_PER_OP; ++k2)
-              if (vk[k2] == vk[k] && gk[k2] > mx) mx = gk[k2];
-            temp_total += mx;
+        for (int A = 0; A < T.n_axes; ++A) {          // phase 2: reduce_scatter / all_reduce
+          if (!((P >> A) & 1)) continue;
+          if (((dimU >> (4 * A)) & 15) != 15) {
+            size = exdiv(T, size, 1u << A);
+            S.pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
+            S.cnt[(A * 4 + TOAST_RS) * 32 + lane] += 1u;
+          } else {
+            S.pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
+            S.cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
           }
         }
+        const long long grow = (long long)exdiv(T, dgb, presU) - (long long)exdiv(T, dgb, presD);
+        if (grow > gmax) gmax = grow;
       }
-      // values whose last use is this op (C12)
-      long long dying = 0;
-      for (uint32_t i = 0; i < op.n_death; ++i) {
-        uint32_t v = __ldg(T.deaths + op.death_begin + i);
-        if (v == (uint32_t)t) {
-          dying += res;
-        } else {
-          OpRec vo = load_op(T, v);
-          Mat vm = materialize(T, acol, vo.loop_begin, vo.n_loops, zr, on);
-          dying += (long long)exdiv(T, vo.gbytes, dims_or(site_masks(vm.masks, vo.res_roles, vo.rank)));
-        }
+      if (uflags & 2) temp += gmax;
+    }
+    // values whose last use is this op
+    long long dying = 0;
+    for (uint32_t k = 0; k < n_death; ++k, ++q) {
+      const uint4 d = __ldg(q);
+      const uint32_t av = S.a2r[(d.x & 0xFFFF) * 32 + lane], rm = (d.x >> 16) & 0xFF;
+      uint32_t pres = 0;
+#pragma unroll
+      for (int A = 0; A < 4; ++A) {
+        const uint32_t r = (av >> (4 * A)) & 15;
+        pres |= ((r != 15 && !((rm >> r) & 1)) ? 1u : 0u) << A;
       }
-      delta = res - dying;
-      inop = res + temp_total;
+      dying += (long long)exdiv(T, u64of(d.z, d.w), pres);
     }
-    // H5: warp inclusive scan of the live-byte deltas, then max of M_t
-    long long incl = delta;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      long long y = __shfl_up_sync(FULL, incl, off);
-      if (lane >= off) incl += y;
-    }
-    long long M = live ? carry + (incl - delta) + inop : LLONG_MIN;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      long long y = __shfl_xor_sync(FULL, M, off);
-      M = y > M ? y : M;
-    }
-    if (M > peak) peak = M;
-    carry += __shfl_sync(FULL, incl, 31);
+    // H5 liveness (C12)
+    const long long M = L + res + temp;
+    peak = M > peak ? M : peak;
+    L = L + res - dying;
+    p = q;
   }
-  // ---------------- reductions
+  // H6 score (C13): fixed order, explicit round-to-nearest, no FMA
+  double fl = __dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo));
+  double tt = __ddiv_rn(fl, T.F);
+  unsigned long long ncoll = 0;
+  __align__(16) toast_cost c;
+  memset(&c, 0, sizeof c);
+  for (int A = 0; A < T.n_axes; ++A) {
+    const double n = (double)T.sizes[A];
+    const unsigned long long pag = S.pay[(A * 4 + 0) * 32 + lane], prs = S.pay[(A * 4 + 1) * 32 + lane];
+    const unsigned long long par = S.pay[(A * 4 + 2) * 32 + lane], pa2 = S.pay[(A * 4 + 3) * 32 + lane];
+    const double ag = __ull2double_rn(pag), rs = __ull2double_rn(prs), ar = __ull2double_rn(par), a2a = __ull2double_rn(pa2);
+    const double n1 = __dsub_rn(n, 1.0);
+    const double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
+    const double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
+    tt = __dadd_rn(tt, __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]));
+    c.payload[A][0] = pag; c.payload[A][1] = prs; c.payload[A][2] = par; c.payload[A][3] = pa2;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    key += __shfl_xor_sync(FULL, key, off);
-    uint64_t olo = __shfl_xor_sync(FULL, flo, off), ohi = __shfl_xor_sync(FULL, fhi, off);
-    uint64_t nlo = flo + olo;
-    fhi = fhi + ohi + (nlo < flo ? 1 : 0);
-    flo = nlo;
-  }
-  __syncwarp();
-  // ---------------- H6 score (C13), fixed evaluation order, no FMA
-  if (lane == 0) {
-    double fl = __dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo));
-    double t = __ddiv_rn(fl, T.F);
-    unsigned long long ncoll = 0;
-    for (int A = 0; A < T.n_axes; ++A) {
-      double n = (double)T.sizes[A];
-      double ag = __ull2double_rn(acc->payload[A * 4 + 0]), rs = __ull2double_rn(acc->payload[A * 4 + 1]);
-      double ar = __ull2double_rn(acc->payload[A * 4 + 2]), a2a = __ull2double_rn(acc->payload[A * 4 + 3]);
-      double n1 = __dsub_rn(n, 1.0);
-      double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
-      double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
-      double term = __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]);
-      t = __dadd_rn(t, term);
-    }
-    uint64_t pk = (uint64_t)peak;
-    double RT = __ddiv_rn(t, T.t0);
-    double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
-    double score = __dadd_rn(RT, MP);
-    toast_cost* c = reinterpret_cast<toast_cost*>(rec);
-    memset(c, 0, sizeof(toast_cost));
-    c->runtime_s = t;
-    c->score = score;
-    c->peak_bytes = pk;
-    c->flops = flo;
-    c->flops_hi = fhi;
-    c->state_key = key;
-    c->status = 0;
-    for (int q = 0; q < 16; ++q) {
-      unsigned int cq = acc->count[q];
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t cq = S.cnt[(A * 4 + k) * 32 + lane];
       ncoll += cq;
-      c->payload[q >> 2][q & 3] = acc->payload[q];
-      c->count[q >> 2][q & 3] = (uint16_t)(cq > 65535u ? 65535u : cq);
+      c.count[A][k] = (uint16_t)(cq > 65535u ? 65535u : cq);
     }
-    c->n_collectives = (uint32_t)ncoll;
+  }
+  const uint64_t pk = (uint64_t)peak;
+  const double RT = __ddiv_rn(tt, T.t0);
+  const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
+  if (status == 0) {
+    c.runtime_s = tt;
+    c.score = __dadd_rn(RT, MP);
+    c.peak_bytes = pk;
+    c.flops = flo;
+    c.flops_hi = fhi;
+    c.state_key = key;
+    c.n_collectives = (uint32_t)ncoll;
+  } else {
+    memset(&c, 0, sizeof c);
+    c.status = status;
   }
   __syncwarp();
-  reinterpret_cast<unsigned long long*>(out)[lane] = rec[lane];
-  if (ok) acol[ac] = 0u;   // restore the all-zero invariant for the next candidate
-  __syncwarp();
+  if (valid) {
+    const uint4* src = reinterpret_cast<const uint4*>(&c);
+    uint4* dst = reinterpret_cast<uint4*>(out);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) dst[k] = src[k];
+  }
 }
 
-struct WarpSmem {
-  uint32_t* acol;
-  Acc* acc;
-  unsigned long long* rec;
-};
-
-__device__ __forceinline__ WarpSmem warp_smem(int n_acolors) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5;
-  const int acol_bytes = ((n_acolors * 4) + 15) & ~15;
-  const int per = acol_bytes + (int)sizeof(Acc) + 256;
-  unsigned char* base = smem + (size_t)warp * per;
-  WarpSmem w;
-  w.rec = reinterpret_cast<unsigned long long*>(base);
-  w.acc = reinterpret_cast<Acc*>(base + 256);
-  w.acol = reinterpret_cast<uint32_t*>(base + 256 + sizeof(Acc));
-  const int lane = threadIdx.x & 31;
-  for (int i = lane; i < n_acolors; i += 32) w.acol[i] = 0u;
-  __syncwarp();
-  return w;
+__device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restrict__ g, int lane, bool valid) {
+  uint4 w[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  if (valid) {
+    const uint4* src = reinterpret_cast<const uint4*>(g);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = __ldg(src + k);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    S.seq[(4 * k + 0) * 32 + lane] = w[k].x;
+    S.seq[(4 * k + 1) * 32 + lane] = w[k].y;
+    S.seq[(4 * k + 2) * 32 + lane] = w[k].z;
+    S.seq[(4 * k + 3) * 32 + lane] = w[k].w;
+  }
 }
 
 __global__ void __launch_bounds__(256) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
-  WarpSmem w = warp_smem(T.n_acolors);
+  const Smem S = warp_smem(T);
   const int lane = threadIdx.x & 31;
+  const int64_t nbatch = (n + 31) / 32;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
-    uint32_t sid = seqs[i * 32 + lane];
-    eval_warp(T, sid, w.acol, w.acc, w.rec, out + i);
+  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nbatch; b += warps) {
+    const int64_t i = b * 32 + lane;
+    const bool valid = i < n;
+    load_seq(S, seqs + i * 32, lane, valid);
+    eval_lane(T, S, lane, valid, out + i);
   }
 }
 
-// ---------------- K2: rollouts (C15)
+// ---------------------------------------------------------------- K2: rollouts (C15)
 __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
                                               uint32_t k1, uint32_t& o0, uint32_t& o1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
-    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
   }
   o0 = c0;
@@ -437,63 +405,72 @@ __global__ void __launch_bounds__(256) toast_rollout_kernel(const DeviceTables T
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
                                                             toast_cost* __restrict__ out) {
-  WarpSmem w = warp_smem(T.n_acolors);
+  const Smem S = warp_smem(T);
   const int lane = threadIdx.x & 31;
+  const int64_t nbatch = (n + 31) / 32;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t seed_lo = (uint32_t)seed, seed_hi = (uint32_t)(seed >> 32);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
-    uint32_t p = pre[i * 32 + lane];
-    unsigned zb = __ballot_sync(FULL, p == 0);
-    int stop = zb ? __ffs(zb) - 1 : 32;
-    bool bad = __ballot_sync(FULL, (lane > stop && p != 0) || (lane < stop && (int)p >= T.n_actions)) != 0;
-    uint32_t sv = p;
-    if (!bad) {
-      uint32_t legal = 0;
-      if (lane < T.n_words) {
-        legal = FULL;
-        int hi = T.n_actions - lane * 32;   // ids >= n_actions are not actions
-        if (hi < 32) legal = hi <= 0 ? 0u : ((1u << hi) - 1u);
-        if (lane == 0) legal &= ~1u;        // STOP is not in the legal set
+  const int nw = T.n_words;
+  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nbatch; b += warps) {
+    const int64_t i = b * 32 + lane;
+    const bool valid = i < n;
+    load_seq(S, pre + i * 32, lane, valid);
+    // validate the prefix: ids < n_actions before the first 0, zeros after it
+    int stop = 32;
+    bool bad = false;
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t id = (S.seq[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+      if (stop < 32) { bad |= id != 0; continue; }
+      if (id == 0) { stop = j; continue; }
+      bad |= (int)id >= T.n_actions;
+    }
+    if (valid && !bad) {
+      for (int w = 0; w < nw; ++w) {
+        uint32_t v = FULL;
+        const int hi = T.n_actions - w * 32;   // ids >= n_actions are not actions
+        if (hi < 32) v = hi <= 0 ? 0u : ((1u << hi) - 1u);
+        if (w == 0) v &= ~1u;                 // STOP is not in the legal set
+        S.legal[w * 32 + lane] = v;
       }
       for (int j = 0; j < stop; ++j) {
-        uint32_t a = __shfl_sync(FULL, p, j);
-        if (lane < T.n_words) legal &= ~__ldg(T.kill + (size_t)a * T.n_words + lane);
+        const uint32_t a = (S.seq[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+        for (int w = 0; w < nw; ++w) S.legal[w * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w);
       }
       const uint64_t id = id_base + (uint64_t)i;
       for (int d = stop; d < T.max_depth; ++d) {
         uint32_t r0, r1;
         philox4x32_10((uint32_t)id, (uint32_t)(id >> 32), (uint32_t)d, 0u, seed_lo, seed_hi, r0, r1);
         if ((uint64_t)r0 * (uint64_t)T.max_depth < ((uint64_t)d << 32)) break;   // p_stop = d / max_depth
-        uint32_t cnt = __popc(legal);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          uint32_t y = __shfl_up_sync(FULL, incl, off);
-          if (lane >= off) incl += y;
-        }
-        uint32_t total = __shfl_sync(FULL, incl, 31);
+        uint32_t total = 0;
+        for (int w = 0; w < nw; ++w) total += __popc(S.legal[w * 32 + lane]);
         if (total == 0) break;
         uint32_t k = (uint32_t)(((uint64_t)r1 * total) >> 32);
-        uint32_t excl = incl - cnt;
-        bool own = k >= excl && k < incl;
-        int owner = __ffs(__ballot_sync(FULL, own)) - 1;
-        uint32_t a = 0;
-        if (own) {
-          uint32_t wv = legal;
-          for (uint32_t q = excl; q < k; ++q) wv &= wv - 1;
-          a = (uint32_t)lane * 32 + (uint32_t)(__ffs(wv) - 1);
+        int w = 0;
+        uint32_t word = 0;
+        for (; w < nw; ++w) {
+          word = S.legal[w * 32 + lane];
+          const uint32_t c = __popc(word);
+          if (k < c) break;
+          k -= c;
         }
-        a = __shfl_sync(FULL, a, owner);
-        if (lane < T.n_words) legal &= ~__ldg(T.kill + (size_t)a * T.n_words + lane);
-        if (lane == d) sv = a;
+        for (uint32_t q = 0; q < k; ++q) word &= word - 1;
+        const uint32_t a = (uint32_t)w * 32 + (uint32_t)(__ffs(word) - 1);
+        for (int w2 = 0; w2 < nw; ++w2) S.legal[w2 * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w2);
+        uint32_t& sw = S.seq[(d >> 1) * 32 + lane];
+        sw = (d & 1) ? ((sw & 0xFFFFu) | (a << 16)) : ((sw & 0xFFFF0000u) | a);
       }
     }
-    out_seqs[i * 32 + lane] = (uint16_t)sv;
-    eval_warp(T, sv, w.acol, w.acc, w.rec, out + i);
+    __syncwarp();
+    if (valid) {
+      uint4* dst = reinterpret_cast<uint4*>(out_seqs + i * 32);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_uint4(S.seq[(4 * k) * 32 + lane], S.seq[(4 * k + 1) * 32 + lane], S.seq[(4 * k + 2) * 32 + lane],
+                            S.seq[(4 * k + 3) * 32 + lane]);
+    }
+    eval_lane(T, S, lane, valid, out + i);
   }
 }
-
-int smem_per_warp(int n_acolors) { return (((n_acolors * 4) + 15) & ~15) + (int)sizeof(Acc) + 256; }
 
 }  // namespace
 
@@ -517,13 +494,13 @@ bool is_device_pointer(const void* p) {
   } while (0)
 
 template <typename V>
-static toast_status upload(toast_analysis* a, const V& v, const typename V::value_type** dst, std::string& err) {
+static toast_status upload(toast_analysis* a, const V& v, const void** dst, std::string& err) {
   size_t bytes = std::max<size_t>(v.size() * sizeof(typename V::value_type), 16);
   void* d = nullptr;
   TOAST_CUDA(cudaMalloc(&d, bytes));
   a->dev_allocs.push_back(d);
   if (!v.empty()) TOAST_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(typename V::value_type), cudaMemcpyHostToDevice));
-  *dst = reinterpret_cast<const typename V::value_type*>(d);
+  *dst = d;
   return TOAST_OK;
 }
 
@@ -531,25 +508,37 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaSetDevice(a->device));
   DeviceTables& T = a->dt;
   toast_status st;
-  if ((st = upload(a, a->h_ops, &T.ops, err))) return st;
-  if ((st = upload(a, a->h_gflops, &T.gflops, err))) return st;
-  if ((st = upload(a, a->h_loops, &T.loops, err))) return st;
-  if ((st = upload(a, a->h_uses, &T.uses, err))) return st;
-  if ((st = upload(a, a->h_deaths, &T.deaths, err))) return st;
-  if ((st = upload(a, a->h_desel, &T.desel, err))) return st;
-  if ((st = upload(a, a->h_actions, &T.actions, err))) return st;
-  if ((st = upload(a, a->h_acol_groups, &T.acol_groups, err))) return st;
-  if ((st = upload(a, a->h_kill, &T.kill, err))) return st;
-  a->smem_per_warp = smem_per_warp(T.n_acolors);
-  const int smem = 8 * a->smem_per_warp;
-  if (smem > 48 * 1024) {
-    TOAST_CUDA(cudaFuncSetAttribute(toast_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    TOAST_CUDA(cudaFuncSetAttribute(toast_rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  }
-  int sms = 0, be = 0, br = 0;
+  const void* p;
+  if ((st = upload(a, a->h_stream, &p, err))) return st;
+  T.stream = reinterpret_cast<const uint4*>(p);
+  if ((st = upload(a, a->h_sig_roles, &p, err))) return st;
+  T.sig_roles = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_sig_nroles, &p, err))) return st;
+  T.sig_nroles = reinterpret_cast<const uint8_t*>(p);
+  if ((st = upload(a, a->h_desel_cls, &p, err))) return st;
+  T.desel = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_actions, &p, err))) return st;
+  T.actions = reinterpret_cast<const uint32_t*>(p);
+  if ((st = upload(a, a->h_acol_groups, &p, err))) return st;
+  T.acol_groups = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_kill, &p, err))) return st;
+  T.kill = reinterpret_cast<const uint32_t*>(p);
+
+  a->smem_per_warp = smem_warp_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes);
+  int dev_smem = 0, sms = 0;
+  TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel, 256, smem));
-  TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel, 256, smem));
+  int wpb = 8;
+  while (wpb > 1 && wpb * a->smem_per_warp > dev_smem) wpb >>= 1;
+  if (wpb * a->smem_per_warp > dev_smem) { err = "op-signature tables do not fit in shared memory"; return TOAST_E_LIMIT; }
+  a->warps_per_block = wpb;
+  const int smem = wpb * a->smem_per_warp;
+  // the attribute is per function, shared by every analysis in the process: allow the device maximum
+  TOAST_CUDA(cudaFuncSetAttribute(toast_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_smem));
+  TOAST_CUDA(cudaFuncSetAttribute(toast_rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_smem));
+  int be = 0, br = 0;
+  TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel, wpb * 32, smem));
+  TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel, wpb * 32, smem));
   a->eval_blocks = sms * std::max(be, 1);
   a->rollout_blocks = sms * std::max(br, 1);
   return TOAST_OK;
@@ -564,11 +553,17 @@ void free_tables(toast_analysis* a) {
   a->scratch_bytes = 0;
 }
 
+static inline int64_t grid_for(const toast_analysis* a, int64_t n, int resident) {
+  const int64_t batches = (n + 31) / 32;
+  return std::max<int64_t>(1, std::min<int64_t>((batches + a->warps_per_block - 1) / a->warps_per_block, resident));
+}
+
 toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, toast_cost* d_out, void* stream,
                          std::string& err) {
   if (n <= 0) return TOAST_OK;
-  int64_t blocks = std::min<int64_t>((n + 7) / 8, a->eval_blocks);
-  toast_eval_kernel<<<(unsigned)blocks, 256, 8 * a->smem_per_warp, (cudaStream_t)stream>>>(a->dt, d_seqs, n, d_out);
+  const int64_t blocks = grid_for(a, n, a->eval_blocks);
+  toast_eval_kernel<<<(unsigned)blocks, a->warps_per_block * 32, a->warps_per_block * a->smem_per_warp,
+                      (cudaStream_t)stream>>>(a->dt, d_seqs, n, d_out);
   TOAST_CUDA(cudaGetLastError());
   return TOAST_OK;
 }
@@ -576,9 +571,9 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
 toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
                             uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err) {
   if (n <= 0) return TOAST_OK;
-  int64_t blocks = std::min<int64_t>((n + 7) / 8, a->rollout_blocks);
-  toast_rollout_kernel<<<(unsigned)blocks, 256, 8 * a->smem_per_warp, (cudaStream_t)stream>>>(a->dt, d_pre, n, seed,
-                                                                                             id_base, d_seqs, d_out);
+  const int64_t blocks = grid_for(a, n, a->rollout_blocks);
+  toast_rollout_kernel<<<(unsigned)blocks, a->warps_per_block * 32, a->warps_per_block * a->smem_per_warp,
+                         (cudaStream_t)stream>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out);
   TOAST_CUDA(cudaGetLastError());
   return TOAST_OK;
 }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector_types.h>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -51,7 +52,8 @@ struct toast_graph {
 
 namespace toast {
 
-// ------------------------------------------------------------ device tables
+// ------------------------------------------------------------ host tables
+// (used by toast_materialize on the host and to build the device stream)
 // one op, 32 bytes
 struct DOp {
   uint32_t loop_begin;   // global id of the op's role-0 loop
@@ -88,19 +90,53 @@ constexpr int MAX_RANK = 8;
 constexpr int MAX_ACTIONS = 1024;
 constexpr int MAX_GROUPS = 64;
 
+// ------------------------------------------------------------ device stream
+// The kernels walk the program as one contiguous stream of 16-byte words, in
+// op order: a 32-byte header, then n_uses 32-byte use records (sorted by the
+// used value so repeated operands are adjacent), then n_death 16-byte death
+// records.  Every field a warp needs for one op is in this record, so a
+// warp's reads are warp-uniform (broadcast) and sequential.
+struct KHead {           // 32 B
+  uint32_t lb;           // global loop id of role 0 (state key, C14)
+  uint16_t sig;          // op signature (materialisation class)
+  uint8_t rmask;         // reduction roles
+  uint8_t flags;         // bit0 matmul-class, bit1 ret
+  uint8_t n_uses;
+  uint8_t n_death;
+  uint16_t pad0;
+  uint32_t pad1;
+  uint64_t gbytes;       // result global bytes (0 for ret)
+  uint64_t gflops;       // 2 * prod(loop extents) for matmul-class ops, else 0
+};
+struct KUse {            // 32 B
+  uint16_t def_sig;
+  uint8_t def_rmask;
+  uint8_t flags;         // bit0 first use of this value at the op, bit1 last
+  uint32_t value;        // defining op of the used value
+  uint64_t def_dimof;    // nibble r: result dim of the def op's role r (0xF: none)
+  uint64_t use_dimof;    // nibble r: operand dim of this op's role r (0xF: none)
+  uint64_t def_gbytes;
+};
+struct KDeath {          // 16 B
+  uint16_t sig;
+  uint8_t rmask;
+  uint8_t pad0;
+  uint32_t pad1;
+  uint64_t gbytes;
+};
+static_assert(sizeof(KHead) == 32 && sizeof(KUse) == 32 && sizeof(KDeath) == 16, "stream records");
+
+// signature role word: acolor [0,10) | div_ok [10,26) | deselection class [26,34)
 struct DeviceTables {
-  // device pointers
-  const DOp* ops = nullptr;
-  const uint64_t* gflops = nullptr;      // per op (0 unless matmul-class)
-  const uint64_t* loops = nullptr;
-  const DUse* uses = nullptr;
-  const uint32_t* deaths = nullptr;
-  const uint64_t* desel = nullptr;       // [id][2] = need0, need1
+  const uint4* stream = nullptr;         // op stream (16-byte words)
+  const uint64_t* sig_roles = nullptr;   // [n_sigs][8] role words (acolor 0x3FF = untouchable)
+  const uint8_t* sig_nroles = nullptr;   // [n_sigs]
+  const uint64_t* desel = nullptr;       // [class][2] = need0, need1 (class 0 = none)
   const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
-  const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids
+  const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids (0xFF = unused)
   const uint32_t* kill = nullptr;        // [n_actions][n_words]
   // constants
-  int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, pad;
+  int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -136,6 +172,11 @@ struct toast_analysis {
   std::vector<uint64_t> h_gflops, h_loops, h_desel, h_acol_groups;
   std::vector<toast::DUse> h_uses;
   std::vector<uint32_t> h_deaths, h_actions, h_kill;
+  // device-stream images
+  std::vector<uint32_t> h_stream;           // 16-byte aligned words (as 4 x u32)
+  std::vector<uint64_t> h_sig_roles, h_desel_cls;
+  std::vector<uint8_t> h_sig_nroles;
+  std::vector<uint32_t> op_sig;
   std::vector<int32_t> axis_size;
 
   toast::DeviceTables dt;       // device pointers valid iff device >= 0
@@ -146,7 +187,7 @@ struct toast_analysis {
   std::mutex scratch_mu;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
-  int32_t smem_per_warp = 0;
+  int32_t smem_per_warp = 0, warps_per_block = 8;
   int32_t eval_blocks = 0, rollout_blocks = 0;
 };
 
