@@ -1200,10 +1200,17 @@ struct Oracle {
       for (int v : dying[t]) dying_bytes += (i64)local_bytes_of(v, layout_D(mask, v));
       L = L + res - dying_bytes;
     }
-    // C14: state key
+    // C14 (reading R14): the state is "the final sharding configuration
+    // itself".  Per op with at least one sharded loop, hash (first loop
+    // id, axis->role map: nibble A = role holding axis A, 0xF if none); sum over ops.
     u64 key = 0;
-    for (size_t l = 0; l < loops.size(); l++)
-      if (mask[l]) key += mix64(((u64)l << 8) | (u64)mask[l]);
+    for (size_t t = 0; t < M.ops.size(); t++) {
+      u64 a2r = 0xFFFF;
+      for (int r = 0; r < nloops((int)t); r++)
+        for (int A = 0; A < 4; A++)
+          if (mask[loop_of((int)t, r)] & (1 << A)) a2r = (a2r & ~(0xFULL << (4 * A))) | ((u64)r << (4 * A));
+      if (a2r != 0xFFFF) key += mix64(((u64)op_loop_begin[t] << 16) | a2r);
+    }
     // C13: runtime and score
     u64 flo = (u64)flops, fhi = (u64)(flops >> 64);
     double fl = (double)fhi * 18446744073709551616.0 + (double)flo;

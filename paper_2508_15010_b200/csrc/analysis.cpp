@@ -639,10 +639,10 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       a->h_stream.insert(a->h_stream.end(), w, w + bytes / 4);
     };
     auto dimof_def = [&](int32_t v) {
-      uint64_t m = ~0ULL;
+      uint32_t m = ~0u;
       for (size_t i = 0; i < OL[v].res_role.size(); ++i) {
-        uint64_t r = OL[v].res_role[i];
-        m = (m & ~(0xFULL << (4 * r))) | ((uint64_t)i << (4 * r));
+        uint32_t r = OL[v].res_role[i];
+        m = (m & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
       }
       return m;
     };
@@ -674,14 +674,16 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         bool first = q == 0 || g->values[op.operands[order[q - 1]]].def_op != v;
         bool last = q + 1 == order.size() || g->values[op.operands[order[q + 1]]].def_op != v;
         u.flags = (uint8_t)((first ? 1 : 0) | (last ? 2 : 0));
-        u.value = (uint32_t)v;
         u.def_dimof = dimof_def(v);
-        uint64_t um = ~0ULL;
+        uint32_t um = ~0u, tr = 0xEEEEEEEEu;
         for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
-          uint64_t r = OL[t].use_role[k][i];
-          um = (um & ~(0xFULL << (4 * r))) | ((uint64_t)i << (4 * r));
+          uint32_t r = OL[t].use_role[k][i];
+          um = (um & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
+          uint32_t rd = OL[v].res_role[i];
+          tr = (tr & ~(0xFu << (4 * rd))) | (r << (4 * rd));
         }
         u.use_dimof = um;
+        u.tr = tr;
         u.def_gbytes = a->h_ops[v].gbytes;
         push(&u, sizeof u);
       }

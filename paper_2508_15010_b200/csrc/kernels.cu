@@ -185,15 +185,17 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
 }
 
 // ---------------------------------------------------------------- the per-lane evaluation
-// S.seq holds the lane's candidate; `valid` lanes write `out`.
+// S.seq holds the lane's candidate; `valid` lanes write `out`.  NA = number
+// of mesh axes (compile-time so the per-axis loops are fully unrolled).
+template <int NA>
 __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, int lane, bool valid,
                                           toast_cost* __restrict__ out) {
   uint64_t fixed0, ones;
   const uint32_t status = decode(T, S, lane, fixed0, ones);
   for (int s = 0; s < T.n_sigs; ++s) S.a2r[s * 32 + lane] = (uint16_t)materialize_sig(T, S, lane, s, fixed0, ones);
   __syncwarp();
-  const int nq = T.n_axes * 4;
-  for (int q = 0; q < nq; ++q) { S.pay[q * 32 + lane] = 0ULL; S.cnt[q * 32 + lane] = 0u; }
+#pragma unroll
+  for (int q = 0; q < NA * 4; ++q) { S.pay[q * 32 + lane] = 0ULL; S.cnt[q * 32 + lane] = 0u; }
 
   uint64_t key = 0, flo = 0, fhi = 0;
   long long L = 0, peak = 0;
@@ -203,24 +205,14 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
     const uint32_t lb = h0.x, sig = h0.y & 0xFFFF, rmask = (h0.y >> 16) & 0xFF, flags = h0.y >> 24;
     const uint32_t n_uses = h0.z & 0xFF, n_death = (h0.z >> 8) & 0xFF;
     const uint32_t a2r = S.a2r[sig * 32 + lane];
-    // axes of this op, axes of its result dims, state key (C14)
+    // H7 state key (C14, reading R14): one hash per op with a sharded loop
+    if (a2r != 0xFFFFu) key += mix64(((uint64_t)lb << 16) | a2r);
     uint32_t opmask = 0, present = 0;
 #pragma unroll
-    for (int A = 0; A < 4; ++A) {
+    for (int A = 0; A < NA; ++A) {
       const uint32_t r = (a2r >> (4 * A)) & 15;
-      if (r != 15) {
-        opmask |= 1u << A;
-        if (!((rmask >> r) & 1)) present |= 1u << A;
-        bool first = true;
-        uint32_t m = 1u << A;
-#pragma unroll
-        for (int B = 0; B < 4; ++B) {
-          const uint32_t rb = (a2r >> (4 * B)) & 15;
-          if (B < A && rb == r) first = false;
-          if (B > A && rb == r) m |= 1u << B;
-        }
-        if (first) key += mix64(((uint64_t)(lb + r) << 8) | m);
-      }
+      opmask |= (r != 15 ? 1u : 0u) << A;
+      present |= ((r != 15 && !((rmask >> r) & 1)) ? 1u : 0u) << A;
     }
     if (flags & 1) {   // H3 local FLOPs, matmul-class ops only
       const uint64_t f = exdiv(T, u64of(h1.z, h1.w), opmask);
@@ -233,60 +225,77 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
     const uint4* q = p + 2;
     const uint4* gq = q;
     for (uint32_t k = 0; k < n_uses; ++k, q += 2) {
-      const uint4 u0 = __ldg(q), u1 = __ldg(q + 1);
-      const uint32_t def_sig = u0.x & 0xFFFF, def_rmask = (u0.x >> 16) & 0xFF, uflags = u0.x >> 24;
-      const uint64_t def_dimof = u64of(u0.z, u0.w), use_dimof = u64of(u1.x, u1.y), dgb = u64of(u1.z, u1.w);
+      const uint4 u0 = __ldg(q);
+      const uint32_t def_sig = u0.x & 0xFFFF, uflags = u0.x >> 24;
       if (uflags & 1) { gmax = 0; gq = q; }
       const uint32_t da = S.a2r[def_sig * 32 + lane];
-      uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
+      // fast test: every axis sits where the def->use role translation expects it
+      uint32_t mism = 0;
 #pragma unroll
-      for (int A = 0; A < 4; ++A) {
+      for (int A = 0; A < NA; ++A) {
         const uint32_t rd = (da >> (4 * A)) & 15, ru = (a2r >> (4 * A)) & 15;
-        const uint32_t dd = (uint32_t)(def_dimof >> (4 * rd)) & 15, du = (uint32_t)(use_dimof >> (4 * ru)) & 15;
-        dimD |= dd << (4 * A);
-        dimU |= du << (4 * A);
-        P |= ((def_rmask >> rd) & 1) << A;
-        presD |= (dd != 15 ? 1u : 0u) << A;
-        presU |= (du != 15 ? 1u : 0u) << A;
+        const uint32_t e = rd == 15 ? 15u : (u0.y >> (4 * rd)) & 15;
+        mism |= e != ru ? 1u : 0u;
       }
-      bool dup = false;
-      if (!(uflags & 1)) {   // same value used again at this op: cost it once per distinct layout
-        for (const uint4* q2 = gq; q2 < q; q2 += 2) {
-          const uint4 w1 = __ldg(q2 + 1);
-          const uint64_t ud2 = u64of(w1.x, w1.y);
-          uint32_t dimU2 = 0;
+      if (mism) {
+        const uint4 u1 = __ldg(q + 1);
+        const uint32_t def_rmask = (u0.x >> 16) & 0xFF;
+        const uint64_t dgb = u64of(u1.x, u1.y);
+        uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
-          for (int A = 0; A < 4; ++A) dimU2 |= ((uint32_t)(ud2 >> (4 * ((a2r >> (4 * A)) & 15))) & 15) << (4 * A);
-          dup |= dimU2 == dimU;
+        for (int A = 0; A < NA; ++A) {
+          const uint32_t rd = (da >> (4 * A)) & 15, ru = (a2r >> (4 * A)) & 15;
+          const uint32_t dd = rd == 15 ? 15u : (u0.z >> (4 * rd)) & 15;
+          const uint32_t du = ru == 15 ? 15u : (u0.w >> (4 * ru)) & 15;
+          dimD |= dd << (4 * A);
+          dimU |= du << (4 * A);
+          P |= ((rd != 15 && ((def_rmask >> rd) & 1)) ? 1u : 0u) << A;
+          presD |= (dd != 15 ? 1u : 0u) << A;
+          presU |= (du != 15 ? 1u : 0u) << A;
         }
-      }
-      if (!dup && (dimD != dimU || P)) {
-        uint64_t size = exdiv(T, dgb, presD);
-        for (int A = 0; A < T.n_axes; ++A) {          // phase 1: all_gather / all_to_all
-          const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
-          if (dd == 15 || dd == du) continue;
-          if (du != 15) {
-            S.pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
-            S.cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
-          } else {
-            S.pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
-            S.cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
-            size *= (uint64_t)T.sizes[A];
+        bool dup = false;
+        if (!(uflags & 1)) {   // the same value used again at this op: cost it once per distinct layout
+          for (const uint4* q2 = gq; q2 < q; q2 += 2) {
+            const uint32_t ud2 = __ldg(q2).w;
+            uint32_t dimU2 = 0;
+#pragma unroll
+            for (int A = 0; A < NA; ++A) {
+              const uint32_t ru = (a2r >> (4 * A)) & 15;
+              dimU2 |= (ru == 15 ? 15u : (ud2 >> (4 * ru)) & 15) << (4 * A);
+            }
+            dup |= dimU2 == dimU;
           }
         }
-        for (int A = 0; A < T.n_axes; ++A) {          // phase 2: reduce_scatter / all_reduce
-          if (!((P >> A) & 1)) continue;
-          if (((dimU >> (4 * A)) & 15) != 15) {
-            size = exdiv(T, size, 1u << A);
-            S.pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
-            S.cnt[(A * 4 + TOAST_RS) * 32 + lane] += 1u;
-          } else {
-            S.pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
-            S.cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
+        if (!dup && (dimD != dimU || P)) {
+          uint64_t size = exdiv(T, dgb, presD);
+#pragma unroll
+          for (int A = 0; A < NA; ++A) {          // phase 1: all_gather / all_to_all
+            const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+            if (dd == 15 || dd == du) continue;
+            if (du != 15) {
+              S.pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
+              S.cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
+            } else {
+              S.pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
+              S.cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
+              size *= (uint64_t)T.sizes[A];
+            }
           }
+#pragma unroll
+          for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
+            if (!((P >> A) & 1)) continue;
+            if (((dimU >> (4 * A)) & 15) != 15) {
+              size = exdiv(T, size, 1u << A);
+              S.pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
+              S.cnt[(A * 4 + TOAST_RS) * 32 + lane] += 1u;
+            } else {
+              S.pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
+              S.cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
+            }
+          }
+          const long long grow = (long long)exdiv(T, dgb, presU) - (long long)exdiv(T, dgb, presD);
+          if (grow > gmax) gmax = grow;
         }
-        const long long grow = (long long)exdiv(T, dgb, presU) - (long long)exdiv(T, dgb, presD);
-        if (grow > gmax) gmax = grow;
       }
       if (uflags & 2) temp += gmax;
     }
@@ -297,7 +306,7 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
       const uint32_t av = S.a2r[(d.x & 0xFFFF) * 32 + lane], rm = (d.x >> 16) & 0xFF;
       uint32_t pres = 0;
 #pragma unroll
-      for (int A = 0; A < 4; ++A) {
+      for (int A = 0; A < NA; ++A) {
         const uint32_t r = (av >> (4 * A)) & 15;
         pres |= ((r != 15 && !((rm >> r) & 1)) ? 1u : 0u) << A;
       }
@@ -310,49 +319,58 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
     p = q;
   }
   // H6 score (C13): fixed order, explicit round-to-nearest, no FMA
-  double fl = __dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo));
-  double tt = __ddiv_rn(fl, T.F);
+  double tt = __ddiv_rn(__dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo)), T.F);
   unsigned long long ncoll = 0;
-  __align__(16) toast_cost c;
-  memset(&c, 0, sizeof c);
-  for (int A = 0; A < T.n_axes; ++A) {
-    const double n = (double)T.sizes[A];
-    const unsigned long long pag = S.pay[(A * 4 + 0) * 32 + lane], prs = S.pay[(A * 4 + 1) * 32 + lane];
-    const unsigned long long par = S.pay[(A * 4 + 2) * 32 + lane], pa2 = S.pay[(A * 4 + 3) * 32 + lane];
-    const double ag = __ull2double_rn(pag), rs = __ull2double_rn(prs), ar = __ull2double_rn(par), a2a = __ull2double_rn(pa2);
-    const double n1 = __dsub_rn(n, 1.0);
-    const double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
-    const double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
-    tt = __dadd_rn(tt, __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]));
-    c.payload[A][0] = pag; c.payload[A][1] = prs; c.payload[A][2] = par; c.payload[A][3] = pa2;
+  unsigned long long pw[16];
+  uint32_t cw[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cw[k] = 0;
+#pragma unroll
+  for (int A = 0; A < 4; ++A) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t cq = S.cnt[(A * 4 + k) * 32 + lane];
-      ncoll += cq;
-      c.count[A][k] = (uint16_t)(cq > 65535u ? 65535u : cq);
+      pw[A * 4 + k] = 0;
+      if (A < NA) {
+        pw[A * 4 + k] = S.pay[(A * 4 + k) * 32 + lane];
+        const uint32_t cq = S.cnt[(A * 4 + k) * 32 + lane];
+        ncoll += cq;
+        cw[(A * 4 + k) >> 1] |= (cq > 65535u ? 65535u : cq) << (16 * (k & 1));
+      }
+    }
+    if (A < NA) {
+      const double n = (double)T.sizes[A];
+      const double ag = __ull2double_rn(pw[A * 4 + 0]), rs = __ull2double_rn(pw[A * 4 + 1]);
+      const double ar = __ull2double_rn(pw[A * 4 + 2]), a2a = __ull2double_rn(pw[A * 4 + 3]);
+      const double n1 = __dsub_rn(n, 1.0);
+      const double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
+      const double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
+      tt = __dadd_rn(tt, __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]));
     }
   }
   const uint64_t pk = (uint64_t)peak;
   const double RT = __ddiv_rn(tt, T.t0);
   const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
-  if (status == 0) {
-    c.runtime_s = tt;
-    c.score = __dadd_rn(RT, MP);
-    c.peak_bytes = pk;
-    c.flops = flo;
-    c.flops_hi = fhi;
-    c.state_key = key;
-    c.n_collectives = (uint32_t)ncoll;
-  } else {
-    memset(&c, 0, sizeof c);
-    c.status = status;
-  }
-  __syncwarp();
   if (valid) {
-    const uint4* src = reinterpret_cast<const uint4*>(&c);
+    // record layout = toast_cost (include/toast.h), written as 16 x 16 B
     uint4* dst = reinterpret_cast<uint4*>(out);
+    const bool ok = status == 0;
+    auto d2 = [](double x) { return (unsigned long long)__double_as_longlong(x); };
+    const unsigned long long w0 = ok ? d2(tt) : 0ULL, w1 = ok ? d2(__dadd_rn(RT, MP)) : 0ULL;
+    const unsigned long long w2 = ok ? pk : 0ULL, w3 = ok ? flo : 0ULL, w4 = ok ? key : 0ULL;
+    const unsigned long long w5 = ok ? ((unsigned long long)(uint32_t)ncoll << 32) : (unsigned long long)status;
+    dst[0] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+    dst[1] = make_uint4((uint32_t)w2, (uint32_t)(w2 >> 32), (uint32_t)w3, (uint32_t)(w3 >> 32));
+    dst[2] = make_uint4((uint32_t)w4, (uint32_t)(w4 >> 32), (uint32_t)w5, (uint32_t)(w5 >> 32));
 #pragma unroll
-    for (int k = 0; k < 16; ++k) dst[k] = src[k];
+    for (int k = 0; k < 8; ++k) {
+      const unsigned long long a = ok ? pw[2 * k] : 0ULL, b = ok ? pw[2 * k + 1] : 0ULL;
+      dst[3 + k] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+    }
+    dst[11] = ok ? make_uint4(cw[0], cw[1], cw[2], cw[3]) : make_uint4(0, 0, 0, 0);
+    dst[12] = ok ? make_uint4(cw[4], cw[5], cw[6], cw[7]) : make_uint4(0, 0, 0, 0);
+    dst[13] = ok ? make_uint4((uint32_t)fhi, (uint32_t)(fhi >> 32), 0, 0) : make_uint4(0, 0, 0, 0);
+    dst[14] = make_uint4(0, 0, 0, 0);
+    dst[15] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -372,6 +390,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
   }
 }
 
+template <int NA>
 __global__ void __launch_bounds__(256) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
   const Smem S = warp_smem(T);
@@ -382,7 +401,7 @@ __global__ void __launch_bounds__(256) toast_eval_kernel(const DeviceTables T, c
     const int64_t i = b * 32 + lane;
     const bool valid = i < n;
     load_seq(S, seqs + i * 32, lane, valid);
-    eval_lane(T, S, lane, valid, out + i);
+    eval_lane<NA>(T, S, lane, valid, out + i);
   }
 }
 
@@ -401,6 +420,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
   o1 = c1;
 }
 
+template <int NA>
 __global__ void __launch_bounds__(256) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
@@ -468,8 +488,14 @@ __global__ void __launch_bounds__(256) toast_rollout_kernel(const DeviceTables T
         dst[k] = make_uint4(S.seq[(4 * k) * 32 + lane], S.seq[(4 * k + 1) * 32 + lane], S.seq[(4 * k + 2) * 32 + lane],
                             S.seq[(4 * k + 3) * 32 + lane]);
     }
-    eval_lane(T, S, lane, valid, out + i);
+    eval_lane<NA>(T, S, lane, valid, out + i);
   }
+}
+
+template <int NA>
+void set_smem_attr(int bytes) {
+  cudaFuncSetAttribute(toast_eval_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(toast_rollout_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 }  // namespace
@@ -534,11 +560,22 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   a->warps_per_block = wpb;
   const int smem = wpb * a->smem_per_warp;
   // the attribute is per function, shared by every analysis in the process: allow the device maximum
-  TOAST_CUDA(cudaFuncSetAttribute(toast_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_smem));
-  TOAST_CUDA(cudaFuncSetAttribute(toast_rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev_smem));
+  set_smem_attr<1>(dev_smem);
+  set_smem_attr<2>(dev_smem);
+  set_smem_attr<3>(dev_smem);
+  set_smem_attr<4>(dev_smem);
+  TOAST_CUDA(cudaGetLastError());
   int be = 0, br = 0;
-  TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel, wpb * 32, smem));
-  TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel, wpb * 32, smem));
+  switch (T.n_axes) {
+    case 1: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<1>, wpb * 32, smem));
+            TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<1>, wpb * 32, smem)); break;
+    case 2: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<2>, wpb * 32, smem));
+            TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<2>, wpb * 32, smem)); break;
+    case 3: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<3>, wpb * 32, smem));
+            TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<3>, wpb * 32, smem)); break;
+    default: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<4>, wpb * 32, smem));
+             TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<4>, wpb * 32, smem)); break;
+  }
   a->eval_blocks = sms * std::max(be, 1);
   a->rollout_blocks = sms * std::max(br, 1);
   return TOAST_OK;
@@ -562,8 +599,15 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
                          std::string& err) {
   if (n <= 0) return TOAST_OK;
   const int64_t blocks = grid_for(a, n, a->eval_blocks);
-  toast_eval_kernel<<<(unsigned)blocks, a->warps_per_block * 32, a->warps_per_block * a->smem_per_warp,
-                      (cudaStream_t)stream>>>(a->dt, d_seqs, n, d_out);
+  const dim3 g((unsigned)blocks), b(a->warps_per_block * 32);
+  const size_t sm = (size_t)a->warps_per_block * a->smem_per_warp;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (a->dt.n_axes) {
+    case 1: toast_eval_kernel<1><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
+    case 2: toast_eval_kernel<2><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
+    case 3: toast_eval_kernel<3><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
+    default: toast_eval_kernel<4><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
+  }
   TOAST_CUDA(cudaGetLastError());
   return TOAST_OK;
 }
@@ -572,8 +616,15 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
                             uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err) {
   if (n <= 0) return TOAST_OK;
   const int64_t blocks = grid_for(a, n, a->rollout_blocks);
-  toast_rollout_kernel<<<(unsigned)blocks, a->warps_per_block * 32, a->warps_per_block * a->smem_per_warp,
-                         (cudaStream_t)stream>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out);
+  const dim3 g((unsigned)blocks), b(a->warps_per_block * 32);
+  const size_t sm = (size_t)a->warps_per_block * a->smem_per_warp;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (a->dt.n_axes) {
+    case 1: toast_rollout_kernel<1><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
+    case 2: toast_rollout_kernel<2><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
+    case 3: toast_rollout_kernel<3><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
+    default: toast_rollout_kernel<4><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
+  }
   TOAST_CUDA(cudaGetLastError());
   return TOAST_OK;
 }

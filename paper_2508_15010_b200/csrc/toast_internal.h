@@ -112,10 +112,12 @@ struct KUse {            // 32 B
   uint16_t def_sig;
   uint8_t def_rmask;
   uint8_t flags;         // bit0 first use of this value at the op, bit1 last
-  uint32_t value;        // defining op of the used value
-  uint64_t def_dimof;    // nibble r: result dim of the def op's role r (0xF: none)
-  uint64_t use_dimof;    // nibble r: operand dim of this op's role r (0xF: none)
+  uint32_t tr;           // nibble rd: this op's role expected to hold what the def's role rd holds
+                         //   (0xE: rd is not a result dim -> never "nothing to do")
+  uint32_t def_dimof;    // nibble r: result dim of the def op's role r (0xF: none)
+  uint32_t use_dimof;    // nibble r: operand dim of this op's role r (0xF: none)
   uint64_t def_gbytes;
+  uint64_t pad;
 };
 struct KDeath {          // 16 B
   uint16_t sig;
