@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--n", type=int, default=1 << 18, help="rollouts per step per GPU")
+    p.add_argument("--n", type=int, default=1 << 18, help="rollouts per step per GPU (rounded down to whole waves)")
     p.add_argument("--config", default="gpt24")
     p.add_argument("--impl", default="toast", choices=["toast", "reference"])
     p.add_argument("--seed", type=int, default=2024)
@@ -207,7 +207,8 @@ def run_toast(args, cfg, rank, world, local):
                          cuda_device=local)
     nda_s = time.perf_counter() - t
     dump = a.dump()
-    N = args.n
+    wave = a.preferred_batch()
+    N = max(wave, (args.n // wave) * wave)      # whole waves
     stream = torch.cuda.current_stream(dev)
     pre = torch.zeros((N, 32), dtype=torch.int16, device=dev)
     seqs = torch.empty_like(pre)
@@ -275,7 +276,7 @@ def run_toast(args, cfg, rank, world, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": cfg.name, "rollouts_per_step_per_gpu": N, "mesh": [list(x) for x in cfg.axes],
+            "config": {"workload": cfg.name, "rollouts_per_step_per_gpu": N, "wave": wave, "mesh": [list(x) for x in cfg.axes],
                        "ops": dump["n_ops"], "loops": dump["n_loops"], "actions": len(dump["actions"]) + 1,
                        "l2": "flushed (256 MiB write) between timed steps", "description": cfg.description},
             "gpu_launches": args.steps,

@@ -98,9 +98,9 @@ typedef struct {
   double score;            /* RT + MP */
   uint64_t peak_bytes;     /* C12: max over program points of live device-local bytes */
   uint64_t flops;          /* C10: low 64 bits of the local matmul-class FLOP total */
-  uint64_t state_key;      /* C14: order-independent hash of the materialised masks */
+  uint64_t state_key;      /* C14 (R14): sum over sharded ops of mix64(first loop << 16 | axis->role map) */
   uint32_t status;         /* TOAST_ST_* bits; 0 = ok */
-  uint32_t n_collectives;  /* sum of count[][] */
+  uint32_t n_collectives;  /* total number of collectives (count[][] saturates at 65535) */
   uint64_t payload[4][4];  /* C11 bytes per [axis][AG, RS, AR, A2A] */
   uint16_t count[4][4];    /* number of collectives per [axis][kind] */
   uint64_t flops_hi;       /* high 64 bits of the FLOP total */
@@ -137,6 +137,9 @@ toast_status toast_num_actions(const toast_analysis* a, int32_t* n);
 toast_status toast_query_actions(const toast_analysis* a, toast_action_info* out, int32_t cap, int32_t* n);
 /* the empty sequence's record (RT = 1) */
 toast_status toast_query_baseline(const toast_analysis* a, toast_cost* out);
+/* candidates one full wave of the GPU evaluates at once (resident warps x 32);
+ * batch sizes that are multiples of it leave no partially filled last wave. */
+toast_status toast_preferred_batch(const toast_analysis* a, int64_t* n);
 /* JSON dump of the H0 tables (loops, conflicts, sets, groups, super-colors,
  * actions, baseline).  *needed = bytes incl. NUL; writes only if cap >= *needed. */
 toast_status toast_dump_analysis(const toast_analysis* a, char* buf, size_t cap, size_t* needed);
@@ -187,13 +190,29 @@ typedef struct {
 
 typedef struct toast_search_state toast_search_state;
 
+/* The per-round record one rank contributes to the all-gather (host memory,
+   toast_search_export_bytes() bytes).  Written by toast_search_round; the
+   gathered array [world] is passed to toast_search_import on every rank. */
+typedef struct {
+  double best_score;       /* this rank's best score (after adopting the last global best) */
+  uint64_t best_key;
+  uint16_t best_seq[32];
+  int64_t evals;           /* evaluations done by this rank so far */
+  double elapsed_s;        /* this rank's wall clock since begin (rank 0's decides time limits) */
+  int32_t rank;
+  int32_t pad;
+  toast_cost best;         /* full record of the rank's best */
+} toast_search_export;
+
 toast_status toast_search(const toast_analysis* a, const toast_search_opts* o, toast_search_result* out);
 
 /* bytes one rank contributes to the per-round all_gather */
 size_t toast_search_export_bytes(const toast_analysis* a);
+/* seed of rank r = o->seed + r.  A host-only analysis (cuda_device = -1) may
+   begin and import (the exchange logic is host code) but not run rounds. */
 toast_status toast_search_begin(const toast_analysis* a, const toast_search_opts* o, int32_t rank, int32_t world,
                                 toast_search_state** out);
-/* runs one round; writes this rank's export record to `export_buf` (host memory) */
+/* runs one round on the GPU; writes this rank's toast_search_export to `export_buf` (host memory) */
 toast_status toast_search_round(toast_search_state* s, void* export_buf);
 /* imports world records ([world][export_bytes], host memory); *stop = 1 when all ranks must stop */
 toast_status toast_search_import(toast_search_state* s, const void* gathered, int32_t* stop);

@@ -36,7 +36,18 @@ def _newer(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, obj: str = OBJ, extra=()) -> str:
+    """extra: additional nvcc flags for the kernels (used by scripts/kernel_sweep.py)."""
+    global LIB, OBJ
+    saved = (LIB, OBJ)
+    LIB, OBJ = lib, obj
+    try:
+        return _build(force, verbose, list(extra))
+    finally:
+        LIB, OBJ = saved
+
+
+def _build(force: bool, verbose: bool, extra) -> str:
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hdrs = [os.path.join(SRC, h) for h in HEADERS] + [os.path.join(INC, "toast.h")]
@@ -47,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if force or _newer(obj, [src] + hdrs):
             if s.endswith(".cu"):
-                cmd = [NVCC] + CU_FLAGS + ["-c", src, "-o", obj]
+                cmd = [NVCC] + CU_FLAGS + extra + ["-c", src, "-o", obj]
             else:
                 cmd = ["g++"] + CXX_FLAGS + ["-c", src, "-o", obj]
             if verbose:

@@ -3,6 +3,7 @@
 // ir.cpp (parse), analysis.cpp (H0), kernels.cu (H1-H8) and search.cpp.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -118,6 +119,13 @@ toast_status toast_query_baseline(const toast_analysis* a, toast_cost* out) {
   return ret(TOAST_OK, "");
 }
 
+toast_status toast_preferred_batch(const toast_analysis* a, int64_t* n) {
+  if (!a || !n) return fail(TOAST_E_INVALID_ARG, "NULL argument");
+  if (!has_device(a)) return fail(TOAST_E_CUDA, "the analysis has no device tables");
+  *n = (int64_t)std::min(a->eval_blocks, a->rollout_blocks) * a->warps_per_block * 32;
+  return ret(TOAST_OK, "");
+}
+
 toast_status toast_dump_analysis(const toast_analysis* a, char* buf, size_t cap, size_t* needed) {
   if (!a || !needed) return fail(TOAST_E_INVALID_ARG, "NULL argument");
   std::string s = toast::dump_json(a);
@@ -175,8 +183,7 @@ size_t toast_search_export_bytes(const toast_analysis* a) {
 toast_status toast_search_begin(const toast_analysis* a, const toast_search_opts* o, int32_t rank, int32_t world,
                                 toast_search_state** out) {
   if (!a || !o || !out) return fail(TOAST_E_INVALID_ARG, "NULL argument");
-  if (!has_device(a)) return fail(TOAST_E_CUDA, "the analysis has no device tables");
-  cudaSetDevice(a->device);
+  if (a->device >= 0) cudaSetDevice(a->device);
   std::string err;
   return ret(toast::search_begin(a, o, rank, world, out, err), err);
 }
@@ -202,6 +209,7 @@ toast_status toast_search_end(toast_search_state* s, toast_search_result* out) {
 
 toast_status toast_search(const toast_analysis* a, const toast_search_opts* o, toast_search_result* out) {
   if (!a || !o || !out) return fail(TOAST_E_INVALID_ARG, "NULL argument");
+  if (!has_device(a)) return fail(TOAST_E_CUDA, "the analysis has no device tables");
   toast_search_state* s = nullptr;
   toast_status st = toast_search_begin(a, o, 0, 1, &s);
   if (st) return st;

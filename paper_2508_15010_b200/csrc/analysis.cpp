@@ -8,6 +8,8 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <cstdio>
+#include <cstdlib>
 
 #include "toast_internal.h"
 
@@ -607,9 +609,19 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       loop_cls[kv.first] = it->second;
     }
     if (a->h_desel_cls.size() / 2 > 255) { err = "more than 255 deselection classes"; return TOAST_E_LIMIT; }
-    // op signatures: the per-role words that decide materialisation (C9)
+    // op signatures: the per-role words that decide materialisation (C9) plus
+    // each role's result dim (so a candidate's entry also gives the result layout)
+    auto resdim_of = [&](int32_t t) {
+      uint32_t m = ~0u;
+      for (size_t i = 0; i < OL[t].res_role.size(); ++i) {
+        uint32_t r = OL[t].res_role[i];
+        m = (m & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
+      }
+      return m;
+    };
     std::map<std::vector<uint64_t>, uint32_t> sig_id;
     std::vector<std::vector<uint64_t>> sig_words;
+    std::vector<uint32_t> sig_rd;
     a->op_sig.assign(n_ops, 0);
     for (int32_t t = 0; t < n_ops; ++t) {
       std::vector<uint64_t> w;
@@ -619,16 +631,21 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         else w.push_back(ac | (((a->h_loops[l] >> 12) & 0xFFFF) << 10) | ((uint64_t)loop_cls[l] << 26));
       }
       while (!w.empty() && w.back() == NO_ACOLOR) w.pop_back();
-      auto it = sig_id.find(w);
+      const uint32_t rd = resdim_of(t);
+      std::vector<uint64_t> key = w;
+      key.push_back((uint64_t)rd << 40 | 0xFFull << 32);   // disjoint from role words
+      auto it = sig_id.find(key);
       if (it == sig_id.end()) {
-        it = sig_id.emplace(w, (uint32_t)sig_words.size()).first;
+        it = sig_id.emplace(key, (uint32_t)sig_words.size()).first;
         sig_words.push_back(w);
+        sig_rd.push_back(rd);
       }
       a->op_sig[t] = it->second;
     }
     if (sig_words.size() > 65535) { err = "more than 65535 op signatures"; return TOAST_E_LIMIT; }
     a->h_sig_roles.assign(sig_words.size() * 8, NO_ACOLOR);
     a->h_sig_nroles.assign(sig_words.size(), 0);
+    a->h_sig_resdim = sig_rd;
     for (size_t q = 0; q < sig_words.size(); ++q) {
       a->h_sig_nroles[q] = (uint8_t)sig_words[q].size();
       for (size_t r = 0; r < sig_words[q].size(); ++r) a->h_sig_roles[q * 8 + r] = sig_words[q][r];
@@ -638,25 +655,16 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       const uint32_t* w = reinterpret_cast<const uint32_t*>(rec);
       a->h_stream.insert(a->h_stream.end(), w, w + bytes / 4);
     };
-    auto dimof_def = [&](int32_t v) {
-      uint32_t m = ~0u;
-      for (size_t i = 0; i < OL[v].res_role.size(); ++i) {
-        uint32_t r = OL[v].res_role[i];
-        m = (m & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
-      }
-      return m;
-    };
     a->h_stream.clear();
     for (int32_t t = 0; t < n_ops; ++t) {
       const GOp& op = g->ops[t];
       KHead h{};
       h.lb = (uint32_t)lbeg[t];
       h.sig = (uint16_t)a->op_sig[t];
-      h.rmask = a->h_ops[t].rmask;
       h.flags = a->h_ops[t].flags;
       h.n_uses = (uint8_t)op.operands.size();
-      h.n_death = (uint8_t)deaths[t].size();
       if (deaths[t].size() > 255) { err = "too many values die at one op"; return TOAST_E_LIMIT; }
+      h.n_death = (uint8_t)deaths[t].size();
       h.gbytes = a->h_ops[t].gbytes;
       h.gflops = a->h_gflops[t];
       push(&h, sizeof h);
@@ -670,31 +678,28 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         int32_t v = g->values[op.operands[k]].def_op;
         KUse u{};
         u.def_sig = (uint16_t)a->op_sig[v];
-        u.def_rmask = a->h_ops[v].rmask;
         bool first = q == 0 || g->values[op.operands[order[q - 1]]].def_op != v;
         bool last = q + 1 == order.size() || g->values[op.operands[order[q + 1]]].def_op != v;
         u.flags = (uint8_t)((first ? 1 : 0) | (last ? 2 : 0));
-        u.def_dimof = dimof_def(v);
-        uint32_t um = ~0u, tr = 0xEEEEEEEEu;
+        uint32_t um = ~0u;
         for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
           uint32_t r = OL[t].use_role[k][i];
           um = (um & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
-          uint32_t rd = OL[v].res_role[i];
-          tr = (tr & ~(0xFu << (4 * rd))) | (r << (4 * rd));
         }
         u.use_dimof = um;
-        u.tr = tr;
         u.def_gbytes = a->h_ops[v].gbytes;
         push(&u, sizeof u);
       }
       for (int32_t v : deaths[t]) {
         KDeath d{};
         d.sig = (uint16_t)a->op_sig[v];
-        d.rmask = a->h_ops[v].rmask;
         d.gbytes = a->h_ops[v].gbytes;
         push(&d, sizeof d);
       }
     }
+    if (getenv("TOAST_DEBUG"))
+      fprintf(stderr, "[toast] ops %d loops %lld signatures %zu stream %zu B actions %zu desel classes %zu\n", n_ops,
+              (long long)NL, sig_words.size(), a->h_stream.size() * 4, a->actions.size(), a->h_desel_cls.size() / 2);
   }
 
   // ------------------------------------------------------------ baseline (empty sequence)

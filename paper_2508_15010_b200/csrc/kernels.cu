@@ -30,24 +30,42 @@
 
 #include "toast_internal.h"
 
+#ifndef TOAST_MAX_THREADS
+#define TOAST_MAX_THREADS 256
+#endif
+#ifndef TOAST_MIN_BLOCKS
+#define TOAST_MIN_BLOCKS 3
+#endif
+#ifndef TOAST_MAX_WPB
+#define TOAST_MAX_WPB 8
+#endif
+
 namespace toast {
 
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__host__ __device__ inline int smem_a_bytes(int n_sigs) { return ((n_sigs * 64) + 15) & ~15; }
-__host__ __device__ inline int smem_b_bytes(int n_ac, int n_words, int n_axes) {
-  int b1 = n_ac * 128 + 2048 + n_words * 128;
-  int b2 = n_axes * 4 * (256 + 128);
+// per-warp shared memory = region A (the signature table, overlaid with the
+// sequence + rollout legal set, which are dead once the table is written) +
+// region B (per-color event lists during decode/materialise, then the
+// payload/count accumulators during the sweep)
+__host__ __device__ inline int sig_entry_bytes(int n_axes) { return n_axes <= 2 ? 2 : 4; }
+__host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes) {
+  int a1 = n_sigs * 32 * sig_entry_bytes(n_axes), a2 = 2048 + n_words * 128;
+  return ((a1 > a2 ? a1 : a2) + 15) & ~15;
+}
+__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes) {
+  int b1 = n_ac * 128, b2 = n_axes * 4 * (256 + 128);
   return ((b1 > b2 ? b1 : b2) + 15) & ~15;
 }
 __host__ __device__ inline int smem_warp_bytes(int n_sigs, int n_ac, int n_words, int n_axes) {
-  return smem_a_bytes(n_sigs) + smem_b_bytes(n_ac, n_words, n_axes);
+  return smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes);
 }
 
 struct Smem {
-  uint16_t* a2r;            // [n_sigs][32]  axis -> role map of each signature (nibble A; 0xF = none)
+  void* sig;                // [n_sigs][32]  per signature: axis->role | axis->result dim (4 bits per axis each);
+                            //               u16 entries for <= 2 axes, u32 otherwise
   uint32_t* acol;           // [n_acolors][32] up to 4 events (valid | axis << 5 | position) per action color
   uint32_t* seq;            // [16][32] the candidate's 32 ids as 16 words
   uint32_t* legal;          // [n_words][32] rollout legal bitset
@@ -58,15 +76,15 @@ struct Smem {
 __device__ __forceinline__ Smem warp_smem(const DeviceTables& T) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
-  const int sa = smem_a_bytes(T.n_sigs);
-  const int per = sa + smem_b_bytes(T.n_acolors, T.n_words, T.n_axes);
+  const int sa = smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
+  const int per = sa + smem_b_bytes(T.n_acolors, T.n_axes);
   unsigned char* base = smem + (size_t)warp * per;
   Smem s;
-  s.a2r = reinterpret_cast<uint16_t*>(base);
+  s.sig = base;
+  s.seq = reinterpret_cast<uint32_t*>(base);
+  s.legal = reinterpret_cast<uint32_t*>(base + 2048);
   unsigned char* b = base + sa;
   s.acol = reinterpret_cast<uint32_t*>(b);
-  s.seq = reinterpret_cast<uint32_t*>(b + T.n_acolors * 128);
-  s.legal = reinterpret_cast<uint32_t*>(b + T.n_acolors * 128 + 2048);
   s.pay = reinterpret_cast<unsigned long long*>(b);
   s.cnt = reinterpret_cast<uint32_t*>(b + T.n_axes * 4 * 256);
   return s;
@@ -85,6 +103,26 @@ __device__ __forceinline__ uint64_t exdiv(const DeviceTables& T, uint64_t x, uin
 }
 
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+// signature entry per lane: bits [0, 4NA) axis->role, [4NA, 8NA) axis->result dim
+template <int NA> struct Ent { typedef uint32_t T; };
+template <> struct Ent<1> { typedef uint16_t T; };
+template <> struct Ent<2> { typedef uint16_t T; };
+template <int NA>
+__device__ __forceinline__ uint32_t ent_load(const Smem& S, uint32_t sig, int lane) {
+  return reinterpret_cast<const typename Ent<NA>::T*>(S.sig)[sig * 32 + lane];
+}
+template <int NA>
+__device__ __forceinline__ void ent_store(const Smem& S, uint32_t sig, int lane, uint32_t e) {
+  reinterpret_cast<typename Ent<NA>::T*>(S.sig)[sig * 32 + lane] = (typename Ent<NA>::T)e;
+}
+// axis A's role / result dim in an entry (15 = none)
+template <int NA> __device__ __forceinline__ uint32_t e_role(uint32_t e, int A) { return (e >> (4 * A)) & 15; }
+template <int NA> __device__ __forceinline__ uint32_t e_dim(uint32_t e, int A) { return (e >> (4 * NA + 4 * A)) & 15; }
+// the 16-bit axis->role map of the state key (axes >= NA read as 0xF)
+template <int NA> __device__ __forceinline__ uint32_t e_a2r16(uint32_t e) {
+  return NA >= 4 ? (e & 0xFFFFu) : ((e & ((1u << (4 * NA)) - 1u)) | (0xFFFFu & ~((1u << (4 * NA)) - 1u)));
+}
 
 // ---------------------------------------------------------------- H1 decode (C9)
 __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
@@ -158,7 +196,7 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
     }
   }
   uint32_t a2r = 0xFFFFu;
-  if (!any) return a2r;
+  if (!any) return 0xFFFFFFFFu;   // nothing sharded: every axis "none" in both maps
   uint32_t masks = 0, opmask = 0;
   while (true) {
     int best = -1;
@@ -181,7 +219,21 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
       a2r = (a2r & ~(0xFu << (4 * A))) | ((uint32_t)best << (4 * A));
     }
   }
-  return a2r;
+  const uint32_t rdm = __ldg(T.sig_resdim + s);
+  uint32_t dims = 0;
+#pragma unroll
+  for (int A = 0; A < 4; ++A) {
+    const uint32_t r = (a2r >> (4 * A)) & 15;
+    dims |= (r == 15 ? 15u : (rdm >> (4 * r)) & 15) << (4 * A);
+  }
+  return a2r | (dims << 16);
+}
+
+// pack the 16+16-bit (role, dim) maps into an NA-entry
+template <int NA>
+__device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
+  const uint32_t m = NA >= 4 ? 0xFFFFu : ((1u << (4 * NA)) - 1u);
+  return (full & m) | (((full >> 16) & m) << (4 * NA));
 }
 
 // ---------------------------------------------------------------- the per-lane evaluation
@@ -192,7 +244,7 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
                                           toast_cost* __restrict__ out) {
   uint64_t fixed0, ones;
   const uint32_t status = decode(T, S, lane, fixed0, ones);
-  for (int s = 0; s < T.n_sigs; ++s) S.a2r[s * 32 + lane] = (uint16_t)materialize_sig(T, S, lane, s, fixed0, ones);
+  for (int s = 0; s < T.n_sigs; ++s) ent_store<NA>(S, s, lane, pack_entry<NA>(materialize_sig(T, S, lane, s, fixed0, ones)));
   __syncwarp();
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { S.pay[q * 32 + lane] = 0ULL; S.cnt[q * 32 + lane] = 0u; }
@@ -202,17 +254,17 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
   const uint4* p = T.stream;
   for (int t = 0; t < T.n_ops; ++t) {
     const uint4 h0 = __ldg(p), h1 = __ldg(p + 1);
-    const uint32_t lb = h0.x, sig = h0.y & 0xFFFF, rmask = (h0.y >> 16) & 0xFF, flags = h0.y >> 24;
-    const uint32_t n_uses = h0.z & 0xFF, n_death = (h0.z >> 8) & 0xFF;
-    const uint32_t a2r = S.a2r[sig * 32 + lane];
+    const uint32_t lb = h0.x, sig = h0.y & 0xFFFF, flags = (h0.y >> 16) & 0xFF;
+    const uint32_t n_uses = h0.y >> 24, n_death = h0.z & 0xFF;
+    const uint32_t ent = ent_load<NA>(S, sig, lane);
+    const uint32_t a2r = e_a2r16<NA>(ent);
     // H7 state key (C14, reading R14): one hash per op with a sharded loop
     if (a2r != 0xFFFFu) key += mix64(((uint64_t)lb << 16) | a2r);
     uint32_t opmask = 0, present = 0;
 #pragma unroll
     for (int A = 0; A < NA; ++A) {
-      const uint32_t r = (a2r >> (4 * A)) & 15;
-      opmask |= (r != 15 ? 1u : 0u) << A;
-      present |= ((r != 15 && !((rmask >> r) & 1)) ? 1u : 0u) << A;
+      opmask |= (e_role<NA>(ent, A) != 15 ? 1u : 0u) << A;
+      present |= (e_dim<NA>(ent, A) != 15 ? 1u : 0u) << A;
     }
     if (flags & 1) {   // H3 local FLOPs, matmul-class ops only
       const uint64_t f = exdiv(T, u64of(h1.z, h1.w), opmask);
@@ -224,49 +276,45 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
     long long temp = 0, gmax = 0;
     const uint4* q = p + 2;
     const uint4* gq = q;
-    for (uint32_t k = 0; k < n_uses; ++k, q += 2) {
-      const uint4 u0 = __ldg(q);
-      const uint32_t def_sig = u0.x & 0xFFFF, uflags = u0.x >> 24;
+    for (uint32_t k = 0; k < n_uses; ++k, ++q) {
+      const uint4 u = __ldg(q);
+      const uint32_t uflags = (u.x >> 16) & 0xFF;
       if (uflags & 1) { gmax = 0; gq = q; }
-      const uint32_t da = S.a2r[def_sig * 32 + lane];
-      // fast test: every axis sits where the def->use role translation expects it
-      uint32_t mism = 0;
+      const uint32_t de = ent_load<NA>(S, u.x & 0xFFFF, lane);
+      // def layout D (axis -> result dim), partial axes P, use layout U (axis -> operand dim)
+      uint32_t dimU = 0, P = 0;
+      bool nothing = true;
 #pragma unroll
       for (int A = 0; A < NA; ++A) {
-        const uint32_t rd = (da >> (4 * A)) & 15, ru = (a2r >> (4 * A)) & 15;
-        const uint32_t e = rd == 15 ? 15u : (u0.y >> (4 * rd)) & 15;
-        mism |= e != ru ? 1u : 0u;
+        const uint32_t ru = (a2r >> (4 * A)) & 15;
+        const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
+        const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+        dimU |= du << (4 * A);
+        const bool pa = rd != 15 && dd == 15;
+        P |= (pa ? 1u : 0u) << A;
+        nothing &= !pa && (dd == 15 || dd == du);
       }
-      if (mism) {
-        const uint4 u1 = __ldg(q + 1);
-        const uint32_t def_rmask = (u0.x >> 16) & 0xFF;
-        const uint64_t dgb = u64of(u1.x, u1.y);
-        uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
-#pragma unroll
-        for (int A = 0; A < NA; ++A) {
-          const uint32_t rd = (da >> (4 * A)) & 15, ru = (a2r >> (4 * A)) & 15;
-          const uint32_t dd = rd == 15 ? 15u : (u0.z >> (4 * rd)) & 15;
-          const uint32_t du = ru == 15 ? 15u : (u0.w >> (4 * ru)) & 15;
-          dimD |= dd << (4 * A);
-          dimU |= du << (4 * A);
-          P |= ((rd != 15 && ((def_rmask >> rd) & 1)) ? 1u : 0u) << A;
-          presD |= (dd != 15 ? 1u : 0u) << A;
-          presU |= (du != 15 ? 1u : 0u) << A;
-        }
+      if (!nothing) {   // a collective (not just a free local slice) is needed
+        const uint32_t dimD = (de >> (4 * NA)) & ((1u << (4 * NA)) - 1u);
         bool dup = false;
-        if (!(uflags & 1)) {   // the same value used again at this op: cost it once per distinct layout
-          for (const uint4* q2 = gq; q2 < q; q2 += 2) {
-            const uint32_t ud2 = __ldg(q2).w;
-            uint32_t dimU2 = 0;
+        for (const uint4* q2 = gq; q2 < q; ++q2) {   // the same value again at this op: once per layout
+          const uint32_t ud2 = __ldg(q2).y;
+          uint32_t dimU2 = 0;
 #pragma unroll
-            for (int A = 0; A < NA; ++A) {
-              const uint32_t ru = (a2r >> (4 * A)) & 15;
-              dimU2 |= (ru == 15 ? 15u : (ud2 >> (4 * ru)) & 15) << (4 * A);
-            }
-            dup |= dimU2 == dimU;
+          for (int A = 0; A < NA; ++A) {
+            const uint32_t ru = (a2r >> (4 * A)) & 15;
+            dimU2 |= (ru == 15 ? 15u : (ud2 >> (4 * ru)) & 15) << (4 * A);
           }
+          dup |= dimU2 == dimU;
         }
-        if (!dup && (dimD != dimU || P)) {
+        if (!dup) {
+          const uint64_t dgb = u64of(u.z, u.w);
+          uint32_t presD = 0, presU = 0;
+#pragma unroll
+          for (int A = 0; A < NA; ++A) {
+            presD |= (((dimD >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
+            presU |= (((dimU >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
+          }
           uint64_t size = exdiv(T, dgb, presD);
 #pragma unroll
           for (int A = 0; A < NA; ++A) {          // phase 1: all_gather / all_to_all
@@ -303,13 +351,10 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
     long long dying = 0;
     for (uint32_t k = 0; k < n_death; ++k, ++q) {
       const uint4 d = __ldg(q);
-      const uint32_t av = S.a2r[(d.x & 0xFFFF) * 32 + lane], rm = (d.x >> 16) & 0xFF;
+      const uint32_t ev = ent_load<NA>(S, d.x & 0xFFFF, lane);
       uint32_t pres = 0;
 #pragma unroll
-      for (int A = 0; A < NA; ++A) {
-        const uint32_t r = (av >> (4 * A)) & 15;
-        pres |= ((r != 15 && !((rm >> r) & 1)) ? 1u : 0u) << A;
-      }
+      for (int A = 0; A < NA; ++A) pres |= (e_dim<NA>(ev, A) != 15 ? 1u : 0u) << A;
       dying += (long long)exdiv(T, u64of(d.z, d.w), pres);
     }
     // H5 liveness (C12)
@@ -391,7 +436,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
 }
 
 template <int NA>
-__global__ void __launch_bounds__(256) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, TOAST_MIN_BLOCKS) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
   const Smem S = warp_smem(T);
   const int lane = threadIdx.x & 31;
@@ -421,7 +466,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
 }
 
 template <int NA>
-__global__ void __launch_bounds__(256) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, TOAST_MIN_BLOCKS) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
                                                             toast_cost* __restrict__ out) {
@@ -541,6 +586,8 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   T.sig_roles = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_sig_nroles, &p, err))) return st;
   T.sig_nroles = reinterpret_cast<const uint8_t*>(p);
+  if ((st = upload(a, a->h_sig_resdim, &p, err))) return st;
+  T.sig_resdim = reinterpret_cast<const uint32_t*>(p);
   if ((st = upload(a, a->h_desel_cls, &p, err))) return st;
   T.desel = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_actions, &p, err))) return st;
@@ -554,28 +601,41 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  int wpb = 8;
-  while (wpb > 1 && wpb * a->smem_per_warp > dev_smem) wpb >>= 1;
-  if (wpb * a->smem_per_warp > dev_smem) { err = "op-signature tables do not fit in shared memory"; return TOAST_E_LIMIT; }
-  a->warps_per_block = wpb;
-  const int smem = wpb * a->smem_per_warp;
+  const int smem_max_wpb = std::max(1, std::min(32, dev_smem / a->smem_per_warp));
+  if (a->smem_per_warp > dev_smem) { err = "op-signature tables do not fit in shared memory"; return TOAST_E_LIMIT; }
   // the attribute is per function, shared by every analysis in the process: allow the device maximum
   set_smem_attr<1>(dev_smem);
   set_smem_attr<2>(dev_smem);
   set_smem_attr<3>(dev_smem);
   set_smem_attr<4>(dev_smem);
   TOAST_CUDA(cudaGetLastError());
-  int be = 0, br = 0;
-  switch (T.n_axes) {
-    case 1: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<1>, wpb * 32, smem));
-            TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<1>, wpb * 32, smem)); break;
-    case 2: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<2>, wpb * 32, smem));
-            TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<2>, wpb * 32, smem)); break;
-    case 3: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<3>, wpb * 32, smem));
-            TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<3>, wpb * 32, smem)); break;
-    default: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<4>, wpb * 32, smem));
-             TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<4>, wpb * 32, smem)); break;
+  // choose warps per block to maximise resident warps per SM (registers and
+  // shared memory both limit), preferring smaller blocks on ties
+  auto occ = [&](int wpb, int& be, int& br) -> cudaError_t {
+    const int sm = wpb * a->smem_per_warp;
+    cudaError_t e1, e2;
+    switch (T.n_axes) {
+      case 1: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<1>, wpb * 32, sm);
+              e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<1>, wpb * 32, sm); break;
+      case 2: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<2>, wpb * 32, sm);
+              e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<2>, wpb * 32, sm); break;
+      case 3: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<3>, wpb * 32, sm);
+              e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<3>, wpb * 32, sm); break;
+      default: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<4>, wpb * 32, sm);
+               e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<4>, wpb * 32, sm); break;
+    }
+    return e1 != cudaSuccess ? e1 : e2;
+  };
+  int best_wpb = 1, best_warps = -1, be = 0, br = 0;
+  for (int wpb = 1; wpb <= std::min(TOAST_MAX_WPB, smem_max_wpb); ++wpb) {
+    int e = 0, r = 0;
+    TOAST_CUDA(occ(wpb, e, r));
+    const int warps = std::min(e, r) * wpb;
+    if (warps > best_warps) { best_warps = warps; best_wpb = wpb; be = e; br = r; }
   }
+  a->warps_per_block = best_wpb;
+  const int smem = best_wpb * a->smem_per_warp;
+  (void)smem;
   a->eval_blocks = sms * std::max(be, 1);
   a->rollout_blocks = sms * std::max(br, 1);
   return TOAST_OK;

@@ -28,17 +28,7 @@ struct SNode {
   int64_t N = 0;
 };
 
-// per-round exchange record (fixed size, host memory)
-struct ExportRec {
-  double best_score;
-  uint64_t best_key;
-  uint16_t best_seq[32];
-  int64_t evals;          // evaluations done by this rank so far
-  double elapsed_s;       // this rank's wall clock since begin
-  int32_t rank;
-  int32_t pad;
-  toast_cost best;        // full record of the rank's best
-};
+using ExportRec = toast_search_export;   // include/toast.h
 
 }  // namespace toast
 
@@ -133,14 +123,17 @@ toast_status search_begin(const toast_analysis* a, const toast_search_opts* o, i
   s->h_lcost.resize((size_t)L);
   s->h_cost.resize((size_t)L * R);
   s->d_bytes = (size_t)L * 64 + (size_t)L * sizeof(toast_cost) + (size_t)L * R * (64 + 64 + sizeof(toast_cost));
-  cudaError_t e = cudaMalloc(&s->d_buf, s->d_bytes);
-  if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_OOM; }
+  if (a->device >= 0) {
+    cudaError_t e = cudaMalloc(&s->d_buf, s->d_bytes);
+    if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_OOM; }
+  }
   *out = s.release();
   return TOAST_OK;
 }
 
 toast_status search_round(toast_search_state* s, void* export_buf, std::string& err) {
   const toast_analysis* a = s->a;
+  if (!s->d_buf) { err = "search rounds need device tables (the analysis is host-only)"; return TOAST_E_CUDA; }
   const int L = s->o.leaves_per_round, R = s->o.rollouts_per_leaf;
   std::vector<SNode*> leaves;
   for (int l = 0; l < L; ++l) {

@@ -92,47 +92,45 @@ constexpr int MAX_GROUPS = 64;
 
 // ------------------------------------------------------------ device stream
 // The kernels walk the program as one contiguous stream of 16-byte words, in
-// op order: a 32-byte header, then n_uses 32-byte use records (sorted by the
-// used value so repeated operands are adjacent), then n_death 16-byte death
-// records.  Every field a warp needs for one op is in this record, so a
-// warp's reads are warp-uniform (broadcast) and sequential.
+// op order: a 32-byte header, then one 16-byte record per use edge (sorted by
+// the used value so repeated operands are adjacent), then one 16-byte record
+// per value whose last use is this op.  Every field a warp needs for one op is
+// in this record, so a warp's reads are warp-uniform (broadcast) and
+// sequential.  An op's SIGNATURE fixes how it materialises (per role: action
+// color, divisibility, deselection class, result dim), so per candidate the
+// kernel keeps one 32-bit entry per signature: axis->role | axis->result dim.
 struct KHead {           // 32 B
-  uint32_t lb;           // global loop id of role 0 (state key, C14)
-  uint16_t sig;          // op signature (materialisation class)
-  uint8_t rmask;         // reduction roles
+  uint32_t lb;           // global loop id of role 0 (state key, C14 / R14)
+  uint16_t sig;          // op signature
   uint8_t flags;         // bit0 matmul-class, bit1 ret
   uint8_t n_uses;
   uint8_t n_death;
-  uint16_t pad0;
+  uint8_t pad0[3];
   uint32_t pad1;
   uint64_t gbytes;       // result global bytes (0 for ret)
   uint64_t gflops;       // 2 * prod(loop extents) for matmul-class ops, else 0
 };
-struct KUse {            // 32 B
-  uint16_t def_sig;
-  uint8_t def_rmask;
+struct KUse {            // 16 B
+  uint16_t def_sig;      // signature of the defining op
   uint8_t flags;         // bit0 first use of this value at the op, bit1 last
-  uint32_t tr;           // nibble rd: this op's role expected to hold what the def's role rd holds
-                         //   (0xE: rd is not a result dim -> never "nothing to do")
-  uint32_t def_dimof;    // nibble r: result dim of the def op's role r (0xF: none)
-  uint32_t use_dimof;    // nibble r: operand dim of this op's role r (0xF: none)
+  uint8_t pad;
+  uint32_t use_dimof;    // nibble r: operand dim held by this op's role r (0xF: none)
   uint64_t def_gbytes;
-  uint64_t pad;
 };
 struct KDeath {          // 16 B
   uint16_t sig;
-  uint8_t rmask;
-  uint8_t pad0;
+  uint16_t pad0;
   uint32_t pad1;
   uint64_t gbytes;
 };
-static_assert(sizeof(KHead) == 32 && sizeof(KUse) == 32 && sizeof(KDeath) == 16, "stream records");
+static_assert(sizeof(KHead) == 32 && sizeof(KUse) == 16 && sizeof(KDeath) == 16, "stream records");
 
 // signature role word: acolor [0,10) | div_ok [10,26) | deselection class [26,34)
 struct DeviceTables {
   const uint4* stream = nullptr;         // op stream (16-byte words)
   const uint64_t* sig_roles = nullptr;   // [n_sigs][8] role words (acolor 0x3FF = untouchable)
   const uint8_t* sig_nroles = nullptr;   // [n_sigs]
+  const uint32_t* sig_resdim = nullptr;  // [n_sigs] nibble r: result dim of role r (0xF: none)
   const uint64_t* desel = nullptr;       // [class][2] = need0, need1 (class 0 = none)
   const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
   const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids (0xFF = unused)
@@ -178,6 +176,7 @@ struct toast_analysis {
   std::vector<uint32_t> h_stream;           // 16-byte aligned words (as 4 x u32)
   std::vector<uint64_t> h_sig_roles, h_desel_cls;
   std::vector<uint8_t> h_sig_nroles;
+  std::vector<uint32_t> h_sig_resdim;
   std::vector<uint32_t> op_sig;
   std::vector<int32_t> axis_size;
 

@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtoast.so")
+LIB_PATH = os.environ.get("TOAST_LIB") or os.path.join(_HERE, "lib", "libtoast.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libtoast.so not built ({LIB_PATH}); run `python -m paper_2508_15010_b200.build`")
@@ -84,6 +84,7 @@ _sigs = {
     "toast_num_actions": [_P, ctypes.POINTER(ctypes.c_int32)],
     "toast_query_actions": [_P, ctypes.POINTER(_ActionInfo), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
     "toast_query_baseline": [_P, _P],
+    "toast_preferred_batch": [_P, ctypes.POINTER(ctypes.c_int64)],
     "toast_dump_analysis": [_P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
     "toast_eval_batch": [_P, _P, ctypes.c_int64, _P, _P],
     "toast_rollout_batch": [_P, _P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _P, _P, _P],
@@ -204,6 +205,11 @@ class Analysis:
         out = np.zeros(1, dtype=COST_DTYPE)
         _check(_lib.toast_query_baseline(self._h, out.ctypes.data))
         return out[0]
+
+    def preferred_batch(self) -> int:
+        n = ctypes.c_int64()
+        _check(_lib.toast_preferred_batch(self._h, ctypes.byref(n)))
+        return n.value
 
     def dump(self) -> dict:
         need = ctypes.c_size_t()

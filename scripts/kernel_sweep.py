@@ -1,0 +1,72 @@
+"""Build kernel variants (launch bounds / register caps) and time each on the
+GPU: `python scripts/kernel_sweep.py build` here, `... run` on the box."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VAR = os.path.join(ROOT, "paper_2508_15010_b200", "lib", "variants")
+VARIANTS = {
+    "t512b1": ["-DTOAST_MAX_THREADS=512", "-DTOAST_MIN_BLOCKS=1"],
+    "t256b3": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=3", "-DTOAST_MAX_WPB=8"],
+    "t256b4": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=4", "-DTOAST_MAX_WPB=8"],
+    "t128b6": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=6", "-DTOAST_MAX_WPB=4"],
+    "r72": ["-maxrregcount=72"],
+    "r80": ["-maxrregcount=80"],
+    "r96": ["-maxrregcount=96"],
+}
+
+
+def build_all():
+    from paper_2508_15010_b200 import build as b
+    os.makedirs(VAR, exist_ok=True)
+    for tag, fl in VARIANTS.items():
+        b.build(force=True, lib=os.path.join(VAR, f"libtoast_{tag}.so"), obj=os.path.join(ROOT, "paper_2508_15010_b200", "build", tag), extra=fl)
+        print("built", tag, flush=True)
+
+
+def run_all(config="gpt24", n=1 << 18):
+    out = {}
+    for tag in VARIANTS:
+        lib = os.path.join(VAR, f"libtoast_{tag}.so")
+        r = subprocess.run([sys.executable, __file__, "one", lib, config, str(n)], capture_output=True, text=True,
+                           env=dict(os.environ, TOAST_LIB=lib))
+        out[tag] = r.stdout.strip().splitlines()[-1] if r.returncode == 0 else ("ERR " + r.stderr[-300:])
+        print(tag, out[tag], flush=True)
+    return out
+
+
+def one(lib, config, n):
+    import torch
+    from paper_2508_15010_b200 import toast as T
+    from workloads import configs
+    c = configs.get(config)
+    a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0)
+    pre = torch.zeros((n, 32), dtype=torch.int16, device="cuda")
+    seq = torch.empty_like(pre)
+    out = torch.empty((n, 256), dtype=torch.uint8, device="cuda")
+    for w in range(3):
+        T.rollout_batch(a, pre, 1, w * n, seq, out)
+    torch.cuda.synchronize()
+    ts = []
+    for s in range(8):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        T.rollout_batch(a, pre, 1, s * n, seq, out)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    ms = ts[len(ts) // 2]
+    print(json.dumps({"config": config, "n": n, "ms": ms, "evals_per_s": n / ms * 1e3}))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build_all()
+    elif sys.argv[1] == "run":
+        run_all(*(sys.argv[2:3] or ["gpt24"]))
+    else:
+        one(sys.argv[2], sys.argv[3], int(sys.argv[4]))

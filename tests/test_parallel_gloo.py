@@ -1,0 +1,83 @@
+"""The N > 1 path on CPU: world_size-2 gloo process group, the per-round
+all-gather of toast_search_export records and the library's import logic
+(the same code the NCCL ranks run), with the round's records built from
+oracle rollouts of each rank's seed."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_2508_15010_b200 import parallel as P
+        from paper_2508_15010_b200 import toast as T
+        from workloads import configs
+        c = configs.get("gpt2")
+        a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=-1)
+        o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth)
+        opts = T.SearchOptions(seed=10, patience=2, max_evals=10 ** 9)
+        st = T.SearchState(a, opts, rank, world)
+        assert st.export_bytes == P.EXPORT_DTYPE.itemsize
+        out = []
+        for rnd in range(4):
+            # this rank's "round": a batch of rollouts for its own seed; best = min (score, key)
+            seqs, costs = o.rollout(np.zeros((64, 32), np.uint16), seed=opts.seed + rank, id_base=rnd * 64)
+            i = int(np.lexsort((costs["state_key"], costs["score"]))[0])
+            rec = np.zeros(1, dtype=P.EXPORT_DTYPE)
+            rec["best_score"] = costs["score"][i]
+            rec["best_key"] = costs["state_key"][i]
+            rec["best_seq"] = seqs[i]
+            rec["evals"] = 65 * (rnd + 1)
+            rec["elapsed_s"] = 0.1 * rnd
+            rec["rank"] = rank
+            rec["best"] = costs[i]
+            gathered = P.all_gather_bytes(rec.view(np.uint8).reshape(-1))
+            stop = st.import_(gathered)
+            g = gathered.view(P.EXPORT_DTYPE)
+            out.append((stop, float(g["best_score"].min()), int(g["evals"].sum())))
+            if stop:
+                break
+        res = st.end()
+        q.put((rank, out, float(res["best"]["score"]), res["best_seq"].tolist(), int(res["evals"])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_root_parallel_exchange_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, out0, s0, q0, e0), (r1, out1, s1, q1, e1) = res
+    # identical decisions, identical global best, on both ranks
+    assert out0 == out1
+    assert (s0, q0, e0) == (s1, q1, e1)
+    # the global best is the best of both ranks' records; evals are summed
+    assert s0 == min(o[1] for o in out0)
+    assert e0 == out0[-1][2]
+    # patience 2: it stops after two non-improving rounds or runs all 4
+    stops = [o[0] for o in out0]
+    assert stops.count(True) <= 1 and (not any(stops[:-1]))
