@@ -687,6 +687,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
           um = (um & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
         }
         u.use_dimof = um;
+        if (op.result >= 0 && um == resdim_of(t)) u.flags |= 4;   // operand dims == result dims (elementwise)
         u.def_gbytes = a->h_ops[v].gbytes;
         push(&u, sizeof u);
       }

@@ -252,10 +252,16 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
   uint64_t key = 0, flo = 0, fhi = 0;
   long long L = 0, peak = 0;
   const uint4* p = T.stream;
+  uint4 nh0 = __ldg(p), nh1 = __ldg(p + 1);
   for (int t = 0; t < T.n_ops; ++t) {
-    const uint4 h0 = __ldg(p), h1 = __ldg(p + 1);
+    const uint4 h0 = nh0, h1 = nh1;
     const uint32_t lb = h0.x, sig = h0.y & 0xFFFF, flags = (h0.y >> 16) & 0xFF;
     const uint32_t n_uses = h0.y >> 24, n_death = h0.z & 0xFF;
+    {   // prefetch the next op's header (the stream always has a next 32 B after the last op: see upload)
+      const uint4* pn = p + 2 + n_uses + n_death;
+      nh0 = __ldg(pn);
+      nh1 = __ldg(pn + 1);
+    }
     const uint32_t ent = ent_load<NA>(S, sig, lane);
     const uint32_t a2r = e_a2r16<NA>(ent);
     // H7 state key (C14, reading R14): one hash per op with a sharded loop
@@ -282,19 +288,28 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
       if (uflags & 1) { gmax = 0; gq = q; }
       const uint32_t de = ent_load<NA>(S, u.x & 0xFFFF, lane);
       // def layout D (axis -> result dim), partial axes P, use layout U (axis -> operand dim)
-      uint32_t dimU = 0, P = 0;
+      uint32_t dimU = 0;
       bool nothing = true;
+      if (uflags & 4) {   // elementwise use: U is this op's result layout; nothing iff D == U and no partial axis
+        const uint32_t MK = (1u << (4 * NA)) - 1u;
+        dimU = (ent >> (4 * NA)) & MK;
+        nothing = ((de >> (4 * NA)) & MK) == dimU;
 #pragma unroll
-      for (int A = 0; A < NA; ++A) {
-        const uint32_t ru = (a2r >> (4 * A)) & 15;
-        const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
-        const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
-        dimU |= du << (4 * A);
-        const bool pa = rd != 15 && dd == 15;
-        P |= (pa ? 1u : 0u) << A;
-        nothing &= !pa && (dd == 15 || dd == du);
+        for (int A = 0; A < NA; ++A) nothing &= !(e_role<NA>(de, A) != 15 && e_dim<NA>(de, A) == 15);
+      } else {
+#pragma unroll
+        for (int A = 0; A < NA; ++A) {
+          const uint32_t ru = (a2r >> (4 * A)) & 15;
+          const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
+          const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+          dimU |= du << (4 * A);
+          nothing &= !(rd != 15 && dd == 15) && (dd == 15 || dd == du);
+        }
       }
       if (!nothing) {   // a collective (not just a free local slice) is needed
+        uint32_t P = 0;
+#pragma unroll
+        for (int A = 0; A < NA; ++A) P |= ((e_role<NA>(de, A) != 15 && e_dim<NA>(de, A) == 15) ? 1u : 0u) << A;
         const uint32_t dimD = (de >> (4 * NA)) & ((1u << (4 * NA)) - 1u);
         bool dup = false;
         for (const uint4* q2 = gq; q2 < q; ++q2) {   // the same value again at this op: once per layout
@@ -580,6 +595,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   DeviceTables& T = a->dt;
   toast_status st;
   const void* p;
+  a->h_stream.resize(a->h_stream.size() + 8, 0u);   // 32 B tail: the kernels prefetch one header past the end
   if ((st = upload(a, a->h_stream, &p, err))) return st;
   T.stream = reinterpret_cast<const uint4*>(p);
   if ((st = upload(a, a->h_sig_roles, &p, err))) return st;

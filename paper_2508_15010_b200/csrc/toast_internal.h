@@ -112,7 +112,7 @@ struct KHead {           // 32 B
 };
 struct KUse {            // 16 B
   uint16_t def_sig;      // signature of the defining op
-  uint8_t flags;         // bit0 first use of this value at the op, bit1 last
+  uint8_t flags;         // bit0 first use of this value at the op, bit1 last, bit2 operand dims == result dims
   uint8_t pad;
   uint32_t use_dimof;    // nibble r: operand dim held by this op's role r (0xF: none)
   uint64_t def_gbytes;
