@@ -1611,16 +1611,19 @@ int orc_search(void* h, uint64_t seed, int64_t max_evals, double time_limit_s, i
     rollouts_done += (i64)L * R;
     for (Node* lf : leaves) for (Node* x = lf; x; x = x->parent) { x->N -= 1; x->W += 1.0; }
     bool improved = false;
-    auto consider = [&](const Cost& c, const u16* s, Node* leaf) {
-      double reward = -c.score;
-      for (Node* x = leaf; x; x = x->parent) { x->N += 1; x->W += reward; }
+    auto consider = [&](const Cost& c, const u16* s) {
       if (c.status == 0 && (!have || Oracle::better(c, s, best, best_seq))) {
         best = c; memcpy(best_seq, s, 32 * sizeof(u16)); have = true; improved = true;
       }
     };
+    // backup (reading R16): a leaf's R+1 rewards are summed in order (its own
+    // state first, then rollouts 0..R-1), then added once to every node on its path
     for (int l = 0; l < L; l++) {
-      consider(lcost[l], &lpre[(size_t)l * 32], leaves[l]);
-      for (int j = 0; j < R; j++) consider(costs[(size_t)l * R + j], &outs[((size_t)l * R + j) * 32], leaves[l]);
+      double sum = -lcost[l].score;
+      for (int j = 0; j < R; j++) sum = sum + (-costs[(size_t)l * R + j].score);
+      for (Node* x = leaves[l]; x; x = x->parent) { x->N += R + 1; x->W += sum; }
+      consider(lcost[l], &lpre[(size_t)l * 32]);
+      for (int j = 0; j < R; j++) consider(costs[(size_t)l * R + j], &outs[((size_t)l * R + j) * 32]);
     }
     evals += (i64)L * (R + 1);
     if (trace && rounds < trace_cap) trace[rounds] = best.score;

@@ -122,7 +122,8 @@ toast_status toast_query_baseline(const toast_analysis* a, toast_cost* out) {
 toast_status toast_preferred_batch(const toast_analysis* a, int64_t* n) {
   if (!a || !n) return fail(TOAST_E_INVALID_ARG, "NULL argument");
   if (!has_device(a)) return fail(TOAST_E_CUDA, "the analysis has no device tables");
-  *n = (int64_t)std::min(a->eval_blocks, a->rollout_blocks) * a->warps_per_block * 32;
+  const int i = a->k_throughput >= 8 ? 3 : a->k_throughput >= 4 ? 2 : a->k_throughput >= 2 ? 1 : 0;
+  *n = (int64_t)std::min(a->occ_eval[i], a->occ_roll[i]) * a->n_sms * 32;
   return ret(TOAST_OK, "");
 }
 
@@ -158,7 +159,7 @@ toast_status toast_rollout_batch(const toast_analysis* a, const uint16_t* prefix
   cudaSetDevice(a->device);
   bool d1 = toast::is_device_pointer(prefixes), d2 = toast::is_device_pointer(out_seqs), d3 = toast::is_device_pointer(out);
   if (d1 != d2 || d1 != d3) return fail(TOAST_E_INVALID_ARG, "buffers must all be host or all be device memory");
-  toast_status st = d1 ? toast::launch_rollout(a, prefixes, n, seed, id_base, out_seqs, out, cuda_stream, err)
+  toast_status st = d1 ? toast::launch_rollout(a, prefixes, n, seed, id_base, out_seqs, out, cuda_stream, err, 1)
                        : toast::run_host_buffers(const_cast<toast_analysis*>(a), true, prefixes, n, seed, id_base,
                                                  out_seqs, out, cuda_stream, err);
   return ret(st, err);

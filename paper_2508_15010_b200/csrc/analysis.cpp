@@ -698,6 +698,26 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         push(&d, sizeof d);
       }
     }
+    // op segments (balanced by stream words) for K = 1, 2, 4, 8 sweeping warps
+    {
+      std::vector<uint32_t> off(n_ops + 1, 0);
+      size_t w = 0;
+      for (int32_t t = 0; t < n_ops; ++t) {
+        off[t] = (uint32_t)w;
+        w += 2 + g->ops[t].operands.size() + deaths[t].size();
+      }
+      off[n_ops] = (uint32_t)w;
+      for (int K = 1, lg = 0; K <= 8; K *= 2, ++lg) {
+        const int b = K - 1 + lg;
+        int t = 0;
+        for (int q = 0; q <= K; ++q) {
+          const double target = (double)w * q / K;
+          while (t < n_ops && (double)off[t] < target) ++t;
+          a->dt.seg_op[b + q] = q == K ? n_ops : t;
+          a->dt.seg_off[b + q] = off[a->dt.seg_op[b + q]];
+        }
+      }
+    }
     if (getenv("TOAST_DEBUG"))
       fprintf(stderr, "[toast] ops %d loops %lld signatures %zu stream %zu B actions %zu desel classes %zu\n", n_ops,
               (long long)NL, sig_words.size(), a->h_stream.size() * 4, a->actions.size(), a->h_desel_cls.size() / 2);

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -51,42 +52,53 @@ constexpr unsigned FULL = 0xffffffffu;
 // region B (per-color event lists during decode/materialise, then the
 // payload/count accumulators during the sweep)
 __host__ __device__ inline int sig_entry_bytes(int n_axes) { return n_axes <= 2 ? 2 : 4; }
+__host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
+// Block shared memory for one batch of 32 candidates swept by K warps:
+//   C  per lane: decode status and the fixed SetGroup bits (read by all warps)
+//   A  the per-lane signature table [n_sigs][32], overlaid with the staged
+//      sequence [16][32] and the rollout legal set [n_words][32] (dead once
+//      the table is written)
+//   B  the per-color event lists [n_acolors][32] (decode/materialise), then,
+//      per warp, the payload/count accumulators and the segment results
+__host__ __device__ inline int smem_c_bytes() { return 32 * (8 + 8 + 4); }
 __host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes) {
   int a1 = n_sigs * 32 * sig_entry_bytes(n_axes), a2 = 2048 + n_words * 128;
-  return ((a1 > a2 ? a1 : a2) + 15) & ~15;
+  return r16(a1 > a2 ? a1 : a2);
 }
-__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes) {
-  int b1 = n_ac * 128, b2 = n_axes * 4 * (256 + 128);
-  return ((b1 > b2 ? b1 : b2) + 15) & ~15;
+__host__ __device__ inline int smem_acc_bytes(int n_axes) { return n_axes * 4 * 32 * (8 + 4) + 32 * 5 * 8; }
+__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
+  int b1 = n_ac * 128, b2 = K * smem_acc_bytes(n_axes);
+  return r16(b1 > b2 ? b1 : b2);
 }
-__host__ __device__ inline int smem_warp_bytes(int n_sigs, int n_ac, int n_words, int n_axes) {
-  return smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes);
+__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K) {
+  return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K);
 }
 
 struct Smem {
-  void* sig;                // [n_sigs][32]  per signature: axis->role | axis->result dim (4 bits per axis each);
-                            //               u16 entries for <= 2 axes, u32 otherwise
+  void* sig;                // [n_sigs][32] per signature: axis->role | axis->result dim (4 bits per axis each)
   uint32_t* acol;           // [n_acolors][32] up to 4 events (valid | axis << 5 | position) per action color
-  uint32_t* seq;            // [16][32] the candidate's 32 ids as 16 words
+  uint32_t* seq;            // [16][32] the candidates' 32 ids as 16 words
   uint32_t* legal;          // [n_words][32] rollout legal bitset
-  unsigned long long* pay;  // [n_axes*4][32] payload bytes per (axis, kind)   (overlays acol/seq/legal)
-  uint32_t* cnt;            // [n_axes*4][32] collective counts
+  unsigned long long* f0;   // [32] SetGroups fixed to 0
+  unsigned long long* on;   // [32] SetGroups fixed to 1
+  uint32_t* status;         // [32]
+  unsigned char* acc;       // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
 };
 
-__device__ __forceinline__ Smem warp_smem(const DeviceTables& T) {
+__device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5;
-  const int sa = smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
-  const int per = sa + smem_b_bytes(T.n_acolors, T.n_axes);
-  unsigned char* base = smem + (size_t)warp * per;
   Smem s;
-  s.sig = base;
-  s.seq = reinterpret_cast<uint32_t*>(base);
-  s.legal = reinterpret_cast<uint32_t*>(base + 2048);
-  unsigned char* b = base + sa;
+  s.f0 = reinterpret_cast<unsigned long long*>(smem);
+  s.on = s.f0 + 32;
+  s.status = reinterpret_cast<uint32_t*>(smem + 512);
+  unsigned char* a = smem + smem_c_bytes();
+  s.sig = a;
+  s.seq = reinterpret_cast<uint32_t*>(a);
+  s.legal = reinterpret_cast<uint32_t*>(a + 2048);
+  unsigned char* b = a + smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
   s.acol = reinterpret_cast<uint32_t*>(b);
-  s.pay = reinterpret_cast<unsigned long long*>(b);
-  s.cnt = reinterpret_cast<uint32_t*>(b + T.n_axes * 4 * 256);
+  s.acc = b;
+  (void)K;
   return s;
 }
 
@@ -236,24 +248,42 @@ __device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
   return (full & m) | (((full >> 16) & m) << (4 * NA));
 }
 
-// ---------------------------------------------------------------- the per-lane evaluation
-// S.seq holds the lane's candidate; `valid` lanes write `out`.  NA = number
-// of mesh axes (compile-time so the per-axis loops are fully unrolled).
+// ---------------------------------------------------------------- one batch of 32 candidates
+// The K warps of the block share the batch: warp 0 decodes, all warps
+// materialise a share of the signatures, warp w sweeps op segment w (its own
+// payload accumulators and relative liveness), and warp 0 combines the
+// segments (peak = max_w (L before segment w + segment w's relative peak)),
+// scores and writes the records.  S.seq holds the candidates on entry.
 template <int NA>
-__device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, int lane, bool valid,
-                                          toast_cost* __restrict__ out) {
-  uint64_t fixed0, ones;
-  const uint32_t status = decode(T, S, lane, fixed0, ones);
-  for (int s = 0; s < T.n_sigs; ++s) ent_store<NA>(S, s, lane, pack_entry<NA>(materialize_sig(T, S, lane, s, fixed0, ones)));
-  __syncwarp();
+__device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
+                                           toast_cost* __restrict__ out) {
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t f0, on;
+    S.status[lane] = decode(T, S, lane, f0, on);
+    S.f0[lane] = f0;
+    S.on[lane] = on;
+  }
+  __syncthreads();
+  {
+    const uint64_t f0 = S.f0[lane], on = S.on[lane];
+    for (int s = warp; s < T.n_sigs; s += K) ent_store<NA>(S, s, lane, pack_entry<NA>(materialize_sig(T, S, lane, s, f0, on)));
+  }
+  __syncthreads();
+  const int sb = K - 1 + (K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0);   // segment table base for this K
+  unsigned char* acc = S.acc + (size_t)warp * smem_acc_bytes(NA);
+  unsigned long long* pay = reinterpret_cast<unsigned long long*>(acc);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(acc + NA * 4 * 32 * 8);
+  unsigned long long* seg = reinterpret_cast<unsigned long long*>(acc + NA * 4 * 32 * 12);
 #pragma unroll
-  for (int q = 0; q < NA * 4; ++q) { S.pay[q * 32 + lane] = 0ULL; S.cnt[q * 32 + lane] = 0u; }
+  for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = 0ULL; cnt[q * 32 + lane] = 0u; }
 
   uint64_t key = 0, flo = 0, fhi = 0;
-  long long L = 0, peak = 0;
-  const uint4* p = T.stream;
+  long long L = 0, peak = LLONG_MIN;   // relative to the segment start (combined across segments below)
+  const uint4* p = T.stream + T.seg_off[sb + warp];
   uint4 nh0 = __ldg(p), nh1 = __ldg(p + 1);
-  for (int t = 0; t < T.n_ops; ++t) {
+  const int t_end = T.seg_op[sb + warp + 1];
+  for (int t = T.seg_op[sb + warp]; t < t_end; ++t) {
     const uint4 h0 = nh0, h1 = nh1;
     const uint32_t lb = h0.x, sig = h0.y & 0xFFFF, flags = (h0.y >> 16) & 0xFF;
     const uint32_t n_uses = h0.y >> 24, n_death = h0.z & 0xFF;
@@ -336,11 +366,11 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
             const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
             if (dd == 15 || dd == du) continue;
             if (du != 15) {
-              S.pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
-              S.cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
+              pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
+              cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
             } else {
-              S.pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
-              S.cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
+              pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
+              cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
               size *= (uint64_t)T.sizes[A];
             }
           }
@@ -349,11 +379,11 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
             if (!((P >> A) & 1)) continue;
             if (((dimU >> (4 * A)) & 15) != 15) {
               size = exdiv(T, size, 1u << A);
-              S.pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
-              S.cnt[(A * 4 + TOAST_RS) * 32 + lane] += 1u;
+              pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
+              cnt[(A * 4 + TOAST_RS) * 32 + lane] += 1u;
             } else {
-              S.pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
-              S.cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
+              pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
+              cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
             }
           }
           const long long grow = (long long)exdiv(T, dgb, presU) - (long long)exdiv(T, dgb, presD);
@@ -378,60 +408,87 @@ __device__ __forceinline__ void eval_lane(const DeviceTables& T, const Smem& S, 
     L = L + res - dying;
     p = q;
   }
-  // H6 score (C13): fixed order, explicit round-to-nearest, no FMA
-  double tt = __ddiv_rn(__dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo)), T.F);
-  unsigned long long ncoll = 0;
-  unsigned long long pw[16];
-  uint32_t cw[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) cw[k] = 0;
-#pragma unroll
-  for (int A = 0; A < 4; ++A) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      pw[A * 4 + k] = 0;
-      if (A < NA) {
-        pw[A * 4 + k] = S.pay[(A * 4 + k) * 32 + lane];
-        const uint32_t cq = S.cnt[(A * 4 + k) * 32 + lane];
-        ncoll += cq;
-        cw[(A * 4 + k) >> 1] |= (cq > 65535u ? 65535u : cq) << (16 * (k & 1));
+  seg[0 * 32 + lane] = key;
+  seg[1 * 32 + lane] = flo;
+  seg[2 * 32 + lane] = fhi;
+  seg[3 * 32 + lane] = (unsigned long long)L;
+  seg[4 * 32 + lane] = (unsigned long long)peak;
+  __syncthreads();
+  if (warp == 0) {
+    // combine the K segments: sums into warp 0's slots, peak by the segment scan
+    key = 0; flo = 0; fhi = 0;
+    long long Lrun = 0, pk_all = 0;
+    for (int w = 0; w < K; ++w) {
+      const unsigned char* aw = S.acc + (size_t)w * smem_acc_bytes(NA);
+      const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(aw + NA * 4 * 32 * 12);
+      key += sw[0 * 32 + lane];
+      const uint64_t f = sw[1 * 32 + lane];
+      flo += f;
+      fhi += sw[2 * 32 + lane] + ((flo < f) ? 1 : 0);
+      const long long segpk = (long long)sw[4 * 32 + lane];
+      if (segpk != LLONG_MIN && Lrun + segpk > pk_all) pk_all = Lrun + segpk;
+      Lrun += (long long)sw[3 * 32 + lane];
+      if (w) {
+        const unsigned long long* pww = reinterpret_cast<const unsigned long long*>(aw);
+        const uint32_t* cww = reinterpret_cast<const uint32_t*>(aw + NA * 4 * 32 * 8);
+        for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] += pww[q * 32 + lane]; cnt[q * 32 + lane] += cww[q * 32 + lane]; }
       }
     }
-    if (A < NA) {
+    const uint32_t status = S.status[lane];
+    // H6 score (C13): fixed order, explicit round-to-nearest, no FMA
+    double tt = __ddiv_rn(__dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo)), T.F);
+    unsigned long long ncoll = 0;
+#pragma unroll
+    for (int A = 0; A < NA; ++A) {
       const double n = (double)T.sizes[A];
-      const double ag = __ull2double_rn(pw[A * 4 + 0]), rs = __ull2double_rn(pw[A * 4 + 1]);
-      const double ar = __ull2double_rn(pw[A * 4 + 2]), a2a = __ull2double_rn(pw[A * 4 + 3]);
+      const double ag = __ull2double_rn(pay[(A * 4 + 0) * 32 + lane]), rs = __ull2double_rn(pay[(A * 4 + 1) * 32 + lane]);
+      const double ar = __ull2double_rn(pay[(A * 4 + 2) * 32 + lane]), a2a = __ull2double_rn(pay[(A * 4 + 3) * 32 + lane]);
       const double n1 = __dsub_rn(n, 1.0);
       const double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
       const double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
       tt = __dadd_rn(tt, __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]));
-    }
-  }
-  const uint64_t pk = (uint64_t)peak;
-  const double RT = __ddiv_rn(tt, T.t0);
-  const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
-  if (valid) {
-    // record layout = toast_cost (include/toast.h), written as 16 x 16 B
-    uint4* dst = reinterpret_cast<uint4*>(out);
-    const bool ok = status == 0;
-    auto d2 = [](double x) { return (unsigned long long)__double_as_longlong(x); };
-    const unsigned long long w0 = ok ? d2(tt) : 0ULL, w1 = ok ? d2(__dadd_rn(RT, MP)) : 0ULL;
-    const unsigned long long w2 = ok ? pk : 0ULL, w3 = ok ? flo : 0ULL, w4 = ok ? key : 0ULL;
-    const unsigned long long w5 = ok ? ((unsigned long long)(uint32_t)ncoll << 32) : (unsigned long long)status;
-    dst[0] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
-    dst[1] = make_uint4((uint32_t)w2, (uint32_t)(w2 >> 32), (uint32_t)w3, (uint32_t)(w3 >> 32));
-    dst[2] = make_uint4((uint32_t)w4, (uint32_t)(w4 >> 32), (uint32_t)w5, (uint32_t)(w5 >> 32));
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const unsigned long long a = ok ? pw[2 * k] : 0ULL, b = ok ? pw[2 * k + 1] : 0ULL;
-      dst[3 + k] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+      for (int k = 0; k < 4; ++k) ncoll += cnt[(A * 4 + k) * 32 + lane];
     }
-    dst[11] = ok ? make_uint4(cw[0], cw[1], cw[2], cw[3]) : make_uint4(0, 0, 0, 0);
-    dst[12] = ok ? make_uint4(cw[4], cw[5], cw[6], cw[7]) : make_uint4(0, 0, 0, 0);
-    dst[13] = ok ? make_uint4((uint32_t)fhi, (uint32_t)(fhi >> 32), 0, 0) : make_uint4(0, 0, 0, 0);
-    dst[14] = make_uint4(0, 0, 0, 0);
-    dst[15] = make_uint4(0, 0, 0, 0);
+    const uint64_t pk = (uint64_t)pk_all;
+    const double RT = __ddiv_rn(tt, T.t0);
+    const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
+    if (valid) {
+      // record layout = toast_cost (include/toast.h), written as 16 x 16 B
+      uint4* dst = reinterpret_cast<uint4*>(out);
+      const bool ok = status == 0;
+      auto d2 = [](double x) { return (unsigned long long)__double_as_longlong(x); };
+      const unsigned long long w0 = ok ? d2(tt) : 0ULL, w1 = ok ? d2(__dadd_rn(RT, MP)) : 0ULL;
+      const unsigned long long w2 = ok ? pk : 0ULL, w3 = ok ? flo : 0ULL, w4 = ok ? key : 0ULL;
+      const unsigned long long w5 = ok ? ((unsigned long long)(uint32_t)ncoll << 32) : (unsigned long long)status;
+      dst[0] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+      dst[1] = make_uint4((uint32_t)w2, (uint32_t)(w2 >> 32), (uint32_t)w3, (uint32_t)(w3 >> 32));
+      dst[2] = make_uint4((uint32_t)w4, (uint32_t)(w4 >> 32), (uint32_t)w5, (uint32_t)(w5 >> 32));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        unsigned long long a = 0ULL, b = 0ULL;
+        if (ok && 2 * k < NA * 4) { a = pay[(2 * k) * 32 + lane]; b = pay[(2 * k + 1) * 32 + lane]; }
+        dst[3 + k] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+      }
+      uint32_t cw[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t lo = 0, hi = 0;
+        if (2 * k < NA * 4) {
+          const uint32_t c0 = cnt[(2 * k) * 32 + lane], c1 = cnt[(2 * k + 1) * 32 + lane];
+          lo = c0 > 65535u ? 65535u : c0;
+          hi = c1 > 65535u ? 65535u : c1;
+        }
+        cw[k] = ok ? (lo | (hi << 16)) : 0u;
+      }
+      dst[11] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+      dst[12] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
+      dst[13] = ok ? make_uint4((uint32_t)fhi, (uint32_t)(fhi >> 32), 0, 0) : make_uint4(0, 0, 0, 0);
+      dst[14] = make_uint4(0, 0, 0, 0);
+      dst[15] = make_uint4(0, 0, 0, 0);
+    }
   }
+  __syncthreads();
 }
 
 __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restrict__ g, int lane, bool valid) {
@@ -451,17 +508,16 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
 }
 
 template <int NA>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, TOAST_MIN_BLOCKS) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
-  const Smem S = warp_smem(T);
-  const int lane = threadIdx.x & 31;
+  const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Smem S = block_smem(T, K);
   const int64_t nbatch = (n + 31) / 32;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nbatch; b += warps) {
+  for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
     const int64_t i = b * 32 + lane;
     const bool valid = i < n;
-    load_seq(S, seqs + i * 32, lane, valid);
-    eval_lane<NA>(T, S, lane, valid, out + i);
+    if (warp == 0) load_seq(S, seqs + i * 32, lane, valid);
+    batch_eval<NA>(T, S, K, warp, lane, valid, out + i);
   }
 }
 
@@ -481,20 +537,20 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
 }
 
 template <int NA>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, TOAST_MIN_BLOCKS) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
-                                                            toast_cost* __restrict__ out) {
-  const Smem S = warp_smem(T);
-  const int lane = threadIdx.x & 31;
+                                                            toast_cost* __restrict__ out, int64_t rep) {
+  const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Smem S = block_smem(T, K);
   const int64_t nbatch = (n + 31) / 32;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t seed_lo = (uint32_t)seed, seed_hi = (uint32_t)(seed >> 32);
   const int nw = T.n_words;
-  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nbatch; b += warps) {
+  for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
     const int64_t i = b * 32 + lane;
     const bool valid = i < n;
-    load_seq(S, pre + i * 32, lane, valid);
+    if (warp == 0) {
+    load_seq(S, pre + (i / rep) * 32, lane, valid);
     // validate the prefix: ids < n_actions before the first 0, zeros after it
     int stop = 32;
     bool bad = false;
@@ -548,7 +604,44 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, TOAST_MIN_BLOCKS) toast_rol
         dst[k] = make_uint4(S.seq[(4 * k) * 32 + lane], S.seq[(4 * k + 1) * 32 + lane], S.seq[(4 * k + 2) * 32 + lane],
                             S.seq[(4 * k + 3) * 32 + lane]);
     }
-    eval_lane<NA>(T, S, lane, valid, out + i);
+    }   // warp 0
+    batch_eval<NA>(T, S, K, warp, lane, valid, out + i);
+  }
+}
+
+// ---------------------------------------------------------------- K3: per-leaf round reduction (search)
+// For leaf l: the sum of its R+1 rewards (-score) in order — its own state,
+// then rollouts 0..R-1 (reading R16, bit-identical to the oracle's backup) —
+// and its best candidate by (score, key, sequence), copied out with its sequence.
+__device__ __forceinline__ bool better_dev(const toast_cost& x, const uint16_t* sx, const toast_cost& y, const uint16_t* sy) {
+  if (x.score != y.score) return x.score < y.score;
+  if (x.state_key != y.state_key) return x.state_key < y.state_key;
+  for (int i = 0; i < 32; ++i)
+    if (sx[i] != sy[i]) return sx[i] < sy[i];
+  return false;
+}
+
+__global__ void toast_round_reduce_kernel(const toast_cost* __restrict__ lcost, const uint16_t* __restrict__ lpre,
+                                          const toast_cost* __restrict__ cost, const uint16_t* __restrict__ seqs,
+                                          int L, int R, LeafRed* __restrict__ out) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const toast_cost* bc = nullptr;
+  const uint16_t* bs = nullptr;
+  int best = -2;
+  double sum = -lcost[l].score;
+  if (lcost[l].status == 0) { bc = lcost + l; bs = lpre + (size_t)l * 32; best = -1; }
+  for (int j = 0; j < R; ++j) {
+    const toast_cost* c = cost + (size_t)l * R + j;
+    const uint16_t* q = seqs + ((size_t)l * R + j) * 32;
+    sum = __dadd_rn(sum, -c->score);
+    if (c->status == 0 && (!bc || better_dev(*c, q, *bc, bs))) { bc = c; bs = q; best = j; }
+  }
+  out[l].reward_sum = sum;
+  out[l].best = best;
+  if (bc) {
+    out[l].cost = *bc;
+    for (int i = 0; i < 32; ++i) out[l].seq[i] = bs[i];
   }
 }
 
@@ -613,47 +706,52 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   if ((st = upload(a, a->h_kill, &p, err))) return st;
   T.kill = reinterpret_cast<const uint32_t*>(p);
 
-  a->smem_per_warp = smem_warp_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes);
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  const int smem_max_wpb = std::max(1, std::min(32, dev_smem / a->smem_per_warp));
-  if (a->smem_per_warp > dev_smem) { err = "op-signature tables do not fit in shared memory"; return TOAST_E_LIMIT; }
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1) > dev_smem) {
+    err = "op-signature tables do not fit in shared memory";
+    return TOAST_E_LIMIT;
+  }
   // the attribute is per function, shared by every analysis in the process: allow the device maximum
   set_smem_attr<1>(dev_smem);
   set_smem_attr<2>(dev_smem);
   set_smem_attr<3>(dev_smem);
   set_smem_attr<4>(dev_smem);
   TOAST_CUDA(cudaGetLastError());
-  // choose warps per block to maximise resident warps per SM (registers and
-  // shared memory both limit), preferring smaller blocks on ties
-  auto occ = [&](int wpb, int& be, int& br) -> cudaError_t {
-    const int sm = wpb * a->smem_per_warp;
-    cudaError_t e1, e2;
-    switch (T.n_axes) {
-      case 1: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<1>, wpb * 32, sm);
-              e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<1>, wpb * 32, sm); break;
-      case 2: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<2>, wpb * 32, sm);
-              e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<2>, wpb * 32, sm); break;
-      case 3: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<3>, wpb * 32, sm);
-              e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<3>, wpb * 32, sm); break;
-      default: e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<4>, wpb * 32, sm);
-               e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<4>, wpb * 32, sm); break;
+  a->n_sms = sms;
+  for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K);
+    int be = 0, br = 0;
+    if (sm <= dev_smem) {
+      switch (T.n_axes) {
+        case 1: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<1>, 32 * K, sm));
+                TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<1>, 32 * K, sm)); break;
+        case 2: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<2>, 32 * K, sm));
+                TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<2>, 32 * K, sm)); break;
+        case 3: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<3>, 32 * K, sm));
+                TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<3>, 32 * K, sm)); break;
+        default: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<4>, 32 * K, sm));
+                 TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<4>, 32 * K, sm)); break;
+      }
     }
-    return e1 != cudaSuccess ? e1 : e2;
-  };
-  int best_wpb = 1, best_warps = -1, be = 0, br = 0;
-  for (int wpb = 1; wpb <= std::min(TOAST_MAX_WPB, smem_max_wpb); ++wpb) {
-    int e = 0, r = 0;
-    TOAST_CUDA(occ(wpb, e, r));
-    const int warps = std::min(e, r) * wpb;
-    if (warps > best_warps) { best_warps = warps; best_wpb = wpb; be = e; br = r; }
+    a->occ_eval[i] = be;
+    a->occ_roll[i] = br;
   }
-  a->warps_per_block = best_wpb;
-  const int smem = best_wpb * a->smem_per_warp;
-  (void)smem;
-  a->eval_blocks = sms * std::max(be, 1);
-  a->rollout_blocks = sms * std::max(br, 1);
+  if (a->occ_eval[0] < 1 || a->occ_roll[0] < 1) { err = "kernels cannot be resident"; return TOAST_E_LIMIT; }
+  // throughput K: the most resident warps per SM (sharing one signature table
+  // between K warps saves shared memory), ties to the smaller K
+  const char* fk = getenv("TOAST_FORCE_K");
+  int best_k = 1, best_w = 0;
+  for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
+    const int w = std::min(a->occ_eval[i], a->occ_roll[i]) * K;
+    // a larger K costs block barriers and segment imbalance: it must buy >= 25% more warps
+    if (4 * w > 5 * best_w && T.n_ops >= 64 * K) { best_w = w; best_k = K; }
+  }
+  a->k_throughput = fk ? std::max(1, std::min(8, atoi(fk))) : best_k;
+  a->warps_per_block = 1;
+  a->eval_blocks = sms * a->occ_eval[0];
+  a->rollout_blocks = sms * a->occ_roll[0];
   return TOAST_OK;
 }
 
@@ -666,17 +764,27 @@ void free_tables(toast_analysis* a) {
   a->scratch_bytes = 0;
 }
 
-static inline int64_t grid_for(const toast_analysis* a, int64_t n, int resident) {
-  const int64_t batches = (n + 31) / 32;
-  return std::max<int64_t>(1, std::min<int64_t>((batches + a->warps_per_block - 1) / a->warps_per_block, resident));
+// K (warps sweeping one batch): big batches keep K = 1 (throughput); a batch
+// count below one wave spreads each batch over more warps (latency)
+static inline int pick_k(const toast_analysis* a, int64_t batches, const int32_t* occ) {
+  const char* fk = getenv("TOAST_FORCE_K");
+  int K = a->k_throughput;
+  if (!fk && batches < (int64_t)occ[0] * a->n_sms) {
+    for (int i = 3; i >= 1; --i)
+      if (occ[i] > 0 && batches <= (int64_t)occ[i] * a->n_sms && a->dt.n_ops >= 64 * (1 << i)) { K = 1 << i; break; }
+  }
+  return K;
 }
+static inline int kidx(int K) { return K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0; }
 
 toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, toast_cost* d_out, void* stream,
                          std::string& err) {
   if (n <= 0) return TOAST_OK;
-  const int64_t blocks = grid_for(a, n, a->eval_blocks);
-  const dim3 g((unsigned)blocks), b(a->warps_per_block * 32);
-  const size_t sm = (size_t)a->warps_per_block * a->smem_per_warp;
+  const int64_t batches = (n + 31) / 32;
+  const int K = pick_k(a, batches, a->occ_eval);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
+  const dim3 g((unsigned)blocks), b(32 * K);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K);
   cudaStream_t st = (cudaStream_t)stream;
   switch (a->dt.n_axes) {
     case 1: toast_eval_kernel<1><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
@@ -689,21 +797,33 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
 }
 
 toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
-                            uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err) {
+                            uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err, int64_t rep) {
   if (n <= 0) return TOAST_OK;
-  const int64_t blocks = grid_for(a, n, a->rollout_blocks);
-  const dim3 g((unsigned)blocks), b(a->warps_per_block * 32);
-  const size_t sm = (size_t)a->warps_per_block * a->smem_per_warp;
+  const int64_t batches = (n + 31) / 32;
+  const int K = pick_k(a, batches, a->occ_roll);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
+  const dim3 g((unsigned)blocks), b(32 * K);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K);
   cudaStream_t st = (cudaStream_t)stream;
   switch (a->dt.n_axes) {
-    case 1: toast_rollout_kernel<1><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
-    case 2: toast_rollout_kernel<2><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
-    case 3: toast_rollout_kernel<3><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
-    default: toast_rollout_kernel<4><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out); break;
+    case 1: toast_rollout_kernel<1><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
+    case 2: toast_rollout_kernel<2><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
+    case 3: toast_rollout_kernel<3><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
+    default: toast_rollout_kernel<4><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
   }
   TOAST_CUDA(cudaGetLastError());
   return TOAST_OK;
 }
+
+toast_status launch_round_reduce(const toast_cost* d_lcost, const uint16_t* d_lpre, const toast_cost* d_cost,
+                                 const uint16_t* d_seqs, int L, int R, void* d_out, void* stream, std::string& err) {
+  if (L <= 0) return TOAST_OK;
+  toast_round_reduce_kernel<<<(L + 63) / 64, 64, 0, (cudaStream_t)stream>>>(d_lcost, d_lpre, d_cost, d_seqs, L, R,
+                                                                            reinterpret_cast<LeafRed*>(d_out));
+  TOAST_CUDA(cudaGetLastError());
+  return TOAST_OK;
+}
+size_t leaf_red_bytes() { return sizeof(LeafRed); }
 
 // host-pointer path: stage through device scratch on `stream`, then wait
 toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h_in, int64_t n, uint64_t seed,
@@ -724,7 +844,7 @@ toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h
   uint16_t* d_in = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(a->scratch) + out_b);
   uint16_t* d_seqs = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(a->scratch) + out_b + in_b);
   TOAST_CUDA(cudaMemcpyAsync(d_in, h_in, in_b, cudaMemcpyHostToDevice, s));
-  toast_status st = rollout ? launch_rollout(a, d_in, n, seed, id_base, d_seqs, d_out, stream, err)
+  toast_status st = rollout ? launch_rollout(a, d_in, n, seed, id_base, d_seqs, d_out, stream, err, 1)
                             : launch_eval(a, d_in, n, d_out, stream, err);
   if (st) return st;
   TOAST_CUDA(cudaMemcpyAsync(h_out, d_out, out_b, cudaMemcpyDeviceToHost, s));

@@ -49,9 +49,9 @@ struct toast_search_state {
   int32_t rounds = 0, nonimprove = 0, hit_target = 0, done = 0;
   double time_to_target = -1.0;
   std::chrono::steady_clock::time_point t_start;
-  // buffers
-  std::vector<uint16_t> h_lpre, h_pre, h_outs;
-  std::vector<toast_cost> h_lcost, h_cost;
+  // buffers: pinned host (prefixes in, per-leaf reductions out) and device scratch
+  uint16_t* h_lpre = nullptr;
+  toast::LeafRed* h_red = nullptr;
   void* d_buf = nullptr;
   size_t d_bytes = 0;
   ~toast_search_state();
@@ -117,14 +117,13 @@ toast_status search_begin(const toast_analysis* a, const toast_search_opts* o, i
   s->gbest = s->best;
   memset(s->gbest_seq, 0, sizeof s->gbest_seq);
   const int64_t L = o->leaves_per_round, R = o->rollouts_per_leaf;
-  s->h_lpre.assign((size_t)L * 32, 0);
-  s->h_pre.assign((size_t)L * R * 32, 0);
-  s->h_outs.assign((size_t)L * R * 32, 0);
-  s->h_lcost.resize((size_t)L);
-  s->h_cost.resize((size_t)L * R);
-  s->d_bytes = (size_t)L * 64 + (size_t)L * sizeof(toast_cost) + (size_t)L * R * (64 + 64 + sizeof(toast_cost));
+  // device: [L][32] prefixes | [L] leaf records | [L*R][32] sequences | [L*R] records | [L] reductions
+  s->d_bytes = (size_t)L * 64 + (size_t)L * sizeof(toast_cost) + (size_t)L * R * (64 + sizeof(toast_cost)) +
+               (size_t)L * sizeof(LeafRed);
   if (a->device >= 0) {
     cudaError_t e = cudaMalloc(&s->d_buf, s->d_bytes);
+    if (e == cudaSuccess) e = cudaMallocHost((void**)&s->h_lpre, (size_t)L * 64);
+    if (e == cudaSuccess) e = cudaMallocHost((void**)&s->h_red, (size_t)L * sizeof(LeafRed));
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_OOM; }
   }
   *out = s.release();
@@ -162,50 +161,41 @@ toast_status search_round(toast_search_state* s, void* export_buf, std::string& 
     for (SNode* x = node; x; x = x->parent) { x->N += 1; x->W -= 1.0; }   // virtual loss
     leaves.push_back(node);
   }
-  // device batch: L exact leaf evals + L*R rollouts
-  std::fill(s->h_lpre.begin(), s->h_lpre.end(), 0);
-  std::fill(s->h_pre.begin(), s->h_pre.end(), 0);
+  // device batch: L exact leaf evals + L*R rollouts (R per leaf prefix) + the per-leaf reduction
+  memset(s->h_lpre, 0, (size_t)L * 64);
   for (int l = 0; l < L; ++l) {
     const auto& p = leaves[l]->prefix;
     for (size_t i = 0; i < p.size(); ++i) s->h_lpre[(size_t)l * 32 + i] = p[i];
-    for (int j = 0; j < R; ++j)
-      for (size_t i = 0; i < p.size(); ++i) s->h_pre[((size_t)l * R + j) * 32 + i] = p[i];
   }
   char* d = reinterpret_cast<char*>(s->d_buf);
   uint16_t* d_lpre = reinterpret_cast<uint16_t*>(d);
   toast_cost* d_lcost = reinterpret_cast<toast_cost*>(d + (size_t)L * 64);
-  uint16_t* d_pre = reinterpret_cast<uint16_t*>(d + (size_t)L * (64 + sizeof(toast_cost)));
-  uint16_t* d_outs = d_pre + (size_t)L * R * 32;
-  toast_cost* d_cost = reinterpret_cast<toast_cost*>(d_outs + (size_t)L * R * 32);
+  uint16_t* d_outs = reinterpret_cast<uint16_t*>(d + (size_t)L * (64 + sizeof(toast_cost)));
+  toast_cost* d_cost = reinterpret_cast<toast_cost*>(reinterpret_cast<char*>(d_outs) + (size_t)L * R * 64);
+  void* d_red = reinterpret_cast<char*>(d_cost) + (size_t)L * R * sizeof(toast_cost);
   cudaStream_t st = (cudaStream_t)s->o.cuda_stream;
   auto ck = [&](cudaError_t e) { if (e != cudaSuccess) { err = cudaGetErrorString(e); return false; } return true; };
-  if (!ck(cudaMemcpyAsync(d_lpre, s->h_lpre.data(), (size_t)L * 64, cudaMemcpyHostToDevice, st))) return TOAST_E_CUDA;
-  if (R > 0 && !ck(cudaMemcpyAsync(d_pre, s->h_pre.data(), (size_t)L * R * 64, cudaMemcpyHostToDevice, st))) return TOAST_E_CUDA;
+  if (!ck(cudaMemcpyAsync(d_lpre, s->h_lpre, (size_t)L * 64, cudaMemcpyHostToDevice, st))) return TOAST_E_CUDA;
   toast_status ts = launch_eval(a, d_lpre, L, d_lcost, st, err);
   if (ts) return ts;
   if (R > 0) {
-    ts = launch_rollout(a, d_pre, (int64_t)L * R, s->seed, (uint64_t)s->rollouts_done, d_outs, d_cost, st, err);
+    ts = launch_rollout(a, d_lpre, (int64_t)L * R, s->seed, (uint64_t)s->rollouts_done, d_outs, d_cost, st, err, R);
     if (ts) return ts;
   }
-  if (!ck(cudaMemcpyAsync(s->h_lcost.data(), d_lcost, (size_t)L * sizeof(toast_cost), cudaMemcpyDeviceToHost, st))) return TOAST_E_CUDA;
-  if (R > 0) {
-    if (!ck(cudaMemcpyAsync(s->h_cost.data(), d_cost, (size_t)L * R * sizeof(toast_cost), cudaMemcpyDeviceToHost, st))) return TOAST_E_CUDA;
-    if (!ck(cudaMemcpyAsync(s->h_outs.data(), d_outs, (size_t)L * R * 64, cudaMemcpyDeviceToHost, st))) return TOAST_E_CUDA;
-  }
+  ts = launch_round_reduce(d_lcost, d_lpre, d_cost, d_outs, L, R, d_red, st, err);
+  if (ts) return ts;
+  if (!ck(cudaMemcpyAsync(s->h_red, d_red, (size_t)L * sizeof(LeafRed), cudaMemcpyDeviceToHost, st))) return TOAST_E_CUDA;
   if (!ck(cudaStreamSynchronize(st))) return TOAST_E_CUDA;
   s->rollouts_done += (int64_t)L * R;
   for (SNode* lf : leaves) for (SNode* x = lf; x; x = x->parent) { x->N -= 1; x->W += 1.0; }
-  auto consider = [&](const toast_cost& c, const uint16_t* sq, SNode* leaf) {
-    double reward = -c.score;
-    for (SNode* x = leaf; x; x = x->parent) { x->N += 1; x->W += reward; }
-    if (c.status == 0 && better(c, sq, s->best, s->best_seq)) {
-      s->best = c;
-      memcpy(s->best_seq, sq, 64);
-    }
-  };
+  // backup (R16): each leaf's in-order reward sum, once per node on its path
   for (int l = 0; l < L; ++l) {
-    consider(s->h_lcost[l], &s->h_lpre[(size_t)l * 32], leaves[l]);
-    for (int j = 0; j < R; ++j) consider(s->h_cost[(size_t)l * R + j], &s->h_outs[((size_t)l * R + j) * 32], leaves[l]);
+    const LeafRed& rr = s->h_red[l];
+    for (SNode* x = leaves[l]; x; x = x->parent) { x->N += R + 1; x->W += rr.reward_sum; }
+    if (rr.best != -2 && better(rr.cost, rr.seq, s->best, s->best_seq)) {
+      s->best = rr.cost;
+      memcpy(s->best_seq, rr.seq, 64);
+    }
   }
   s->evals += (int64_t)L * (R + 1);
   s->rounds++;
@@ -276,4 +266,6 @@ void search_free(toast_search_state* s) { delete s; }
 toast_search_state::~toast_search_state() {
   toast::free_tree(root);
   if (d_buf) cudaFree(d_buf);
+  if (h_lpre) cudaFreeHost(h_lpre);
+  if (h_red) cudaFreeHost(h_red);
 }

@@ -125,6 +125,16 @@ struct KDeath {          // 16 B
 };
 static_assert(sizeof(KHead) == 32 && sizeof(KUse) == 16 && sizeof(KDeath) == 16, "stream records");
 
+// search round reduction record (K3), one per leaf
+struct LeafRed {
+  double reward_sum;     // sum of the leaf's R+1 rewards (-score), in order (R16)
+  int32_t best;          // -1 = the leaf's own state, j = rollout j, -2 = none valid
+  int32_t pad;
+  uint64_t pad2;
+  toast_cost cost;       // the leaf's best record
+  uint16_t seq[32];      // and its sequence
+};
+
 // signature role word: acolor [0,10) | div_ok [10,26) | deselection class [26,34)
 struct DeviceTables {
   const uint4* stream = nullptr;         // op stream (16-byte words)
@@ -143,6 +153,9 @@ struct DeviceTables {
   uint64_t DM, peak0;
   uint64_t inv[16];     // exact division by prod(subset): (x >> shift) * inv
   uint32_t shift[16];
+  // op segments for K = 1, 2, 4, 8 sweeping warps: entries [K-1+log2 K, +K]
+  int32_t seg_op[19];   // first op of each segment (last entry = n_ops)
+  uint32_t seg_off[19]; // its 16-byte word offset in the stream
 };
 
 }  // namespace toast
@@ -190,6 +203,8 @@ struct toast_analysis {
   size_t scratch_bytes = 0;
   int32_t smem_per_warp = 0, warps_per_block = 8;
   int32_t eval_blocks = 0, rollout_blocks = 0;
+  int32_t occ_eval[4] = {0, 0, 0, 0}, occ_roll[4] = {0, 0, 0, 0};   // blocks per SM for K = 1, 2, 4, 8
+  int32_t n_sms = 0, k_throughput = 1;
 };
 
 namespace toast {
@@ -205,7 +220,11 @@ void free_tables(toast_analysis* a);
 toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, toast_cost* d_out, void* stream,
                          std::string& err);
 toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
-                            uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err);
+                            uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err, int64_t rep = 1);
+// search round reduction (K3): per leaf, reward sum + best candidate; d_out = [L] records of leaf_red_bytes()
+toast_status launch_round_reduce(const toast_cost* d_lcost, const uint16_t* d_lpre, const toast_cost* d_cost,
+                                 const uint16_t* d_seqs, int L, int R, void* d_out, void* stream, std::string& err);
+size_t leaf_red_bytes();
 toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h_in, int64_t n, uint64_t seed,
                               uint64_t id_base, uint16_t* h_seqs, toast_cost* h_out, void* stream, std::string& err);
 bool is_device_pointer(const void* p);
