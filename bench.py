@@ -45,7 +45,11 @@ def parse():
     p.add_argument("--seed", type=int, default=2024)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--search", action="store_true", help="also time toast_search (time-to-best)")
+    p.add_argument("--no-search", action="store_true", help="skip the time-to-best-partition measurement")
+    p.add_argument("--search-budget", type=int, default=5_000_000, help="evals of the long search that fixes S*")
+    p.add_argument("--search-cpu-seconds", type=float, default=60.0, help="time limit of the CPU oracle search")
+    p.add_argument("--L", type=int, default=64, help="search leaves per round")
+    p.add_argument("--R", type=int, default=256, help="search rollouts per leaf")
     return p.parse_args()
 
 
@@ -188,6 +192,56 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- time to best partition
+def time_to_best_gpu(a, args, rank, world, stream):
+    """S* = the best of a long search (seed 0, patience off, fixed
+    eval budget; every rank computes the same S* deterministically); then the
+    search races to S*: one GPU = toast_search, N GPUs = root-parallel
+    (seed + rank, per-round all-gather of the ranks' bests over NCCL)."""
+    from paper_2508_15010_b200 import toast as T
+    never = 1 << 30
+    r = T.search(a, T.SearchOptions(seed=0, max_evals=args.search_budget, leaves_per_round=args.L,
+                                    rollouts_per_leaf=args.R, patience=never), stream=stream)
+    s_star = float(r["best"]["score"])
+    opts = T.SearchOptions(seed=0, max_evals=args.search_budget, leaves_per_round=args.L, rollouts_per_leaf=args.R,
+                           patience=never, target_score=s_star)
+    if world == 1:
+        g = T.search(a, opts, stream=stream)
+    else:
+        from paper_2508_15010_b200 import parallel as P
+        g = P.search_root_parallel(a, opts, stream=stream)
+    return {"target_score": s_star, "target_seq": [int(x) for x in r["best_seq"] if x],
+            "target_source": f"best of a {int(r['evals'])}-eval single-GPU search (seed 0, L={args.L}, R={args.R})",
+            "gpu_time_to_target_s": float(g["time_to_target_s"]), "gpu_hit": bool(g["hit_target"]),
+            "gpu_evals": int(g["evals"]), "gpu_rounds": int(g["rounds"]), "n_gpus": world,
+            "search": {"leaves_per_round": args.L, "rollouts_per_leaf": args.R, "patience": "off",
+                       "budget_evals": args.search_budget}}
+
+
+def time_to_best_cpu(cfg, args, ttb):
+    """cpu_baseline leg: the oracle re-evaluates S*'s sequence bit-exactly, then
+    runs the same C16 search (same seed -> same trajectory) on all host cores
+    with target S* and a time limit."""
+    import numpy as np
+    from oracle.oracle import Oracle
+    o = Oracle(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth)
+    seq = np.zeros((1, 32), np.uint16)
+    seq[0, :len(ttb["target_seq"])] = ttb["target_seq"]
+    ttb["target_verified_by_oracle"] = bool(o.eval(seq)[0]["score"] == ttb["target_score"])
+    cores = os.cpu_count() or 1
+    never = 1 << 30
+    ro, _ = o.search(seed=0, max_evals=args.search_budget, time_limit_s=args.search_cpu_seconds, L=args.L, R=args.R,
+                     patience=never, target_score=ttb["target_score"], threads=cores)
+    hit = bool(ro["hit_target"])
+    cpu_t = float(ro["time_to_target_s"]) if hit else float(ro["wall_s"])
+    ttb["cpu_oracle"] = {"time_to_target_s": cpu_t if hit else None, "hit": hit, "evals": int(ro["evals"]),
+                         "wall_s": float(ro["wall_s"]), "cores": cores,
+                         "evals_per_s": int(ro["evals"]) / max(float(ro["wall_s"]), 1e-9)}
+    g = ttb["gpu_time_to_target_s"]
+    ttb["speedup_vs_cpu_oracle"] = (cpu_t / g) if (hit and g > 0) else None
+    ttb["speedup_lower_bound"] = None if hit else (cpu_t / g if g > 0 else None)
+
+
 # --------------------------------------------------------------------------- main arm
 def algorithmic_ops_per_eval(dump: dict, n_axes: int) -> int:
     """one check per loop (H2), rank x axes transitions
@@ -290,13 +344,15 @@ def run_toast(args, cfg, rank, world, local):
             "e2e": {"value": N * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": N * 64,
                     "d2h_bytes_per_step": N * (64 + 256)},
         }
-    if args.search and rank == 0:
-        r = T.search(a, T.SearchOptions(seed=args.seed, max_evals=2_000_000, leaves_per_round=64,
-                                        rollouts_per_leaf=256, patience=3), stream=stream)
-        line["search"] = {"best_score": float(r["best"]["score"]), "evals": int(r["evals"]),
-                          "rounds": int(r["rounds"]), "wall_s": float(r["wall_s"])}
+    ttb = None
+    if not args.no_search:
+        ttb = time_to_best_gpu(a, args, rank, world, stream)
+        if rank == 0:
+            line["time_to_best"] = ttb
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
+        if ttb is not None:
+            time_to_best_cpu(cfg, args, ttb)
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -185,12 +185,13 @@ def test_rollout_bad_prefix_is_not_extended():
 
 
 def test_full_size_bench_launch_sampled():
-    """GPT-24 at BASELINE size in bench.py's launch configuration (2^16 rollouts
-    from the empty prefix): a sample of outputs is recomputed one by one by the
-    oracle (sequence and record)."""
+    """GPT-24 at BASELINE size in bench.py's launch configuration (2^18 rollouts
+    rounded down to whole waves, from the empty prefix, bench's seed): a sample
+    of outputs is recomputed one by one by the oracle (sequence and record)."""
     a, o = setup("gpt24")
-    n = 1 << 16
-    seed, id_base = 2024, 0
+    wave = a.preferred_batch()
+    n = max(wave, ((1 << 18) // wave) * wave)
+    seed, id_base = 2024, 3 * n
     gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), seed, id_base)
     assert (gc["status"] == 0).all()
     idx = np.random.default_rng(0).choice(n, size=48, replace=False)
@@ -236,3 +237,31 @@ def test_search_mlp_c_finds_bruteforce_optimum():
     _, best, bc = o.bruteforce()
     r = T.search(a, T.SearchOptions(seed=0, max_evals=20000, leaves_per_round=8, rollouts_per_leaf=32, patience=4))
     assert r["best"]["score"] == bc["score"]
+
+
+def test_root_parallel_search_nccl_single_rank():
+    """The multi-GPU search driver (NCCL all-gather + import) at world size 1
+    reproduces toast_search exactly (same seed, same trajectory)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    T = _T()
+    from paper_2508_15010_b200 import parallel as P
+    a, o = setup("gpt2")
+    opts = T.SearchOptions(seed=4, max_evals=20000, leaves_per_round=8, rollouts_per_leaf=32, patience=3)
+    ref = T.search(a, opts)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        trace = []
+        r = P.search_root_parallel(a, opts, trace=trace)
+    finally:
+        dist.destroy_process_group()
+    assert int(r["rounds"]) == int(ref["rounds"]) and int(r["evals"]) == int(ref["evals"])
+    assert np.array_equal(r["best_seq"], ref["best_seq"]) and r["best"]["score"] == ref["best"]["score"]
+    assert len(trace) == int(r["rounds"]) and trace[-1] == r["best"]["score"]
