@@ -1201,16 +1201,13 @@ struct Oracle {
       L = L + res - dying_bytes;
     }
     // C14 (reading R14): the state is "the final sharding configuration
-    // itself".  Per op with at least one sharded loop, hash (first loop
-    // id, axis->role map: nibble A = role holding axis A, 0xF if none); sum over ops.
+    // itself": the set of (op, axis, loop role holding the axis).
+    // key = sum over that set of mix64(first loop id << 8 | axis << 4 | role), mod 2^64.
     u64 key = 0;
-    for (size_t t = 0; t < M.ops.size(); t++) {
-      u64 a2r = 0xFFFF;
+    for (size_t t = 0; t < M.ops.size(); t++)
       for (int r = 0; r < nloops((int)t); r++)
         for (int A = 0; A < 4; A++)
-          if (mask[loop_of((int)t, r)] & (1 << A)) a2r = (a2r & ~(0xFULL << (4 * A))) | ((u64)r << (4 * A));
-      if (a2r != 0xFFFF) key += mix64(((u64)op_loop_begin[t] << 16) | a2r);
-    }
+          if (mask[loop_of((int)t, r)] & (1 << A)) key += mix64(((u64)op_loop_begin[t] << 8) | ((u64)A << 4) | (u64)r);
     // C13: runtime and score
     u64 flo = (u64)flops, fhi = (u64)(flops >> 64);
     double fl = (double)fhi * 18446744073709551616.0 + (double)flo;

@@ -650,23 +650,37 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       a->h_sig_nroles[q] = (uint8_t)sig_words[q].size();
       for (size_t r = 0; r < sig_words[q].size(); ++r) a->h_sig_roles[q * 8 + r] = sig_words[q][r];
     }
-    // the stream
+    // per-signature state-key terms (R14) and FLOP sums
+    const size_t NS = sig_words.size();
+    a->h_sig_key.assign(NS * 32, 0);
+    a->h_sig_flops.assign(NS * 2, 0);
+    for (int32_t t = 0; t < n_ops; ++t) {
+      const uint32_t q = a->op_sig[t];
+      for (int A = 0; A < 4; ++A)
+        for (int r = 0; r < (int)OL[t].ext.size(); ++r)
+          a->h_sig_key[q * 32 + A * 8 + r] += splitmix_fin(((uint64_t)lbeg[t] << 8) | ((uint64_t)A << 4) | (uint64_t)r);
+      unsigned __int128 f = ((unsigned __int128)a->h_sig_flops[q * 2 + 1] << 64) | a->h_sig_flops[q * 2];
+      f += a->h_gflops[t];
+      a->h_sig_flops[q * 2] = (uint64_t)f;
+      a->h_sig_flops[q * 2 + 1] = (uint64_t)(f >> 64);
+    }
+    // the stream (+ edge templates)
     auto push = [&](const void* rec, size_t bytes) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(rec);
       a->h_stream.insert(a->h_stream.end(), w, w + bytes / 4);
     };
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint32_t> tmpl_id;
+    a->h_tmpl.clear();
     a->h_stream.clear();
     for (int32_t t = 0; t < n_ops; ++t) {
       const GOp& op = g->ops[t];
       KHead h{};
-      h.lb = (uint32_t)lbeg[t];
       h.sig = (uint16_t)a->op_sig[t];
       h.flags = a->h_ops[t].flags;
       h.n_uses = (uint8_t)op.operands.size();
       if (deaths[t].size() > 255) { err = "too many values die at one op"; return TOAST_E_LIMIT; }
       h.n_death = (uint8_t)deaths[t].size();
       h.gbytes = a->h_ops[t].gbytes;
-      h.gflops = a->h_gflops[t];
       push(&h, sizeof h);
       std::vector<int> order(op.operands.size());
       std::iota(order.begin(), order.end(), 0);
@@ -680,15 +694,34 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         u.def_sig = (uint16_t)a->op_sig[v];
         bool first = q == 0 || g->values[op.operands[order[q - 1]]].def_op != v;
         bool last = q + 1 == order.size() || g->values[op.operands[order[q + 1]]].def_op != v;
-        u.flags = (uint8_t)((first ? 1 : 0) | (last ? 2 : 0));
         uint32_t um = ~0u;
         for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
           uint32_t r = OL[t].use_role[k][i];
           um = (um & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
         }
         u.use_dimof = um;
-        if (op.result >= 0 && um == resdim_of(t)) u.flags |= 4;   // operand dims == result dims (elementwise)
-        u.def_gbytes = a->h_ops[v].gbytes;
+        const uint64_t gb = a->h_ops[v].gbytes;
+        if (gb >> 56) { err = "a value larger than 2^56 bytes"; return TOAST_E_LIMIT; }
+        u.gb_flags = gb | ((uint64_t)((first ? 1 : 0) | (last ? 2 : 0)) << 56);
+        if (first && last) {   // the value is used once here: cost it through its template
+          auto key = std::make_tuple(a->op_sig[v], a->op_sig[t], um);
+          auto it = tmpl_id.find(key);
+          if (it == tmpl_id.end()) {
+            it = tmpl_id.emplace(key, (uint32_t)a->h_tmpl.size()).first;
+            KTmpl tm{};
+            tm.def_sig = (uint16_t)a->op_sig[v];
+            tm.use_sig = (uint16_t)a->op_sig[t];
+            tm.use_dimof = um;
+            a->h_tmpl.push_back(tm);
+          }
+          KTmpl& tm = a->h_tmpl[it->second];
+          if (tm.sum_gbytes + gb < tm.sum_gbytes) { err = "template byte sum overflows"; return TOAST_E_LIMIT; }
+          tm.sum_gbytes += gb;
+          tm.n_edges += 1;
+          u.tmpl = (uint16_t)it->second;
+        } else {
+          u.tmpl = NO_TMPL;
+        }
         push(&u, sizeof u);
       }
       for (int32_t v : deaths[t]) {
@@ -698,13 +731,14 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         push(&d, sizeof d);
       }
     }
+    if (a->h_tmpl.size() >= NO_TMPL) { err = "more than 65534 edge templates"; return TOAST_E_LIMIT; }
     // op segments (balanced by stream words) for K = 1, 2, 4, 8 sweeping warps
     {
       std::vector<uint32_t> off(n_ops + 1, 0);
       size_t w = 0;
       for (int32_t t = 0; t < n_ops; ++t) {
         off[t] = (uint32_t)w;
-        w += 2 + g->ops[t].operands.size() + deaths[t].size();
+        w += 1 + g->ops[t].operands.size() + deaths[t].size();
       }
       off[n_ops] = (uint32_t)w;
       for (int K = 1, lg = 0; K <= 8; K *= 2, ++lg) {
@@ -719,8 +753,9 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       }
     }
     if (getenv("TOAST_DEBUG"))
-      fprintf(stderr, "[toast] ops %d loops %lld signatures %zu stream %zu B actions %zu desel classes %zu\n", n_ops,
-              (long long)NL, sig_words.size(), a->h_stream.size() * 4, a->actions.size(), a->h_desel_cls.size() / 2);
+      fprintf(stderr, "[toast] ops %d loops %lld signatures %zu templates %zu stream %zu B actions %zu desel classes %zu\n",
+              n_ops, (long long)NL, sig_words.size(), a->h_tmpl.size(), a->h_stream.size() * 4, a->actions.size(),
+              a->h_desel_cls.size() / 2);
   }
 
   // ------------------------------------------------------------ baseline (empty sequence)
@@ -764,6 +799,9 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
   T.n_axes = n_axes;
   T.max_depth = o->max_depth;
   T.n_sigs = (int32_t)a->h_sig_nroles.size();
+  T.n_tmpl = (int32_t)a->h_tmpl.size();
+  T.pow2 = 1;
+  for (int A = 0; A < n_axes; ++A) if (g->axis_size[A] & (g->axis_size[A] - 1)) T.pow2 = 0;
   for (int A = 0; A < 4; ++A) {
     T.sizes[A] = A < n_axes ? g->axis_size[A] : 1;
     T.bw[A] = A < n_axes ? g->axis_bw[A] : 1.0;
@@ -782,6 +820,10 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     for (int it = 0; it < 6; ++it) inv *= 2 - d * inv;
     T.shift[S] = sh;
     T.inv[S] = inv;
+    unsigned __int128 d128 = d, inv128 = d;   // Newton for the inverse mod 2^128
+    for (int it = 0; it < 7; ++it) inv128 *= (unsigned __int128)2 - d128 * inv128;
+    T.inv128_lo[S] = (uint64_t)inv128;
+    T.inv128_hi[S] = (uint64_t)(inv128 >> 64);
   }
   return TOAST_OK;
 }

@@ -70,8 +70,9 @@ __host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
   int b1 = n_ac * 128, b2 = K * smem_acc_bytes(n_axes);
   return r16(b1 > b2 ? b1 : b2);
 }
-__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K) {
-  return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K);
+__host__ __device__ inline int smem_d_bytes(int n_tmpl) { return r16(n_tmpl * 32); }
+__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl) {
+  return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl);
 }
 
 struct Smem {
@@ -83,6 +84,7 @@ struct Smem {
   unsigned long long* on;   // [32] SetGroups fixed to 1
   uint32_t* status;         // [32]
   unsigned char* acc;       // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
+  uint8_t* tb;              // D: [n_tmpl][32] per edge template: presU | presD << 4 (equal: no temporary)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -98,7 +100,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   unsigned char* b = a + smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
   s.acol = reinterpret_cast<uint32_t*>(b);
   s.acc = b;
-  (void)K;
+  s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
   return s;
 }
 
@@ -111,7 +113,12 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // exact division by the product of the sizes of axis subset S (always exact
 // on this path): (x >> twos(d)) * odd(d)^-1 mod 2^64
 __device__ __forceinline__ uint64_t exdiv(const DeviceTables& T, uint64_t x, uint32_t S) {
-  return (x >> T.shift[S]) * T.inv[S];
+  return T.pow2 ? (x >> T.shift[S]) : (x >> T.shift[S]) * T.inv[S];
+}
+__device__ __forceinline__ unsigned __int128 exdiv128(const DeviceTables& T, unsigned __int128 x, uint32_t S) {
+  x >>= T.shift[S];
+  if (T.pow2) return x;
+  return x * (((unsigned __int128)T.inv128_hi[S] << 64) | T.inv128_lo[S]);
 }
 
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
@@ -265,9 +272,31 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     S.on[lane] = on;
   }
   __syncthreads();
+  // H2: materialise this warp's share of the signatures; per signature the
+  // state-key terms (H7, R14) and the local FLOPs (H3) of all its ops at once
+  uint64_t key = 0, flo = 0, fhi = 0;
   {
     const uint64_t f0 = S.f0[lane], on = S.on[lane];
-    for (int s = warp; s < T.n_sigs; s += K) ent_store<NA>(S, s, lane, pack_entry<NA>(materialize_sig(T, S, lane, s, f0, on)));
+    for (int s = warp; s < T.n_sigs; s += K) {
+      const uint32_t e = pack_entry<NA>(materialize_sig(T, S, lane, s, f0, on));
+      ent_store<NA>(S, s, lane, e);
+      uint32_t opmask = 0;
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {
+        const uint32_t r = e_role<NA>(e, A);
+        if (r != 15) {
+          key += __ldg(T.sig_key + (size_t)s * 32 + A * 8 + r);
+          opmask |= 1u << A;
+        }
+      }
+      const uint64_t glo = __ldg(T.sig_flops + 2 * s), ghi = __ldg(T.sig_flops + 2 * s + 1);
+      if (glo | ghi) {
+        const unsigned __int128 f = exdiv128(T, ((unsigned __int128)ghi << 64) | glo, opmask);
+        const uint64_t l = (uint64_t)f;
+        flo += l;
+        fhi += (uint64_t)(f >> 64) + ((flo < l) ? 1 : 0);
+      }
+    }
   }
   __syncthreads();
   const int sb = K - 1 + (K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0);   // segment table base for this K
@@ -278,71 +307,114 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = 0ULL; cnt[q * 32 + lane] = 0u; }
 
-  uint64_t key = 0, flo = 0, fhi = 0;
-  long long L = 0, peak = LLONG_MIN;   // relative to the segment start (combined across segments below)
-  const uint4* p = T.stream + T.seg_off[sb + warp];
-  uint4 nh0 = __ldg(p), nh1 = __ldg(p + 1);
-  const int t_end = T.seg_op[sb + warp + 1];
-  for (int t = T.seg_op[sb + warp]; t < t_end; ++t) {
-    const uint4 h0 = nh0, h1 = nh1;
-    const uint32_t lb = h0.x, sig = h0.y & 0xFFFF, flags = (h0.y >> 16) & 0xFF;
-    const uint32_t n_uses = h0.y >> 24, n_death = h0.z & 0xFF;
-    {   // prefetch the next op's header (the stream always has a next 32 B after the last op: see upload)
-      const uint4* pn = p + 2 + n_uses + n_death;
-      nh0 = __ldg(pn);
-      nh1 = __ldg(pn + 1);
-    }
-    const uint32_t ent = ent_load<NA>(S, sig, lane);
-    const uint32_t a2r = e_a2r16<NA>(ent);
-    // H7 state key (C14, reading R14): one hash per op with a sharded loop
-    if (a2r != 0xFFFFu) key += mix64(((uint64_t)lb << 16) | a2r);
-    uint32_t opmask = 0, present = 0;
+  // H4 per edge template: every use edge of the template communicates the
+  // same way, so its payloads are costed once from the template's summed
+  // bytes; the sweep only needs each edge's temporary (presU/presD)
+  for (int tix = warp; tix < T.n_tmpl; tix += K) {
+    const uint2 t0 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix));
+    const uint2 t1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix) + 1);
+    const uint2 t2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix) + 2);
+    const uint32_t de = ent_load<NA>(S, t0.x & 0xFFFF, lane), ue = ent_load<NA>(S, t0.x >> 16, lane);
+    const uint32_t use_dimof = t0.y;
+    uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
     for (int A = 0; A < NA; ++A) {
-      opmask |= (e_role<NA>(ent, A) != 15 ? 1u : 0u) << A;
-      present |= (e_dim<NA>(ent, A) != 15 ? 1u : 0u) << A;
+      const uint32_t ru = e_role<NA>(ue, A);
+      const uint32_t du = ru == 15 ? 15u : (use_dimof >> (4 * ru)) & 15;
+      const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+      dimD |= dd << (4 * A);
+      dimU |= du << (4 * A);
+      P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
+      presD |= (dd != 15 ? 1u : 0u) << A;
+      presU |= (du != 15 ? 1u : 0u) << A;
     }
-    if (flags & 1) {   // H3 local FLOPs, matmul-class ops only
-      const uint64_t f = exdiv(T, u64of(h1.z, h1.w), opmask);
-      flo += f;
-      fhi += (flo < f) ? 1 : 0;
+    uint8_t tbv = 0;
+    if (dimD != dimU || P) {
+      const uint64_t sgb = u64of(t1.x, t1.y);
+      const uint32_t ne = t2.x;
+      uint64_t size = exdiv(T, sgb, presD);
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {          // phase 1: all_gather / all_to_all
+        const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+        if (dd == 15 || dd == du) continue;
+        if (du != 15) {
+          pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
+          cnt[(A * 4 + TOAST_A2A) * 32 + lane] += ne;
+        } else {
+          pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
+          cnt[(A * 4 + TOAST_AG) * 32 + lane] += ne;
+          size *= (uint64_t)T.sizes[A];
+        }
+      }
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
+        if (!((P >> A) & 1)) continue;
+        if (((dimU >> (4 * A)) & 15) != 15) {
+          size = exdiv(T, size, 1u << A);
+          pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
+          cnt[(A * 4 + TOAST_RS) * 32 + lane] += ne;
+        } else {
+          pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
+          cnt[(A * 4 + TOAST_AR) * 32 + lane] += ne;
+        }
+      }
+      tbv = (uint8_t)(presU | (presD << 4));
     }
-    const long long res = (flags & 2) ? 0 : (long long)exdiv(T, u64of(h1.x, h1.y), present);
-    // H4: use edges (C11)
+    S.tb[tix * 32 + lane] = tbv;
+  }
+  __syncthreads();
+
+  // the sweep: H5 liveness over this warp's op segment (plus the rare use
+  // edges whose value is used twice by one op, costed edge by edge)
+  long long L = 0, peak = LLONG_MIN;   // relative to the segment start (combined across segments below)
+  const uint4* p = T.stream + T.seg_off[sb + warp];
+  const int t_end = T.seg_op[sb + warp + 1];
+  uint4 nh = __ldg(p);
+  for (int t = T.seg_op[sb + warp]; t < t_end; ++t) {
+    const uint4 h = nh;
+    const uint32_t sig = h.x & 0xFFFF, flags = (h.x >> 16) & 0xFF, n_uses = h.x >> 24, n_death = h.y & 0xFF;
+    nh = __ldg(p + 1 + n_uses + n_death);   // prefetch the next header (the stream has a 16 B tail)
+    const uint32_t ent = ent_load<NA>(S, sig, lane);
+    uint32_t present = 0;
+#pragma unroll
+    for (int A = 0; A < NA; ++A) present |= (e_dim<NA>(ent, A) != 15 ? 1u : 0u) << A;
+    const long long res = (flags & 2) ? 0 : (long long)exdiv(T, u64of(h.z, h.w), present);
     long long temp = 0, gmax = 0;
-    const uint4* q = p + 2;
+    const uint4* q = p + 1;
     const uint4* gq = q;
     for (uint32_t k = 0; k < n_uses; ++k, ++q) {
       const uint4 u = __ldg(q);
-      const uint32_t uflags = (u.x >> 16) & 0xFF;
+      const uint32_t tix = u.x >> 16;
+      const uint64_t gb = u64of(u.z, u.w & 0x00FFFFFFu);
+      if (tix != NO_TMPL) {
+        const uint32_t b = S.tb[tix * 32 + lane];
+        const uint32_t pU = b & 15, pD = b >> 4;
+        if (pU != pD) {
+          const long long g = (long long)exdiv(T, gb, pU) - (long long)exdiv(T, gb, pD);
+          if (g > 0) temp += g;
+        }
+        continue;
+      }
+      // a value used more than once by this op: costed per edge, once per distinct layout
+      const uint32_t uflags = u.w >> 24;
       if (uflags & 1) { gmax = 0; gq = q; }
       const uint32_t de = ent_load<NA>(S, u.x & 0xFFFF, lane);
-      // def layout D (axis -> result dim), partial axes P, use layout U (axis -> operand dim)
-      uint32_t dimU = 0;
-      bool nothing = true;
-      if (uflags & 4) {   // elementwise use: U is this op's result layout; nothing iff D == U and no partial axis
-        const uint32_t MK = (1u << (4 * NA)) - 1u;
-        dimU = (ent >> (4 * NA)) & MK;
-        nothing = ((de >> (4 * NA)) & MK) == dimU;
+      const uint32_t a2r = e_a2r16<NA>(ent);
+      uint32_t dimU = 0, dimD = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
-        for (int A = 0; A < NA; ++A) nothing &= !(e_role<NA>(de, A) != 15 && e_dim<NA>(de, A) == 15);
-      } else {
-#pragma unroll
-        for (int A = 0; A < NA; ++A) {
-          const uint32_t ru = (a2r >> (4 * A)) & 15;
-          const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
-          const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
-          dimU |= du << (4 * A);
-          nothing &= !(rd != 15 && dd == 15) && (dd == 15 || dd == du);
-        }
+      for (int A = 0; A < NA; ++A) {
+        const uint32_t ru = (a2r >> (4 * A)) & 15;
+        const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
+        const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+        dimU |= du << (4 * A);
+        dimD |= dd << (4 * A);
+        P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
+        presD |= (dd != 15 ? 1u : 0u) << A;
+        presU |= (du != 15 ? 1u : 0u) << A;
       }
-      if (!nothing) {   // a collective (not just a free local slice) is needed
-        uint32_t P = 0;
-#pragma unroll
-        for (int A = 0; A < NA; ++A) P |= ((e_role<NA>(de, A) != 15 && e_dim<NA>(de, A) == 15) ? 1u : 0u) << A;
-        const uint32_t dimD = (de >> (4 * NA)) & ((1u << (4 * NA)) - 1u);
+      if (dimD != dimU || P) {
         bool dup = false;
-        for (const uint4* q2 = gq; q2 < q; ++q2) {   // the same value again at this op: once per layout
+        for (const uint4* q2 = gq; q2 < q; ++q2) {
           const uint32_t ud2 = __ldg(q2).y;
           uint32_t dimU2 = 0;
 #pragma unroll
@@ -353,16 +425,9 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
           dup |= dimU2 == dimU;
         }
         if (!dup) {
-          const uint64_t dgb = u64of(u.z, u.w);
-          uint32_t presD = 0, presU = 0;
+          uint64_t size = exdiv(T, gb, presD);
 #pragma unroll
           for (int A = 0; A < NA; ++A) {
-            presD |= (((dimD >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
-            presU |= (((dimU >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
-          }
-          uint64_t size = exdiv(T, dgb, presD);
-#pragma unroll
-          for (int A = 0; A < NA; ++A) {          // phase 1: all_gather / all_to_all
             const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
             if (dd == 15 || dd == du) continue;
             if (du != 15) {
@@ -375,7 +440,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
             }
           }
 #pragma unroll
-          for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
+          for (int A = 0; A < NA; ++A) {
             if (!((P >> A) & 1)) continue;
             if (((dimU >> (4 * A)) & 15) != 15) {
               size = exdiv(T, size, 1u << A);
@@ -386,7 +451,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
               cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
             }
           }
-          const long long grow = (long long)exdiv(T, dgb, presU) - (long long)exdiv(T, dgb, presD);
+          const long long grow = (long long)exdiv(T, gb, presU) - (long long)exdiv(T, gb, presD);
           if (grow > gmax) gmax = grow;
         }
       }
@@ -402,7 +467,6 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       for (int A = 0; A < NA; ++A) pres |= (e_dim<NA>(ev, A) != 15 ? 1u : 0u) << A;
       dying += (long long)exdiv(T, u64of(d.z, d.w), pres);
     }
-    // H5 liveness (C12)
     const long long M = L + res + temp;
     peak = M > peak ? M : peak;
     L = L + res - dying;
@@ -688,7 +752,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   DeviceTables& T = a->dt;
   toast_status st;
   const void* p;
-  a->h_stream.resize(a->h_stream.size() + 8, 0u);   // 32 B tail: the kernels prefetch one header past the end
+  a->h_stream.resize(a->h_stream.size() + 4, 0u);   // 16 B tail: the kernels prefetch one header past the end
   if ((st = upload(a, a->h_stream, &p, err))) return st;
   T.stream = reinterpret_cast<const uint4*>(p);
   if ((st = upload(a, a->h_sig_roles, &p, err))) return st;
@@ -697,6 +761,12 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   T.sig_nroles = reinterpret_cast<const uint8_t*>(p);
   if ((st = upload(a, a->h_sig_resdim, &p, err))) return st;
   T.sig_resdim = reinterpret_cast<const uint32_t*>(p);
+  if ((st = upload(a, a->h_sig_key, &p, err))) return st;
+  T.sig_key = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_sig_flops, &p, err))) return st;
+  T.sig_flops = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_tmpl, &p, err))) return st;
+  T.tmpl = reinterpret_cast<const KTmpl*>(p);
   if ((st = upload(a, a->h_desel_cls, &p, err))) return st;
   T.desel = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_actions, &p, err))) return st;
@@ -709,7 +779,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1) > dev_smem) {
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -721,7 +791,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K);
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
       switch (T.n_axes) {
@@ -784,7 +854,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
   cudaStream_t st = (cudaStream_t)stream;
   switch (a->dt.n_axes) {
     case 1: toast_eval_kernel<1><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
@@ -803,7 +873,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
   cudaStream_t st = (cudaStream_t)stream;
   switch (a->dt.n_axes) {
     case 1: toast_rollout_kernel<1><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;

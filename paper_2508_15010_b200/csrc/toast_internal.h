@@ -99,23 +99,19 @@ constexpr int MAX_GROUPS = 64;
 // sequential.  An op's SIGNATURE fixes how it materialises (per role: action
 // color, divisibility, deselection class, result dim), so per candidate the
 // kernel keeps one 32-bit entry per signature: axis->role | axis->result dim.
-struct KHead {           // 32 B
-  uint32_t lb;           // global loop id of role 0 (state key, C14 / R14)
+struct KHead {           // 16 B
   uint16_t sig;          // op signature
-  uint8_t flags;         // bit0 matmul-class, bit1 ret
+  uint8_t flags;         // bit1 ret
   uint8_t n_uses;
   uint8_t n_death;
   uint8_t pad0[3];
-  uint32_t pad1;
   uint64_t gbytes;       // result global bytes (0 for ret)
-  uint64_t gflops;       // 2 * prod(loop extents) for matmul-class ops, else 0
 };
 struct KUse {            // 16 B
   uint16_t def_sig;      // signature of the defining op
-  uint8_t flags;         // bit0 first use of this value at the op, bit1 last, bit2 operand dims == result dims
-  uint8_t pad;
+  uint16_t tmpl;         // edge template, or NO_TMPL: the value is used again at this op (costed per edge)
   uint32_t use_dimof;    // nibble r: operand dim held by this op's role r (0xF: none)
-  uint64_t def_gbytes;
+  uint64_t gb_flags;     // def global bytes (bits 0-55) | flags << 56 (bit0 first use of the value here, bit1 last)
 };
 struct KDeath {          // 16 B
   uint16_t sig;
@@ -123,7 +119,20 @@ struct KDeath {          // 16 B
   uint32_t pad1;
   uint64_t gbytes;
 };
-static_assert(sizeof(KHead) == 32 && sizeof(KUse) == 16 && sizeof(KDeath) == 16, "stream records");
+constexpr uint16_t NO_TMPL = 0xFFFF;
+// edge template: use edges with the same (def signature, use signature, use
+// role->dim map) communicate identically for every candidate; their payloads
+// are costed once per candidate from the template's summed def bytes
+struct KTmpl {           // 24 B
+  uint16_t def_sig;
+  uint16_t use_sig;
+  uint32_t use_dimof;
+  uint64_t sum_gbytes;
+  uint32_t n_edges;
+  uint32_t pad;
+};
+static_assert(sizeof(KHead) == 16 && sizeof(KUse) == 16 && sizeof(KDeath) == 16 && sizeof(KTmpl) == 24, "records");
+
 
 // search round reduction record (K3), one per leaf
 struct LeafRed {
@@ -141,18 +150,23 @@ struct DeviceTables {
   const uint64_t* sig_roles = nullptr;   // [n_sigs][8] role words (acolor 0x3FF = untouchable)
   const uint8_t* sig_nroles = nullptr;   // [n_sigs]
   const uint32_t* sig_resdim = nullptr;  // [n_sigs] nibble r: result dim of role r (0xF: none)
+  const uint64_t* sig_key = nullptr;     // [n_sigs][4 axes][8 roles] summed state-key terms (R14)
+  const uint64_t* sig_flops = nullptr;   // [n_sigs][2] summed global FLOPs of matmul-class ops (lo, hi)
+  const KTmpl* tmpl = nullptr;           // [n_tmpl]
   const uint64_t* desel = nullptr;       // [class][2] = need0, need1 (class 0 = none)
   const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
   const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids (0xFF = unused)
   const uint32_t* kill = nullptr;        // [n_actions][n_words]
   // constants
   int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
+  int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
   uint64_t DM, peak0;
   uint64_t inv[16];     // exact division by prod(subset): (x >> shift) * inv
   uint32_t shift[16];
+  uint64_t inv128_lo[16], inv128_hi[16];   // the same inverse mod 2^128 (FLOP totals)
   // op segments for K = 1, 2, 4, 8 sweeping warps: entries [K-1+log2 K, +K]
   int32_t seg_op[19];   // first op of each segment (last entry = n_ops)
   uint32_t seg_off[19]; // its 16-byte word offset in the stream
@@ -190,6 +204,8 @@ struct toast_analysis {
   std::vector<uint64_t> h_sig_roles, h_desel_cls;
   std::vector<uint8_t> h_sig_nroles;
   std::vector<uint32_t> h_sig_resdim;
+  std::vector<uint64_t> h_sig_key, h_sig_flops;
+  std::vector<toast::KTmpl> h_tmpl;
   std::vector<uint32_t> op_sig;
   std::vector<int32_t> axis_size;
 
