@@ -21,7 +21,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_FLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
+CU_FLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++20", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
                       f"-I{INC}", f"-I{SRC}"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", f"-I{CUDA}/include", f"-I{INC}", f"-I{SRC}"]
 

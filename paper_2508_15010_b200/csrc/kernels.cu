@@ -72,56 +72,64 @@ __host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
 }
 __host__ __device__ inline int smem_d_bytes(int n_tmpl) { return r16(n_tmpl * 32); }
 __host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl) {
-  return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl);
+  return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl) +
+         r16(n_sigs * 32);
 }
 
-struct Smem {
-  void* sig;                // [n_sigs][32] per signature: axis->role | axis->result dim (4 bits per axis each)
-  uint32_t* acol;           // [n_acolors][32] up to 4 events (valid | axis << 5 | position) per action color
-  uint32_t* seq;            // [16][32] the candidates' 32 ids as 16 words
-  uint32_t* legal;          // [n_words][32] rollout legal bitset
-  unsigned long long* f0;   // [32] SetGroups fixed to 0
-  unsigned long long* on;   // [32] SetGroups fixed to 1
-  uint32_t* status;         // [32]
-  unsigned char* acc;       // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
-  uint8_t* tb;              // D: [n_tmpl][32] per edge template: presU | presD << 4 (equal: no temporary)
+// the block's dynamic shared memory; every access indexes this symbol so the
+// compiler emits plain LDS/STS (no generic-address conversion)
+extern __shared__ __align__(16) unsigned char g_smem[];
+template <typename V>
+__device__ __forceinline__ V* sp(uint32_t off) { return reinterpret_cast<V*>(g_smem + off); }
+
+struct Smem {               // byte offsets into g_smem
+  uint32_t sig;             // [n_sigs][32] per signature: axis->role | axis->result dim (4 bits per axis each)
+  uint32_t acol;            // [n_acolors][32] up to 4 events (valid | axis << 5 | position) per action color
+  uint32_t seq;             // [16][32] the candidates' 32 ids as 16 words
+  uint32_t legal;           // [n_words][32] rollout legal bitset
+  uint32_t f0;              // [32] SetGroups fixed to 0 (u64)
+  uint32_t on;              // [32] SetGroups fixed to 1 (u64)
+  uint32_t status;          // [32]
+  uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
+  uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
+  uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
-  extern __shared__ __align__(16) unsigned char smem[];
   Smem s;
-  s.f0 = reinterpret_cast<unsigned long long*>(smem);
-  s.on = s.f0 + 32;
-  s.status = reinterpret_cast<uint32_t*>(smem + 512);
-  unsigned char* a = smem + smem_c_bytes();
+  s.f0 = 0;
+  s.on = 256;
+  s.status = 512;
+  const uint32_t a = smem_c_bytes();
   s.sig = a;
-  s.seq = reinterpret_cast<uint32_t*>(a);
-  s.legal = reinterpret_cast<uint32_t*>(a + 2048);
-  unsigned char* b = a + smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
-  s.acol = reinterpret_cast<uint32_t*>(b);
+  s.seq = a;
+  s.legal = a + 2048;
+  const uint32_t b = a + smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
+  s.acol = b;
   s.acc = b;
   s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
+  s.pc = s.tb + smem_d_bytes(T.n_tmpl);
   return s;
 }
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  return z ^ (z >> 31);
-}
+__device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
 
-// exact division by the product of the sizes of axis subset S (always exact
-// on this path): (x >> twos(d)) * odd(d)^-1 mod 2^64
-__device__ __forceinline__ uint64_t exdiv(const DeviceTables& T, uint64_t x, uint32_t S) {
-  return T.pow2 ? (x >> T.shift[S]) : (x >> T.shift[S]) * T.inv[S];
+// "division codes": for power-of-two meshes (P2) the code of an axis subset is
+// log2 of its size product and exact division is a shift; otherwise the code
+// is the subset itself and division is (x >> twos) * odd^-1 mod 2^64 (the
+// divisor always divides x exactly on this path)
+template <bool P2>
+__device__ __forceinline__ uint32_t dcode(const DeviceTables& T, uint32_t S) { return P2 ? T.shift[S] : S; }
+template <bool P2>
+__device__ __forceinline__ uint64_t dv(const DeviceTables& T, uint64_t x, uint32_t code) {
+  return P2 ? (x >> code) : (x >> T.shift[code]) * T.inv[code];
 }
-__device__ __forceinline__ unsigned __int128 exdiv128(const DeviceTables& T, unsigned __int128 x, uint32_t S) {
+template <bool P2>
+__device__ __forceinline__ unsigned __int128 dv128(const DeviceTables& T, unsigned __int128 x, uint32_t S) {
   x >>= T.shift[S];
-  if (T.pow2) return x;
+  if (P2) return x;
   return x * (((unsigned __int128)T.inv128_hi[S] << 64) | T.inv128_lo[S]);
 }
-
-__device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
 
 // signature entry per lane: bits [0, 4NA) axis->role, [4NA, 8NA) axis->result dim
 template <int NA> struct Ent { typedef uint32_t T; };
@@ -129,11 +137,11 @@ template <> struct Ent<1> { typedef uint16_t T; };
 template <> struct Ent<2> { typedef uint16_t T; };
 template <int NA>
 __device__ __forceinline__ uint32_t ent_load(const Smem& S, uint32_t sig, int lane) {
-  return reinterpret_cast<const typename Ent<NA>::T*>(S.sig)[sig * 32 + lane];
+  return sp<const typename Ent<NA>::T>(S.sig)[sig * 32 + lane];
 }
 template <int NA>
 __device__ __forceinline__ void ent_store(const Smem& S, uint32_t sig, int lane, uint32_t e) {
-  reinterpret_cast<typename Ent<NA>::T*>(S.sig)[sig * 32 + lane] = (typename Ent<NA>::T)e;
+  sp<typename Ent<NA>::T>(S.sig)[sig * 32 + lane] = (typename Ent<NA>::T)e;
 }
 // axis A's role / result dim in an entry (15 = none)
 template <int NA> __device__ __forceinline__ uint32_t e_role(uint32_t e, int A) { return (e >> (4 * A)) & 15; }
@@ -146,12 +154,12 @@ template <int NA> __device__ __forceinline__ uint32_t e_a2r16(uint32_t e) {
 // ---------------------------------------------------------------- H1 decode (C9)
 __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
                                            uint64_t& ones) {
-  for (int c = 0; c < T.n_acolors; ++c) S.acol[c * 32 + lane] = 0u;
+  for (int c = 0; c < T.n_acolors; ++c) sp<uint32_t>(S.acol)[c * 32 + lane] = 0u;
   uint32_t status = 0;
   bool stopped = false;
   uint64_t fx = 0, on = 0;
   for (int j = 0; j < 32; ++j) {
-    uint32_t id = (S.seq[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+    uint32_t id = (sp<uint32_t>(S.seq)[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
     if (stopped) {
       if (id) status |= TOAST_ST_NONZERO_AFTER_STOP;
       continue;
@@ -160,7 +168,7 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
     if ((int)id >= T.n_actions) { status |= TOAST_ST_BAD_ACTION_ID; continue; }
     uint32_t aw = __ldg(T.actions + id);
     uint32_t ac = aw & 0x3FF, rr = (aw >> 10) & 0xFF, ax = (aw >> 18) & 3;
-    uint32_t list = S.acol[ac * 32 + lane];
+    uint32_t list = sp<uint32_t>(S.acol)[ac * 32 + lane];
     uint32_t nent = 0;
     bool dup = false;
 #pragma unroll
@@ -169,7 +177,7 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
       if (e & 0x80) { ++nent; dup |= ((e >> 5) & 3) == ax; }
     }
     if (dup) status |= TOAST_ST_DUP_COLOR_AXIS;
-    else if (nent < 4) S.acol[ac * 32 + lane] = list | ((0x80u | (ax << 5) | (uint32_t)j) << (8 * nent));
+    else if (nent < 4) sp<uint32_t>(S.acol)[ac * 32 + lane] = list | ((0x80u | (ax << 5) | (uint32_t)j) << (8 * nent));
     uint64_t gw = __ldg(T.acol_groups + ac);
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -202,7 +210,7 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
       uint64_t rw = __ldg(T.sig_roles + (size_t)s * 8 + r);
       uint32_t ac = (uint32_t)rw & 0x3FF;
       if (ac != NO_ACOLOR) {
-        uint32_t l = S.acol[ac * 32 + lane];
+        uint32_t l = sp<uint32_t>(S.acol)[ac * 32 + lane];
         uint32_t cls = (uint32_t)(rw >> 26) & 0xFF;
         if (l && cls) {
           uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
@@ -261,25 +269,29 @@ __device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
 // payload accumulators and relative liveness), and warp 0 combines the
 // segments (peak = max_w (L before segment w + segment w's relative peak)),
 // scores and writes the records.  S.seq holds the candidates on entry.
-template <int NA>
+template <int NA, bool P2>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
                                            toast_cost* __restrict__ out) {
   __syncthreads();
   if (warp == 0) {
     uint64_t f0, on;
-    S.status[lane] = decode(T, S, lane, f0, on);
-    S.f0[lane] = f0;
-    S.on[lane] = on;
+    sp<uint32_t>(S.status)[lane] = decode(T, S, lane, f0, on);
+    sp<unsigned long long>(S.f0)[lane] = f0;
+    sp<unsigned long long>(S.on)[lane] = on;
   }
   __syncthreads();
   // H2: materialise this warp's share of the signatures; per signature the
   // state-key terms (H7, R14) and the local FLOPs (H3) of all its ops at once
   uint64_t key = 0, flo = 0, fhi = 0;
   {
-    const uint64_t f0 = S.f0[lane], on = S.on[lane];
+    const uint64_t f0 = sp<unsigned long long>(S.f0)[lane], on = sp<unsigned long long>(S.on)[lane];
     for (int s = warp; s < T.n_sigs; s += K) {
       const uint32_t e = pack_entry<NA>(materialize_sig(T, S, lane, s, f0, on));
       ent_store<NA>(S, s, lane, e);
+      uint32_t present = 0;
+#pragma unroll
+      for (int A = 0; A < NA; ++A) present |= (e_dim<NA>(e, A) != 15 ? 1u : 0u) << A;
+      sp<uint8_t>(S.pc)[s * 32 + lane] = (uint8_t)dcode<P2>(T, present);
       uint32_t opmask = 0;
 #pragma unroll
       for (int A = 0; A < NA; ++A) {
@@ -291,7 +303,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       }
       const uint64_t glo = __ldg(T.sig_flops + 2 * s), ghi = __ldg(T.sig_flops + 2 * s + 1);
       if (glo | ghi) {
-        const unsigned __int128 f = exdiv128(T, ((unsigned __int128)ghi << 64) | glo, opmask);
+        const unsigned __int128 f = dv128<P2>(T, ((unsigned __int128)ghi << 64) | glo, opmask);
         const uint64_t l = (uint64_t)f;
         flo += l;
         fhi += (uint64_t)(f >> 64) + ((flo < l) ? 1 : 0);
@@ -300,10 +312,10 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   }
   __syncthreads();
   const int sb = K - 1 + (K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0);   // segment table base for this K
-  unsigned char* acc = S.acc + (size_t)warp * smem_acc_bytes(NA);
-  unsigned long long* pay = reinterpret_cast<unsigned long long*>(acc);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(acc + NA * 4 * 32 * 8);
-  unsigned long long* seg = reinterpret_cast<unsigned long long*>(acc + NA * 4 * 32 * 12);
+  const uint32_t acc = S.acc + (uint32_t)warp * smem_acc_bytes(NA);
+  unsigned long long* pay = sp<unsigned long long>(acc);
+  uint32_t* cnt = sp<uint32_t>(acc + NA * 4 * 32 * 8);
+  unsigned long long* seg = sp<unsigned long long>(acc + NA * 4 * 32 * 12);
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = 0ULL; cnt[q * 32 + lane] = 0u; }
 
@@ -332,7 +344,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     if (dimD != dimU || P) {
       const uint64_t sgb = u64of(t1.x, t1.y);
       const uint32_t ne = t2.x;
-      uint64_t size = exdiv(T, sgb, presD);
+      uint64_t size = dv<P2>(T, sgb, dcode<P2>(T, presD));
 #pragma unroll
       for (int A = 0; A < NA; ++A) {          // phase 1: all_gather / all_to_all
         const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
@@ -350,7 +362,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
         if (!((P >> A) & 1)) continue;
         if (((dimU >> (4 * A)) & 15) != 15) {
-          size = exdiv(T, size, 1u << A);
+          size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
           pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
           cnt[(A * 4 + TOAST_RS) * 32 + lane] += ne;
         } else {
@@ -358,9 +370,9 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
           cnt[(A * 4 + TOAST_AR) * 32 + lane] += ne;
         }
       }
-      tbv = (uint8_t)(presU | (presD << 4));
+      tbv = (uint8_t)(dcode<P2>(T, presU) | (dcode<P2>(T, presD) << 4));
     }
-    S.tb[tix * 32 + lane] = tbv;
+    sp<uint8_t>(S.tb)[tix * 32 + lane] = tbv;
   }
   __syncthreads();
 
@@ -374,11 +386,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     const uint4 h = nh;
     const uint32_t sig = h.x & 0xFFFF, flags = (h.x >> 16) & 0xFF, n_uses = h.x >> 24, n_death = h.y & 0xFF;
     nh = __ldg(p + 1 + n_uses + n_death);   // prefetch the next header (the stream has a 16 B tail)
-    const uint32_t ent = ent_load<NA>(S, sig, lane);
-    uint32_t present = 0;
-#pragma unroll
-    for (int A = 0; A < NA; ++A) present |= (e_dim<NA>(ent, A) != 15 ? 1u : 0u) << A;
-    const long long res = (flags & 2) ? 0 : (long long)exdiv(T, u64of(h.z, h.w), present);
+    const long long res = (flags & 2) ? 0 : (long long)dv<P2>(T, u64of(h.z, h.w), sp<uint8_t>(S.pc)[sig * 32 + lane]);
     long long temp = 0, gmax = 0;
     const uint4* q = p + 1;
     const uint4* gq = q;
@@ -387,10 +395,10 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       const uint32_t tix = u.x >> 16;
       const uint64_t gb = u64of(u.z, u.w & 0x00FFFFFFu);
       if (tix != NO_TMPL) {
-        const uint32_t b = S.tb[tix * 32 + lane];
-        const uint32_t pU = b & 15, pD = b >> 4;
-        if (pU != pD) {
-          const long long g = (long long)exdiv(T, gb, pU) - (long long)exdiv(T, gb, pD);
+        const uint32_t b = sp<uint8_t>(S.tb)[tix * 32 + lane];
+        const uint32_t cU = b & 15, cD = b >> 4;
+        if (cU != cD) {
+          const long long g = (long long)dv<P2>(T, gb, cU) - (long long)dv<P2>(T, gb, cD);
           if (g > 0) temp += g;
         }
         continue;
@@ -399,7 +407,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       const uint32_t uflags = u.w >> 24;
       if (uflags & 1) { gmax = 0; gq = q; }
       const uint32_t de = ent_load<NA>(S, u.x & 0xFFFF, lane);
-      const uint32_t a2r = e_a2r16<NA>(ent);
+      const uint32_t a2r = e_a2r16<NA>(ent_load<NA>(S, sig, lane));
       uint32_t dimU = 0, dimD = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
       for (int A = 0; A < NA; ++A) {
@@ -425,7 +433,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
           dup |= dimU2 == dimU;
         }
         if (!dup) {
-          uint64_t size = exdiv(T, gb, presD);
+          uint64_t size = dv<P2>(T, gb, dcode<P2>(T, presD));
 #pragma unroll
           for (int A = 0; A < NA; ++A) {
             const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
@@ -443,7 +451,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
           for (int A = 0; A < NA; ++A) {
             if (!((P >> A) & 1)) continue;
             if (((dimU >> (4 * A)) & 15) != 15) {
-              size = exdiv(T, size, 1u << A);
+              size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
               pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
               cnt[(A * 4 + TOAST_RS) * 32 + lane] += 1u;
             } else {
@@ -451,7 +459,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
               cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
             }
           }
-          const long long grow = (long long)exdiv(T, gb, presU) - (long long)exdiv(T, gb, presD);
+          const long long grow = (long long)dv<P2>(T, gb, dcode<P2>(T, presU)) - (long long)dv<P2>(T, gb, dcode<P2>(T, presD));
           if (grow > gmax) gmax = grow;
         }
       }
@@ -461,11 +469,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     long long dying = 0;
     for (uint32_t k = 0; k < n_death; ++k, ++q) {
       const uint4 d = __ldg(q);
-      const uint32_t ev = ent_load<NA>(S, d.x & 0xFFFF, lane);
-      uint32_t pres = 0;
-#pragma unroll
-      for (int A = 0; A < NA; ++A) pres |= (e_dim<NA>(ev, A) != 15 ? 1u : 0u) << A;
-      dying += (long long)exdiv(T, u64of(d.z, d.w), pres);
+      dying += (long long)dv<P2>(T, u64of(d.z, d.w), sp<uint8_t>(S.pc)[(d.x & 0xFFFF) * 32 + lane]);
     }
     const long long M = L + res + temp;
     peak = M > peak ? M : peak;
@@ -483,8 +487,8 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     key = 0; flo = 0; fhi = 0;
     long long Lrun = 0, pk_all = 0;
     for (int w = 0; w < K; ++w) {
-      const unsigned char* aw = S.acc + (size_t)w * smem_acc_bytes(NA);
-      const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(aw + NA * 4 * 32 * 12);
+      const uint32_t aw = S.acc + (uint32_t)w * smem_acc_bytes(NA);
+      const unsigned long long* sw = sp<const unsigned long long>(aw + NA * 4 * 32 * 12);
       key += sw[0 * 32 + lane];
       const uint64_t f = sw[1 * 32 + lane];
       flo += f;
@@ -493,12 +497,12 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       if (segpk != LLONG_MIN && Lrun + segpk > pk_all) pk_all = Lrun + segpk;
       Lrun += (long long)sw[3 * 32 + lane];
       if (w) {
-        const unsigned long long* pww = reinterpret_cast<const unsigned long long*>(aw);
-        const uint32_t* cww = reinterpret_cast<const uint32_t*>(aw + NA * 4 * 32 * 8);
+        const unsigned long long* pww = sp<const unsigned long long>(aw);
+        const uint32_t* cww = sp<const uint32_t>(aw + NA * 4 * 32 * 8);
         for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] += pww[q * 32 + lane]; cnt[q * 32 + lane] += cww[q * 32 + lane]; }
       }
     }
-    const uint32_t status = S.status[lane];
+    const uint32_t status = sp<uint32_t>(S.status)[lane];
     // H6 score (C13): fixed order, explicit round-to-nearest, no FMA
     double tt = __ddiv_rn(__dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo)), T.F);
     unsigned long long ncoll = 0;
@@ -564,14 +568,14 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    S.seq[(4 * k + 0) * 32 + lane] = w[k].x;
-    S.seq[(4 * k + 1) * 32 + lane] = w[k].y;
-    S.seq[(4 * k + 2) * 32 + lane] = w[k].z;
-    S.seq[(4 * k + 3) * 32 + lane] = w[k].w;
+    sp<uint32_t>(S.seq)[(4 * k + 0) * 32 + lane] = w[k].x;
+    sp<uint32_t>(S.seq)[(4 * k + 1) * 32 + lane] = w[k].y;
+    sp<uint32_t>(S.seq)[(4 * k + 2) * 32 + lane] = w[k].z;
+    sp<uint32_t>(S.seq)[(4 * k + 3) * 32 + lane] = w[k].w;
   }
 }
 
-template <int NA>
+template <int NA, bool P2>
 __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -581,7 +585,7 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
     const int64_t i = b * 32 + lane;
     const bool valid = i < n;
     if (warp == 0) load_seq(S, seqs + i * 32, lane, valid);
-    batch_eval<NA>(T, S, K, warp, lane, valid, out + i);
+    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i);
   }
 }
 
@@ -600,7 +604,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
   o1 = c1;
 }
 
-template <int NA>
+template <int NA, bool P2>
 __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
     int stop = 32;
     bool bad = false;
     for (int j = 0; j < 32; ++j) {
-      const uint32_t id = (S.seq[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+      const uint32_t id = (sp<uint32_t>(S.seq)[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
       if (stop < 32) { bad |= id != 0; continue; }
       if (id == 0) { stop = j; continue; }
       bad |= (int)id >= T.n_actions;
@@ -630,11 +634,11 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
         const int hi = T.n_actions - w * 32;   // ids >= n_actions are not actions
         if (hi < 32) v = hi <= 0 ? 0u : ((1u << hi) - 1u);
         if (w == 0) v &= ~1u;                 // STOP is not in the legal set
-        S.legal[w * 32 + lane] = v;
+        sp<uint32_t>(S.legal)[w * 32 + lane] = v;
       }
       for (int j = 0; j < stop; ++j) {
-        const uint32_t a = (S.seq[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
-        for (int w = 0; w < nw; ++w) S.legal[w * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w);
+        const uint32_t a = (sp<uint32_t>(S.seq)[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+        for (int w = 0; w < nw; ++w) sp<uint32_t>(S.legal)[w * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w);
       }
       const uint64_t id = id_base + (uint64_t)i;
       for (int d = stop; d < T.max_depth; ++d) {
@@ -642,21 +646,21 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
         philox4x32_10((uint32_t)id, (uint32_t)(id >> 32), (uint32_t)d, 0u, seed_lo, seed_hi, r0, r1);
         if ((uint64_t)r0 * (uint64_t)T.max_depth < ((uint64_t)d << 32)) break;   // p_stop = d / max_depth
         uint32_t total = 0;
-        for (int w = 0; w < nw; ++w) total += __popc(S.legal[w * 32 + lane]);
+        for (int w = 0; w < nw; ++w) total += __popc(sp<uint32_t>(S.legal)[w * 32 + lane]);
         if (total == 0) break;
         uint32_t k = (uint32_t)(((uint64_t)r1 * total) >> 32);
         int w = 0;
         uint32_t word = 0;
         for (; w < nw; ++w) {
-          word = S.legal[w * 32 + lane];
+          word = sp<uint32_t>(S.legal)[w * 32 + lane];
           const uint32_t c = __popc(word);
           if (k < c) break;
           k -= c;
         }
         for (uint32_t q = 0; q < k; ++q) word &= word - 1;
         const uint32_t a = (uint32_t)w * 32 + (uint32_t)(__ffs(word) - 1);
-        for (int w2 = 0; w2 < nw; ++w2) S.legal[w2 * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w2);
-        uint32_t& sw = S.seq[(d >> 1) * 32 + lane];
+        for (int w2 = 0; w2 < nw; ++w2) sp<uint32_t>(S.legal)[w2 * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w2);
+        uint32_t& sw = sp<uint32_t>(S.seq)[(d >> 1) * 32 + lane];
         sw = (d & 1) ? ((sw & 0xFFFFu) | (a << 16)) : ((sw & 0xFFFF0000u) | a);
       }
     }
@@ -665,11 +669,11 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
       uint4* dst = reinterpret_cast<uint4*>(out_seqs + i * 32);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        dst[k] = make_uint4(S.seq[(4 * k) * 32 + lane], S.seq[(4 * k + 1) * 32 + lane], S.seq[(4 * k + 2) * 32 + lane],
-                            S.seq[(4 * k + 3) * 32 + lane]);
+        dst[k] = make_uint4(sp<uint32_t>(S.seq)[(4 * k) * 32 + lane], sp<uint32_t>(S.seq)[(4 * k + 1) * 32 + lane], sp<uint32_t>(S.seq)[(4 * k + 2) * 32 + lane],
+                            sp<uint32_t>(S.seq)[(4 * k + 3) * 32 + lane]);
     }
     }   // warp 0
-    batch_eval<NA>(T, S, K, warp, lane, valid, out + i);
+    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i);
   }
 }
 
@@ -709,10 +713,25 @@ __global__ void toast_round_reduce_kernel(const toast_cost* __restrict__ lcost, 
   }
 }
 
-template <int NA>
+template <int NA, bool P2>
 void set_smem_attr(int bytes) {
-  cudaFuncSetAttribute(toast_eval_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(toast_rollout_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(toast_eval_kernel<NA, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(toast_rollout_kernel<NA, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// call f.template operator()<NA, P2>() for the analysis' (axis count, power-of-two) variant
+template <typename F>
+auto dispatch(int n_axes, bool p2, F&& f) {
+  switch (n_axes * 2 + (p2 ? 1 : 0)) {
+    case 2: return f.template operator()<1, false>();
+    case 3: return f.template operator()<1, true>();
+    case 4: return f.template operator()<2, false>();
+    case 5: return f.template operator()<2, true>();
+    case 6: return f.template operator()<3, false>();
+    case 7: return f.template operator()<3, true>();
+    case 8: return f.template operator()<4, false>();
+    default: return f.template operator()<4, true>();
+  }
 }
 
 }  // namespace
@@ -784,26 +803,19 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     return TOAST_E_LIMIT;
   }
   // the attribute is per function, shared by every analysis in the process: allow the device maximum
-  set_smem_attr<1>(dev_smem);
-  set_smem_attr<2>(dev_smem);
-  set_smem_attr<3>(dev_smem);
-  set_smem_attr<4>(dev_smem);
+  dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() { set_smem_attr<NA, P2>(dev_smem); return 0; });
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
     const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
-      switch (T.n_axes) {
-        case 1: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<1>, 32 * K, sm));
-                TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<1>, 32 * K, sm)); break;
-        case 2: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<2>, 32 * K, sm));
-                TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<2>, 32 * K, sm)); break;
-        case 3: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<3>, 32 * K, sm));
-                TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<3>, 32 * K, sm)); break;
-        default: TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<4>, 32 * K, sm));
-                 TOAST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<4>, 32 * K, sm)); break;
-      }
+      cudaError_t e = dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
+        cudaError_t e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<NA, P2>, 32 * K, sm);
+        cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<NA, P2>, 32 * K, sm);
+        return e1 != cudaSuccess ? e1 : e2;
+      });
+      TOAST_CUDA(e);
     }
     a->occ_eval[i] = be;
     a->occ_roll[i] = br;
@@ -856,12 +868,11 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const dim3 g((unsigned)blocks), b(32 * K);
   const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
   cudaStream_t st = (cudaStream_t)stream;
-  switch (a->dt.n_axes) {
-    case 1: toast_eval_kernel<1><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
-    case 2: toast_eval_kernel<2><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
-    case 3: toast_eval_kernel<3><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
-    default: toast_eval_kernel<4><<<g, b, sm, st>>>(a->dt, d_seqs, n, d_out); break;
-  }
+  const DeviceTables& T = a->dt;
+  dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
+    toast_eval_kernel<NA, P2><<<g, b, sm, st>>>(T, d_seqs, n, d_out);
+    return 0;
+  });
   TOAST_CUDA(cudaGetLastError());
   return TOAST_OK;
 }
@@ -875,12 +886,11 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const dim3 g((unsigned)blocks), b(32 * K);
   const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
   cudaStream_t st = (cudaStream_t)stream;
-  switch (a->dt.n_axes) {
-    case 1: toast_rollout_kernel<1><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
-    case 2: toast_rollout_kernel<2><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
-    case 3: toast_rollout_kernel<3><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
-    default: toast_rollout_kernel<4><<<g, b, sm, st>>>(a->dt, d_pre, n, seed, id_base, d_seqs, d_out, rep); break;
-  }
+  const DeviceTables& T = a->dt;
+  dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
+    toast_rollout_kernel<NA, P2><<<g, b, sm, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep);
+    return 0;
+  });
   TOAST_CUDA(cudaGetLastError());
   return TOAST_OK;
 }
