@@ -732,6 +732,14 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       }
     }
     if (a->h_tmpl.size() >= NO_TMPL) { err = "more than 65534 edge templates"; return TOAST_E_LIMIT; }
+    // stream window for the kernels' bulk copies: chunk stride W, overlap E >= the largest op record
+    {
+      int32_t maxrec = 1;
+      for (int32_t t = 0; t < n_ops; ++t)
+        maxrec = std::max<int32_t>(maxrec, 1 + (int32_t)g->ops[t].operands.size() + (int32_t)deaths[t].size());
+      a->dt.win_w = 64;
+      a->dt.win_e = (maxrec + 7) & ~7;
+    }
     // op segments (balanced by stream words) for K = 1, 2, 4, 8 sweeping warps
     {
       std::vector<uint32_t> off(n_ops + 1, 0);

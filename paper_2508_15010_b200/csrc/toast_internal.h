@@ -160,6 +160,7 @@ struct DeviceTables {
   // constants
   int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
+  int32_t win_w, win_e;  // stream window: chunk stride and overlap in 16-byte words (overlap >= largest op record)
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
