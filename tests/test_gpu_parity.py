@@ -76,13 +76,13 @@ def assert_same(g: np.ndarray, o: np.ndarray, ctx=""):
         assert len(bad) == 0, (ctx, f, bad[:5], g[f][bad[:5]], o[f][bad[:5]])
 
 
-ALL = ["mlp_c", "attn_toy", "gpt2", "gpt24", "gns16", "unet"]
+ALL = ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt24", "gns16", "unet"]
 
 
 @pytest.mark.parametrize("name", ALL)
 def test_eval_parity_on_oracle_rollouts(name):
     a, o = setup(name)
-    n = 3000 if name in ("mlp_c", "attn_toy", "gpt2") else 300
+    n = 3000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2") else 300
     seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=1234, threads=8)
     assert_same(gpu_eval(a, seqs), oc, name)
 
@@ -153,11 +153,11 @@ def test_eval_host_pointer_path_and_edges():
     T.eval_batch(a, seqs[:0], one[:0], n=0)
 
 
-@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt24", "unet", "gns16"])
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt24", "unet", "gns16"])
 def test_rollout_parity(name):
     """K2 vs C15: same (seed, id) -> same sequence and same cost record."""
     a, o = setup(name)
-    n = 2000 if name in ("mlp_c", "attn_toy", "gpt2") else 200
+    n = 2000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2") else 200
     pre = np.zeros((n, 32), np.uint16)
     # half the rows start from a (legal) prefix drawn by the oracle
     s0, _ = o.rollout(np.zeros((n // 2, 32), np.uint16), seed=77)
@@ -265,3 +265,35 @@ def test_root_parallel_search_nccl_single_rank():
     assert int(r["rounds"]) == int(ref["rounds"]) and int(r["evals"]) == int(ref["evals"])
     assert np.array_equal(r["best_seq"], ref["best_seq"]) and r["best"]["score"] == ref["best"]["score"]
     assert len(trace) == int(r["rounds"]) and trace[-1] == r["best"]["score"]
+
+
+def test_random_programs_parity_including_repeated_operands():
+    """Random programs (repeated operands such as mul(x, x) / matmul(x, x) take
+    the per-edge path; the rest go through edge templates), two meshes, oracle
+    rollouts and raw ids, compared record by record."""
+    from workloads import models
+    T = _T()
+    n_rep = 0
+    for seed in range(24):
+        ir = models.random_program(seed, n_ops=18)
+        n_rep += sum(1 for l in ir.splitlines() if "(" in l and len(set(x.strip() for x in l[l.index("(") + 1:l.rindex(")")].split(","))) == 1 and "," in l)
+        for axes in ([("a", 2, 1e10), ("b", 4, 1e11)], [("a", 3, 1e10), ("b", 2, 2e10)]):
+            try:
+                o = Oracle(ir, axes, 1e12, 1 << 12, 100.0, 1, 30)
+            except Exception:
+                continue
+            a = T.build_analysis(ir, axes, 1e12, 1 << 12, 100.0, 1, 30, cuda_device=0)
+            seqs, oc = o.rollout(np.zeros((256, 32), np.uint16), seed=seed)
+            assert_same(gpu_eval(a, seqs), oc, f"random {seed} {axes}")
+            raw = candidates.uniform(128, o.n_actions + 1, seed=seed)
+            assert_same(gpu_eval(a, raw), o.eval(raw), f"random raw {seed}")
+    assert n_rep > 0   # the per-edge (repeated operand) path was exercised
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 64, 200, 1000])
+def test_small_batches_use_segmented_sweep(n):
+    """Batches below one wave are swept by K > 1 warps per block (segmented
+    liveness scan); results must not depend on K."""
+    a, o = setup("gpt24")
+    seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=n)
+    assert_same(gpu_eval(a, seqs), oc, f"n={n}")

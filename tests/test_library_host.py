@@ -38,7 +38,7 @@ def _both(name):
     return a, o, c
 
 
-@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt24", "gns16", "unet"])
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt24", "gns16", "unet"])
 def test_h0_analysis_equals_oracle(name):
     """H0 parity: loop table, components, super-colors, conflicts, sets, sides,
     WL signatures, groups, action table and baseline are identical."""

@@ -63,6 +63,11 @@ def get(name: str, **kw) -> Config:
         return Config("gpt2", models.gpt(layers=2, B=8, S=64, D=64, H=4, Dh=16, F=256, V=512, name="gpt2"),
                       _b200_mesh(("data", 8), ("model", 4)), F_B200, 1 << 22, 100.0, 10,
                       description="2-layer GPT (small widths), mesh {data:8, model:4}")
+    if name == "gpt2_np2":
+        # non-power-of-two mesh {data:3, model:6}: exact division by odd products
+        return Config("gpt2_np2", models.gpt(layers=2, B=12, S=48, D=96, H=6, Dh=16, F=384, V=384, name="gpt2np2"),
+                      (("data", 3, BW_NIC), ("model", 6, BW_NVLINK)), F_B200, 1 << 22, 100.0, 10,
+                      description="2-layer GPT on a non-power-of-two mesh {data:3, model:6}")
     if name == "unet":
         return Config("unet", models.unet(), _b200_mesh(("batch", 4), ("model", 8)), F_B200, DM_B200, 100.0, 10,
                       description="M3 U-Net, mesh {batch:4, model:8}")
