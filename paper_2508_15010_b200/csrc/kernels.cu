@@ -933,6 +933,11 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
 
 void free_tables(toast_analysis* a) {
   if (a->device >= 0) cudaSetDevice(a->device);
+  for (int i = 0; i < 2; ++i)
+    if (a->pipe_stream[i]) cudaStreamDestroy((cudaStream_t)a->pipe_stream[i]);
+  if (a->pipe_event) cudaEventDestroy((cudaEvent_t)a->pipe_event);
+  a->pipe_stream[0] = a->pipe_stream[1] = nullptr;
+  a->pipe_event = nullptr;
   for (void* p : a->dev_allocs) cudaFree(p);
   a->dev_allocs.clear();
   if (a->scratch) cudaFree(a->scratch);
@@ -999,7 +1004,18 @@ toast_status launch_round_reduce(const toast_cost* d_lcost, const uint16_t* d_lp
 }
 size_t leaf_red_bytes() { return sizeof(LeafRed); }
 
-// host-pointer path: stage through device scratch on `stream`, then wait
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// host-pointer path: stage through device scratch, then wait.  Pinned host
+// buffers are pipelined in chunks on two internal streams (after the caller's
+// stream's prior work) so PCIe transfers overlap the kernels.
 toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h_in, int64_t n, uint64_t seed,
                               uint64_t id_base, uint16_t* h_seqs, toast_cost* h_out, void* stream, std::string& err) {
   if (n <= 0) return TOAST_OK;
@@ -1017,13 +1033,39 @@ toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h
   toast_cost* d_out = reinterpret_cast<toast_cost*>(a->scratch);
   uint16_t* d_in = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(a->scratch) + out_b);
   uint16_t* d_seqs = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(a->scratch) + out_b + in_b);
-  TOAST_CUDA(cudaMemcpyAsync(d_in, h_in, in_b, cudaMemcpyHostToDevice, s));
-  toast_status st = rollout ? launch_rollout(a, d_in, n, seed, id_base, d_seqs, d_out, stream, err, 1)
-                            : launch_eval(a, d_in, n, d_out, stream, err);
-  if (st) return st;
-  TOAST_CUDA(cudaMemcpyAsync(h_out, d_out, out_b, cudaMemcpyDeviceToHost, s));
-  if (rollout) TOAST_CUDA(cudaMemcpyAsync(h_seqs, d_seqs, in_b, cudaMemcpyDeviceToHost, s));
-  TOAST_CUDA(cudaStreamSynchronize(s));
+  const int64_t wave = (int64_t)std::min(a->occ_eval[0], a->occ_roll[0]) * a->n_sms * 32;
+  const bool pipelined = n >= 2 * std::max<int64_t>(wave / 2, 1) && is_pinned(h_in) && is_pinned(h_out) &&
+                         (!rollout || is_pinned(h_seqs));
+  if (!pipelined) {
+    TOAST_CUDA(cudaMemcpyAsync(d_in, h_in, in_b, cudaMemcpyHostToDevice, s));
+    toast_status st = rollout ? launch_rollout(a, d_in, n, seed, id_base, d_seqs, d_out, stream, err, 1)
+                              : launch_eval(a, d_in, n, d_out, stream, err);
+    if (st) return st;
+    TOAST_CUDA(cudaMemcpyAsync(h_out, d_out, out_b, cudaMemcpyDeviceToHost, s));
+    if (rollout) TOAST_CUDA(cudaMemcpyAsync(h_seqs, d_seqs, in_b, cudaMemcpyDeviceToHost, s));
+    TOAST_CUDA(cudaStreamSynchronize(s));
+    return TOAST_OK;
+  }
+  if (!a->pipe_stream[0]) {
+    for (int i = 0; i < 2; ++i) TOAST_CUDA(cudaStreamCreateWithFlags((cudaStream_t*)&a->pipe_stream[i], cudaStreamNonBlocking));
+    TOAST_CUDA(cudaEventCreateWithFlags((cudaEvent_t*)&a->pipe_event, cudaEventDisableTiming));
+  }
+  TOAST_CUDA(cudaEventRecord((cudaEvent_t)a->pipe_event, s));
+  for (int i = 0; i < 2; ++i) TOAST_CUDA(cudaStreamWaitEvent((cudaStream_t)a->pipe_stream[i], (cudaEvent_t)a->pipe_event, 0));
+  const int64_t chunk = std::max<int64_t>(wave / 2, 32);
+  int c = 0;
+  for (int64_t o = 0; o < n; o += chunk, ++c) {
+    const int64_t m = std::min(chunk, n - o);
+    cudaStream_t ps = (cudaStream_t)a->pipe_stream[c & 1];
+    TOAST_CUDA(cudaMemcpyAsync(d_in + o * 32, h_in + o * 32, (size_t)m * 64, cudaMemcpyHostToDevice, ps));
+    toast_status st = rollout ? launch_rollout(a, d_in + o * 32, m, seed, id_base + (uint64_t)o, d_seqs + o * 32,
+                                               d_out + o, ps, err, 1)
+                              : launch_eval(a, d_in + o * 32, m, d_out + o, ps, err);
+    if (st) return st;
+    TOAST_CUDA(cudaMemcpyAsync(h_out + o, d_out + o, (size_t)m * sizeof(toast_cost), cudaMemcpyDeviceToHost, ps));
+    if (rollout) TOAST_CUDA(cudaMemcpyAsync(h_seqs + o * 32, d_seqs + o * 32, (size_t)m * 64, cudaMemcpyDeviceToHost, ps));
+  }
+  for (int i = 0; i < 2; ++i) TOAST_CUDA(cudaStreamSynchronize((cudaStream_t)a->pipe_stream[i]));
   return TOAST_OK;
 }
 

@@ -297,3 +297,24 @@ def test_small_batches_use_segmented_sweep(n):
     a, o = setup("gpt24")
     seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=n)
     assert_same(gpu_eval(a, seqs), oc, f"n={n}")
+
+
+def test_pinned_host_pipeline_matches_device_path():
+    """Pinned host buffers take the chunked two-stream pipeline; results equal
+    the device-resident call (and hence the oracle) record for record."""
+    import torch
+    T = _T()
+    a, o = setup("gpt24")
+    n = 2 * a.preferred_batch() + 77
+    h_pre = torch.zeros((n, 32), dtype=torch.int16).pin_memory()
+    h_seq = torch.empty_like(h_pre).pin_memory()
+    h_out = torch.empty((n, 256), dtype=torch.uint8).pin_memory()
+    T.rollout_batch(a, h_pre, 99, 5, h_seq, h_out)
+    gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), 99, 5)
+    assert np.array_equal(h_seq.numpy().view(np.uint16), gs)
+    assert h_out.numpy().tobytes() == gc.tobytes()
+    idx = np.random.default_rng(2).choice(n, 16, replace=False)
+    for i in idx:
+        s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=99, id_base=5 + int(i))
+        assert np.array_equal(gs[i], s1[0])
+        assert_same(gc[i:i + 1], c1)
