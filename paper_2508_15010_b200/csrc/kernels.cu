@@ -87,7 +87,23 @@ template <typename V>
 __device__ __forceinline__ V* sp(uint32_t off) { return reinterpret_cast<V*>(g_smem + off); }
 // 32-bit shared-window loads for the sweep's read-only tables (the generic
 // path re-derives the CTA's shared window on every access)
-__device__ __forceinline__ uint32_t smem_base() { return (uint32_t)__cvta_generic_to_shared(g_smem); }
+__device__ __forceinline__ uint32_t smem_base() {
+  // opaque to the compiler, so the base stays in a register instead of being
+  // re-derived from the CTA's shared window at every access
+  uint32_t r;
+  asm volatile("{\n .reg .u64 t;\n cvta.to.shared.u64 t, %1;\n cvt.u32.u64 %0, t;\n}" : "=r"(r) : "l"(g_smem));
+  return r;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -475,8 +491,10 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         // a value used more than once by this op: costed per edge, once per distinct layout
         const uint32_t uflags = u.w >> 24;
         if (uflags & 1) { gmax = 0; gq = q; }
-        const uint32_t de = ent_load<NA>(S, u.x & 0xFFFF, lane);
-        const uint32_t a2r = e_a2r16<NA>(ent_load<NA>(S, sig, lane));
+        const uint32_t esz = sizeof(typename Ent<NA>::T);
+        const uint32_t ea = sh + S.sig + (uint32_t)lane * esz;
+        const uint32_t de = esz == 2 ? lds_u16(ea + (u.x & 0xFFFF) * 32 * esz) : lds_u32(ea + (u.x & 0xFFFF) * 32 * esz);
+        const uint32_t a2r = e_a2r16<NA>(esz == 2 ? lds_u16(ea + sig * 32 * esz) : lds_u32(ea + sig * 32 * esz));
         uint32_t dimU = 0, dimD = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
         for (int A = 0; A < NA; ++A) {
