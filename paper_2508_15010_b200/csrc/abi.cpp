@@ -33,7 +33,7 @@ toast_status ret(toast_status st, const std::string& msg) {
   g_err = st == TOAST_OK ? std::string() : msg;
   return st;
 }
-bool has_device(const toast_analysis* a) { return a && a->device >= 0 && a->dt.stream != nullptr; }
+bool has_device(const toast_analysis* a) { return a && a->device >= 0 && a->dt.points != nullptr; }
 }  // namespace
 
 extern "C" {

@@ -664,24 +664,16 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       a->h_sig_flops[q * 2] = (uint64_t)f;
       a->h_sig_flops[q * 2 + 1] = (uint64_t)(f >> 64);
     }
-    // the stream (+ edge templates)
-    auto push = [&](const void* rec, size_t bytes) {
-      const uint32_t* w = reinterpret_cast<const uint32_t*>(rec);
-      a->h_stream.insert(a->h_stream.end(), w, w + bytes / 4);
-    };
+    // edge templates (C11): use edges with the same (def signature, use
+    // signature, use role->dim map) communicate identically for a candidate;
+    // a value used more than once by one op is a "special" edge group, costed
+    // edge by edge (within-op dedup, G26)
     std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint32_t> tmpl_id;
     a->h_tmpl.clear();
-    a->h_stream.clear();
+    std::vector<std::vector<std::pair<uint32_t, uint64_t>>> op_tmpl(n_ops);   // per op: (template, def bytes)
+    std::vector<std::vector<KUse>> op_spec(n_ops);                            // per op: its special edges
     for (int32_t t = 0; t < n_ops; ++t) {
       const GOp& op = g->ops[t];
-      KHead h{};
-      h.sig = (uint16_t)a->op_sig[t];
-      h.flags = a->h_ops[t].flags;
-      h.n_uses = (uint8_t)op.operands.size();
-      if (deaths[t].size() > 255) { err = "too many values die at one op"; return TOAST_E_LIMIT; }
-      h.n_death = (uint8_t)deaths[t].size();
-      h.gbytes = a->h_ops[t].gbytes;
-      push(&h, sizeof h);
       std::vector<int> order(op.operands.size());
       std::iota(order.begin(), order.end(), 0);
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
@@ -690,8 +682,6 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       for (size_t q = 0; q < order.size(); ++q) {
         int k = order[q];
         int32_t v = g->values[op.operands[k]].def_op;
-        KUse u{};
-        u.def_sig = (uint16_t)a->op_sig[v];
         bool first = q == 0 || g->values[op.operands[order[q - 1]]].def_op != v;
         bool last = q + 1 == order.size() || g->values[op.operands[order[q + 1]]].def_op != v;
         uint32_t um = ~0u;
@@ -699,10 +689,8 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
           uint32_t r = OL[t].use_role[k][i];
           um = (um & ~(0xFu << (4 * r))) | ((uint32_t)i << (4 * r));
         }
-        u.use_dimof = um;
         const uint64_t gb = a->h_ops[v].gbytes;
-        if (gb >> 56) { err = "a value larger than 2^56 bytes"; return TOAST_E_LIMIT; }
-        u.gb_flags = gb | ((uint64_t)((first ? 1 : 0) | (last ? 2 : 0)) << 56);
+        if (gb >> 48) { err = "a value larger than 2^48 bytes"; return TOAST_E_LIMIT; }
         if (first && last) {   // the value is used once here: cost it through its template
           auto key = std::make_tuple(a->op_sig[v], a->op_sig[t], um);
           auto it = tmpl_id.find(key);
@@ -718,52 +706,116 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
           if (tm.sum_gbytes + gb < tm.sum_gbytes) { err = "template byte sum overflows"; return TOAST_E_LIMIT; }
           tm.sum_gbytes += gb;
           tm.n_edges += 1;
-          u.tmpl = (uint16_t)it->second;
+          op_tmpl[t].push_back({it->second, gb});
         } else {
+          KUse u{};
+          u.def_sig = (uint16_t)a->op_sig[v];
           u.tmpl = NO_TMPL;
+          u.use_dimof = um;
+          u.gb_flags = gb | ((uint64_t)((first ? 1 : 0) | (last ? 2 : 0)) << 56);
+          op_spec[t].push_back(u);
         }
-        push(&u, sizeof u);
-      }
-      for (int32_t v : deaths[t]) {
-        KDeath d{};
-        d.sig = (uint16_t)a->op_sig[v];
-        d.gbytes = a->h_ops[v].gbytes;
-        push(&d, sizeof d);
       }
     }
     if (a->h_tmpl.size() >= NO_TMPL) { err = "more than 65534 edge templates"; return TOAST_E_LIMIT; }
-    // stream window for the kernels' bulk copies: chunk stride W, overlap E >= the largest op record
+
+    // peak-memory frontier (C12, reading R19).  For a candidate with
+    // per-signature result divisors d_s and per-template growth factors g_tm,
+    //   M_t = sum_s Live_t[s] / d_s + sum_tm Tmp_t[tm] * g_tm + special_t,
+    // where Live_t[s] = global bytes of signature-s values live after t-1 plus
+    // t's result, and Tmp_t[tm] = global bytes of t's template-tm edges (every
+    // term is an exact integer: each value divides exactly).  M_t is linear in
+    // the weights w = (1/d_s, g_tm), and w lies in the box
+    //   1/prod(all axes) <= 1/d_s <= 1,   0 <= g_tm <= 1 - 1/prod(all axes)
+    // (a signature none of whose result dims an action can shard has
+    // 1/d_s = 1; a template whose def signature is such has g_tm = 0).  So op t
+    // can be dropped whenever another kept op q has M_q >= M_t for EVERY w in
+    // the box — peak = max_t M_t is unchanged, bit for bit.  Ops with special
+    // edges are always kept (their own term is not linear).
     {
-      int32_t maxrec = 1;
-      for (int32_t t = 0; t < n_ops; ++t)
-        maxrec = std::max<int32_t>(maxrec, 1 + (int32_t)g->ops[t].operands.size() + (int32_t)deaths[t].size());
-      a->dt.win_w = 64;
-      a->dt.win_e = (maxrec + 7) & ~7;
-    }
-    // op segments (balanced by stream words) for K = 1, 2, 4, 8 sweeping warps
-    {
-      std::vector<uint32_t> off(n_ops + 1, 0);
-      size_t w = 0;
-      for (int32_t t = 0; t < n_ops; ++t) {
-        off[t] = (uint32_t)w;
-        w += 1 + g->ops[t].operands.size() + deaths[t].size();
-      }
-      off[n_ops] = (uint32_t)w;
-      for (int K = 1, lg = 0; K <= 8; K *= 2, ++lg) {
-        const int b = K - 1 + lg;
-        int t = 0;
-        for (int q = 0; q <= K; ++q) {
-          const double target = (double)w * q / K;
-          while (t < n_ops && (double)off[t] < target) ++t;
-          a->dt.seg_op[b + q] = q == K ? n_ops : t;
-          a->dt.seg_off[b + q] = off[a->dt.seg_op[b + q]];
+      const size_t NS = sig_words.size(), NT = a->h_tmpl.size(), D = 1 + NS + NT;   // [0] = constant
+      int64_t prodall = 1;
+      for (int A = 0; A < n_axes; ++A) prodall *= g->axis_size[A];
+      std::vector<char> sig_fixed(NS, 1);
+      for (size_t q = 0; q < NS; ++q)
+        for (size_t r = 0; r < sig_words[q].size(); ++r)
+          if ((sig_words[q][r] & 0x3FF) != NO_ACOLOR && ((sig_rd[q] >> (4 * r)) & 15) != 15) sig_fixed[q] = 0;
+      std::vector<int64_t> lo(D), hi(D);   // weight bounds x prodall
+      lo[0] = hi[0] = prodall;
+      for (size_t q = 0; q < NS; ++q) { lo[1 + q] = sig_fixed[q] ? prodall : 1; hi[1 + q] = prodall; }
+      for (size_t q = 0; q < NT; ++q) { lo[1 + NS + q] = 0; hi[1 + NS + q] = sig_fixed[a->h_tmpl[q].def_sig] ? 0 : prodall - 1; }
+      auto geq = [&](const std::vector<int64_t>& x, const std::vector<int64_t>& y) {   // x >= y for every w in the box
+        __int128 m = 0;
+        for (size_t d = 0; d < D; ++d) {
+          const __int128 df = (__int128)x[d] - y[d];
+          m += df * (df > 0 ? lo[d] : hi[d]);
         }
+        return m >= 0;
+      };
+      std::vector<int64_t> Lv(NS, 0);
+      std::vector<std::vector<int64_t>> P;
+      std::vector<int32_t> Pt;
+      for (int32_t t = 0; t < n_ops; ++t) {
+        std::vector<int64_t> p(D, 0);
+        for (size_t q = 0; q < NS; ++q) p[1 + q] = Lv[q];
+        p[1 + a->op_sig[t]] += (int64_t)a->h_ops[t].gbytes;
+        for (auto& e : op_tmpl[t]) p[1 + NS + e.first] += (int64_t)e.second;
+        // fold the fixed weights into the constant
+        for (size_t q = 0; q < NS; ++q)
+          if (sig_fixed[q]) { p[0] += p[1 + q]; p[1 + q] = 0; }
+        for (size_t q = 0; q < NT; ++q)
+          if (hi[1 + NS + q] == 0) p[1 + NS + q] = 0;
+        Lv[a->op_sig[t]] += (int64_t)a->h_ops[t].gbytes;
+        for (int32_t v : deaths[t]) Lv[a->op_sig[v]] -= (int64_t)a->h_ops[v].gbytes;
+        const bool special = !op_spec[t].empty();
+        if (!special) {
+          bool dom = false;
+          for (auto& x : P) if (geq(x, p)) { dom = true; break; }
+          if (dom) continue;
+        }
+        for (size_t i = 0; i < P.size();) {
+          if (op_spec[Pt[i]].empty() && geq(p, P[i])) {
+            P[i] = std::move(P.back()); P.pop_back();
+            Pt[i] = Pt.back(); Pt.pop_back();
+          } else {
+            ++i;
+          }
+        }
+        P.push_back(std::move(p));
+        Pt.push_back(t);
+      }
+      std::vector<size_t> ord(P.size());
+      std::iota(ord.begin(), ord.end(), 0);
+      std::sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return Pt[x] < Pt[y]; });
+      a->h_points.clear();
+      a->h_terms.clear();
+      a->h_spec.clear();
+      a->point_op.clear();
+      for (size_t i : ord) {
+        const auto& p = P[i];
+        const int32_t t = Pt[i];
+        KPoint kp{};
+        kp.term_begin = (uint32_t)a->h_terms.size();
+        a->h_terms.push_back((uint64_t)p[0]);
+        for (size_t q = 0; q < NS; ++q)
+          if (p[1 + q]) { a->h_terms.push_back((uint64_t)p[1 + q] | ((uint64_t)q << 48)); ++kp.n_sig; }
+        for (size_t q = 0; q < NT; ++q)
+          if (p[1 + NS + q]) { a->h_terms.push_back((uint64_t)p[1 + NS + q] | ((uint64_t)q << 48)); ++kp.n_tmpl; }
+        for (size_t d = 1; d < D; ++d)
+          if ((uint64_t)p[d] >> 48) { err = "a live-byte sum of 2^48 bytes or more"; return TOAST_E_LIMIT; }
+        kp.spec_begin = (uint32_t)a->h_spec.size();
+        kp.n_spec = (uint16_t)op_spec[t].size();
+        if (op_spec[t].size() > 65535) { err = "too many repeated operands at one op"; return TOAST_E_LIMIT; }
+        kp.use_sig = (uint16_t)a->op_sig[t];
+        for (auto& u : op_spec[t]) a->h_spec.push_back(u);
+        a->h_points.push_back(kp);
+        a->point_op.push_back(t);
       }
     }
     if (getenv("TOAST_DEBUG"))
-      fprintf(stderr, "[toast] ops %d loops %lld signatures %zu templates %zu stream %zu B actions %zu desel classes %zu\n",
-              n_ops, (long long)NL, sig_words.size(), a->h_tmpl.size(), a->h_stream.size() * 4, a->actions.size(),
-              a->h_desel_cls.size() / 2);
+      fprintf(stderr, "[toast] ops %d loops %lld signatures %zu templates %zu frontier points %zu terms %zu actions %zu desel classes %zu\n",
+              n_ops, (long long)NL, sig_words.size(), a->h_tmpl.size(), a->h_points.size(), a->h_terms.size(),
+              a->actions.size(), a->h_desel_cls.size() / 2);
   }
 
   // ------------------------------------------------------------ baseline (empty sequence)
@@ -808,6 +860,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
   T.max_depth = o->max_depth;
   T.n_sigs = (int32_t)a->h_sig_nroles.size();
   T.n_tmpl = (int32_t)a->h_tmpl.size();
+  T.n_points = (int32_t)a->h_points.size();
   T.pow2 = 1;
   for (int A = 0; A < n_axes; ++A) if (g->axis_size[A] & (g->axis_size[A] - 1)) T.pow2 = 0;
   for (int A = 0; A < 4; ++A) {

@@ -71,13 +71,9 @@ __host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
   return r16(b1 > b2 ? b1 : b2);
 }
 __host__ __device__ inline int smem_d_bytes(int n_tmpl) { return r16(n_tmpl * 32); }
-// F: per sweeping warp, a double-buffered window over its op-stream segment
-// (2 x (W + E) 16-byte words, filled by cp.async.bulk) and its 2 mbarriers
-__host__ __device__ inline int smem_win_bytes(int win_w, int win_e) { return 2 * (win_w + win_e) * 16 + 16; }
-__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl, int win_w,
-                                                int win_e) {
+__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl) {
   return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl) +
-         r16(n_sigs * 32) + K * smem_win_bytes(win_w, win_e);
+         r16(n_sigs * 32);
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -120,7 +116,6 @@ struct Smem {               // byte offsets into g_smem
   uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
   uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
-  uint32_t win;             // per warp: stream window buffers + mbarriers
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -137,33 +132,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.acc = b;
   s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
   s.pc = s.tb + smem_d_bytes(T.n_tmpl);
-  s.win = s.pc + r16(T.n_sigs * 32);
   return s;
-}
-
-// ---- bulk copy (TMA engine, no tensor map) + mbarrier, raw PTX
-__device__ __forceinline__ void mbar_init(uint32_t mb, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t mb, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(mb),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(mb)
-               : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ uint4 lds_u128(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
 }
 
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
@@ -325,7 +294,7 @@ __device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
 // scores and writes the records.  S.seq holds the candidates on entry.
 template <int NA, bool P2>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
-                                           toast_cost* __restrict__ out, uint32_t win_base, uint2& wph) {
+                                           toast_cost* __restrict__ out) {
   __syncthreads();
   if (warp == 0) {
     uint64_t f0, on;
@@ -365,7 +334,6 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     }
   }
   __syncthreads();
-  const int sb = K - 1 + (K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0);   // segment table base for this K
   const uint32_t acc = S.acc + (uint32_t)warp * smem_acc_bytes(NA);
   unsigned long long* pay = sp<unsigned long long>(acc);
   uint32_t* cnt = sp<uint32_t>(acc + NA * 4 * 32 * 8);
@@ -430,71 +398,51 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   }
   __syncthreads();
 
-  // the sweep: H5 liveness over this warp's op segment (plus the rare use
-  // edges whose value is used twice by one op, costed edge by edge)
+  // H5 (C12, reading R19): peak = max over the kept ops of the peak-memory
+  // frontier of M_t = constant + sum_s Live_t[s] / d_s + sum_tm growth_tm(Tmp_t[tm])
+  // (+ the special edges of ops that use one value twice); this warp takes
+  // every K-th point
   const uint32_t sh = smem_base();
   const uint32_t pc_base = sh + S.pc + lane, tb_base = sh + S.tb + lane;
-  long long L = 0, peak = LLONG_MIN;   // relative to the segment start (combined across segments below)
-  // the op stream of this segment arrives through a double-buffered window:
-  // chunk c = words [s0 + cW, s0 + cW + W + E) of the stream, copied by the
-  // bulk-copy engine two chunks ahead; an op starting in [cW, cW + W) lies
-  // entirely inside chunk c because E >= the largest op record
-  const uint32_t Ww = (uint32_t)T.win_w, CH = (uint32_t)(T.win_w + T.win_e) * 16;
-  const uint32_t buf0 = win_base, buf1 = win_base + CH, mb0 = win_base + 2 * CH, mb1 = mb0 + 8;
-  const uint32_t s0 = T.seg_off[sb + warp], s1 = T.seg_off[sb + warp + 1];
-  const int t_beg = T.seg_op[sb + warp], t_end = T.seg_op[sb + warp + 1];
-  if (t_beg < t_end) {
-    uint32_t out0 = 0, out1 = 0;   // copies issued and not yet waited on, per buffer
-    auto issue = [&](uint32_t c) {
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async();   // this warp's generic reads of the buffer precede the async overwrite
-        const uint32_t mb = (c & 1) ? mb1 : mb0;
-        mbar_expect_tx(mb, CH);
-        bulk_g2s((c & 1) ? buf1 : buf0, T.stream + s0 + c * Ww, CH, mb);
+  constexpr uint64_t M48 = (1ULL << 48) - 1;
+  unsigned long long peak = 0;
+  for (int pi = warp; pi < T.n_points; pi += K) {
+    const uint4 pw = __ldg(reinterpret_cast<const uint4*>(T.points) + pi);
+    const uint32_t n_sig = pw.y & 0xFFFF, n_tm = pw.y >> 16, n_spec = pw.w & 0xFFFF;
+    const uint64_t* tp = T.terms + pw.x;
+    uint64_t M = __ldg(tp++);
+#pragma unroll 4
+    for (uint32_t k = 0; k < n_sig; ++k) {
+      const uint64_t w = __ldg(tp + k);
+      M += dv<P2>(T, w & M48, lds_u8(pc_base + (uint32_t)(w >> 48) * 32));
+    }
+    tp += n_sig;
+#pragma unroll 2
+    for (uint32_t k = 0; k < n_tm; ++k) {
+      const uint64_t w = __ldg(tp + k);
+      const uint32_t b = lds_u8(tb_base + (uint32_t)(w >> 48) * 32);
+      const uint32_t cU = b & 15, cD = b >> 4;
+      if (cU != cD) {
+        const long long g = (long long)dv<P2>(T, w & M48, cU) - (long long)dv<P2>(T, w & M48, cD);
+        if (g > 0) M += (uint64_t)g;
       }
-      if (c & 1) ++out1; else ++out0;
-    };
-    issue(0);
-    if (s0 + Ww < s1) issue(1);
-    mbar_wait(mb0, wph.x & 1);
-    ++wph.x;
-    --out0;
-    uint32_t c = 0, off = 0, cur = buf0;
-    for (int t = t_beg; t < t_end; ++t) {
-      while (off >= Ww) {   // the next op starts in the next chunk
-        if (s0 + (c + 2) * Ww < s1) issue(c + 2);
-        ++c;
-        off -= Ww;
-        if (c & 1) { mbar_wait(mb1, wph.y & 1); ++wph.y; --out1; cur = buf1; }
-        else { mbar_wait(mb0, wph.x & 1); ++wph.x; --out0; cur = buf0; }
-      }
-      const uint4 h = lds_u128(cur + off * 16);
-      const uint32_t sig = h.x & 0xFFFF, flags = (h.x >> 16) & 0xFF, n_uses = h.x >> 24, n_death = h.y & 0xFF;
-      const long long res = (flags & 2) ? 0 : (long long)dv<P2>(T, u64of(h.z, h.w), lds_u8(pc_base + sig * 32));
+    }
+    if (n_spec) {
+      // a value used more than once by this op: costed per edge, once per distinct layout
+      const uint32_t sig = pw.w >> 16;
+      const KUse* ue = T.spec + pw.z;
+      const uint32_t esz = sizeof(typename Ent<NA>::T);
+      const uint32_t ea = sh + S.sig + (uint32_t)lane * esz;
+      const uint32_t a2r = e_a2r16<NA>(esz == 2 ? lds_u16(ea + sig * 32 * esz) : lds_u32(ea + sig * 32 * esz));
       long long temp = 0, gmax = 0;
-      uint32_t q = off + 1, gq = q;
+      uint32_t gq = 0;
 #pragma unroll 1
-      for (uint32_t k = 0; k < n_uses; ++k, ++q) {
-        const uint4 u = lds_u128(cur + q * 16);
-        const uint32_t tix = u.x >> 16;
+      for (uint32_t q = 0; q < n_spec; ++q) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(ue + q));
         const uint64_t gb = u64of(u.z, u.w & 0x00FFFFFFu);
-        if (tix != NO_TMPL) {
-          const uint32_t b = lds_u8(tb_base + tix * 32);
-          const uint32_t cU = b & 15, cD = b >> 4;
-          if (cU != cD) {
-            const long long g = (long long)dv<P2>(T, gb, cU) - (long long)dv<P2>(T, gb, cD);
-            if (g > 0) temp += g;
-          }
-          continue;
-        }
-        // a value used more than once by this op: costed per edge, once per distinct layout
         const uint32_t uflags = u.w >> 24;
         if (uflags & 1) { gmax = 0; gq = q; }
-        const uint32_t esz = sizeof(typename Ent<NA>::T);
-        const uint32_t ea = sh + S.sig + (uint32_t)lane * esz;
         const uint32_t de = esz == 2 ? lds_u16(ea + (u.x & 0xFFFF) * 32 * esz) : lds_u32(ea + (u.x & 0xFFFF) * 32 * esz);
-        const uint32_t a2r = e_a2r16<NA>(esz == 2 ? lds_u16(ea + sig * 32 * esz) : lds_u32(ea + sig * 32 * esz));
         uint32_t dimU = 0, dimD = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
         for (int A = 0; A < NA; ++A) {
@@ -510,7 +458,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         if (dimD != dimU || P) {
           bool dup = false;
           for (uint32_t q2 = gq; q2 < q; ++q2) {
-            const uint32_t ud2 = lds_u128(cur + q2 * 16).y;
+            const uint32_t ud2 = __ldg(&ue[q2].use_dimof);
             uint32_t dimU2 = 0;
 #pragma unroll
             for (int A = 0; A < NA; ++A) {
@@ -552,33 +500,20 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         }
         if (uflags & 2) temp += gmax;
       }
-      // values whose last use is this op
-      long long dying = 0;
-#pragma unroll 1
-      for (uint32_t k = 0; k < n_death; ++k, ++q) {
-        const uint4 d = lds_u128(cur + q * 16);
-        dying += (long long)dv<P2>(T, u64of(d.z, d.w), lds_u8(pc_base + (d.x & 0xFFFF) * 32));
-      }
-      // H5 liveness (C12)
-      const long long M = L + res + temp;
-      peak = M > peak ? M : peak;
-      L = L + res - dying;
-      off = q;
+      M += (uint64_t)temp;
     }
-    // no copy may stay in flight into a buffer the next batch reuses
-    while (out0) { mbar_wait(mb0, wph.x & 1); ++wph.x; --out0; }
-    while (out1) { mbar_wait(mb1, wph.y & 1); ++wph.y; --out1; }
+    peak = M > peak ? M : peak;
   }
   seg[0 * 32 + lane] = key;
   seg[1 * 32 + lane] = flo;
   seg[2 * 32 + lane] = fhi;
-  seg[3 * 32 + lane] = (unsigned long long)L;
-  seg[4 * 32 + lane] = (unsigned long long)peak;
+  seg[3 * 32 + lane] = 0ULL;
+  seg[4 * 32 + lane] = peak;
   __syncthreads();
   if (warp == 0) {
     // combine the K segments: sums into warp 0's slots, peak by the segment scan
     key = 0; flo = 0; fhi = 0;
-    long long Lrun = 0, pk_all = 0;
+    unsigned long long pk_all = 0;
     for (int w = 0; w < K; ++w) {
       const uint32_t aw = S.acc + (uint32_t)w * smem_acc_bytes(NA);
       const unsigned long long* sw = sp<const unsigned long long>(aw + NA * 4 * 32 * 12);
@@ -586,9 +521,8 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       const uint64_t f = sw[1 * 32 + lane];
       flo += f;
       fhi += sw[2 * 32 + lane] + ((flo < f) ? 1 : 0);
-      const long long segpk = (long long)sw[4 * 32 + lane];
-      if (segpk != LLONG_MIN && Lrun + segpk > pk_all) pk_all = Lrun + segpk;
-      Lrun += (long long)sw[3 * 32 + lane];
+      const unsigned long long segpk = sw[4 * 32 + lane];
+      pk_all = segpk > pk_all ? segpk : pk_all;
       if (w) {
         const unsigned long long* pww = sp<const unsigned long long>(aw);
         const uint32_t* cww = sp<const uint32_t>(aw + NA * 4 * 32 * 8);
@@ -611,7 +545,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
 #pragma unroll
       for (int k = 0; k < 4; ++k) ncoll += cnt[(A * 4 + k) * 32 + lane];
     }
-    const uint64_t pk = (uint64_t)pk_all;
+    const uint64_t pk = pk_all;
     const double RT = __ddiv_rn(tt, T.t0);
     const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
     if (valid) {
@@ -673,21 +607,12 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
                                                          int64_t n, toast_cost* __restrict__ out) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
-  const uint32_t win_base = smem_base() + S.win + (uint32_t)warp * smem_win_bytes(T.win_w, T.win_e);
-  if (lane == 0) {
-    const uint32_t mb = win_base + 2 * (uint32_t)(T.win_w + T.win_e) * 16;
-    mbar_init(mb, 1);
-    mbar_init(mb + 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  uint2 wph = make_uint2(0, 0);   // completed uses of this warp's window buffers (mbarrier phases)
   const int64_t nbatch = (n + 31) / 32;
   for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
     const int64_t i = b * 32 + lane;
     const bool valid = i < n;
     if (warp == 0) load_seq(S, seqs + i * 32, lane, valid);
-    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i, win_base, wph);
+    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i);
   }
 }
 
@@ -713,15 +638,6 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
                                                             toast_cost* __restrict__ out, int64_t rep) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
-  const uint32_t win_base = smem_base() + S.win + (uint32_t)warp * smem_win_bytes(T.win_w, T.win_e);
-  if (lane == 0) {
-    const uint32_t mb = win_base + 2 * (uint32_t)(T.win_w + T.win_e) * 16;
-    mbar_init(mb, 1);
-    mbar_init(mb + 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  uint2 wph = make_uint2(0, 0);   // completed uses of this warp's window buffers (mbarrier phases)
   const int64_t nbatch = (n + 31) / 32;
   const uint32_t seed_lo = (uint32_t)seed, seed_hi = (uint32_t)(seed >> 32);
   const int nw = T.n_words;
@@ -784,7 +700,7 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
                             sp<uint32_t>(S.seq)[(4 * k + 3) * 32 + lane]);
     }
     }   // warp 0
-    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i, win_base, wph);
+    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i);
   }
 }
 
@@ -883,9 +799,12 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   toast_status st;
   const void* p;
   // tail: the last window chunk may read W + E words past the end
-  a->h_stream.resize(a->h_stream.size() + 4 * (size_t)(a->dt.win_w + a->dt.win_e + 1), 0u);
-  if ((st = upload(a, a->h_stream, &p, err))) return st;
-  T.stream = reinterpret_cast<const uint4*>(p);
+  if ((st = upload(a, a->h_points, &p, err))) return st;
+  T.points = reinterpret_cast<const KPoint*>(p);
+  if ((st = upload(a, a->h_terms, &p, err))) return st;
+  T.terms = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_spec, &p, err))) return st;
+  T.spec = reinterpret_cast<const KUse*>(p);
   if ((st = upload(a, a->h_sig_roles, &p, err))) return st;
   T.sig_roles = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_sig_nroles, &p, err))) return st;
@@ -910,7 +829,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl, T.win_w, T.win_e) > dev_smem) {
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -919,7 +838,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl, T.win_w, T.win_e);
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
       cudaError_t e = dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
@@ -983,7 +902,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.win_w, a->dt.win_e);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
@@ -1001,7 +920,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.win_w, a->dt.win_e);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {

@@ -53,7 +53,7 @@ struct toast_graph {
 namespace toast {
 
 // ------------------------------------------------------------ host tables
-// (used by toast_materialize on the host and to build the device stream)
+// (used by toast_materialize on the host and to build the device tables)
 // one op, 32 bytes
 struct DOp {
   uint32_t loop_begin;   // global id of the op's role-0 loop
@@ -90,34 +90,26 @@ constexpr int MAX_RANK = 8;
 constexpr int MAX_ACTIONS = 1024;
 constexpr int MAX_GROUPS = 64;
 
-// ------------------------------------------------------------ device stream
-// The kernels walk the program as one contiguous stream of 16-byte words, in
-// op order: a 32-byte header, then one 16-byte record per use edge (sorted by
-// the used value so repeated operands are adjacent), then one 16-byte record
-// per value whose last use is this op.  Every field a warp needs for one op is
-// in this record, so a warp's reads are warp-uniform (broadcast) and
-// sequential.  An op's SIGNATURE fixes how it materialises (per role: action
-// color, divisibility, deselection class, result dim), so per candidate the
-// kernel keeps one 32-bit entry per signature: axis->role | axis->result dim.
-struct KHead {           // 16 B
-  uint16_t sig;          // op signature
-  uint8_t flags;         // bit1 ret
-  uint8_t n_uses;
-  uint8_t n_death;
-  uint8_t pad0[3];
-  uint64_t gbytes;       // result global bytes (0 for ret)
-};
-struct KUse {            // 16 B
+// ------------------------------------------------------------ device tables
+// An op's SIGNATURE fixes how it materialises (per role: action color,
+// divisibility, deselection class, result dim), so per candidate the kernel
+// keeps one entry per signature: axis->role | axis->result dim.  Everything
+// per op is then aggregated per signature (state key, FLOPs), per edge
+// template (collectives) and per frontier point (peak memory, reading R19).
+struct KUse {            // 16 B: one "special" use edge (a value used more than once by one op)
   uint16_t def_sig;      // signature of the defining op
-  uint16_t tmpl;         // edge template, or NO_TMPL: the value is used again at this op (costed per edge)
+  uint16_t tmpl;         // NO_TMPL
   uint32_t use_dimof;    // nibble r: operand dim held by this op's role r (0xF: none)
   uint64_t gb_flags;     // def global bytes (bits 0-55) | flags << 56 (bit0 first use of the value here, bit1 last)
 };
-struct KDeath {          // 16 B
-  uint16_t sig;
-  uint16_t pad0;
-  uint32_t pad1;
-  uint64_t gbytes;
+// one kept op of the peak-memory frontier: M_t = terms[term_begin] (constant)
+// + n_sig signature terms + n_tmpl template terms (+ its special edges)
+struct KPoint {          // 16 B
+  uint32_t term_begin;
+  uint16_t n_sig, n_tmpl;
+  uint32_t spec_begin;
+  uint16_t n_spec;
+  uint16_t use_sig;      // the op's own signature (special edges)
 };
 constexpr uint16_t NO_TMPL = 0xFFFF;
 // edge template: use edges with the same (def signature, use signature, use
@@ -131,7 +123,7 @@ struct KTmpl {           // 24 B
   uint32_t n_edges;
   uint32_t pad;
 };
-static_assert(sizeof(KHead) == 16 && sizeof(KUse) == 16 && sizeof(KDeath) == 16 && sizeof(KTmpl) == 24, "records");
+static_assert(sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
 
 
 // search round reduction record (K3), one per leaf
@@ -146,7 +138,9 @@ struct LeafRed {
 
 // signature role word: acolor [0,10) | div_ok [10,26) | deselection class [26,34)
 struct DeviceTables {
-  const uint4* stream = nullptr;         // op stream (16-byte words)
+  const KPoint* points = nullptr;        // [n_points] peak-memory frontier (R19)
+  const uint64_t* terms = nullptr;       // per point: constant, then value | feature << 48
+  const KUse* spec = nullptr;            // special edges of the points
   const uint64_t* sig_roles = nullptr;   // [n_sigs][8] role words (acolor 0x3FF = untouchable)
   const uint8_t* sig_nroles = nullptr;   // [n_sigs]
   const uint32_t* sig_resdim = nullptr;  // [n_sigs] nibble r: result dim of role r (0xF: none)
@@ -160,7 +154,7 @@ struct DeviceTables {
   // constants
   int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
-  int32_t win_w, win_e;  // stream window: chunk stride and overlap in 16-byte words (overlap >= largest op record)
+  int32_t n_points, pad_;
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -168,9 +162,6 @@ struct DeviceTables {
   uint64_t inv[16];     // exact division by prod(subset): (x >> shift) * inv
   uint32_t shift[16];
   uint64_t inv128_lo[16], inv128_hi[16];   // the same inverse mod 2^128 (FLOP totals)
-  // op segments for K = 1, 2, 4, 8 sweeping warps: entries [K-1+log2 K, +K]
-  int32_t seg_op[19];   // first op of each segment (last entry = n_ops)
-  uint32_t seg_off[19]; // its 16-byte word offset in the stream
 };
 
 }  // namespace toast
@@ -200,8 +191,11 @@ struct toast_analysis {
   std::vector<uint64_t> h_gflops, h_loops, h_desel, h_acol_groups;
   std::vector<toast::DUse> h_uses;
   std::vector<uint32_t> h_deaths, h_actions, h_kill;
-  // device-stream images
-  std::vector<uint32_t> h_stream;           // 16-byte aligned words (as 4 x u32)
+  // device-table images
+  std::vector<toast::KPoint> h_points;      // peak-memory frontier
+  std::vector<uint64_t> h_terms;
+  std::vector<toast::KUse> h_spec;
+  std::vector<int32_t> point_op;            // op index of each frontier point
   std::vector<uint64_t> h_sig_roles, h_desel_cls;
   std::vector<uint8_t> h_sig_nroles;
   std::vector<uint32_t> h_sig_resdim;
