@@ -643,12 +643,41 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       a->op_sig[t] = it->second;
     }
     if (sig_words.size() > 65535) { err = "more than 65535 op signatures"; return TOAST_E_LIMIT; }
+    if (getenv("TOAST_DEBUG")) {
+      int hist[9] = {0};
+      for (auto& w : sig_words) {
+        std::vector<uint64_t> cs;
+        for (uint64_t x : w) if ((x & 0x3FF) != NO_ACOLOR && std::find(cs.begin(), cs.end(), x & 0x3FF) == cs.end()) cs.push_back(x & 0x3FF);
+        hist[std::min<size_t>(cs.size(), 8)]++;
+      }
+      fprintf(stderr, "[toast] signatures by distinct action colors:");
+      for (int i = 0; i <= 8; ++i) fprintf(stderr, " %d:%d", i, hist[i]);
+      fprintf(stderr, "\n");
+    }
     a->h_sig_roles.assign(sig_words.size() * 8, NO_ACOLOR);
     a->h_sig_nroles.assign(sig_words.size(), 0);
     a->h_sig_resdim = sig_rd;
     for (size_t q = 0; q < sig_words.size(); ++q) {
       a->h_sig_nroles[q] = (uint8_t)sig_words[q].size();
       for (size_t r = 0; r < sig_words[q].size(); ++r) a->h_sig_roles[q * 8 + r] = sig_words[q][r];
+    }
+    a->h_sigs.assign(sig_words.size(), KSig{});
+    for (size_t q = 0; q < sig_words.size(); ++q) {
+      KSig& k = a->h_sigs[q];
+      k.resdim = sig_rd[q];
+      k.nr = (uint8_t)sig_words[q].size();
+      for (size_t r = 0; r < sig_words[q].size(); ++r) {
+        const uint64_t w = sig_words[q][r];
+        const uint32_t ac = (uint32_t)(w & 0x3FF);
+        if (ac == NO_ACOLOR) continue;
+        k.div[r >> 1] |= (uint32_t)((w >> 10) & 0xFFFF) << (16 * (r & 1));
+        const uint32_t cls = (uint32_t)(w >> 26) & 0xFF;
+        if (cls) { k.dsel_roles |= (uint8_t)(1u << r); k.cls |= (uint64_t)cls << (8 * r); }
+        int kk = 0;
+        while (kk < k.m && (k.col[kk] & 0x3FF) != ac) ++kk;
+        if (kk == k.m) k.col[k.m++] = ac;
+        k.col[kk] |= 1u << (10 + r);
+      }
     }
     // per-signature state-key terms (R14) and FLOP sums
     const size_t NS = sig_words.size();

@@ -60,7 +60,7 @@ __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
 //      the table is written)
 //   B  the per-color event lists [n_acolors][32] (decode/materialise), then,
 //      per warp, the payload/count accumulators and the segment results
-__host__ __device__ inline int smem_c_bytes() { return 32 * (8 + 8 + 4); }
+__host__ __device__ inline int smem_c_bytes() { return 32 * (8 + 8 + 4 + 8); }
 __host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes) {
   int a1 = n_sigs * 32 * sig_entry_bytes(n_axes), a2 = 2048 + n_words * 128;
   return r16(a1 > a2 ? a1 : a2);
@@ -113,6 +113,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t f0;              // [32] SetGroups fixed to 0 (u64)
   uint32_t on;              // [32] SetGroups fixed to 1 (u64)
   uint32_t status;          // [32]
+  uint32_t axpos;           // [32] 2-bit axis of every sequence position (u64)
   uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
   uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
@@ -123,6 +124,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.f0 = 0;
   s.on = 256;
   s.status = 512;
+  s.axpos = 640;
   const uint32_t a = smem_c_bytes();
   s.sig = a;
   s.seq = a;
@@ -175,12 +177,14 @@ template <int NA> __device__ __forceinline__ uint32_t e_a2r16(uint32_t e) {
 }
 
 // ---------------------------------------------------------------- H1 decode (C9)
+// per action color: the bitmap of sequence positions holding an action of that
+// color (S.acol[c][lane]); per lane the 2-bit axis of every position (axpos)
 __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
-                                           uint64_t& ones) {
+                                           uint64_t& ones, uint64_t& axpos) {
   for (int c = 0; c < T.n_acolors; ++c) sp<uint32_t>(S.acol)[c * 32 + lane] = 0u;
   uint32_t status = 0;
   bool stopped = false;
-  uint64_t fx = 0, on = 0;
+  uint64_t fx = 0, on = 0, ap = 0;
   for (int j = 0; j < 32; ++j) {
     uint32_t id = (sp<uint32_t>(S.seq)[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
     if (stopped) {
@@ -191,16 +195,14 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
     if ((int)id >= T.n_actions) { status |= TOAST_ST_BAD_ACTION_ID; continue; }
     uint32_t aw = __ldg(T.actions + id);
     uint32_t ac = aw & 0x3FF, rr = (aw >> 10) & 0xFF, ax = (aw >> 18) & 3;
-    uint32_t list = sp<uint32_t>(S.acol)[ac * 32 + lane];
-    uint32_t nent = 0;
+    uint32_t pm = sp<uint32_t>(S.acol)[ac * 32 + lane];
     bool dup = false;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t e = (list >> (8 * q)) & 0xFF;
-      if (e & 0x80) { ++nent; dup |= ((e >> 5) & 3) == ax; }
-    }
+    for (uint32_t b = pm; b; b &= b - 1) dup |= ((ap >> (2 * (__ffs(b) - 1))) & 3) == ax;
     if (dup) status |= TOAST_ST_DUP_COLOR_AXIS;
-    else if (nent < 4) sp<uint32_t>(S.acol)[ac * 32 + lane] = list | ((0x80u | (ax << 5) | (uint32_t)j) << (8 * nent));
+    else {
+      sp<uint32_t>(S.acol)[ac * 32 + lane] = pm | (1u << j);
+      ap |= (uint64_t)ax << (2 * j);
+    }
     uint64_t gw = __ldg(T.acol_groups + ac);
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -214,62 +216,69 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
   }
   fixed0 = fx & ~on;
   ones = on;
+  axpos = ap;
   return status;
 }
 
 // ---------------------------------------------------------------- H2 materialise one signature (C9)
 // events (action position j, role) in action order, roles in role order; an
-// axis shards at most one loop of the op; divisibility by div_ok.
+// axis shards at most one loop of the op; divisibility by div_ok.  The
+// positions of the signature's events are the union of its colors' position
+// bitmaps, walked in ascending order.
 __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, int s,
-                                                    uint64_t fixed0, uint64_t ones) {
-  const int nr = __ldg(T.sig_nroles + s);
-  uint32_t li[MAX_LOOPS_PER_OP], dv[MAX_LOOPS_PER_OP];
-  uint32_t any = 0;
+                                                    uint64_t fixed0, uint64_t ones, uint64_t axpos) {
+  const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
+  const uint4 mt = __ldg(kp + 3);
+  const uint32_t m = mt.y & 0xFF, dr = (mt.y >> 8) & 0xFF;
+  if (m == 0) return 0xFFFFFFFFu;
+  // roles deselected by the fixed SetGroup bits
+  uint32_t dmask = 0;
+  for (uint32_t b = dr; b; b &= b - 1) {
+    const uint32_t r = __ffs(b) - 1;
+    const uint32_t cls = (uint32_t)(u64of(mt.z, mt.w) >> (8 * r)) & 0xFF;
+    const uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
+    if ((fixed0 & n0) | (ones & n1)) dmask |= 1u << r;
+  }
+  const uint4 c0 = __ldg(kp + 1), c1 = __ldg(kp + 2);
+  const uint32_t col[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+  uint32_t pm[8], rm[8], bits = 0;
 #pragma unroll
-  for (int r = 0; r < MAX_LOOPS_PER_OP; ++r) {
-    li[r] = 0;
-    dv[r] = 0;
-    if (r < nr) {
-      uint64_t rw = __ldg(T.sig_roles + (size_t)s * 8 + r);
-      uint32_t ac = (uint32_t)rw & 0x3FF;
-      if (ac != NO_ACOLOR) {
-        uint32_t l = sp<uint32_t>(S.acol)[ac * 32 + lane];
-        uint32_t cls = (uint32_t)(rw >> 26) & 0xFF;
-        if (l && cls) {
-          uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
-          if ((fixed0 & n0) | (ones & n1)) l = 0;
-        }
-        li[r] = l;
-        dv[r] = (uint32_t)(rw >> 10) & 0xFFFF;
-        any |= l;
+  for (int k = 0; k < 8; ++k) {
+    pm[k] = 0;
+    rm[k] = 0;
+    if (k < (int)m) {
+      rm[k] = (col[k] >> 10) & ~dmask & 0xFF;
+      if (rm[k]) pm[k] = sp<uint32_t>(S.acol)[(col[k] & 0x3FF) * 32 + lane];
+      bits |= pm[k];
+    }
+  }
+  if (!bits) return 0xFFFFFFFFu;   // nothing sharded: every axis "none" in both maps
+  const uint4 dw = __ldg(kp);
+  uint32_t a2r = 0xFFFFu, masks = 0, opmask = 0;
+  while (bits) {
+    const uint32_t j = __ffs(bits) - 1;
+    bits &= bits - 1;
+    const uint32_t A = (uint32_t)(axpos >> (2 * j)) & 3;
+    if ((opmask >> A) & 1) continue;
+    uint32_t roles = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < (int)m) roles |= ((pm[k] >> j) & 1) ? rm[k] : 0u;
+    while (roles) {
+      const uint32_t r = __ffs(roles) - 1;
+      roles &= roles - 1;
+      const uint32_t w = (r & 4) ? ((r & 2) ? dw.w : dw.z) : ((r & 2) ? dw.y : dw.x);
+      const uint32_t d = (w >> (16 * (r & 1))) & 0xFFFF;
+      const uint32_t cur = (masks >> (4 * r)) & 15;
+      if ((d >> (cur | (1u << A))) & 1) {
+        masks |= (1u << A) << (4 * r);
+        opmask |= 1u << A;
+        a2r = (a2r & ~(0xFu << (4 * A))) | (r << (4 * A));
+        break;
       }
     }
   }
-  uint32_t a2r = 0xFFFFu;
-  if (!any) return 0xFFFFFFFFu;   // nothing sharded: every axis "none" in both maps
-  uint32_t masks = 0, opmask = 0;
-  while (true) {
-    int best = -1;
-    uint32_t bj = 64;
-#pragma unroll
-    for (int r = 0; r < MAX_LOOPS_PER_OP; ++r) {
-      uint32_t e = li[r];
-      if ((e & 0x80) && (e & 31) < bj) { bj = e & 31; best = r; }
-    }
-    if (best < 0) break;
-    uint32_t e = 0, d = 0;
-#pragma unroll
-    for (int r = 0; r < MAX_LOOPS_PER_OP; ++r)
-      if (r == best) { e = li[r]; d = dv[r]; li[r] = e >> 8; }
-    const uint32_t A = (e >> 5) & 3;
-    const uint32_t cur = (masks >> (4 * best)) & 15;
-    if (!((opmask >> A) & 1) && ((d >> (cur | (1u << A))) & 1)) {
-      masks |= (1u << A) << (4 * best);
-      opmask |= 1u << A;
-      a2r = (a2r & ~(0xFu << (4 * A))) | ((uint32_t)best << (4 * A));
-    }
-  }
-  const uint32_t rdm = __ldg(T.sig_resdim + s);
+  const uint32_t rdm = mt.x;
   uint32_t dims = 0;
 #pragma unroll
   for (int A = 0; A < 4; ++A) {
@@ -297,10 +306,11 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
                                            toast_cost* __restrict__ out) {
   __syncthreads();
   if (warp == 0) {
-    uint64_t f0, on;
-    sp<uint32_t>(S.status)[lane] = decode(T, S, lane, f0, on);
+    uint64_t f0, on, ap;
+    sp<uint32_t>(S.status)[lane] = decode(T, S, lane, f0, on, ap);
     sp<unsigned long long>(S.f0)[lane] = f0;
     sp<unsigned long long>(S.on)[lane] = on;
+    sp<unsigned long long>(S.axpos)[lane] = ap;
   }
   __syncthreads();
   // H2: materialise this warp's share of the signatures; per signature the
@@ -308,8 +318,9 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   uint64_t key = 0, flo = 0, fhi = 0;
   {
     const uint64_t f0 = sp<unsigned long long>(S.f0)[lane], on = sp<unsigned long long>(S.on)[lane];
+    const uint64_t ap = sp<unsigned long long>(S.axpos)[lane];
     for (int s = warp; s < T.n_sigs; s += K) {
-      const uint32_t e = pack_entry<NA>(materialize_sig(T, S, lane, s, f0, on));
+      const uint32_t e = pack_entry<NA>(materialize_sig(T, S, lane, s, f0, on, ap));
       ent_store<NA>(S, s, lane, e);
       uint32_t present = 0;
 #pragma unroll
@@ -805,12 +816,8 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   T.terms = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_spec, &p, err))) return st;
   T.spec = reinterpret_cast<const KUse*>(p);
-  if ((st = upload(a, a->h_sig_roles, &p, err))) return st;
-  T.sig_roles = reinterpret_cast<const uint64_t*>(p);
-  if ((st = upload(a, a->h_sig_nroles, &p, err))) return st;
-  T.sig_nroles = reinterpret_cast<const uint8_t*>(p);
-  if ((st = upload(a, a->h_sig_resdim, &p, err))) return st;
-  T.sig_resdim = reinterpret_cast<const uint32_t*>(p);
+  if ((st = upload(a, a->h_sigs, &p, err))) return st;
+  T.sigs = reinterpret_cast<const KSig*>(p);
   if ((st = upload(a, a->h_sig_key, &p, err))) return st;
   T.sig_key = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_sig_flops, &p, err))) return st;

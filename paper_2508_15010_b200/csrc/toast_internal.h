@@ -123,7 +123,19 @@ struct KTmpl {           // 24 B
   uint32_t n_edges;
   uint32_t pad;
 };
-static_assert(sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
+// one op signature, 64 B (one warp-uniform 4 x 16-B load): per role its
+// divisibility word, per distinct action color of the signature the roles it
+// covers, each role's deselection class and result dim
+struct KSig {
+  uint32_t div[4];       // role r: div_ok (bit S <=> extent divisible by prod(axis subset S)) = div[r >> 1] >> 16 * (r & 1)
+  uint32_t col[8];       // k < m: acolor | role mask << 10
+  uint32_t resdim;       // nibble r: result dim of role r (0xF: none)
+  uint8_t m;             // distinct action colors among the roles
+  uint8_t dsel_roles;    // roles with a deselection class
+  uint8_t nr, pad;
+  uint64_t cls;          // byte r: deselection class of role r (0 = never deselected)
+};
+static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
 
 
 // search round reduction record (K3), one per leaf
@@ -141,9 +153,7 @@ struct DeviceTables {
   const KPoint* points = nullptr;        // [n_points] peak-memory frontier (R19)
   const uint64_t* terms = nullptr;       // per point: constant, then value | feature << 48
   const KUse* spec = nullptr;            // special edges of the points
-  const uint64_t* sig_roles = nullptr;   // [n_sigs][8] role words (acolor 0x3FF = untouchable)
-  const uint8_t* sig_nroles = nullptr;   // [n_sigs]
-  const uint32_t* sig_resdim = nullptr;  // [n_sigs] nibble r: result dim of role r (0xF: none)
+  const KSig* sigs = nullptr;            // [n_sigs]
   const uint64_t* sig_key = nullptr;     // [n_sigs][4 axes][8 roles] summed state-key terms (R14)
   const uint64_t* sig_flops = nullptr;   // [n_sigs][2] summed global FLOPs of matmul-class ops (lo, hi)
   const KTmpl* tmpl = nullptr;           // [n_tmpl]
@@ -196,6 +206,7 @@ struct toast_analysis {
   std::vector<uint64_t> h_terms;
   std::vector<toast::KUse> h_spec;
   std::vector<int32_t> point_op;            // op index of each frontier point
+  std::vector<toast::KSig> h_sigs;
   std::vector<uint64_t> h_sig_roles, h_desel_cls;
   std::vector<uint8_t> h_sig_nroles;
   std::vector<uint32_t> h_sig_resdim;
