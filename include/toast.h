@@ -141,7 +141,10 @@ toast_status toast_query_baseline(const toast_analysis* a, toast_cost* out);
  * batch sizes that are multiples of it leave no partially filled last wave. */
 toast_status toast_preferred_batch(const toast_analysis* a, int64_t* n);
 /* JSON dump of the H0 tables (loops, conflicts, sets, groups, super-colors,
- * actions, baseline).  *needed = bytes incl. NUL; writes only if cap >= *needed. */
+ * actions, baseline) plus "kernel_tables": the sizes of the per-candidate
+ * tables the kernels read and the op index of every peak-memory frontier
+ * point (reading R19).  *needed = bytes incl. NUL; writes only if
+ * cap >= *needed. */
 toast_status toast_dump_analysis(const toast_analysis* a, char* buf, size_t cap, size_t* needed);
 
 /* toast_eval_batch — H1-H7 for n candidates.  seqs: uint16[n][32] action ids,

@@ -68,6 +68,7 @@ def lib():
         L.orc_rollout.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64,
                                   ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         L.orc_materialize.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.orc_profile.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_bruteforce.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_bruteforce.restype = ctypes.c_int64
         L.orc_philox.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
@@ -175,6 +176,14 @@ class Oracle:
         m = np.zeros(self.n_loops, dtype=np.uint8)
         lib().orc_materialize(self.h, s.ctypes.data, m.ctypes.data)
         return m
+
+    def profile(self, seq) -> np.ndarray:
+        """M_t of every op t for one sequence (C12: peak = max_t M_t)."""
+        s = np.zeros(32, dtype=np.uint16)
+        s[:len(seq)] = seq
+        out = np.zeros(lib().orc_n_ops(self.h), dtype=np.int64)
+        lib().orc_profile(self.h, s.ctypes.data, out.ctypes.data)
+        return out
 
     def bruteforce(self):
         best = np.zeros(32, dtype=np.uint16)

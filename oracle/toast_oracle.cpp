@@ -1118,7 +1118,8 @@ struct Oracle {
     return global_bytes(v) / axes_prod(all);
   }
 
-  void eval_masks(const std::vector<int>& mask, Cost& out) const {
+  // profile (optional): M_t of every op t, the quantity C12 maximises
+  void eval_masks(const std::vector<int>& mask, Cost& out, std::vector<i64>* profile = nullptr) const {
     // C10: FLOPs over matmul-class ops only
     u128 flops = 0;
     for (size_t t = 0; t < M.ops.size(); t++) {
@@ -1195,6 +1196,7 @@ struct Oracle {
       int rv = M.ops[t].result;
       i64 res = rv >= 0 ? (i64)local_bytes_of(rv, layout_D(mask, rv)) : 0;
       i64 Mt = L + res + (i64)temp_total[t];
+      if (profile) profile->push_back(Mt);
       if (Mt > peak) peak = Mt;
       i64 dying_bytes = 0;
       for (int v : dying[t]) dying_bytes += (i64)local_bytes_of(v, layout_D(mask, v));
@@ -1472,6 +1474,17 @@ void orc_materialize(void* h, const uint16_t* seq, uint8_t* masks) {
   std::vector<int> m;
   O->materialize(seq, m);
   for (size_t i = 0; i < m.size(); i++) masks[i] = (uint8_t)m[i];
+}
+
+// the liveness profile of one sequence: M_t for every op t (C12), n_ops values
+void orc_profile(void* h, const uint16_t* seq, int64_t* out) {
+  Oracle* O = (Oracle*)h;
+  std::vector<int> m;
+  O->materialize(seq, m);
+  Cost c;
+  std::vector<i64> prof;
+  O->eval_masks(m, c, &prof);
+  for (size_t t = 0; t < prof.size(); t++) out[t] = prof[t];
 }
 
 int64_t orc_bruteforce(void* h, uint16_t* best_seq, void* best_cost) {

@@ -985,7 +985,17 @@ std::string dump_json(const toast_analysis* a) {
     if (i) s += ',';
     s += '[' + I(c.op) + ',' + I(c.u) + ',' + I(c.v) + ',' + I(c.set) + ',' + I(c.side0) + ']';
   }
-  s += "],\"n_boxes\":" + I(a->n_boxes) + ",\"dropped_boxes\":" + I(a->dropped_boxes) + ",\"set_group\":[";
+  {   // the per-candidate tables the kernels read (signatures, templates, peak-memory frontier)
+    int64_t roles = 0, cols = 0;
+    for (const auto& k : a->h_sigs) { roles += k.nr; cols += k.m; }
+    s += "],\"kernel_tables\":{\"n_sigs\":" + I((int64_t)a->h_sigs.size()) + ",\"sig_roles\":" + I(roles) +
+         ",\"sig_colors\":" + I(cols) + ",\"n_tmpl\":" + I((int64_t)a->h_tmpl.size()) + ",\"n_points\":" +
+         I((int64_t)a->h_points.size()) + ",\"n_terms\":" + I((int64_t)a->h_terms.size()) + ",\"n_spec\":" +
+         I((int64_t)a->h_spec.size()) + ",\"frontier_ops\":[";
+    for (size_t q = 0; q < a->point_op.size(); ++q) { if (q) s += ','; s += I(a->point_op[q]); }
+    s += "]}";
+  }
+  s += ",\"n_boxes\":" + I(a->n_boxes) + ",\"dropped_boxes\":" + I(a->dropped_boxes) + ",\"set_group\":[";
   for (size_t i = 0; i < a->set_group.size(); ++i) { if (i) s += ','; s += I(a->set_group[i]); }
   s += "],\"set_sig\":[";
   for (size_t i = 0; i < a->set_sig.size(); ++i) {

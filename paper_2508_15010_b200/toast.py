@@ -211,12 +211,23 @@ class Analysis:
         _check(_lib.toast_preferred_batch(self._h, ctypes.byref(n)))
         return n.value
 
-    def dump(self) -> dict:
+    def _dump_all(self) -> dict:
         need = ctypes.c_size_t()
         _check(_lib.toast_dump_analysis(self._h, None, 0, ctypes.byref(need)))
         buf = ctypes.create_string_buffer(need.value)
         _check(_lib.toast_dump_analysis(self._h, buf, need.value, ctypes.byref(need)))
         return json.loads(buf.value.decode())
+
+    def dump(self) -> dict:
+        """The H0 analysis (the part comparable with the oracle's own dump)."""
+        d = self._dump_all()
+        d.pop("kernel_tables", None)
+        return d
+
+    def kernel_tables(self) -> dict:
+        """Sizes of the per-candidate tables (signatures, edge templates, the
+        peak-memory frontier) and the op index of every frontier point."""
+        return self._dump_all()["kernel_tables"]
 
 
 def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30) -> Analysis:
