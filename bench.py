@@ -247,10 +247,43 @@ def time_to_best_cpu(cfg, args, ttb):
 
 
 # --------------------------------------------------------------------------- main arm
-def algorithmic_ops_per_eval(dump: dict, n_axes: int) -> int:
-    """one check per loop (H2), rank x axes transitions
-    per use edge (H4), three scan/score steps per op (H5)."""
-    return int(dump["n_loops"]) + int(dump["n_edges"]) * n_axes + 3 * int(dump["n_ops"])
+def expected_draws(max_depth: int) -> float:
+    """Philox draws per rollout from the empty prefix under p_stop = d / max_depth
+    (reading R15): sum over d of P(the rollout reaches depth d)."""
+    e, p = 0.0, 1.0
+    for d in range(max_depth):
+        e += p                       # a draw happens at depth d
+        p *= 1.0 - d / max_depth     # ... and continues with probability 1 - d/max_depth
+    return e
+
+
+def algorithmic_ops_per_eval(kt: dict, n_axes: int, max_depth: int, n_actions: int) -> dict:
+    """the integer operations one evaluation of the
+    reduced method needs, counted from the analysis'
+    own table sizes (independent of how the kernel schedules them)."""
+    words = (n_actions + 31) // 32
+    rows = {
+        "H1 decode": 32 + 4 * max_depth,                          # slot reads; color event + SetGroup bits per action
+        "H2 materialise": n_axes * kt["sig_roles"],               # one divisibility attempt per (role, axis)
+        "H3/H7 flops+key": kt["n_sigs"] * (n_axes + 1),           # one key term per sharded axis, one exact division
+        "H4 collectives": 2 * n_axes * kt["n_tmpl"],              # phase 1 + phase 2 test per (template, axis)
+        "H5 frontier": 2 * kt["n_terms"],                         # one exact division + one add per term
+        "H6 score": 8 * n_axes + 8,                               # fixed-order double epilogue
+        "H8 rollout": round(expected_draws(max_depth) * (80 + 3 * words)),   # Philox4x32-10 + legal-set update per draw
+    }
+    rows["total"] = sum(rows.values())
+    return rows
+
+
+def profile_summary(config: str):
+    """The committed ncu --set full summary of this config's rollout kernel
+    (profiles/ncu_summary.json, written by scripts/ncu_summary.py), with its
+    DRAM bytes scaled to one launch of this bench's size."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))[config]
+    except Exception:
+        return None
+    return d
 
 
 def run_toast(args, cfg, rank, world, local):
@@ -327,8 +360,10 @@ def run_toast(args, cfg, rank, world, local):
             pass
         sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         n_axes = len(cfg.axes)
-        ops = algorithmic_ops_per_eval(dump, n_axes)
+        opr = algorithmic_ops_per_eval(a.kernel_tables(), n_axes, cfg.max_depth, len(dump["actions"]) + 1)
+        ops = opr["total"]
         achieved = ops * (N / (ms_local / 1000.0)) / 1e9          # Gop/s on this GPU
+        prof = profile_summary(cfg.name)
         peak_alu = 148 * 128 * sm_max * 1e6 / 1e9                  # INT32 lanes x clock (Gop/s)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -341,9 +376,17 @@ def run_toast(args, cfg, rank, world, local):
             "wall_s_timed_region": wall,
             "nda_s": nda_s,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_alu, "unit": "Gop/s",
-                         "frac": achieved / peak_alu, "traffic": None,
+                         "frac": achieved / peak_alu,
+                         "traffic": prof.get("dram_bytes_per_launch", None) if prof else None,
+                         "ops_per_eval": opr,
+                         "hbm": {"algorithmic_bytes_per_eval": 64 + 64 + 256,
+                                 "achieved_gbs": 384 * (N / (ms_local / 1000.0)) / 1e9,
+                                 "peak_gbs": float(peaks.get("hbm_gbs", 6450.0)),
+                                 "frac": 384 * (N / (ms_local / 1000.0)) / 1e9 / float(peaks.get("hbm_gbs", 6450.0))},
+                         "ncu": prof,
                          "note": f"{ops} algorithmic int ops/eval (DESIGN.md Roofline); peak = 148 SMs x 128 INT32 "
-                                 f"lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
+                                 f"lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); traffic = ncu dram bytes of "
+                                 f"one launch of this size (profiles/ncu_summary.json)"},
             "clocks": clk,
             "e2e": {"value": N * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": N * 64,
                     "d2h_bytes_per_step": N * (64 + 256)},

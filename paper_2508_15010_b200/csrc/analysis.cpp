@@ -820,18 +820,27 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       a->h_terms.clear();
       a->h_spec.clear();
       a->point_op.clear();
-      for (size_t i : ord) {
-        const auto& p = P[i];
-        const int32_t t = Pt[i];
+      // points in program order, in groups of FRONTIER_GROUP: a group's first
+      // point carries its constant and signature terms absolutely, the others
+      // as signed differences from the previous point (consecutive frontier
+      // ops share most of their live set); template terms are per point
+      const std::vector<int64_t>* prev = nullptr;
+      for (size_t n = 0; n < ord.size(); ++n) {
+        const auto& p = P[ord[n]];
+        const int32_t t = Pt[ord[n]];
+        const bool anchor = n % FRONTIER_GROUP == 0;
+        for (size_t d = 0; d < D; ++d)
+          if ((uint64_t)p[d] >> 47) { err = "a live-byte sum of 2^47 bytes or more"; return TOAST_E_LIMIT; }
         KPoint kp{};
         kp.term_begin = (uint32_t)a->h_terms.size();
-        a->h_terms.push_back((uint64_t)p[0]);
-        for (size_t q = 0; q < NS; ++q)
-          if (p[1 + q]) { a->h_terms.push_back((uint64_t)p[1 + q] | ((uint64_t)q << 48)); ++kp.n_sig; }
+        auto term = [&](int64_t v, size_t fid) { return ((uint64_t)v & ((1ULL << 48) - 1)) | ((uint64_t)fid << 48); };
+        a->h_terms.push_back((uint64_t)(anchor ? p[0] : p[0] - (*prev)[0]));
+        for (size_t q = 0; q < NS; ++q) {
+          const int64_t v = anchor ? p[1 + q] : p[1 + q] - (*prev)[1 + q];
+          if (v) { a->h_terms.push_back(term(v, q)); ++kp.n_sig; }
+        }
         for (size_t q = 0; q < NT; ++q)
-          if (p[1 + NS + q]) { a->h_terms.push_back((uint64_t)p[1 + NS + q] | ((uint64_t)q << 48)); ++kp.n_tmpl; }
-        for (size_t d = 1; d < D; ++d)
-          if ((uint64_t)p[d] >> 48) { err = "a live-byte sum of 2^48 bytes or more"; return TOAST_E_LIMIT; }
+          if (p[1 + NS + q]) { a->h_terms.push_back(term(p[1 + NS + q], q)); ++kp.n_tmpl; }
         kp.spec_begin = (uint32_t)a->h_spec.size();
         kp.n_spec = (uint16_t)op_spec[t].size();
         if (op_spec[t].size() > 65535) { err = "too many repeated operands at one op"; return TOAST_E_LIMIT; }
@@ -839,6 +848,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         for (auto& u : op_spec[t]) a->h_spec.push_back(u);
         a->h_points.push_back(kp);
         a->point_op.push_back(t);
+        prev = &p;
       }
     }
     if (getenv("TOAST_DEBUG"))

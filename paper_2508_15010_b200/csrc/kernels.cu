@@ -149,6 +149,11 @@ template <bool P2>
 __device__ __forceinline__ uint64_t dv(const DeviceTables& T, uint64_t x, uint32_t code) {
   return P2 ? (x >> code) : (x >> T.shift[code]) * T.inv[code];
 }
+// the same for a signed exact multiple (arithmetic shift; the inverse works mod 2^64)
+template <bool P2>
+__device__ __forceinline__ long long dvs(const DeviceTables& T, long long x, uint32_t code) {
+  return P2 ? (x >> code) : (long long)((uint64_t)(x >> T.shift[code]) * T.inv[code]);
+}
 template <bool P2>
 __device__ __forceinline__ unsigned __int128 dv128(const DeviceTables& T, unsigned __int128 x, uint32_t S) {
   x >>= T.shift[S];
@@ -225,6 +230,43 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
 // axis shards at most one loop of the op; divisibility by div_ok.  The
 // positions of the signature's events are the union of its colors' position
 // bitmaps, walked in ascending order.
+template <int M>
+__device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const uint4& c0, const uint4& c1,
+                                                  uint32_t dmask, const uint4& dw, uint64_t axpos) {
+  const uint32_t col[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+  uint32_t pm[M], rm[M], bits = 0;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    rm[k] = (col[k] >> 10) & ~dmask & 0xFF;
+    pm[k] = rm[k] ? sp<uint32_t>(S.acol)[(col[k] & 0x3FF) * 32 + lane] : 0u;
+    bits |= pm[k];
+  }
+  uint32_t a2r = 0xFFFFu, masks = 0, opmask = 0;
+  const uint64_t dlo = u64of(dw.x, dw.y), dhi = u64of(dw.z, dw.w);
+  while (bits) {
+    const uint32_t j = __ffs(bits) - 1;
+    bits &= bits - 1;
+    const uint32_t A = (uint32_t)(axpos >> (2 * j)) & 3;
+    if ((opmask >> A) & 1) continue;
+    uint32_t roles = 0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) roles |= ((pm[k] >> j) & 1) ? rm[k] : 0u;
+    while (roles) {
+      const uint32_t r = __ffs(roles) - 1;
+      roles &= roles - 1;
+      const uint32_t d = (uint32_t)(((r & 4) ? dhi : dlo) >> (16 * (r & 3))) & 0xFFFF;
+      const uint32_t cur = (masks >> (4 * r)) & 15;
+      if ((d >> (cur | (1u << A))) & 1) {
+        masks |= (1u << A) << (4 * r);
+        opmask |= 1u << A;
+        a2r = (a2r & ~(0xFu << (4 * A))) | (r << (4 * A));
+        break;
+      }
+    }
+  }
+  return a2r;
+}
+
 __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, int s,
                                                     uint64_t fixed0, uint64_t ones, uint64_t axpos) {
   const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
@@ -239,45 +281,19 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
     const uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
     if ((fixed0 & n0) | (ones & n1)) dmask |= 1u << r;
   }
-  const uint4 c0 = __ldg(kp + 1), c1 = __ldg(kp + 2);
-  const uint32_t col[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-  uint32_t pm[8], rm[8], bits = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    pm[k] = 0;
-    rm[k] = 0;
-    if (k < (int)m) {
-      rm[k] = (col[k] >> 10) & ~dmask & 0xFF;
-      if (rm[k]) pm[k] = sp<uint32_t>(S.acol)[(col[k] & 0x3FF) * 32 + lane];
-      bits |= pm[k];
-    }
+  const uint4 c0 = __ldg(kp + 1), c1 = __ldg(kp + 2), dw = __ldg(kp);
+  uint32_t a2r;
+  switch (m) {   // warp-uniform: the merge is unrolled over the signature's color count
+    case 1: a2r = materialize_m<1>(S, lane, c0, c1, dmask, dw, axpos); break;
+    case 2: a2r = materialize_m<2>(S, lane, c0, c1, dmask, dw, axpos); break;
+    case 3: a2r = materialize_m<3>(S, lane, c0, c1, dmask, dw, axpos); break;
+    case 4: a2r = materialize_m<4>(S, lane, c0, c1, dmask, dw, axpos); break;
+    case 5: a2r = materialize_m<5>(S, lane, c0, c1, dmask, dw, axpos); break;
+    case 6: a2r = materialize_m<6>(S, lane, c0, c1, dmask, dw, axpos); break;
+    case 7: a2r = materialize_m<7>(S, lane, c0, c1, dmask, dw, axpos); break;
+    default: a2r = materialize_m<8>(S, lane, c0, c1, dmask, dw, axpos); break;
   }
-  if (!bits) return 0xFFFFFFFFu;   // nothing sharded: every axis "none" in both maps
-  const uint4 dw = __ldg(kp);
-  uint32_t a2r = 0xFFFFu, masks = 0, opmask = 0;
-  while (bits) {
-    const uint32_t j = __ffs(bits) - 1;
-    bits &= bits - 1;
-    const uint32_t A = (uint32_t)(axpos >> (2 * j)) & 3;
-    if ((opmask >> A) & 1) continue;
-    uint32_t roles = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (k < (int)m) roles |= ((pm[k] >> j) & 1) ? rm[k] : 0u;
-    while (roles) {
-      const uint32_t r = __ffs(roles) - 1;
-      roles &= roles - 1;
-      const uint32_t w = (r & 4) ? ((r & 2) ? dw.w : dw.z) : ((r & 2) ? dw.y : dw.x);
-      const uint32_t d = (w >> (16 * (r & 1))) & 0xFFFF;
-      const uint32_t cur = (masks >> (4 * r)) & 15;
-      if ((d >> (cur | (1u << A))) & 1) {
-        masks |= (1u << A) << (4 * r);
-        opmask |= 1u << A;
-        a2r = (a2r & ~(0xFu << (4 * A))) | (r << (4 * A));
-        break;
-      }
-    }
-  }
+  if (a2r == 0xFFFFu) return 0xFFFFFFFFu;   // nothing sharded: every axis "none" in both maps
   const uint32_t rdm = mt.x;
   uint32_t dims = 0;
 #pragma unroll
@@ -415,26 +431,32 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   // every K-th point
   const uint32_t sh = smem_base();
   const uint32_t pc_base = sh + S.pc + lane, tb_base = sh + S.tb + lane;
-  constexpr uint64_t M48 = (1ULL << 48) - 1;
   unsigned long long peak = 0;
-  for (int pi = warp; pi < T.n_points; pi += K) {
+  const int n_groups = (T.n_points + FRONTIER_GROUP - 1) / FRONTIER_GROUP;
+  for (int gi = warp; gi < n_groups; gi += K) {
+  long long Ms = 0;   // the group's running constant + signature part
+  const int p_end = min(T.n_points, (gi + 1) * FRONTIER_GROUP);
+  for (int pi = gi * FRONTIER_GROUP; pi < p_end; ++pi) {
     const uint4 pw = __ldg(reinterpret_cast<const uint4*>(T.points) + pi);
     const uint32_t n_sig = pw.y & 0xFFFF, n_tm = pw.y >> 16, n_spec = pw.w & 0xFFFF;
     const uint64_t* tp = T.terms + pw.x;
-    uint64_t M = __ldg(tp++);
+    Ms += (long long)__ldg(tp++);
 #pragma unroll 4
     for (uint32_t k = 0; k < n_sig; ++k) {
       const uint64_t w = __ldg(tp + k);
-      M += dv<P2>(T, w & M48, lds_u8(pc_base + (uint32_t)(w >> 48) * 32));
+      const long long v = (long long)(w << 16) >> 16;    // signed 48-bit value
+      Ms += dvs<P2>(T, v, lds_u8(pc_base + (uint32_t)(w >> 48) * 32));
     }
     tp += n_sig;
+    uint64_t M = (uint64_t)Ms;
 #pragma unroll 2
     for (uint32_t k = 0; k < n_tm; ++k) {
       const uint64_t w = __ldg(tp + k);
+      const uint64_t v = w & ((1ULL << 48) - 1);
       const uint32_t b = lds_u8(tb_base + (uint32_t)(w >> 48) * 32);
       const uint32_t cU = b & 15, cD = b >> 4;
       if (cU != cD) {
-        const long long g = (long long)dv<P2>(T, w & M48, cU) - (long long)dv<P2>(T, w & M48, cD);
+        const long long g = (long long)dv<P2>(T, v, cU) - (long long)dv<P2>(T, v, cD);
         if (g > 0) M += (uint64_t)g;
       }
     }
@@ -514,6 +536,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       M += (uint64_t)temp;
     }
     peak = M > peak ? M : peak;
+  }
   }
   seg[0 * 32 + lane] = key;
   seg[1 * 32 + lane] = flo;
@@ -695,8 +718,14 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
           if (k < c) break;
           k -= c;
         }
-        for (uint32_t q = 0; q < k; ++q) word &= word - 1;
-        const uint32_t a = (uint32_t)w * 32 + (uint32_t)(__ffs(word) - 1);
+        // position of the k-th (0-based) set bit of word: binary search on popcounts
+        uint32_t pos = 0, c;
+        c = __popc(word & 0xFFFFu); if (k >= c) { k -= c; word >>= 16; pos += 16; }
+        c = __popc(word & 0xFFu);   if (k >= c) { k -= c; word >>= 8; pos += 8; }
+        c = __popc(word & 0xFu);    if (k >= c) { k -= c; word >>= 4; pos += 4; }
+        c = __popc(word & 0x3u);    if (k >= c) { k -= c; word >>= 2; pos += 2; }
+        c = word & 1u;              if (k >= c) { pos += 1; }
+        const uint32_t a = (uint32_t)w * 32 + pos;
         for (int w2 = 0; w2 < nw; ++w2) sp<uint32_t>(S.legal)[w2 * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w2);
         uint32_t& sw = sp<uint32_t>(S.seq)[(d >> 1) * 32 + lane];
         sw = (d & 1) ? ((sw & 0xFFFFu) | (a << 16)) : ((sw & 0xFFFF0000u) | a);

@@ -102,8 +102,12 @@ struct KUse {            // 16 B: one "special" use edge (a value used more than
   uint32_t use_dimof;    // nibble r: operand dim held by this op's role r (0xF: none)
   uint64_t gb_flags;     // def global bytes (bits 0-55) | flags << 56 (bit0 first use of the value here, bit1 last)
 };
-// one kept op of the peak-memory frontier: M_t = terms[term_begin] (constant)
-// + n_sig signature terms + n_tmpl template terms (+ its special edges)
+// one kept op of the peak-memory frontier: M_t = constant + n_sig signature
+// terms + n_tmpl template terms (+ its special edges).  Points come in groups
+// of FRONTIER_GROUP: the first carries the constant and the signature terms
+// absolutely, the others as signed differences from the previous point.
+// A term is a signed 48-bit value | feature id << 48.
+constexpr int FRONTIER_GROUP = 8;
 struct KPoint {          // 16 B
   uint32_t term_begin;
   uint16_t n_sig, n_tmpl;

@@ -14,6 +14,7 @@ hdr = None
 agg = {}
 cur = None
 tot_s = tot_i = 0
+tot_st = {}
 for r in rows:
     if len(r) > 4 and r[0] == "Line No":
         hdr = r
@@ -28,11 +29,17 @@ for r in rows:
     num = lambda x: int(x) if x.strip().isdigit() else 0
     s = num(r[4])
     i = num(r[7])
-    a = agg.setdefault(cur, [0, 0])
+    a = agg.setdefault(cur, [0, 0, {}])
     a[0] += s
     a[1] += i
+    for ci, name in enumerate(hdr):
+        if name.startswith("stall_") and "Not Issued" not in name and ci < len(r):
+            a[2][name[6:]] = a[2].get(name[6:], 0) + num(r[ci])
+            tot_st[name[6:]] = tot_st.get(name[6:], 0) + num(r[ci])
     tot_s += s
     tot_i += i
 print(f"total samples {tot_s}, warp instructions {tot_i}")
-for (ln, src), (s, i) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{ln:5d} {100*s/max(tot_s,1):5.1f}% samp {100*i/max(tot_i,1):5.1f}% inst  {src}")
+print("stalls:", ", ".join(f"{k} {100*v/max(tot_s,1):.1f}%" for k, v in sorted(tot_st.items(), key=lambda kv: -kv[1])[:8]))
+for (ln, src), (s, i, st) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    top2 = ",".join(f"{k}:{v}" for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:2])
+    print(f"{ln:5d} {100*s/max(tot_s,1):5.1f}% samp {100*i/max(tot_i,1):5.1f}% inst  [{top2:28s}] {src[:80]}")
