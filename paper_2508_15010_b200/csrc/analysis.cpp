@@ -650,6 +650,14 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         for (uint64_t x : w) if ((x & 0x3FF) != NO_ACOLOR && std::find(cs.begin(), cs.end(), x & 0x3FF) == cs.end()) cs.push_back(x & 0x3FF);
         hist[std::min<size_t>(cs.size(), 8)]++;
       }
+      int fast = 0;
+      const uint32_t full = (1u << (1u << n_axes)) - 1u;
+      for (auto& w : sig_words) {
+        bool f = true;
+        for (uint64_t x : w) if ((x & 0x3FF) != NO_ACOLOR && (((x >> 10) & 0xFFFF) & full) != full) f = false;
+        fast += f;
+      }
+      fprintf(stderr, "[toast] signatures with every axis subset dividing every shardable role: %d of %zu\n", fast, sig_words.size());
       fprintf(stderr, "[toast] signatures by distinct action colors:");
       for (int i = 0; i <= 8; ++i) fprintf(stderr, " %d:%d", i, hist[i]);
       fprintf(stderr, "\n");
@@ -678,6 +686,12 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         if (kk == k.m) k.col[k.m++] = ac;
         k.col[kk] |= 1u << (10 + r);
       }
+      // every axis subset divides every shardable role: materialisation needs one round
+      const uint32_t full = (1u << (1u << n_axes)) - 1u;
+      bool all = true;
+      for (size_t r = 0; r < sig_words[q].size(); ++r)
+        if ((sig_words[q][r] & 0x3FF) != NO_ACOLOR && (((sig_words[q][r] >> 10) & 0xFFFF) & full) != full) all = false;
+      k.pad = all ? 1 : 0;
     }
     // per-signature state-key terms (R14) and FLOP sums
     const size_t NS = sig_words.size();

@@ -60,7 +60,7 @@ __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
 //      the table is written)
 //   B  the per-color event lists [n_acolors][32] (decode/materialise), then,
 //      per warp, the payload/count accumulators and the segment results
-__host__ __device__ inline int smem_c_bytes() { return 32 * (8 + 8 + 4 + 8); }
+__host__ __device__ inline int smem_c_bytes() { return 32 * (8 + 8 + 4 + 8 + 16); }
 __host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes) {
   int a1 = n_sigs * 32 * sig_entry_bytes(n_axes), a2 = 2048 + n_words * 128;
   return r16(a1 > a2 ? a1 : a2);
@@ -114,6 +114,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t on;              // [32] SetGroups fixed to 1 (u64)
   uint32_t status;          // [32]
   uint32_t axpos;           // [32] 2-bit axis of every sequence position (u64)
+  uint32_t axb;             // [4][32] per mesh axis: bitmap of the positions whose action uses it
   uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
   uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
@@ -125,6 +126,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.on = 256;
   s.status = 512;
   s.axpos = 640;
+  s.axb = 896;
   const uint32_t a = smem_c_bytes();
   s.sig = a;
   s.seq = a;
@@ -187,6 +189,8 @@ template <int NA> __device__ __forceinline__ uint32_t e_a2r16(uint32_t e) {
 __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
                                            uint64_t& ones, uint64_t& axpos) {
   for (int c = 0; c < T.n_acolors; ++c) sp<uint32_t>(S.acol)[c * 32 + lane] = 0u;
+#pragma unroll
+  for (int A = 0; A < 4; ++A) sp<uint32_t>(S.axb)[A * 32 + lane] = 0u;
   uint32_t status = 0;
   bool stopped = false;
   uint64_t fx = 0, on = 0, ap = 0;
@@ -206,6 +210,7 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
     if (dup) status |= TOAST_ST_DUP_COLOR_AXIS;
     else {
       sp<uint32_t>(S.acol)[ac * 32 + lane] = pm | (1u << j);
+      sp<uint32_t>(S.axb)[ax * 32 + lane] |= 1u << j;
       ap |= (uint64_t)ax << (2 * j);
     }
     uint64_t gw = __ldg(T.acol_groups + ac);
@@ -230,9 +235,10 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
 // axis shards at most one loop of the op; divisibility by div_ok.  The
 // positions of the signature's events are the union of its colors' position
 // bitmaps, walked in ascending order.
-template <int M>
+template <int M, int NA>
 __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const uint4& c0, const uint4& c1,
-                                                  uint32_t dmask, const uint4& dw, uint64_t axpos) {
+                                                  uint32_t dmask, const uint4& dw, uint64_t axpos, const uint32_t* axb,
+                                                  bool alldiv) {
   const uint32_t col[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
   uint32_t pm[M], rm[M], bits = 0;
 #pragma unroll
@@ -241,8 +247,25 @@ __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const
     pm[k] = rm[k] ? sp<uint32_t>(S.acol)[(col[k] & 0x3FF) * 32 + lane] : 0u;
     bits |= pm[k];
   }
-  uint32_t a2r = 0xFFFFu, masks = 0, opmask = 0;
   const uint64_t dlo = u64of(dw.x, dw.y), dhi = u64of(dw.z, dw.w);
+  // signatures flagged alldiv (every axis subset divides every shardable
+  // role): every event is feasible, so each axis lands on the first role of
+  // its earliest event — the serial result without the walk
+  if (alldiv) {
+    uint32_t a2r = 0xFFFFu;
+#pragma unroll
+    for (int A = 0; A < NA; ++A) {
+      const uint32_t bA = bits & axb[A];
+      if (!bA) continue;
+      const uint32_t j = __ffs(bA) - 1;
+      uint32_t roles = 0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) roles |= ((pm[k] >> j) & 1) ? rm[k] : 0u;
+      a2r = (a2r & ~(0xFu << (4 * A))) | ((uint32_t)(__ffs(roles) - 1) << (4 * A));
+    }
+    return a2r;
+  }
+  uint32_t a2r = 0xFFFFu, masks = 0, opmask = 0;
   while (bits) {
     const uint32_t j = __ffs(bits) - 1;
     bits &= bits - 1;
@@ -267,11 +290,13 @@ __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const
   return a2r;
 }
 
+template <int NA>
 __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, int s,
-                                                    uint64_t fixed0, uint64_t ones, uint64_t axpos) {
+                                                    uint64_t fixed0, uint64_t ones, uint64_t axpos, const uint32_t* axb) {
   const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
   const uint4 mt = __ldg(kp + 3);
   const uint32_t m = mt.y & 0xFF, dr = (mt.y >> 8) & 0xFF;
+  const bool alldiv = (mt.y >> 24) & 1;
   if (m == 0) return 0xFFFFFFFFu;
   // roles deselected by the fixed SetGroup bits
   uint32_t dmask = 0;
@@ -284,14 +309,14 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
   const uint4 c0 = __ldg(kp + 1), c1 = __ldg(kp + 2), dw = __ldg(kp);
   uint32_t a2r;
   switch (m) {   // warp-uniform: the merge is unrolled over the signature's color count
-    case 1: a2r = materialize_m<1>(S, lane, c0, c1, dmask, dw, axpos); break;
-    case 2: a2r = materialize_m<2>(S, lane, c0, c1, dmask, dw, axpos); break;
-    case 3: a2r = materialize_m<3>(S, lane, c0, c1, dmask, dw, axpos); break;
-    case 4: a2r = materialize_m<4>(S, lane, c0, c1, dmask, dw, axpos); break;
-    case 5: a2r = materialize_m<5>(S, lane, c0, c1, dmask, dw, axpos); break;
-    case 6: a2r = materialize_m<6>(S, lane, c0, c1, dmask, dw, axpos); break;
-    case 7: a2r = materialize_m<7>(S, lane, c0, c1, dmask, dw, axpos); break;
-    default: a2r = materialize_m<8>(S, lane, c0, c1, dmask, dw, axpos); break;
+    case 1: a2r = materialize_m<1, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    case 2: a2r = materialize_m<2, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    case 3: a2r = materialize_m<3, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    case 4: a2r = materialize_m<4, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    case 5: a2r = materialize_m<5, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    case 6: a2r = materialize_m<6, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    case 7: a2r = materialize_m<7, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    default: a2r = materialize_m<8, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
   }
   if (a2r == 0xFFFFu) return 0xFFFFFFFFu;   // nothing sharded: every axis "none" in both maps
   const uint32_t rdm = mt.x;
@@ -335,8 +360,11 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   {
     const uint64_t f0 = sp<unsigned long long>(S.f0)[lane], on = sp<unsigned long long>(S.on)[lane];
     const uint64_t ap = sp<unsigned long long>(S.axpos)[lane];
+    uint32_t axb[NA];
+#pragma unroll
+    for (int A = 0; A < NA; ++A) axb[A] = sp<uint32_t>(S.axb)[A * 32 + lane];
     for (int s = warp; s < T.n_sigs; s += K) {
-      const uint32_t e = pack_entry<NA>(materialize_sig(T, S, lane, s, f0, on, ap));
+      const uint32_t e = pack_entry<NA>(materialize_sig<NA>(T, S, lane, s, f0, on, ap, axb));
       ent_store<NA>(S, s, lane, e);
       uint32_t present = 0;
 #pragma unroll

@@ -136,7 +136,8 @@ struct KSig {
   uint32_t resdim;       // nibble r: result dim of role r (0xF: none)
   uint8_t m;             // distinct action colors among the roles
   uint8_t dsel_roles;    // roles with a deselection class
-  uint8_t nr, pad;
+  uint8_t nr;
+  uint8_t pad;           // bit0: every axis subset divides every shardable role (one-round materialisation)
   uint64_t cls;          // byte r: deselection class of role r (0 = never deselected)
 };
 static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");

@@ -9,14 +9,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2508_15010_b200", "lib", "variants")
 VARIANTS = {
-    "t512b1": ["-DTOAST_MAX_THREADS=512", "-DTOAST_MIN_BLOCKS=1"],
-    "t256b3": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=3", "-DTOAST_MAX_WPB=8"],
-    "t256b4": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=4", "-DTOAST_MAX_WPB=8"],
-    "t128b6": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=6", "-DTOAST_MAX_WPB=4"],
-    "r72": ["-maxrregcount=72"],
-    "r80": ["-maxrregcount=80"],
-    "r96": ["-maxrregcount=96"],
+    "b3": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=3"],
+    "b4": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=4"],
+    "b5": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=5"],
+    "b6": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=6"],
 }
+KS = [int(k) for k in os.environ.get("SWEEP_KS", "1,2").split(",")]
 
 
 def build_all():
@@ -30,11 +28,12 @@ def build_all():
 def run_all(config="gpt24", n=1 << 18):
     out = {}
     for tag in VARIANTS:
-        lib = os.path.join(VAR, f"libtoast_{tag}.so")
-        r = subprocess.run([sys.executable, __file__, "one", lib, config, str(n)], capture_output=True, text=True,
-                           env=dict(os.environ, TOAST_LIB=lib))
-        out[tag] = r.stdout.strip().splitlines()[-1] if r.returncode == 0 else ("ERR " + r.stderr[-300:])
-        print(tag, out[tag], flush=True)
+        for K in KS:
+            lib = os.path.join(VAR, f"libtoast_{tag}.so")
+            r = subprocess.run([sys.executable, __file__, "one", lib, config, str(n)], capture_output=True, text=True,
+                               env=dict(os.environ, TOAST_LIB=lib, TOAST_FORCE_K=str(K)))
+            out[f"{tag}K{K}"] = r.stdout.strip().splitlines()[-1] if r.returncode == 0 else ("ERR " + r.stderr[-300:])
+            print(f"{tag}K{K}", out[f"{tag}K{K}"], flush=True)
     return out
 
 
@@ -67,6 +66,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "build":
         build_all()
     elif sys.argv[1] == "run":
-        run_all(*(sys.argv[2:3] or ["gpt24"]))
+        for cfg in (sys.argv[2:] or ["gpt24"]):
+            run_all(cfg)
     else:
         one(sys.argv[2], sys.argv[3], int(sys.argv[4]))
