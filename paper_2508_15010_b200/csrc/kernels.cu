@@ -393,12 +393,15 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   unsigned long long* pay = sp<unsigned long long>(acc);
   uint32_t* cnt = sp<uint32_t>(acc + NA * 4 * 32 * 8);
   unsigned long long* seg = sp<unsigned long long>(acc + NA * 4 * 32 * 12);
-#pragma unroll
-  for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = 0ULL; cnt[q * 32 + lane] = 0u; }
 
   // H4 per edge template: every use edge of the template communicates the
   // same way, so its payloads are costed once from the template's summed
   // bytes; the sweep only needs each edge's temporary (presU/presD)
+  // (payloads and counts accumulate in registers, then land in this warp's slots)
+  unsigned long long rp[NA * 4];
+  uint32_t rc[NA * 4];
+#pragma unroll
+  for (int q = 0; q < NA * 4; ++q) { rp[q] = 0ULL; rc[q] = 0u; }
   for (int tix = warp; tix < T.n_tmpl; tix += K) {
     const uint2 t0 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix));
     const uint2 t1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix) + 1);
@@ -427,11 +430,11 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
         if (dd == 15 || dd == du) continue;
         if (du != 15) {
-          pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
-          cnt[(A * 4 + TOAST_A2A) * 32 + lane] += ne;
+          rp[A * 4 + TOAST_A2A] += size;
+          rc[A * 4 + TOAST_A2A] += ne;
         } else {
-          pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
-          cnt[(A * 4 + TOAST_AG) * 32 + lane] += ne;
+          rp[A * 4 + TOAST_AG] += size;
+          rc[A * 4 + TOAST_AG] += ne;
           size *= (uint64_t)T.sizes[A];
         }
       }
@@ -440,17 +443,19 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         if (!((P >> A) & 1)) continue;
         if (((dimU >> (4 * A)) & 15) != 15) {
           size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
-          pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
-          cnt[(A * 4 + TOAST_RS) * 32 + lane] += ne;
+          rp[A * 4 + TOAST_RS] += size;
+          rc[A * 4 + TOAST_RS] += ne;
         } else {
-          pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
-          cnt[(A * 4 + TOAST_AR) * 32 + lane] += ne;
+          rp[A * 4 + TOAST_AR] += size;
+          rc[A * 4 + TOAST_AR] += ne;
         }
       }
       tbv = (uint8_t)(dcode<P2>(T, presU) | (dcode<P2>(T, presD) << 4));
     }
     sp<uint8_t>(S.tb)[tix * 32 + lane] = tbv;
   }
+#pragma unroll
+  for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = rp[q]; cnt[q * 32 + lane] = rc[q]; }
   __syncthreads();
 
   // H5 (C12, reading R19): peak = max over the kept ops of the peak-memory
