@@ -294,7 +294,8 @@ template <int NA>
 __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, int s,
                                                     uint64_t fixed0, uint64_t ones, uint64_t axpos, const uint32_t* axb) {
   const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
-  const uint4 mt = __ldg(kp + 3);
+  // all four 16-B words of the record in flight at once
+  const uint4 mt = __ldg(kp + 3), c0 = __ldg(kp + 1), c1 = __ldg(kp + 2), dw = __ldg(kp);
   const uint32_t m = mt.y & 0xFF, dr = (mt.y >> 8) & 0xFF;
   const bool alldiv = (mt.y >> 24) & 1;
   if (m == 0) return 0xFFFFFFFFu;
@@ -306,7 +307,6 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
     const uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
     if ((fixed0 & n0) | (ones & n1)) dmask |= 1u << r;
   }
-  const uint4 c0 = __ldg(kp + 1), c1 = __ldg(kp + 2), dw = __ldg(kp);
   uint32_t a2r;
   switch (m) {   // warp-uniform: the merge is unrolled over the signature's color count
     case 1: a2r = materialize_m<1, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
@@ -364,6 +364,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
 #pragma unroll
     for (int A = 0; A < NA; ++A) axb[A] = sp<uint32_t>(S.axb)[A * 32 + lane];
     for (int s = warp; s < T.n_sigs; s += K) {
+      const uint64_t glo = __ldg(T.sig_flops + 2 * s), ghi = __ldg(T.sig_flops + 2 * s + 1);
       const uint32_t e = pack_entry<NA>(materialize_sig<NA>(T, S, lane, s, f0, on, ap, axb));
       ent_store<NA>(S, s, lane, e);
       uint32_t present = 0;
@@ -379,7 +380,6 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
           opmask |= 1u << A;
         }
       }
-      const uint64_t glo = __ldg(T.sig_flops + 2 * s), ghi = __ldg(T.sig_flops + 2 * s + 1);
       if (glo | ghi) {
         const unsigned __int128 f = dv128<P2>(T, ((unsigned __int128)ghi << 64) | glo, opmask);
         const uint64_t l = (uint64_t)f;
@@ -402,10 +402,20 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   uint32_t rc[NA * 4];
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { rp[q] = 0ULL; rc[q] = 0u; }
+  // the next template's record is loaded one iteration ahead
+  uint2 n0 = make_uint2(0, 0), n1 = n0, n2 = n0;
+  if (warp < T.n_tmpl) {
+    n0 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + warp));
+    n1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + warp) + 1);
+    n2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + warp) + 2);
+  }
   for (int tix = warp; tix < T.n_tmpl; tix += K) {
-    const uint2 t0 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix));
-    const uint2 t1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix) + 1);
-    const uint2 t2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix) + 2);
+    const uint2 t0 = n0, t1 = n1, t2 = n2;
+    if (tix + K < T.n_tmpl) {
+      n0 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K));
+      n1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K) + 1);
+      n2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K) + 2);
+    }
     const uint32_t de = ent_load<NA>(S, t0.x & 0xFFFF, lane), ue = ent_load<NA>(S, t0.x >> 16, lane);
     const uint32_t use_dimof = t0.y;
     uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
@@ -944,6 +954,10 @@ void free_tables(toast_analysis* a) {
   if (a->pipe_event) cudaEventDestroy((cudaEvent_t)a->pipe_event);
   a->pipe_stream[0] = a->pipe_stream[1] = nullptr;
   a->pipe_event = nullptr;
+  if (a->spool.d) cudaFree(a->spool.d);
+  if (a->spool.h_pre) cudaFreeHost(a->spool.h_pre);
+  if (a->spool.h_red) cudaFreeHost(a->spool.h_red);
+  a->spool = toast_analysis::SearchPool{};
   for (void* p : a->dev_allocs) cudaFree(p);
   a->dev_allocs.clear();
   if (a->scratch) cudaFree(a->scratch);

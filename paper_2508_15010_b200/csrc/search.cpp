@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "toast_internal.h"
@@ -54,6 +55,7 @@ struct toast_search_state {
   toast::LeafRed* h_red = nullptr;
   void* d_buf = nullptr;
   size_t d_bytes = 0;
+  bool pooled = false;     // the buffers belong to the analysis' search pool
   ~toast_search_state();
 };
 
@@ -121,10 +123,43 @@ toast_status search_begin(const toast_analysis* a, const toast_search_opts* o, i
   s->d_bytes = (size_t)L * 64 + (size_t)L * sizeof(toast_cost) + (size_t)L * R * (64 + sizeof(toast_cost)) +
                (size_t)L * sizeof(LeafRed);
   if (a->device >= 0) {
-    cudaError_t e = cudaMalloc(&s->d_buf, s->d_bytes);
-    if (e == cudaSuccess) e = cudaMallocHost((void**)&s->h_lpre, (size_t)L * 64);
-    if (e == cudaSuccess) e = cudaMallocHost((void**)&s->h_red, (size_t)L * sizeof(LeafRed));
-    if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_OOM; }
+    // buffers: the analysis' pool when it is free (grown to fit), else our own
+    toast_analysis* ma = const_cast<toast_analysis*>(a);
+    std::lock_guard<std::mutex> lk(ma->scratch_mu);
+    auto& P = ma->spool;
+    const size_t hp = (size_t)L * 64, hr = (size_t)L * sizeof(LeafRed);
+    cudaError_t e = cudaSuccess;
+    if (!P.in_use) {
+      if (P.d_bytes < s->d_bytes) {
+        if (P.d) cudaFree(P.d);
+        P.d = nullptr; P.d_bytes = 0;
+        e = cudaMalloc(&P.d, s->d_bytes);
+        if (e == cudaSuccess) P.d_bytes = s->d_bytes;
+      }
+      if (e == cudaSuccess && P.h_pre_bytes < hp) {
+        if (P.h_pre) cudaFreeHost(P.h_pre);
+        P.h_pre = nullptr; P.h_pre_bytes = 0;
+        e = cudaMallocHost(&P.h_pre, hp);
+        if (e == cudaSuccess) P.h_pre_bytes = hp;
+      }
+      if (e == cudaSuccess && P.h_red_bytes < hr) {
+        if (P.h_red) cudaFreeHost(P.h_red);
+        P.h_red = nullptr; P.h_red_bytes = 0;
+        e = cudaMallocHost(&P.h_red, hr);
+        if (e == cudaSuccess) P.h_red_bytes = hr;
+      }
+      if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_OOM; }
+      P.in_use = true;
+      s->pooled = true;
+      s->d_buf = P.d;
+      s->h_lpre = reinterpret_cast<uint16_t*>(P.h_pre);
+      s->h_red = reinterpret_cast<LeafRed*>(P.h_red);
+    } else {
+      e = cudaMalloc(&s->d_buf, s->d_bytes);
+      if (e == cudaSuccess) e = cudaMallocHost((void**)&s->h_lpre, hp);
+      if (e == cudaSuccess) e = cudaMallocHost((void**)&s->h_red, hr);
+      if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_OOM; }
+    }
   }
   *out = s.release();
   return TOAST_OK;
@@ -265,6 +300,12 @@ void search_free(toast_search_state* s) { delete s; }
 
 toast_search_state::~toast_search_state() {
   toast::free_tree(root);
+  if (pooled) {
+    toast_analysis* ma = const_cast<toast_analysis*>(a);
+    std::lock_guard<std::mutex> lk(ma->scratch_mu);
+    ma->spool.in_use = false;
+    return;
+  }
   if (d_buf) cudaFree(d_buf);
   if (h_lpre) cudaFreeHost(h_lpre);
   if (h_red) cudaFreeHost(h_red);

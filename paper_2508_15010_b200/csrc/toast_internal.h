@@ -233,6 +233,16 @@ struct toast_analysis {
   int32_t occ_eval[4] = {0, 0, 0, 0}, occ_roll[4] = {0, 0, 0, 0};   // blocks per SM for K = 1, 2, 4, 8
   int32_t n_sms = 0, k_throughput = 1;
   void* pipe_stream[2] = {nullptr, nullptr};   // host-buffer path: chunked H2D / kernel / D2H overlap
+  // search buffers, kept between searches (a search that finds them in use allocates its own)
+  struct SearchPool {
+    void* d = nullptr;
+    size_t d_bytes = 0;
+    void* h_pre = nullptr;
+    size_t h_pre_bytes = 0;
+    void* h_red = nullptr;
+    size_t h_red_bytes = 0;
+    bool in_use = false;
+  } spool;
   void* pipe_event = nullptr;
 };
 
