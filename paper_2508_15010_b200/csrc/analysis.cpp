@@ -939,6 +939,11 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     T.inv128_lo[S] = (uint64_t)inv128;
     T.inv128_hi[S] = (uint64_t)(inv128 >> 64);
   }
+  T.shift_pack = 0;
+  for (int S = 0; S < 16; ++S) {
+    if (T.shift[S] > 15) T.pow2 = 0;   // the shift path packs 4-bit codes; larger meshes take the general path
+    T.shift_pack |= (uint64_t)(T.shift[S] & 15) << (4 * S);
+  }
   return TOAST_OK;
 }
 

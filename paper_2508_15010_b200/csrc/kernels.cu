@@ -146,7 +146,11 @@ __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((u
 // is the subset itself and division is (x >> twos) * odd^-1 mod 2^64 (the
 // divisor always divides x exactly on this path)
 template <bool P2>
-__device__ __forceinline__ uint32_t dcode(const DeviceTables& T, uint32_t S) { return P2 ? T.shift[S] : S; }
+__device__ __forceinline__ uint32_t dcode(const DeviceTables& T, uint32_t S) {
+  // P2: one nibble per subset of a uniform word (a per-lane index into the
+  // kernel-parameter array would serialise across lanes)
+  return P2 ? (uint32_t)(T.shift_pack >> (4 * S)) & 15u : S;
+}
 template <bool P2>
 __device__ __forceinline__ uint64_t dv(const DeviceTables& T, uint64_t x, uint32_t code) {
   return P2 ? (x >> code) : (x >> T.shift[code]) * T.inv[code];
@@ -158,8 +162,8 @@ __device__ __forceinline__ long long dvs(const DeviceTables& T, long long x, uin
 }
 template <bool P2>
 __device__ __forceinline__ unsigned __int128 dv128(const DeviceTables& T, unsigned __int128 x, uint32_t S) {
+  if (P2) return x >> dcode<true>(T, S);
   x >>= T.shift[S];
-  if (P2) return x;
   return x * (((unsigned __int128)T.inv128_hi[S] << 64) | T.inv128_lo[S]);
 }
 

@@ -176,6 +176,7 @@ struct DeviceTables {
   uint64_t DM, peak0;
   uint64_t inv[16];     // exact division by prod(subset): (x >> shift) * inv
   uint32_t shift[16];
+  uint64_t shift_pack;  // nibble S = shift[S] (pow2 meshes, every subset shift <= 15)
   uint64_t inv128_lo[16], inv128_hi[16];   // the same inverse mod 2^128 (FLOP totals)
 };
 

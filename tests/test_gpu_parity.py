@@ -291,7 +291,7 @@ def test_random_programs_parity_including_repeated_operands():
 
 
 @pytest.mark.parametrize("n", [1, 31, 33, 64, 200, 1000])
-def test_small_batches_use_segmented_sweep(n):
+def test_small_batches_split_across_warps(n):
     """Batches below one wave are swept by K > 1 warps per block (segmented
     liveness scan); results must not depend on K."""
     a, o = setup("gpt24")
