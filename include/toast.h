@@ -165,6 +165,18 @@ toast_status toast_rollout_batch(const toast_analysis* a, const uint16_t* prefix
 toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], uint8_t* masks, int64_t cap,
                                int64_t* n);
 
+/* toast_lower — the device-local program one sequence implies (SURVEY §8(f)
+ * NEXT-1): every value's local shape, layout (per dim, the mesh axes sharding
+ * it) and partial axes, and in front of every use edge the collectives of the
+ * cost model (C11: phase 1 all_to_all/all_gather, phase 2 reduce_scatter /
+ * all_reduce, phase 3 local slice), each with the payload bytes the cost
+ * model charges — the notation of Fig. 2c / Fig. 5b.
+ * Text, one statement per line; format in DESIGN.md "Lowering" and
+ * csrc/lower.cpp.  seq: host uint16[32] (0 = STOP).  *needed = bytes incl.
+ * NUL; writes only if cap >= *needed.  Host-side (no GPU needed).
+ * Errors: TOAST_E_INVALID_ARG (NULL, an id >= the action count). */
+toast_status toast_lower(const toast_analysis* a, const uint16_t seq[32], char* buf, size_t cap, size_t* needed);
+
 /* ---------------------------------------------------------------------------
  * Search (C16).  Single GPU: toast_search.  Root-parallel
  * multi-GPU: the caller drives begin / round / (all_gather of the export

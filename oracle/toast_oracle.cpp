@@ -1154,19 +1154,27 @@ struct Oracle {
         if (D == U && P == 0) continue;
         std::vector<int> cur = D;
         u64 size = local_bytes_of(v, D);
-        // phase 1: axes of D not kept in the same dim
+        // phase 1: axes of D not kept in the same dim (reading R20):
+        // 1a all_gather every axis U holds on no dim, then 1b all_to_all every
+        // axis U holds on another dim — so every intermediate layout keeps
+        // only axes of D (1a) or of U (1b) on each dim and stays divisible
+        for (int A = 0; A < nA; A++) {
+          for (size_t i = 0; i < D.size(); i++) {
+            if (!(cur[i] & (1 << A)) || (U[i] & (1 << A))) continue;
+            bool elsewhere = false;
+            for (size_t j = 0; j < U.size(); j++) if (j != i && (U[j] & (1 << A))) elsewhere = true;
+            if (elsewhere) continue;
+            out.payload[A][K_AG] += size; ncount[A][K_AG]++;
+            cur[i] &= ~(1 << A); size *= (u64)axes[A].size;
+          }
+        }
         for (int A = 0; A < nA; A++) {
           for (size_t i = 0; i < D.size(); i++) {
             if (!(cur[i] & (1 << A)) || (U[i] & (1 << A))) continue;
             int j_other = -1;
             for (size_t j = 0; j < U.size(); j++) if (j != i && (U[j] & (1 << A))) j_other = (int)j;
-            if (j_other >= 0) {
-              out.payload[A][K_A2A] += size; ncount[A][K_A2A]++;
-              cur[i] &= ~(1 << A); cur[j_other] |= 1 << A;
-            } else {
-              out.payload[A][K_AG] += size; ncount[A][K_AG]++;
-              cur[i] &= ~(1 << A); size *= (u64)axes[A].size;
-            }
+            out.payload[A][K_A2A] += size; ncount[A][K_A2A]++;
+            cur[i] &= ~(1 << A); cur[j_other] |= 1 << A;
           }
         }
         // phase 2: partial sums

@@ -25,7 +25,7 @@ CU_FLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++20", "-fmad=false", "-Xcompil
                       f"-I{INC}", f"-I{SRC}"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", f"-I{CUDA}/include", f"-I{INC}", f"-I{SRC}"]
 
-SOURCES = ["ir.cpp", "analysis.cpp", "search.cpp", "abi.cpp", "kernels.cu"]
+SOURCES = ["ir.cpp", "analysis.cpp", "lower.cpp", "search.cpp", "abi.cpp", "kernels.cu"]
 HEADERS = ["toast_internal.h"]
 
 

@@ -88,6 +88,7 @@ toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_anal
     toast_status st = toast::build_analysis(g, o, a, err);
     if (st != TOAST_OK) { delete a; return fail(st, err); }
     a->device = g->device;
+    a->graph = std::make_shared<const toast_graph>(*g);
     if (a->device >= 0) {
       st = toast::upload_tables(a, err);
       if (st != TOAST_OK) { toast::free_tables(a); delete a; return fail(st, err); }
@@ -173,6 +174,18 @@ toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], 
       if (seq[i] >= a->actions.size()) return fail(TOAST_E_INVALID_ARG, "bad action id");
     toast::host_materialize(a, seq, masks);
   }
+  return ret(TOAST_OK, "");
+}
+
+toast_status toast_lower(const toast_analysis* a, const uint16_t seq[32], char* buf, size_t cap, size_t* needed) {
+  if (!a || !seq || !needed) return fail(TOAST_E_INVALID_ARG, "NULL argument");
+  for (int i = 0; i < 32 && seq[i]; ++i)
+    if (seq[i] >= a->actions.size()) return fail(TOAST_E_INVALID_ARG, "bad action id");
+  std::string s, err;
+  toast_status st = toast::lower_program(a, seq, s, err);
+  if (st != TOAST_OK) return fail(st, err);
+  *needed = s.size() + 1;
+  if (buf && cap >= *needed) memcpy(buf, s.c_str(), s.size() + 1);
   return ret(TOAST_OK, "");
 }
 

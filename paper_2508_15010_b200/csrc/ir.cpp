@@ -357,6 +357,10 @@ toast_status parse_ir(const char* text, size_t len, toast_graph* g, std::string&
         attrs.back().push_back(tok);
       }
       c.accept(']');
+      for (size_t gi = 0; gi < attrs.size(); ++gi) {
+        if (gi) op.attr_text += ';';
+        for (size_t ai = 0; ai < attrs[gi].size(); ++ai) op.attr_text += (ai ? "," : "") + attrs[gi][ai];
+      }
     }
     if (!c.expect('(')) return TOAST_E_PARSE;
     if (!c.peek(')')) {

@@ -440,17 +440,19 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       const uint32_t ne = t2.x;
       uint64_t size = dv<P2>(T, sgb, dcode<P2>(T, presD));
 #pragma unroll
-      for (int A = 0; A < NA; ++A) {          // phase 1: all_gather / all_to_all
+      for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather (reading R20)
         const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
-        if (dd == 15 || dd == du) continue;
-        if (du != 15) {
-          rp[A * 4 + TOAST_A2A] += size;
-          rc[A * 4 + TOAST_A2A] += ne;
-        } else {
-          rp[A * 4 + TOAST_AG] += size;
-          rc[A * 4 + TOAST_AG] += ne;
-          size *= (uint64_t)T.sizes[A];
-        }
+        if (dd == 15 || du != 15) continue;
+        rp[A * 4 + TOAST_AG] += size;
+        rc[A * 4 + TOAST_AG] += ne;
+        size *= (uint64_t)T.sizes[A];
+      }
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
+        const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+        if (dd == 15 || du == 15 || dd == du) continue;
+        rp[A * 4 + TOAST_A2A] += size;
+        rc[A * 4 + TOAST_A2A] += ne;
       }
 #pragma unroll
       for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
@@ -550,17 +552,19 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
           if (!dup) {
             uint64_t size = dv<P2>(T, gb, dcode<P2>(T, presD));
 #pragma unroll
-            for (int A = 0; A < NA; ++A) {
+            for (int A = 0; A < NA; ++A) {       // phase 1a: all_gather (reading R20)
               const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
-              if (dd == 15 || dd == du) continue;
-              if (du != 15) {
-                pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
-                cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
-              } else {
-                pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
-                cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
-                size *= (uint64_t)T.sizes[A];
-              }
+              if (dd == 15 || du != 15) continue;
+              pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
+              cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
+              size *= (uint64_t)T.sizes[A];
+            }
+#pragma unroll
+            for (int A = 0; A < NA; ++A) {       // phase 1b: all_to_all
+              const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+              if (dd == 15 || du == 15 || dd == du) continue;
+              pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
+              cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
             }
 #pragma unroll
             for (int A = 0; A < NA; ++A) {

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <vector_types.h>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -35,6 +36,7 @@ struct GOp {
   std::vector<int32_t> operands;
   int32_t result = -1;
   std::string binding;
+  std::string attr_text;       // the bracket attributes as written (groups ';', atoms ',')
 };
 
 }  // namespace toast
@@ -221,6 +223,7 @@ struct toast_analysis {
   std::vector<uint32_t> op_sig;
   std::vector<int32_t> axis_size;
 
+  std::shared_ptr<const toast_graph> graph;   // the program (names, attributes) for toast_lower
   toast::DeviceTables dt;       // device pointers valid iff device >= 0
   int32_t device = -1;
   std::vector<void*> dev_allocs;
@@ -254,6 +257,8 @@ toast_status parse_ir(const char* text, size_t len, toast_graph* g, std::string&
 toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast_analysis* a, std::string& err);
 std::string dump_json(const toast_analysis* a);
 void host_materialize(const toast_analysis* a, const uint16_t* seq, uint8_t* masks);
+// lower.cpp: the device-local program of one action sequence (NEXT-1)
+toast_status lower_program(const toast_analysis* a, const uint16_t* seq, std::string& out, std::string& err);
 // kernels.cu
 toast_status upload_tables(toast_analysis* a, std::string& err);
 void free_tables(toast_analysis* a);

@@ -89,6 +89,7 @@ _sigs = {
     "toast_eval_batch": [_P, _P, ctypes.c_int64, _P, _P],
     "toast_rollout_batch": [_P, _P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _P, _P, _P],
     "toast_materialize": [_P, _P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
+    "toast_lower": [_P, _P, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
     "toast_search": [_P, ctypes.POINTER(_SearchOpts), _P],
     "toast_search_begin": [_P, ctypes.POINTER(_SearchOpts), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_P)],
     "toast_search_round": [_P, _P],
@@ -271,6 +272,17 @@ def materialize(a: Analysis, seq) -> np.ndarray:
     m = np.zeros(n.value, dtype=np.uint8)
     _check(_lib.toast_materialize(a._h, s.ctypes.data, m.ctypes.data, n.value, ctypes.byref(n)))
     return m
+
+
+def lower(a: Analysis, seq) -> str:
+    """The device-local program of one action sequence (toast_lower)."""
+    s = np.zeros(32, dtype=np.uint16)
+    s[:len(seq)] = seq
+    need = ctypes.c_size_t()
+    _check(_lib.toast_lower(a._h, s.ctypes.data, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(_lib.toast_lower(a._h, s.ctypes.data, buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
 
 
 def as_costs(out) -> np.ndarray:
