@@ -218,6 +218,15 @@ typedef struct {
   int32_t pad;
   toast_cost best;         /* full record of the rank's best */
 } toast_search_export;
+/* The export record is this header followed by one toast_root_stat per action
+   id (index = action id, entry 0 unused): the rank's root-child visit count
+   and reward sum (the ranks exchange best sequences AND visit
+   statistics).  toast_search_import sums them over the ranks; read the sums
+   with toast_search_root_stats. */
+typedef struct {
+  int64_t visits;
+  double value_sum;
+} toast_root_stat;
 
 toast_status toast_search(const toast_analysis* a, const toast_search_opts* o, toast_search_result* out);
 
@@ -232,6 +241,10 @@ toast_status toast_search_round(toast_search_state* s, void* export_buf);
 /* imports world records ([world][export_bytes], host memory); *stop = 1 when all ranks must stop */
 toast_status toast_search_import(toast_search_state* s, const void* gathered, int32_t* stop);
 toast_status toast_search_end(toast_search_state* s, toast_search_result* out);
+/* root-child statistics summed over the ranks at the last import (index =
+   action id; visits 0 = the child is not expanded on any rank).  out: cap
+   entries; *n = number of actions. */
+toast_status toast_search_root_stats(const toast_search_state* s, toast_root_stat* out, int32_t cap, int32_t* n);
 
 const char* toast_last_error(void);
 void toast_free_graph(toast_graph* g);

@@ -18,7 +18,8 @@ toast_status search_begin(const toast_analysis* a, const toast_search_opts* o, i
 toast_status search_round(toast_search_state* s, void* export_buf, std::string& err);
 toast_status search_import(toast_search_state* s, const void* gathered, int32_t* stop, std::string& err);
 void search_result(const toast_search_state* s, toast_search_result* out);
-size_t search_export_bytes();
+size_t search_export_bytes(const toast_analysis* a);
+int32_t search_root_stats(const toast_search_state* s, toast_root_stat* out, int32_t cap);
 void search_free(toast_search_state* s);
 }  // namespace toast
 
@@ -190,8 +191,13 @@ toast_status toast_lower(const toast_analysis* a, const uint16_t seq[32], char* 
 }
 
 size_t toast_search_export_bytes(const toast_analysis* a) {
-  (void)a;
-  return toast::search_export_bytes();
+  return a ? toast::search_export_bytes(a) : 0;
+}
+
+toast_status toast_search_root_stats(const toast_search_state* s, toast_root_stat* out, int32_t cap, int32_t* n) {
+  if (!s || !n || (cap > 0 && !out)) return fail(TOAST_E_INVALID_ARG, "NULL argument");
+  *n = toast::search_root_stats(s, out, cap);
+  return ret(TOAST_OK, "");
 }
 
 toast_status toast_search_begin(const toast_analysis* a, const toast_search_opts* o, int32_t rank, int32_t world,
@@ -227,7 +233,7 @@ toast_status toast_search(const toast_analysis* a, const toast_search_opts* o, t
   toast_search_state* s = nullptr;
   toast_status st = toast_search_begin(a, o, 0, 1, &s);
   if (st) return st;
-  std::string buf(toast::search_export_bytes(), '\0');
+  std::string buf(toast::search_export_bytes(a), '\0');
   int32_t stop = 0;
   while (!stop) {
     st = toast_search_round(s, &buf[0]);

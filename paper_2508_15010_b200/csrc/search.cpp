@@ -30,6 +30,7 @@ struct SNode {
 };
 
 using ExportRec = toast_search_export;   // include/toast.h
+size_t search_export_bytes(const toast_analysis* a);
 
 }  // namespace toast
 
@@ -48,6 +49,7 @@ struct toast_search_state {
   int64_t global_evals = 1;
   int64_t rollouts_done = 0;
   int32_t rounds = 0, nonimprove = 0, hit_target = 0, done = 0;
+  std::vector<toast_root_stat> groot;   // root-child statistics summed over the ranks (last import)
   double time_to_target = -1.0;
   std::chrono::steady_clock::time_point t_start;
   // buffers: pinned host (prefixes in, per-leaf reductions out) and device scratch
@@ -243,28 +245,44 @@ toast_status search_round(toast_search_state* s, void* export_buf, std::string& 
   ex->elapsed_s = elapsed(s);
   ex->rank = s->rank;
   ex->best = s->best;
+  // this rank's root-child statistics, indexed by action id
+  toast_root_stat* rs = reinterpret_cast<toast_root_stat*>(reinterpret_cast<char*>(export_buf) + sizeof(ExportRec));
+  memset(rs, 0, sizeof(toast_root_stat) * (size_t)a->dt.n_actions);
+  for (SNode* ch : s->root->children) {
+    rs[ch->prefix[0]].visits = ch->N;
+    rs[ch->prefix[0]].value_sum = ch->W;
+  }
   return TOAST_OK;
 }
 
 toast_status search_import(toast_search_state* s, const void* gathered, int32_t* stop, std::string& err) {
   (void)err;
-  const ExportRec* r = reinterpret_cast<const ExportRec*>(gathered);
+  const size_t rb = search_export_bytes(s->a);
+  auto rec = [&](int i) { return reinterpret_cast<const ExportRec*>(reinterpret_cast<const char*>(gathered) + rb * i); };
   int gb = 0;
   int64_t tot = 0;
+  const int NA = s->a->dt.n_actions;
+  s->groot.assign(NA, toast_root_stat{0, 0.0});
   for (int i = 0; i < s->world; ++i) {
-    tot += r[i].evals;
-    if (i && better(r[i].best, r[i].best_seq, r[gb].best, r[gb].best_seq)) gb = i;
+    tot += rec(i)->evals;
+    if (i && better(rec(i)->best, rec(i)->best_seq, rec(gb)->best, rec(gb)->best_seq)) gb = i;
+    const toast_root_stat* rs = reinterpret_cast<const toast_root_stat*>(rec(i) + 1);
+    for (int x = 0; x < NA; ++x) {   // rank order: the sums are identical on every rank
+      s->groot[x].visits += rs[x].visits;
+      s->groot[x].value_sum += rs[x].value_sum;
+    }
   }
+
   // the global incumbent before this round is identical on every rank
-  bool improved = better(r[gb].best, r[gb].best_seq, s->gbest, s->gbest_seq);
+  bool improved = better(rec(gb)->best, rec(gb)->best_seq, s->gbest, s->gbest_seq);
   if (improved) {
-    s->gbest = r[gb].best;
-    memcpy(s->gbest_seq, r[gb].best_seq, 64);
+    s->gbest = rec(gb)->best;
+    memcpy(s->gbest_seq, rec(gb)->best_seq, 64);
   }
   s->best = s->gbest;
   memcpy(s->best_seq, s->gbest_seq, 64);
   s->global_evals = tot;
-  const double el = r[0].elapsed_s;   // rank 0's clock decides time limits on every rank
+  const double el = rec(0)->elapsed_s;   // rank 0's clock decides time limits on every rank
   if (s->time_to_target < 0 && !std::isnan(s->o.target_score) && s->best.score <= s->o.target_score) {
     s->time_to_target = el;
     s->hit_target = 1;
@@ -292,7 +310,16 @@ void search_result(const toast_search_state* s, toast_search_result* out) {
   out->time_to_target_s = s->time_to_target;
 }
 
-size_t search_export_bytes() { return sizeof(ExportRec); }
+size_t search_export_bytes(const toast_analysis* a) {
+  return sizeof(ExportRec) + sizeof(toast_root_stat) * (size_t)a->dt.n_actions;
+}
+
+int32_t search_root_stats(const toast_search_state* s, toast_root_stat* out, int32_t cap) {
+  const int32_t n = s->a->dt.n_actions;
+  for (int32_t x = 0; x < cap && x < n; ++x)
+    out[x] = x < (int32_t)s->groot.size() ? s->groot[x] : toast_root_stat{0, 0.0};
+  return n;
+}
 
 void search_free(toast_search_state* s) { delete s; }
 

@@ -14,6 +14,12 @@ EXPORT_DTYPE = np.dtype([
     ("elapsed_s", "<f8"), ("rank", "<i4"), ("pad", "<i4"), ("best", T.COST_DTYPE)])
 
 
+def export_dtype(n_actions: int) -> np.dtype:
+    """The full per-rank record: the header above, then (visits, value_sum) of
+    every root child, indexed by action id (include/toast.h toast_root_stat)."""
+    return np.dtype([("hdr", EXPORT_DTYPE), ("root", T.ROOT_STAT_DTYPE, (n_actions,))])
+
+
 def all_gather_bytes(buf: np.ndarray, group=None) -> np.ndarray:
     """all_gather of one fixed-size byte record per rank -> [world * nbytes] uint8."""
     import torch
@@ -27,10 +33,13 @@ def all_gather_bytes(buf: np.ndarray, group=None) -> np.ndarray:
     return out.cpu().numpy()
 
 
-def search_root_parallel(a: "T.Analysis", opts: "T.SearchOptions", group=None, stream=None, trace=None):
+def search_root_parallel(a: "T.Analysis", opts: "T.SearchOptions", group=None, stream=None, trace=None,
+                         root_stats=None):
     """Root-parallel MCTS (R16): every rank grows its own tree (seed + rank);
-    after each round the ranks all-gather their export records and every rank
-    imports the same bytes, so the global best and the stop decision agree."""
+    after each round the ranks all-gather their export records (best sequence
+    and root visit statistics) and every rank imports the same bytes, so the
+    global best, the summed root statistics and the stop decision agree.
+    root_stats: optional list that receives the final summed root statistics."""
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     st = T.SearchState(a, opts, rank, world, stream=stream)
@@ -39,10 +48,12 @@ def search_root_parallel(a: "T.Analysis", opts: "T.SearchOptions", group=None, s
         gathered = all_gather_bytes(rec, group)
         stop = st.import_(gathered)
         if trace is not None:
-            g = gathered.view(EXPORT_DTYPE)
+            g = gathered.reshape(world, -1)[:, :EXPORT_DTYPE.itemsize].copy().view(EXPORT_DTYPE)
             trace.append(float(g["best_score"].min()))
         if stop:
             break
+    if root_stats is not None:
+        root_stats.append(st.root_stats())
     return st.end()
 
 

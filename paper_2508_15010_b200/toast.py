@@ -76,6 +76,8 @@ SEARCH_RESULT_DTYPE = np.dtype([
     ("best_seq", "<u2", (32,)), ("best", COST_DTYPE), ("evals", "<i8"), ("rounds", "<i4"), ("hit_target", "<i4"),
     ("wall_s", "<f8"), ("time_to_target_s", "<f8")])
 
+ROOT_STAT_DTYPE = np.dtype([("visits", "<i8"), ("value_sum", "<f8")])
+
 _P = ctypes.c_void_p
 _sigs = {
     "toast_load_graph": [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(_Axis), ctypes.c_int32,
@@ -90,6 +92,7 @@ _sigs = {
     "toast_rollout_batch": [_P, _P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _P, _P, _P],
     "toast_materialize": [_P, _P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
     "toast_lower": [_P, _P, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
+    "toast_search_root_stats": [_P, _P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
     "toast_search": [_P, ctypes.POINTER(_SearchOpts), _P],
     "toast_search_begin": [_P, ctypes.POINTER(_SearchOpts), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_P)],
     "toast_search_round": [_P, _P],
@@ -343,6 +346,14 @@ class SearchState:
         stop = ctypes.c_int32()
         _check(_lib.toast_search_import(self._h, g.ctypes.data, ctypes.byref(stop)))
         return bool(stop.value)
+
+    def root_stats(self) -> np.ndarray:
+        """Root-child (visits, value_sum) per action id, summed over the ranks at the last import."""
+        n = ctypes.c_int32()
+        _check(_lib.toast_search_root_stats(self._h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, dtype=ROOT_STAT_DTYPE)
+        _check(_lib.toast_search_root_stats(self._h, out.ctypes.data, n.value, ctypes.byref(n)))
+        return out
 
     def end(self):
         res = np.zeros(1, dtype=SEARCH_RESULT_DTYPE)

@@ -33,24 +33,38 @@ def _worker(rank, world, port, q):
         o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth)
         opts = T.SearchOptions(seed=10, patience=2, max_evals=10 ** 9)
         st = T.SearchState(a, opts, rank, world)
-        assert st.export_bytes == P.EXPORT_DTYPE.itemsize
+        na = len(a.dump()["actions"]) + 1
+        RD = P.export_dtype(na)
+        assert st.export_bytes == RD.itemsize
         out = []
         for rnd in range(4):
             # this rank's "round": a batch of rollouts for its own seed; best = min (score, key)
             seqs, costs = o.rollout(np.zeros((64, 32), np.uint16), seed=opts.seed + rank, id_base=rnd * 64)
             i = int(np.lexsort((costs["state_key"], costs["score"]))[0])
-            rec = np.zeros(1, dtype=P.EXPORT_DTYPE)
-            rec["best_score"] = costs["score"][i]
-            rec["best_key"] = costs["state_key"][i]
-            rec["best_seq"] = seqs[i]
-            rec["evals"] = 65 * (rnd + 1)
-            rec["elapsed_s"] = 0.1 * rnd
-            rec["rank"] = rank
-            rec["best"] = costs[i]
+            rec = np.zeros(1, dtype=RD)
+            h = rec["hdr"]
+            h["best_score"] = costs["score"][i]
+            h["best_key"] = costs["state_key"][i]
+            h["best_seq"] = seqs[i]
+            h["evals"] = 65 * (rnd + 1)
+            h["elapsed_s"] = 0.1 * rnd
+            h["rank"] = rank
+            h["best"] = costs[i]
+            rec["hdr"] = h
+            # root statistics: visits / reward sums of the root children this rank's rollouts started with
+            root = np.zeros(na, dtype=T.ROOT_STAT_DTYPE)
+            for s_, c_ in zip(seqs, costs):
+                root["visits"][s_[0]] += 1
+                root["value_sum"][s_[0]] -= c_["score"]
+            rec["root"] = root
             gathered = P.all_gather_bytes(rec.view(np.uint8).reshape(-1))
             stop = st.import_(gathered)
-            g = gathered.view(P.EXPORT_DTYPE)
-            out.append((stop, float(g["best_score"].min()), int(g["evals"].sum())))
+            g = gathered.view(RD)
+            rs = st.root_stats()
+            assert np.array_equal(rs["visits"], g["root"]["visits"].sum(axis=0))
+            assert np.array_equal(rs["value_sum"], g["root"]["value_sum"][0] + g["root"]["value_sum"][1])
+            out.append((stop, float(g["hdr"]["best_score"].min()), int(g["hdr"]["evals"].sum()),
+                        int(rs["visits"].sum())))
             if stop:
                 break
         res = st.end()
@@ -75,8 +89,9 @@ def test_root_parallel_exchange_two_ranks():
     # identical decisions, identical global best, on both ranks
     assert out0 == out1
     assert (s0, q0, e0) == (s1, q1, e1)
-    # the global best is the best of both ranks' records; evals are summed
+    # the global best is the best of both ranks' records; evals and root visits are summed
     assert s0 == min(o[1] for o in out0)
+    assert all(o[3] == 128 for o in out0)
     assert e0 == out0[-1][2]
     # patience 2: it stops after two non-improving rounds or runs all 4
     stops = [o[0] for o in out0]
