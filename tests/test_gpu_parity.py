@@ -130,7 +130,7 @@ def _legal_long(o: Oracle, n: int, seed: int, length: int = 30) -> np.ndarray:
     return out
 
 
-@pytest.mark.parametrize("name", ["unet", "gpt24", "mlp_c"])
+@pytest.mark.parametrize("name", ["unet", "gpt24", "gns16", "mlp_c"])
 def test_eval_parity_worst_case_long_sequences(name):
     a, o = setup(name)
     seqs = _legal_long(o, 200, seed=3)
@@ -184,17 +184,19 @@ def test_rollout_bad_prefix_is_not_extended():
     assert_same(gc, oc)
 
 
-def test_full_size_bench_launch_sampled():
-    """GPT-24 at BASELINE size in bench.py's launch configuration (2^18 rollouts
-    rounded down to whole waves, from the empty prefix, bench's seed): a sample
-    of outputs is recomputed one by one by the oracle (sequence and record)."""
-    a, o = setup("gpt24")
+@pytest.mark.parametrize("name,samples", [("gpt24", 48), ("unet", 24), ("gns16", 24), ("llama80", 6)])
+def test_full_size_bench_launch_sampled(name, samples):
+    """Every BASELINE config at full size in bench.py's launch configuration
+    (2^18 rollouts rounded down to whole waves, from the empty prefix, bench's
+    seed): a sample of outputs is recomputed one by one by the oracle
+    (sequence and record); size-independent properties hold for all rows."""
+    a, o = setup(name)
     wave = a.preferred_batch()
     n = max(wave, ((1 << 18) // wave) * wave)
     seed, id_base = 2024, 3 * n
     gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), seed, id_base)
     assert (gc["status"] == 0).all()
-    idx = np.random.default_rng(0).choice(n, size=48, replace=False)
+    idx = np.random.default_rng(0).choice(n, size=samples, replace=False)
     for i in idx:
         s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=seed, id_base=id_base + int(i))
         assert np.array_equal(gs[i], s1[0])
