@@ -262,12 +262,13 @@ def algorithmic_ops_per_eval(kt: dict, n_axes: int, max_depth: int, n_actions: i
     reduced method needs, counted from the analysis'
     own table sizes (independent of how the kernel schedules them)."""
     words = (n_actions + 31) // 32
+    w = kt["work"]   # per signature / signature-keyed template / absolute frontier term (DESIGN.md Roofline)
     rows = {
         "H1 decode": 32 + 4 * max_depth,                          # slot reads; color event + SetGroup bits per action
-        "H2 materialise": n_axes * kt["sig_roles"],               # one divisibility attempt per (role, axis)
+        "H2 materialise": n_axes * w["sig_roles"],                # one divisibility attempt per (role, axis)
         "H3/H7 flops+key": kt["n_sigs"] * (n_axes + 1),           # one key term per sharded axis, one exact division
-        "H4 collectives": 2 * n_axes * kt["n_tmpl"],              # phase 1 + phase 2 test per (template, axis)
-        "H5 frontier": 2 * kt["n_terms"],                         # one exact division + one add per term
+        "H4 collectives": 2 * n_axes * w["n_tmpl"],               # phase 1 + phase 2 test per (template, axis)
+        "H5 frontier": 2 * w["n_terms"],                          # one exact division + one add per term
         "H6 score": 8 * n_axes + 8,                               # fixed-order double epilogue
         "H8 rollout": round(expected_draws(max_depth) * (80 + 3 * words)),   # Philox4x32-10 + legal-set update per draw
     }

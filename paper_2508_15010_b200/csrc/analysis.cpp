@@ -7,6 +7,7 @@
 #include <array>
 #include <cstring>
 #include <map>
+#include <set>
 #include <numeric>
 #include <cstdio>
 #include <cstdlib>
@@ -658,6 +659,11 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         fast += f;
       }
       fprintf(stderr, "[toast] signatures with every axis subset dividing every shardable role: %d of %zu\n", fast, sig_words.size());
+      {
+        std::map<std::vector<uint64_t>, int> uw;
+        for (auto& w : sig_words) uw[w]++;
+        fprintf(stderr, "[toast] materialisation classes (distinct role-word tuples): %zu of %zu signatures\n", uw.size(), sig_words.size());
+      }
       fprintf(stderr, "[toast] signatures by distinct action colors:");
       for (int i = 0; i <= 8; ++i) fprintf(stderr, " %d:%d", i, hist[i]);
       fprintf(stderr, "\n");
@@ -669,10 +675,25 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       a->h_sig_nroles[q] = (uint8_t)sig_words[q].size();
       for (size_t r = 0; r < sig_words[q].size(); ++r) a->h_sig_roles[q * 8 + r] = sig_words[q][r];
     }
-    a->h_sigs.assign(sig_words.size(), KSig{});
-    for (size_t q = 0; q < sig_words.size(); ++q) {
-      KSig& k = a->h_sigs[q];
-      k.resdim = sig_rd[q];
+    // materialisation classes: signatures with the same role words (they differ
+    // only in which role lands on which result dim) materialise identically
+    std::vector<uint32_t> sig_mc(sig_words.size());
+    std::vector<size_t> mc_rep;
+    {
+      std::map<std::vector<uint64_t>, uint32_t> mcid;
+      for (size_t q = 0; q < sig_words.size(); ++q) {
+        auto it = mcid.emplace(sig_words[q], (uint32_t)mc_rep.size());
+        if (it.second) mc_rep.push_back(q);
+        sig_mc[q] = it.first->second;
+      }
+    }
+    a->h_sig_mr.assign(sig_words.size(), 0);
+    for (size_t q = 0; q < sig_words.size(); ++q) a->h_sig_mr[q] = (uint64_t)sig_mc[q] | ((uint64_t)sig_rd[q] << 32);
+    a->h_sigs.assign(mc_rep.size(), KSig{});
+    for (size_t mcq = 0; mcq < mc_rep.size(); ++mcq) {
+      const size_t q = mc_rep[mcq];
+      KSig& k = a->h_sigs[mcq];
+      k.resdim = sig_rd[q];   // (unused by the kernels: result dims are per signature, h_sig_mr)
       k.nr = (uint8_t)sig_words[q].size();
       for (size_t r = 0; r < sig_words[q].size(); ++r) {
         const uint64_t w = sig_words[q][r];
@@ -712,6 +733,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     // a value used more than once by one op is a "special" edge group, costed
     // edge by edge (within-op dedup, G26)
     std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint32_t> tmpl_id;
+    std::set<std::tuple<uint32_t, uint32_t, uint32_t>> sig_tmpl;   // templates keyed by signatures (work count)
     a->h_tmpl.clear();
     std::vector<std::vector<std::pair<uint32_t, uint64_t>>> op_tmpl(n_ops);   // per op: (template, def bytes)
     std::vector<std::vector<KUse>> op_spec(n_ops);                            // per op: its special edges
@@ -735,13 +757,16 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         const uint64_t gb = a->h_ops[v].gbytes;
         if (gb >> 48) { err = "a value larger than 2^48 bytes"; return TOAST_E_LIMIT; }
         if (first && last) {   // the value is used once here: cost it through its template
-          auto key = std::make_tuple(a->op_sig[v], a->op_sig[t], um);
+          // keyed by the use op's materialisation class: only its axis -> role
+          // map and this edge's role -> operand dim map decide the use layout
+          const uint32_t umc = (uint32_t)(a->h_sig_mr[a->op_sig[t]] & 0xFFFFFFFFu);
+          auto key = std::make_tuple(a->op_sig[v], umc, um);
           auto it = tmpl_id.find(key);
           if (it == tmpl_id.end()) {
             it = tmpl_id.emplace(key, (uint32_t)a->h_tmpl.size()).first;
             KTmpl tm{};
             tm.def_sig = (uint16_t)a->op_sig[v];
-            tm.use_sig = (uint16_t)a->op_sig[t];
+            tm.use_sig = (uint16_t)umc;
             tm.use_dimof = um;
             a->h_tmpl.push_back(tm);
           }
@@ -750,6 +775,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
           tm.sum_gbytes += gb;
           tm.n_edges += 1;
           op_tmpl[t].push_back({it->second, gb});
+          sig_tmpl.insert(std::make_tuple(a->op_sig[v], a->op_sig[t], um));
         } else {
           KUse u{};
           u.def_sig = (uint16_t)a->op_sig[v];
@@ -761,6 +787,9 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       }
     }
     if (a->h_tmpl.size() >= NO_TMPL) { err = "more than 65534 edge templates"; return TOAST_E_LIMIT; }
+    a->work_tmpl = (int64_t)sig_tmpl.size();
+    a->work_sig_roles = 0;
+    for (auto& w : sig_words) a->work_sig_roles += (int64_t)w.size();
 
     // peak-memory frontier (C12, reading R19).  For a candidate with
     // per-signature result divisors d_s and per-template growth factors g_tm,
@@ -849,6 +878,8 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         kp.term_begin = (uint32_t)a->h_terms.size();
         auto term = [&](int64_t v, size_t fid) { return ((uint64_t)v & ((1ULL << 48) - 1)) | ((uint64_t)fid << 48); };
         a->h_terms.push_back((uint64_t)(anchor ? p[0] : p[0] - (*prev)[0]));
+        a->work_terms += 1;
+        for (size_t d = 1; d < D; ++d) a->work_terms += p[d] != 0;   // the point's absolute terms
         for (size_t q = 0; q < NS; ++q) {
           const int64_t v = anchor ? p[1 + q] : p[1 + q] - (*prev)[1 + q];
           if (v) { a->h_terms.push_back(term(v, q)); ++kp.n_sig; }
@@ -912,6 +943,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
   T.n_axes = n_axes;
   T.max_depth = o->max_depth;
   T.n_sigs = (int32_t)a->h_sig_nroles.size();
+  T.n_mc = (int32_t)a->h_sigs.size();
   T.n_tmpl = (int32_t)a->h_tmpl.size();
   T.n_points = (int32_t)a->h_points.size();
   T.pow2 = 1;
@@ -1017,10 +1049,12 @@ std::string dump_json(const toast_analysis* a) {
   {   // the per-candidate tables the kernels read (signatures, templates, peak-memory frontier)
     int64_t roles = 0, cols = 0;
     for (const auto& k : a->h_sigs) { roles += k.nr; cols += k.m; }
-    s += "],\"kernel_tables\":{\"n_sigs\":" + I((int64_t)a->h_sigs.size()) + ",\"sig_roles\":" + I(roles) +
+    s += "],\"kernel_tables\":{\"n_sigs\":" + I((int64_t)a->h_sig_mr.size()) + ",\"n_mc\":" +
+         I((int64_t)a->h_sigs.size()) + ",\"sig_roles\":" + I(roles) +
          ",\"sig_colors\":" + I(cols) + ",\"n_tmpl\":" + I((int64_t)a->h_tmpl.size()) + ",\"n_points\":" +
          I((int64_t)a->h_points.size()) + ",\"n_terms\":" + I((int64_t)a->h_terms.size()) + ",\"n_spec\":" +
-         I((int64_t)a->h_spec.size()) + ",\"frontier_ops\":[";
+         I((int64_t)a->h_spec.size()) + ",\"work\":{\"sig_roles\":" + I(a->work_sig_roles) + ",\"n_tmpl\":" +
+         I(a->work_tmpl) + ",\"n_terms\":" + I(a->work_terms) + "},\"frontier_ops\":[";
     for (size_t q = 0; q < a->point_op.size(); ++q) { if (q) s += ','; s += I(a->point_op[q]); }
     s += "]}";
   }

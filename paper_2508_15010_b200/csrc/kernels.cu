@@ -71,9 +71,10 @@ __host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
   return r16(b1 > b2 ? b1 : b2);
 }
 __host__ __device__ inline int smem_d_bytes(int n_tmpl) { return r16(n_tmpl * 32); }
-__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl) {
+__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl,
+                                                int n_mc) {
   return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl) +
-         r16(n_sigs * 32);
+         r16(n_sigs * 32) + r16(n_mc * 64);
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -118,6 +119,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
   uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
+  uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u16)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -136,6 +138,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.acc = b;
   s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
   s.pc = s.tb + smem_d_bytes(T.n_tmpl);
+  s.mca = s.pc + r16(T.n_sigs * 32);
   return s;
 }
 
@@ -302,7 +305,7 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
   const uint4 mt = __ldg(kp + 3), c0 = __ldg(kp + 1), c1 = __ldg(kp + 2), dw = __ldg(kp);
   const uint32_t m = mt.y & 0xFF, dr = (mt.y >> 8) & 0xFF;
   const bool alldiv = (mt.y >> 24) & 1;
-  if (m == 0) return 0xFFFFFFFFu;
+  if (m == 0) return 0xFFFFu;
   // roles deselected by the fixed SetGroup bits
   uint32_t dmask = 0;
   for (uint32_t b = dr; b; b &= b - 1) {
@@ -322,15 +325,7 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
     case 7: a2r = materialize_m<7, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
     default: a2r = materialize_m<8, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
   }
-  if (a2r == 0xFFFFu) return 0xFFFFFFFFu;   // nothing sharded: every axis "none" in both maps
-  const uint32_t rdm = mt.x;
-  uint32_t dims = 0;
-#pragma unroll
-  for (int A = 0; A < 4; ++A) {
-    const uint32_t r = (a2r >> (4 * A)) & 15;
-    dims |= (r == 15 ? 15u : (rdm >> (4 * r)) & 15) << (4 * A);
-  }
-  return a2r | (dims << 16);
+  return a2r;
 }
 
 // pack the 16+16-bit (role, dim) maps into an NA-entry
@@ -367,9 +362,28 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     uint32_t axb[NA];
 #pragma unroll
     for (int A = 0; A < NA; ++A) axb[A] = sp<uint32_t>(S.axb)[A * 32 + lane];
+    // H2a: one materialisation per class (signatures that differ only in
+    // their result dims share it): the axis -> role map
+    for (int c = warp; c < T.n_mc; c += K)
+      sp<uint16_t>(S.mca)[c * 32 + lane] = (uint16_t)materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
+  }
+  __syncthreads();
+  {
+    // H2b: per signature the entry (axis -> role | axis -> result dim), the
+    // result layout's division code, the state-key terms (H7) and the local
+    // FLOPs (H3) of all its ops
     for (int s = warp; s < T.n_sigs; s += K) {
       const uint64_t glo = __ldg(T.sig_flops + 2 * s), ghi = __ldg(T.sig_flops + 2 * s + 1);
-      const uint32_t e = pack_entry<NA>(materialize_sig<NA>(T, S, lane, s, f0, on, ap, axb));
+      const uint64_t mr = __ldg(T.sig_mr + s);
+      const uint32_t a2r = sp<uint16_t>(S.mca)[(uint32_t)(mr & 0xFFFF) * 32 + lane];
+      const uint32_t rdm = (uint32_t)(mr >> 32);
+      uint32_t dims = 0;
+#pragma unroll
+      for (int A = 0; A < 4; ++A) {
+        const uint32_t r = (a2r >> (4 * A)) & 15;
+        dims |= (r == 15 ? 15u : (rdm >> (4 * r)) & 15) << (4 * A);
+      }
+      const uint32_t e = pack_entry<NA>(a2r | (dims << 16));
       ent_store<NA>(S, s, lane, e);
       uint32_t present = 0;
 #pragma unroll
@@ -420,7 +434,8 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       n1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K) + 1);
       n2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K) + 2);
     }
-    const uint32_t de = ent_load<NA>(S, t0.x & 0xFFFF, lane), ue = ent_load<NA>(S, t0.x >> 16, lane);
+    const uint32_t de = ent_load<NA>(S, t0.x & 0xFFFF, lane);
+    const uint32_t ue = sp<uint16_t>(S.mca)[(t0.x >> 16) * 32 + lane];   // the use class's axis -> role map
     const uint32_t use_dimof = t0.y;
     uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
@@ -898,6 +913,8 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   T.spec = reinterpret_cast<const KUse*>(p);
   if ((st = upload(a, a->h_sigs, &p, err))) return st;
   T.sigs = reinterpret_cast<const KSig*>(p);
+  if ((st = upload(a, a->h_sig_mr, &p, err))) return st;
+  T.sig_mr = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_sig_key, &p, err))) return st;
   T.sig_key = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_sig_flops, &p, err))) return st;
@@ -916,7 +933,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl) > dev_smem) {
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl, T.n_mc) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -925,7 +942,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl);
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl, T.n_mc);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
       cudaError_t e = dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
@@ -993,7 +1010,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
@@ -1011,7 +1028,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {

@@ -123,7 +123,7 @@ constexpr uint16_t NO_TMPL = 0xFFFF;
 // are costed once per candidate from the template's summed def bytes
 struct KTmpl {           // 24 B
   uint16_t def_sig;
-  uint16_t use_sig;
+  uint16_t use_sig;      // the use op's materialisation class
   uint32_t use_dimof;
   uint64_t sum_gbytes;
   uint32_t n_edges;
@@ -160,7 +160,8 @@ struct DeviceTables {
   const KPoint* points = nullptr;        // [n_points] peak-memory frontier (R19)
   const uint64_t* terms = nullptr;       // per point: constant, then value | feature << 48
   const KUse* spec = nullptr;            // special edges of the points
-  const KSig* sigs = nullptr;            // [n_sigs]
+  const KSig* sigs = nullptr;            // [n_mc] per materialisation class
+  const uint64_t* sig_mr = nullptr;      // [n_sigs] materialisation class | role -> result dim nibbles << 32
   const uint64_t* sig_key = nullptr;     // [n_sigs][4 axes][8 roles] summed state-key terms (R14)
   const uint64_t* sig_flops = nullptr;   // [n_sigs][2] summed global FLOPs of matmul-class ops (lo, hi)
   const KTmpl* tmpl = nullptr;           // [n_tmpl]
@@ -171,7 +172,7 @@ struct DeviceTables {
   // constants
   int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
-  int32_t n_points, pad_;
+  int32_t n_points, n_mc;
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -214,7 +215,12 @@ struct toast_analysis {
   std::vector<uint64_t> h_terms;
   std::vector<toast::KUse> h_spec;
   std::vector<int32_t> point_op;            // op index of each frontier point
-  std::vector<toast::KSig> h_sigs;
+  // the reduced method's work per evaluation, before the kernels' table
+  // sharing (materialisation classes, class-keyed templates, delta terms):
+  // roles over signatures, signature-keyed templates, absolute frontier terms
+  int64_t work_sig_roles = 0, work_tmpl = 0, work_terms = 0;
+  std::vector<toast::KSig> h_sigs;          // per materialisation class
+  std::vector<uint64_t> h_sig_mr;           // per signature: class | resdim << 32
   std::vector<uint64_t> h_sig_roles, h_desel_cls;
   std::vector<uint8_t> h_sig_nroles;
   std::vector<uint32_t> h_sig_resdim;
