@@ -58,7 +58,7 @@ def lib():
         L = _lib
         L.orc_new.restype = ctypes.c_void_p
         L.orc_new.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_double, ctypes.c_uint64,
-                              ctypes.c_double, ctypes.c_int, ctypes.c_int]
+                              ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.orc_last_error.restype = ctypes.c_char_p
         L.orc_free.argtypes = [ctypes.c_void_p]
         for f in ("orc_n_actions", "orc_n_loops", "orc_n_ops"):
@@ -100,12 +100,13 @@ def mesh_spec(axes) -> str:
 
 class Oracle:
     def __init__(self, ir: str, axes, flops_per_sec: float, dm: int, penalty_c: float = 100.0,
-                 min_dims: int = 10, max_depth: int = 30):
+                 min_dims: int = 10, max_depth: int = 30, cost_model: int = 0):
+        """cost_model: 0 = straight-line sum (reading G14), 1 = critical path (reading R22)."""
         L = lib()
         self.axes = list(axes)
         self.max_depth = max_depth
         h = L.orc_new(ir.encode(), mesh_spec(axes).encode(), float(flops_per_sec), int(dm),
-                      float(penalty_c), int(min_dims), int(max_depth))
+                      float(penalty_c), int(min_dims), int(max_depth), int(cost_model))
         if not h:
             raise OracleError(L.orc_last_error().decode())
         self.h = ctypes.c_void_p(h)

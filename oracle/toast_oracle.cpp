@@ -691,6 +691,7 @@ struct Oracle {
   std::vector<Axis> axes;
   double F = 1e12; u64 DM = 0; double C = 100.0;
   int min_dims = 10, max_depth = 30;
+  int cost_model = 0;   // 0: straight-line sum (G14); 1: critical path (reading R22)
 
   std::vector<Loop> loops;
   std::vector<int> op_loop_begin;                       // loops of op t: [begin[t], begin[t+1])
@@ -1122,6 +1123,7 @@ struct Oracle {
   void eval_masks(const std::vector<int>& mask, Cost& out, std::vector<i64>* profile = nullptr) const {
     // C10: FLOPs over matmul-class ops only
     u128 flops = 0;
+    std::vector<u128> op_flops(M.ops.size(), 0);   // per op, for the critical path (R22)
     for (size_t t = 0; t < M.ops.size(); t++) {
       const std::string& k = M.ops[t].kind;
       if (k != "matmul" && k != "dot_general" && k != "conv2d" && k != "conv2d_bwd_input" && k != "conv2d_bwd_filter") continue;
@@ -1131,29 +1133,38 @@ struct Oracle {
         f *= (u128)((u64)loops[l].ext / axes_prod(mask[l]));
       }
       flops += f;
+      op_flops[t] = f;
     }
     // C11: collectives per use edge (Fig. 2c; Fig. 5b)
     std::vector<u64> temp_total(M.ops.size(), 0);
     int nA = (int)axes.size();
     u64 ncount[4][4] = {{0}};   // true counts; the record keeps them saturated to 16 bits
+    // R22: per use edge, the duration of its own collectives (the same ring
+    // formula as C13 over this edge's payloads); a within-op duplicate waits
+    // for the same collectives
+    std::vector<std::vector<double>> edge_m(M.ops.size());
     for (size_t t = 0; t < M.ops.size(); t++) {
       const Op& op = M.ops[t];
       std::vector<std::pair<int, std::vector<int>>> done;   // (value, U) already costed at this op
+      std::vector<double> done_m;
       std::map<int, i64> temp;                              // per distinct operand value
+      edge_m[t].assign(op.operands.size(), 0.0);
       for (size_t k = 0; k < op.operands.size(); k++) {
         int v = op.operands[k];
         std::vector<int> U;
         for (size_t i = 0; i < M.values[v].shape.size(); i++) U.push_back(mask[use_loop((int)t, (int)k, (int)i)]);
         if (!temp.count(v)) temp[v] = 0;
-        bool dup = false;
-        for (auto& d : done) if (d.first == v && d.second == U) dup = true;
-        if (dup) continue;
+        int dup = -1;
+        for (size_t q = 0; q < done.size(); q++) if (done[q].first == v && done[q].second == U) dup = (int)q;
+        if (dup >= 0) { edge_m[t][k] = done_m[dup]; continue; }
         done.push_back({v, U});
+        done_m.push_back(0.0);
         std::vector<int> D = layout_D(mask, v);
         int P = partial_P(mask, v);
         if (D == U && P == 0) continue;
         std::vector<int> cur = D;
         u64 size = local_bytes_of(v, D);
+        u64 ep[4][4] = {{0}};   // this edge's payloads [axis][kind]
         // phase 1: axes of D not kept in the same dim (reading R20):
         // 1a all_gather every axis U holds on no dim, then 1b all_to_all every
         // axis U holds on another dim — so every intermediate layout keeps
@@ -1164,7 +1175,7 @@ struct Oracle {
             bool elsewhere = false;
             for (size_t j = 0; j < U.size(); j++) if (j != i && (U[j] & (1 << A))) elsewhere = true;
             if (elsewhere) continue;
-            out.payload[A][K_AG] += size; ncount[A][K_AG]++;
+            ep[A][K_AG] += size; ncount[A][K_AG]++;
             cur[i] &= ~(1 << A); size *= (u64)axes[A].size;
           }
         }
@@ -1173,7 +1184,7 @@ struct Oracle {
             if (!(cur[i] & (1 << A)) || (U[i] & (1 << A))) continue;
             int j_other = -1;
             for (size_t j = 0; j < U.size(); j++) if (j != i && (U[j] & (1 << A))) j_other = (int)j;
-            out.payload[A][K_A2A] += size; ncount[A][K_A2A]++;
+            ep[A][K_A2A] += size; ncount[A][K_A2A]++;
             cur[i] &= ~(1 << A); cur[j_other] |= 1 << A;
           }
         }
@@ -1184,13 +1195,24 @@ struct Oracle {
           for (size_t j = 0; j < U.size(); j++) if (U[j] & (1 << A)) j_u = (int)j;
           if (j_u >= 0) {
             size /= (u64)axes[A].size;
-            out.payload[A][K_RS] += size; ncount[A][K_RS]++;
+            ep[A][K_RS] += size; ncount[A][K_RS]++;
             cur[j_u] |= 1 << A;
           } else {
-            out.payload[A][K_AR] += size; ncount[A][K_AR]++;
+            ep[A][K_AR] += size; ncount[A][K_AR]++;
           }
         }
         // phase 3: free local slices (no payload)
+        double m = 0.0;
+        for (int A = 0; A < nA; A++) {
+          for (int kk = 0; kk < 4; kk++) out.payload[A][kk] += ep[A][kk];
+          double n = (double)axes[A].size;
+          double ag = (double)ep[A][K_AG], rs = (double)ep[A][K_RS];
+          double ar = (double)ep[A][K_AR], a2a = (double)ep[A][K_A2A];
+          double term = ((n - 1.0) * (ag + rs) + ((n - 1.0) * (2.0 * ar + a2a)) / n) / axes[A].bw;
+          m = m + term;
+        }
+        edge_m[t][k] = m;
+        done_m.back() = m;
         // temporaries: only gathers grow the operand buffer
         u64 use_local = local_bytes_of(v, U);
         i64 grow = (i64)use_local - (i64)local_bytes_of(v, D);
@@ -1228,6 +1250,27 @@ struct Oracle {
       double ar = (double)out.payload[A][K_AR], a2a = (double)out.payload[A][K_A2A];
       double term = ((n - 1.0) * (ag + rs) + ((n - 1.0) * (2.0 * ar + a2a)) / n) / axes[A].bw;
       t = t + term;
+    }
+    if (cost_model == 1) {
+      // R22 ("runtime cost is accumulated along the critical path"):
+      // finish(t) = max over t's operands, in operand order, of (finish of the
+      // operand's def + its edge's collective duration) + t's compute time;
+      // parameters finish at 0; runtime = the latest finish
+      std::vector<double> fin(M.values.size(), 0.0);
+      double cp = 0.0;
+      for (size_t tt = 0; tt < M.ops.size(); tt++) {
+        const Op& op = M.ops[tt];
+        double ready = 0.0;
+        for (size_t k = 0; k < op.operands.size(); k++) {
+          double f = fin[op.operands[k]] + edge_m[tt][k];
+          if (f > ready) ready = f;
+        }
+        double ct = (double)(u64)op_flops[tt] / F;
+        double ft = ready + ct;
+        if (op.result >= 0) fin[op.result] = ft;
+        if (ft > cp) cp = ft;
+      }
+      t = cp;
     }
     out.runtime_s = t;
     out.peak_bytes = (u64)peak;
@@ -1420,7 +1463,8 @@ extern "C" {
 const char* orc_last_error() { return g_err.c_str(); }
 
 // axes: "name=size:bw,name=size:bw"
-void* orc_new(const char* ir, const char* mesh, double F, uint64_t DM, double C, int min_dims, int max_depth) {
+void* orc_new(const char* ir, const char* mesh, double F, uint64_t DM, double C, int min_dims, int max_depth,
+              int cost_model) {
   try {
     auto* O = new Oracle();
     std::string ms(mesh);
@@ -1440,6 +1484,8 @@ void* orc_new(const char* ir, const char* mesh, double F, uint64_t DM, double C,
     if (O->axes.empty() || O->axes.size() > 4) throw OracleError("E_MESH", "mesh must have 1..4 axes");
     for (auto& a : O->axes) if (a.size < 2 || !(a.bw > 0)) throw OracleError("E_MESH", "axis size < 2 or bw <= 0");
     O->F = F; O->DM = DM; O->C = C; O->min_dims = min_dims; O->max_depth = max_depth;
+    if (cost_model != 0 && cost_model != 1) throw OracleError("E_INVALID_ARG", "cost_model must be 0 or 1");
+    O->cost_model = cost_model;
     O->M = parse_module(ir);
     O->build();
     return O;

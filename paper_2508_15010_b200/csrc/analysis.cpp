@@ -812,10 +812,36 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       for (size_t q = 0; q < NS; ++q)
         for (size_t r = 0; r < sig_words[q].size(); ++r)
           if ((sig_words[q][r] & 0x3FF) != NO_ACOLOR && ((sig_rd[q] >> (4 * r)) & 15) != 15) sig_fixed[q] = 0;
-      std::vector<int64_t> lo(D), hi(D);   // weight bounds x prodall
+      // dmax[q]: the largest divisor a candidate can give signature q's result
+      // layout — over every placement of distinct axes on its shardable
+      // result-dim roles that keeps each role's extent divisible (div_ok)
+      std::vector<int64_t> dmax(NS, 1);
+      for (size_t q = 0; q < NS; ++q) {
+        if (sig_fixed[q]) continue;
+        int64_t n_assign = 1;
+        for (int A = 0; A < n_axes; ++A) n_assign *= 9;   // each axis: one of 8 roles or none
+        for (int64_t code = 0; code < n_assign; ++code) {
+          int64_t c = code, d = 1;
+          uint32_t per_role[8] = {0};
+          bool ok = true;
+          for (int A = 0; A < n_axes && ok; ++A) {
+            const int r = (int)(c % 9) - 1;
+            c /= 9;
+            if (r < 0) continue;
+            if (r >= (int)sig_words[q].size() || (sig_words[q][r] & 0x3FF) == NO_ACOLOR ||
+                ((sig_rd[q] >> (4 * r)) & 15) == 15) { ok = false; break; }
+            per_role[r] |= 1u << A;
+            d *= g->axis_size[A];
+          }
+          for (int r = 0; r < 8 && ok; ++r)
+            if (per_role[r] && !(((sig_words[q][r] >> 10) & 0xFFFF) >> per_role[r] & 1)) ok = false;
+          if (ok && d > dmax[q]) dmax[q] = d;
+        }
+      }
+      std::vector<int64_t> lo(D), hi(D);   // weight bounds x prodall (exact: dmax divides prodall)
       lo[0] = hi[0] = prodall;
-      for (size_t q = 0; q < NS; ++q) { lo[1 + q] = sig_fixed[q] ? prodall : 1; hi[1 + q] = prodall; }
-      for (size_t q = 0; q < NT; ++q) { lo[1 + NS + q] = 0; hi[1 + NS + q] = sig_fixed[a->h_tmpl[q].def_sig] ? 0 : prodall - 1; }
+      for (size_t q = 0; q < NS; ++q) { lo[1 + q] = prodall / dmax[q]; hi[1 + q] = prodall; }
+      for (size_t q = 0; q < NT; ++q) { lo[1 + NS + q] = 0; hi[1 + NS + q] = prodall - prodall / dmax[a->h_tmpl[q].def_sig]; }
       auto geq = [&](const std::vector<int64_t>& x, const std::vector<int64_t>& y) {   // x >= y for every w in the box
         __int128 m = 0;
         for (size_t d = 0; d < D; ++d) {
