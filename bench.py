@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--search-cpu-seconds", type=float, default=60.0, help="time limit of the CPU oracle search")
     p.add_argument("--L", type=int, default=64, help="search leaves per round")
     p.add_argument("--R", type=int, default=256, help="search rollouts per leaf")
+    p.add_argument("--cost-model", default="sum", choices=["sum", "cp"],
+                   help="runtime model of the timed arm: straight-line sum (G14) or critical path (R22)")
+    p.add_argument("--no-variants", action="store_true", help="skip the critical-path variant measurement")
     return p.parse_args()
 
 
@@ -287,6 +290,36 @@ def profile_summary(config: str):
     return d
 
 
+def variant_cp(args, cfg, local, stream, flush):
+    """the same rollout step under the critical-path cost
+    model (reading R22), timed the same way on this GPU (10 steps)."""
+    import torch
+    from paper_2508_15010_b200 import toast as T
+    a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
+                         cuda_device=local, cost_model=T.COST_CRITICAL_PATH)
+    wave = a.preferred_batch()
+    N = max(wave, (args.n // wave) * wave)
+    dev = torch.device("cuda", local)
+    pre = torch.zeros((N, 32), dtype=torch.int16, device=dev)
+    seqs = torch.empty_like(pre)
+    out = torch.empty((N, 256), dtype=torch.uint8, device=dev)
+    for w in range(3):
+        T.rollout_batch(a, pre, args.seed, (1 << 36) + w * N, seqs, out, stream=stream)
+    torch.cuda.synchronize()
+    ms = []
+    for s in range(10):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        T.rollout_batch(a, pre, args.seed, s * N, seqs, out, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    m = statistics.mean(ms)
+    return {"metric": METRIC, "value": N / (m / 1000.0), "unit": UNIT, "ms_per_step": m, "rollouts_per_step": N,
+            "cost_model": "critical path (DESIGN.md reading R22)", "finish_slots": a.kernel_tables().get("n_slots")}
+
+
 def run_toast(args, cfg, rank, world, local):
     import numpy as np
     import torch
@@ -295,8 +328,9 @@ def run_toast(args, cfg, rank, world, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     t = time.perf_counter()
+    cm = T.COST_CRITICAL_PATH if args.cost_model == "cp" else T.COST_SUM
     a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
-                         cuda_device=local)
+                         cuda_device=local, cost_model=cm)
     nda_s = time.perf_counter() - t
     dump = a.dump()
     wave = a.preferred_batch()
@@ -370,7 +404,8 @@ def run_toast(args, cfg, rank, world, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": cfg.name, "rollouts_per_step_per_gpu": N, "wave": wave, "mesh": [list(x) for x in cfg.axes],
+            "config": {"workload": cfg.name, "cost_model": args.cost_model, "rollouts_per_step_per_gpu": N, "wave": wave,
+                       "mesh": [list(x) for x in cfg.axes],
                        "ops": dump["n_ops"], "loops": dump["n_loops"], "actions": len(dump["actions"]) + 1,
                        "l2": "flushed (256 MiB write) between timed steps", "description": cfg.description},
             "gpu_launches": args.steps,
@@ -392,6 +427,8 @@ def run_toast(args, cfg, rank, world, local):
             "e2e": {"value": N * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": N * 64,
                     "d2h_bytes_per_step": N * (64 + 256)},
         }
+    if rank == 0 and not args.no_variants and args.cost_model == "sum":
+        line["variants"] = {"critical_path": variant_cp(args, cfg, local, stream, flush)}
     ttb = None
     if not args.no_search:
         ttb = time_to_best_gpu(a, args, rank, world, stream)

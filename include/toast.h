@@ -83,10 +83,18 @@ typedef struct {
 } toast_machine;
 
 /* NDA options: prune super-colors with fewer than min_unique_dims value
-   dims (default 10); maximum trajectory depth (default 30). */
+   dims (default 10); maximum trajectory depth (default 30);
+   cost_model: how runtime accumulates — TOAST_COST_SUM (0, reading
+   G14: compute + every collective, straight-line) or TOAST_COST_CRITICAL_PATH
+   (1, reading R22: the latest finish over the op DAG, finish(t) = max over
+   operands of (finish(def) + the edge's collective time) + t's compute time).
+   Every other record field is the same under both. */
+enum { TOAST_COST_SUM = 0, TOAST_COST_CRITICAL_PATH = 1 };
 typedef struct {
   int32_t min_unique_dims;
   int32_t max_depth;
+  int32_t cost_model;
+  int32_t reserved;      /* 0 */
 } toast_nda_opts;
 
 typedef struct toast_graph toast_graph;        /* opaque, library-owned */

@@ -928,6 +928,64 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
               a->actions.size(), a->h_desel_cls.size() / 2);
   }
 
+  // ------------------------------------------------------------ critical-path stream (reading R22)
+  a->cost_model = o->cost_model;
+  int32_t n_slots = 0;
+  a->h_cp.clear();
+  if (o->cost_model == TOAST_COST_CRITICAL_PATH) {
+    // finish-time slots: every non-parameter value holds one from its def to
+    // its last use (reused greedily); parameters finish at 0 and need none.
+    // Values live for at most CP_SHORT ops take one of CP_SMEM_SLOTS on-chip
+    // slots when one is free (bit 31 set), the rest global scratch slots.
+    std::vector<uint32_t> slot_of(g->values.size(), NO_SLOT), free_slots, free_fast;
+    for (int i = CP_SMEM_SLOTS - 1; i >= 0; --i) free_fast.push_back(CP_FAST | (uint32_t)i);
+    auto push = [&](const void* rec) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(rec);
+      a->h_cp.insert(a->h_cp.end(), w, w + 4);
+    };
+    for (int32_t t = 0; t < n_ops; ++t) {
+      const GOp& op = g->ops[t];
+      KCpOp r{};
+      r.sig = (uint16_t)a->op_sig[t];
+      r.n_uses = (uint8_t)op.operands.size();
+      r.flags = (a->h_ops[t].flags & 1) ? 1 : 0;
+      r.gflops = a->h_gflops[t];
+      r.res_slot = NO_SLOT;
+      if (op.result >= 0 && op.kind != OK_PARAM) {
+        if (last_use[op.result] - t <= CP_SHORT && !free_fast.empty()) {
+          slot_of[op.result] = free_fast.back();
+          free_fast.pop_back();
+        } else {
+          if (free_slots.empty()) free_slots.push_back((uint32_t)n_slots++);
+          slot_of[op.result] = free_slots.back();
+          free_slots.pop_back();
+        }
+        r.res_slot = slot_of[op.result];
+      }
+      push(&r);
+      for (size_t k = 0; k < op.operands.size(); ++k) {
+        const int32_t v = op.operands[k];
+        KCpUse u{};
+        u.def_slot = slot_of[v];
+        uint32_t um = ~0u;
+        for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
+          uint32_t rr = OL[t].use_role[k][i];
+          um = (um & ~(0xFu << (4 * rr))) | ((uint32_t)i << (4 * rr));
+        }
+        u.use_dimof = um;
+        u.gb_sig = a->h_ops[g->values[v].def_op].gbytes | ((uint64_t)a->op_sig[g->values[v].def_op] << 48);
+        push(&u);
+      }
+      // values whose last use is t give their slots back (after t read them)
+      for (int32_t dv : deaths[t]) {
+        const int32_t val = g->ops[dv].result;
+        if (val >= 0 && slot_of[val] != NO_SLOT) (slot_of[val] & CP_FAST ? free_fast : free_slots).push_back(slot_of[val]);
+      }
+    }
+  }
+  a->dt.n_slots = n_slots;
+  a->dt.cost_model = o->cost_model;
+
   // ------------------------------------------------------------ baseline (empty sequence)
   {
     unsigned __int128 fl = 0;
@@ -945,6 +1003,25 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     double fd = fhi * 18446744073709551616.0;
     fd = fd + (double)lo;
     double t0 = fd / g->machine.flops_per_sec;
+    if (o->cost_model == TOAST_COST_CRITICAL_PATH) {
+      // R22 with nothing sharded: no collectives; finish(t) = max over operands
+      // of finish(def) + t's compute time (global FLOPs / F)
+      std::vector<double> fin(g->values.size(), 0.0);
+      double cp = 0.0;
+      for (int32_t t = 0; t < n_ops; ++t) {
+        const GOp& op = g->ops[t];
+        double ready = 0.0;
+        for (int32_t v : op.operands) {
+          volatile double f = fin[v] + 0.0;
+          if (f > ready) ready = f;
+        }
+        const double ct = (double)a->h_gflops[t] / g->machine.flops_per_sec;
+        const double ft = ready + ct;
+        if (op.result >= 0) fin[op.result] = ft;
+        if (ft > cp) cp = ft;
+      }
+      t0 = cp;
+    }
     if (!(t0 > 0.0)) { err = "baseline runtime is 0: the program has no contraction op"; return TOAST_E_DEGENERATE; }
     a->t0 = t0;
     a->peak0 = (uint64_t)peak;
@@ -1079,7 +1156,7 @@ std::string dump_json(const toast_analysis* a) {
          I((int64_t)a->h_sigs.size()) + ",\"sig_roles\":" + I(roles) +
          ",\"sig_colors\":" + I(cols) + ",\"n_tmpl\":" + I((int64_t)a->h_tmpl.size()) + ",\"n_points\":" +
          I((int64_t)a->h_points.size()) + ",\"n_terms\":" + I((int64_t)a->h_terms.size()) + ",\"n_spec\":" +
-         I((int64_t)a->h_spec.size()) + ",\"work\":{\"sig_roles\":" + I(a->work_sig_roles) + ",\"n_tmpl\":" +
+         I((int64_t)a->h_spec.size()) + ",\"n_slots\":" + I((int64_t)a->dt.n_slots) + ",\"work\":{\"sig_roles\":" + I(a->work_sig_roles) + ",\"n_tmpl\":" +
          I(a->work_tmpl) + ",\"n_terms\":" + I(a->work_terms) + "},\"frontier_ops\":[";
     for (size_t q = 0; q < a->point_op.size(); ++q) { if (q) s += ','; s += I(a->point_op[q]); }
     s += "]}";

@@ -72,9 +72,9 @@ __host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
 }
 __host__ __device__ inline int smem_d_bytes(int n_tmpl) { return r16(n_tmpl * 32); }
 __host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl,
-                                                int n_mc) {
+                                                int n_mc, int cp) {
   return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl) +
-         r16(n_sigs * 32) + r16(n_mc * 64);
+         r16(n_sigs * 32) + r16(n_mc * 64) + (cp ? CP_SMEM_SLOTS * 32 * 8 : 0);
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -120,6 +120,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
   uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u16)
+  uint32_t cpf;             // R22: [CP_SMEM_SLOTS][32] on-chip finish-time slots (double)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -139,6 +140,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
   s.pc = s.tb + smem_d_bytes(T.n_tmpl);
   s.mca = s.pc + r16(T.n_sigs * 32);
+  s.cpf = s.mca + r16(T.n_mc * 64);
   return s;
 }
 
@@ -335,13 +337,116 @@ __device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
   return (full & m) | (((full >> 16) & m) << (4 * NA));
 }
 
+// ---------------------------------------------------------------- R22: critical path (NEXT-2)
+// One lane = one candidate: the ops in program order, finish(t) = max over
+// operands, in operand order, of (finish(def) + the edge's collective time)
+// + t's compute time; the finish times of live values sit in this warp's
+// global scratch [slot][32].  The edge's collectives are C11's (reading R20)
+// over its own bytes and their time is C13's ring formula — fixed order,
+// explicit round-to-nearest, bit-identical to the oracle.
+template <int NA, bool P2>
+__device__ __forceinline__ double cp_sweep(const DeviceTables& T, const Smem& S, int lane, double* __restrict__ scr) {
+  const uint32_t sh = smem_base();
+  constexpr uint32_t esz = sizeof(typename Ent<NA>::T);
+  const uint32_t ea = sh + S.sig + (uint32_t)lane * esz;
+  auto ent = [&](uint32_t sg) { return esz == 2 ? lds_u16(ea + sg * 32 * esz) : lds_u32(ea + sg * 32 * esz); };
+  double cp = 0.0;
+  uint32_t q = 0;
+#pragma unroll 1
+  for (int t = 0; t < T.n_ops; ++t) {
+    const uint4 h = __ldg(T.cp + q++);
+    const uint32_t sig = h.x & 0xFFFF, nu = (h.x >> 16) & 0xFF, fl = h.x >> 24, res_slot = h.y;
+    const uint32_t a2r = e_a2r16<NA>(ent(sig));
+    double ready = 0.0;
+#pragma unroll 2
+    for (uint32_t k = 0; k < nu; ++k) {
+      const uint4 u = __ldg(T.cp + q++);
+      double f = 0.0;
+      if (u.x & CP_FAST) {
+        if (u.x != NO_SLOT) f = sp<double>(S.cpf)[(u.x & 0xFFFF) * 32 + lane];
+      } else {
+        f = scr[(size_t)u.x * 32 + lane];
+      }
+      const uint64_t gb = u64of(u.z, u.w & 0xFFFFu);
+      const uint32_t de = ent(u.w >> 16);
+      uint32_t dimU = 0, dimD = 0, P = 0, presD = 0;
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {
+        const uint32_t ru = (a2r >> (4 * A)) & 15;
+        const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
+        const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+        dimU |= du << (4 * A);
+        dimD |= dd << (4 * A);
+        P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
+        presD |= (dd != 15 ? 1u : 0u) << A;
+      }
+      if (dimD != dimU || P) {
+        uint64_t ep[NA][4];
+#pragma unroll
+        for (int A = 0; A < NA; ++A) ep[A][0] = ep[A][1] = ep[A][2] = ep[A][3] = 0;
+        uint64_t size = dv<P2>(T, gb, dcode<P2>(T, presD));
+#pragma unroll
+        for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather
+          const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+          if (dd == 15 || du != 15) continue;
+          ep[A][TOAST_AG] += size;
+          size *= (uint64_t)T.sizes[A];
+        }
+#pragma unroll
+        for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
+          const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+          if (dd == 15 || du == 15 || dd == du) continue;
+          ep[A][TOAST_A2A] += size;
+        }
+#pragma unroll
+        for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
+          if (!((P >> A) & 1)) continue;
+          if (((dimU >> (4 * A)) & 15) != 15) {
+            size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
+            ep[A][TOAST_RS] += size;
+          } else {
+            ep[A][TOAST_AR] += size;
+          }
+        }
+        double m = 0.0;
+#pragma unroll
+        for (int A = 0; A < NA; ++A) {
+          const double n = (double)T.sizes[A];
+          const double n1 = __dsub_rn(n, 1.0);
+          const double ag = __ull2double_rn(ep[A][TOAST_AG]), rs = __ull2double_rn(ep[A][TOAST_RS]);
+          const double ar = __ull2double_rn(ep[A][TOAST_AR]), a2a = __ull2double_rn(ep[A][TOAST_A2A]);
+          const double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
+          const double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
+          m = __dadd_rn(m, __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]));
+        }
+        f = __dadd_rn(f, m);
+      }
+      ready = f > ready ? f : ready;
+    }
+    double ct = 0.0;
+    if (fl & 1) {
+      uint32_t opmask = 0;
+#pragma unroll
+      for (int A = 0; A < NA; ++A) opmask |= (((a2r >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
+      ct = __ddiv_rn(__ull2double_rn(dv<P2>(T, u64of(h.z, h.w), dcode<P2>(T, opmask))), T.F);
+    }
+    const double ft = __dadd_rn(ready, ct);
+    if (res_slot != NO_SLOT) {
+      if (res_slot & CP_FAST) sp<double>(S.cpf)[(res_slot & 0xFFFF) * 32 + lane] = ft;
+      else scr[(size_t)res_slot * 32 + lane] = ft;
+    }
+    cp = ft > cp ? ft : cp;
+  }
+  return cp;
+}
+
 // ---------------------------------------------------------------- one batch of 32 candidates
 // The K warps of the block share the batch: warp 0 decodes, all warps
 // materialise a share of the signatures, warp w sweeps op segment w (its own
 // payload accumulators and relative liveness), and warp 0 combines the
 // segments (peak = max_w (L before segment w + segment w's relative peak)),
 // scores and writes the records.  S.seq holds the candidates on entry.
-template <int NA, bool P2>
+template <int NA, bool P2, bool CP>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
                                            toast_cost* __restrict__ out) {
   __syncthreads();
@@ -645,6 +750,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
 #pragma unroll
       for (int k = 0; k < 4; ++k) ncoll += cnt[(A * 4 + k) * 32 + lane];
     }
+    if (CP) tt = cp_sweep<NA, P2>(T, S, lane, T.cp_scratch + (size_t)blockIdx.x * T.n_slots * 32);
     const uint64_t pk = pk_all;
     const double RT = __ddiv_rn(tt, T.t0);
     const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
@@ -702,7 +808,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
   }
 }
 
-template <int NA, bool P2>
+template <int NA, bool P2, bool CP>
 __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -712,7 +818,7 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
     const int64_t i = b * 32 + lane;
     const bool valid = i < n;
     if (warp == 0) load_seq(S, seqs + i * 32, lane, valid);
-    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i);
+    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out + i);
   }
 }
 
@@ -731,7 +837,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
   o1 = c1;
 }
 
-template <int NA, bool P2>
+template <int NA, bool P2, bool CP>
 __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
@@ -806,7 +912,7 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS
                             sp<uint32_t>(S.seq)[(4 * k + 3) * 32 + lane]);
     }
     }   // warp 0
-    batch_eval<NA, P2>(T, S, K, warp, lane, valid, out + i);
+    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out + i);
   }
 }
 
@@ -846,25 +952,31 @@ __global__ void toast_round_reduce_kernel(const toast_cost* __restrict__ lcost, 
   }
 }
 
-template <int NA, bool P2>
+template <int NA, bool P2, bool CP>
 void set_smem_attr(int bytes) {
-  cudaFuncSetAttribute(toast_eval_kernel<NA, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(toast_rollout_kernel<NA, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(toast_eval_kernel<NA, P2, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(toast_rollout_kernel<NA, P2, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-// call f.template operator()<NA, P2>() for the analysis' (axis count, power-of-two) variant
-template <typename F>
-auto dispatch(int n_axes, bool p2, F&& f) {
+// call f.template operator()<NA, P2, CP>() for the analysis' (axis count,
+// power-of-two, critical path) variant
+template <bool CP, typename F>
+auto dispatch_na(int n_axes, bool p2, F&& f) {
   switch (n_axes * 2 + (p2 ? 1 : 0)) {
-    case 2: return f.template operator()<1, false>();
-    case 3: return f.template operator()<1, true>();
-    case 4: return f.template operator()<2, false>();
-    case 5: return f.template operator()<2, true>();
-    case 6: return f.template operator()<3, false>();
-    case 7: return f.template operator()<3, true>();
-    case 8: return f.template operator()<4, false>();
-    default: return f.template operator()<4, true>();
+    case 2: return f.template operator()<1, false, CP>();
+    case 3: return f.template operator()<1, true, CP>();
+    case 4: return f.template operator()<2, false, CP>();
+    case 5: return f.template operator()<2, true, CP>();
+    case 6: return f.template operator()<3, false, CP>();
+    case 7: return f.template operator()<3, true, CP>();
+    case 8: return f.template operator()<4, false, CP>();
+    default: return f.template operator()<4, true, CP>();
   }
+}
+template <typename F>
+auto dispatch(const DeviceTables& T, F&& f) {
+  return T.cost_model == TOAST_COST_CRITICAL_PATH ? dispatch_na<true>(T.n_axes, T.pow2 != 0, f)
+                                                  : dispatch_na<false>(T.n_axes, T.pow2 != 0, f);
 }
 
 }  // namespace
@@ -933,21 +1045,21 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl, T.n_mc) > dev_smem) {
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl, T.n_mc, T.cost_model) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
   // the attribute is per function, shared by every analysis in the process: allow the device maximum
-  dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() { set_smem_attr<NA, P2>(dev_smem); return 0; });
+  dispatch(T, [&]<int NA, bool P2, bool CP>() { set_smem_attr<NA, P2, CP>(dev_smem); return 0; });
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl, T.n_mc);
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl, T.n_mc, T.cost_model);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
-      cudaError_t e = dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
-        cudaError_t e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<NA, P2>, 32 * K, sm);
-        cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<NA, P2>, 32 * K, sm);
+      cudaError_t e = dispatch(T, [&]<int NA, bool P2, bool CP>() {
+        cudaError_t e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<NA, P2, CP>, 32 * K, sm);
+        cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<NA, P2, CP>, 32 * K, sm);
         return e1 != cudaSuccess ? e1 : e2;
       });
       TOAST_CUDA(e);
@@ -966,6 +1078,18 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     if (4 * w > 5 * best_w && T.n_ops >= 64 * K) { best_w = w; best_k = K; }
   }
   a->k_throughput = fk ? std::max(1, std::min(8, atoi(fk))) : best_k;
+  if (T.cost_model == TOAST_COST_CRITICAL_PATH) {
+    // R22: the critical-path stream and one finish-time scratch [n_slots][32] per resident block
+    if ((st = upload(a, a->h_cp, &p, err))) return st;
+    T.cp = reinterpret_cast<const uint4*>(p);
+    int max_blocks = 0;
+    for (int i = 0; i < 4; ++i) max_blocks = std::max(max_blocks, std::max(a->occ_eval[i], a->occ_roll[i]));
+    const size_t bytes = (size_t)max_blocks * sms * (size_t)std::max(T.n_slots, 1) * 32 * sizeof(double);
+    void* d = nullptr;
+    TOAST_CUDA(cudaMalloc(&d, bytes));
+    a->dev_allocs.push_back(d);
+    T.cp_scratch = reinterpret_cast<double*>(d);
+  }
   a->warps_per_block = 1;
   a->eval_blocks = sms * a->occ_eval[0];
   a->rollout_blocks = sms * a->occ_roll[0];
@@ -1010,11 +1134,11 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc, a->dt.cost_model);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
-  dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
-    toast_eval_kernel<NA, P2><<<g, b, sm, st>>>(T, d_seqs, n, d_out);
+  dispatch(T, [&]<int NA, bool P2, bool CP>() {
+    toast_eval_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_seqs, n, d_out);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());
@@ -1028,11 +1152,11 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc, a->dt.cost_model);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
-  dispatch(T.n_axes, T.pow2 != 0, [&]<int NA, bool P2>() {
-    toast_rollout_kernel<NA, P2><<<g, b, sm, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep);
+  dispatch(T, [&]<int NA, bool P2, bool CP>() {
+    toast_rollout_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());

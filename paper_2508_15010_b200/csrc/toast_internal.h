@@ -142,6 +142,25 @@ struct KSig {
   uint8_t pad;           // bit0: every axis subset divides every shardable role (one-round materialisation)
   uint64_t cls;          // byte r: deselection class of role r (0 = never deselected)
 };
+// critical-path stream (reading R22): per op in program order a KCpOp, then
+// one KCpUse per operand (operand order)
+struct KCpOp {           // 16 B
+  uint16_t sig;
+  uint8_t n_uses;
+  uint8_t flags;         // bit0: matmul-class (has compute time)
+  uint32_t res_slot;     // finish-time slot of the result (NO_SLOT: none)
+  uint64_t gflops;       // global FLOPs of the op (< 2^64)
+};
+struct KCpUse {          // 16 B
+  uint32_t def_slot;     // finish-time slot of the operand (NO_SLOT: a parameter, finish 0)
+  uint32_t use_dimof;    // nibble r: operand dim held by the op's role r (0xF: none)
+  uint64_t gb_sig;       // def global bytes (bits 0-47) | def signature << 48
+};
+constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
+constexpr uint32_t CP_FAST = 0x80000000u;   // slot flag: an on-chip (shared-memory) finish-time slot
+constexpr int CP_SMEM_SLOTS = 0;            // on-chip slots per warp ([n][32] doubles; 0: all slots in global scratch — measured faster)
+constexpr int CP_SHORT = 96;                // values live for at most this many ops may take one
+static_assert(sizeof(KCpOp) == 16 && sizeof(KCpUse) == 16, "cp records");
 static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
 
 
@@ -173,6 +192,9 @@ struct DeviceTables {
   int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
   int32_t n_points, n_mc;
+  int32_t cost_model, n_slots;   // R22: critical path; finish-time slots per candidate
+  const uint4* cp = nullptr;     // critical-path stream (KCpOp / KCpUse records)
+  double* cp_scratch = nullptr;  // [resident warps][n_slots][32] finish times
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -219,6 +241,8 @@ struct toast_analysis {
   // sharing (materialisation classes, class-keyed templates, delta terms):
   // roles over signatures, signature-keyed templates, absolute frontier terms
   int64_t work_sig_roles = 0, work_tmpl = 0, work_terms = 0;
+  std::vector<uint32_t> h_cp;               // critical-path stream (16-B records as 4 x u32)
+  int32_t cost_model = 0;
   std::vector<toast::KSig> h_sigs;          // per materialisation class
   std::vector<uint64_t> h_sig_mr;           // per signature: class | resdim << 32
   std::vector<uint64_t> h_sig_roles, h_desel_cls;

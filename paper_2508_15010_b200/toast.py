@@ -57,7 +57,11 @@ class _Machine(ctypes.Structure):
 
 
 class _NdaOpts(ctypes.Structure):
-    _fields_ = [("min_unique_dims", ctypes.c_int32), ("max_depth", ctypes.c_int32)]
+    _fields_ = [("min_unique_dims", ctypes.c_int32), ("max_depth", ctypes.c_int32), ("cost_model", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+COST_SUM, COST_CRITICAL_PATH = 0, 1
 
 
 class _ActionInfo(ctypes.Structure):
@@ -234,18 +238,18 @@ class Analysis:
         return self._dump_all()["kernel_tables"]
 
 
-def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30) -> Analysis:
+def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30, cost_model: int = COST_SUM) -> Analysis:
     """toast_nda (H0)."""
-    o = _NdaOpts(int(min_unique_dims), int(max_depth))
+    o = _NdaOpts(int(min_unique_dims), int(max_depth), int(cost_model), 0)
     h = _P()
     _check(_lib.toast_nda(graph._h, ctypes.byref(o), ctypes.byref(h)))
     return Analysis(h, None)
 
 
 def build_analysis(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c=100.0, min_unique_dims=10,
-                   max_depth=30, cuda_device=0) -> Analysis:
+                   max_depth=30, cuda_device=0, cost_model=COST_SUM) -> Analysis:
     g = load_graph(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c, cuda_device)
-    a = nda(g, min_unique_dims, max_depth)
+    a = nda(g, min_unique_dims, max_depth, cost_model)
     a.axes = list(axes)
     return a
 

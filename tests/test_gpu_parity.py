@@ -320,3 +320,67 @@ def test_pinned_host_pipeline_matches_device_path():
         s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=99, id_base=5 + int(i))
         assert np.array_equal(gs[i], s1[0])
         assert_same(gc[i:i + 1], c1)
+
+
+# --------------------------------------------------------------------------- NEXT-2: critical path (R22)
+_cp_cache = {}
+
+
+def setup_cp(name):
+    if name not in _cp_cache:
+        T = _T()
+        c = configs.get(name)
+        a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0,
+                             cost_model=T.COST_CRITICAL_PATH)
+        o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cost_model=1)
+        _cp_cache[name] = (a, o)
+    return _cp_cache[name]
+
+
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gns16", "unet"])
+def test_critical_path_rollout_parity(name):
+    """Reading R22: rollouts + evaluation under the critical-path cost model,
+    bit-exact to the oracle's critical path (runtime, score and every field)."""
+    a, o = setup_cp(name)
+    n = 2048 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2") else 256
+    pre = np.zeros((n, 32), np.uint16)
+    os_, oc = o.rollout(pre, seed=9, id_base=5)
+    gs, gc = gpu_rollout(a, pre, 9, 5)
+    assert np.array_equal(gs, os_)
+    assert_same(gc, oc, name)
+    assert_same(gpu_eval(a, os_), oc, name)
+
+
+def test_critical_path_full_size_sampled():
+    """GPT-24 at full bench size under R22: sampled rows recomputed by the oracle."""
+    a, o = setup_cp("gpt24")
+    wave = a.preferred_batch()
+    n = max(wave, ((1 << 18) // wave) * wave)
+    gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), 2024, 0)
+    assert (gc["status"] == 0).all()
+    for i in np.random.default_rng(2).choice(n, size=12, replace=False):
+        s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=2024, id_base=int(i))
+        assert np.array_equal(gs[i], s1[0])
+        assert_same(gc[i:i + 1], c1, f"row {i}")
+
+
+def test_critical_path_random_programs():
+    """R22 on random programs (repeated operands, a size-3 axis)."""
+    T = _T()
+    from workloads import models
+    ran = 0
+    for seed in range(30):
+        ir = models.random_program(seed, n_ops=20, max_ext=8)
+        axes = [("a", 2, 1e10), ("b", 3, 1e11)] if seed % 2 else [("a", 2, 1e10), ("b", 4, 1e11)]
+        try:
+            a = T.build_analysis(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cuda_device=0, cost_model=T.COST_CRITICAL_PATH)
+        except T.ToastError:
+            continue
+        o = Oracle(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cost_model=1)
+        pre = np.zeros((256, 32), np.uint16)
+        os_, oc = o.rollout(pre, seed=seed)
+        gs, gc = gpu_rollout(a, pre, seed, 0)
+        assert np.array_equal(gs, os_)
+        assert_same(gc, oc, ir)
+        ran += 1
+    assert ran >= 15
