@@ -76,13 +76,13 @@ def assert_same(g: np.ndarray, o: np.ndarray, ctx=""):
         assert len(bad) == 0, (ctx, f, bad[:5], g[f][bad[:5]], o[f][bad[:5]])
 
 
-ALL = ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt24", "gns16", "unet"]
+ALL = ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2", "gpt24", "gns16", "unet"]
 
 
 @pytest.mark.parametrize("name", ALL)
 def test_eval_parity_on_oracle_rollouts(name):
     a, o = setup(name)
-    n = 3000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2") else 300
+    n = 3000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2") else 300
     seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=1234, threads=8)
     assert_same(gpu_eval(a, seqs), oc, name)
 
@@ -153,11 +153,12 @@ def test_eval_host_pointer_path_and_edges():
     T.eval_batch(a, seqs[:0], one[:0], n=0)
 
 
-@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt24", "unet", "gns16"])
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2", "gpt24", "unet",
+                                  "gns16"])
 def test_rollout_parity(name):
     """K2 vs C15: same (seed, id) -> same sequence and same cost record."""
     a, o = setup(name)
-    n = 2000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2") else 200
+    n = 2000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2") else 200
     pre = np.zeros((n, 32), np.uint16)
     # half the rows start from a (legal) prefix drawn by the oracle
     s0, _ = o.rollout(np.zeros((n // 2, 32), np.uint16), seed=77)
@@ -337,12 +338,12 @@ def setup_cp(name):
     return _cp_cache[name]
 
 
-@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gns16", "unet"])
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gns16", "unet"])
 def test_critical_path_rollout_parity(name):
     """Reading R22: rollouts + evaluation under the critical-path cost model,
     bit-exact to the oracle's critical path (runtime, score and every field)."""
     a, o = setup_cp(name)
-    n = 2048 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2") else 256
+    n = 2048 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax") else 256
     pre = np.zeros((n, 32), np.uint16)
     os_, oc = o.rollout(pre, seed=9, id_base=5)
     gs, gc = gpu_rollout(a, pre, 9, 5)
