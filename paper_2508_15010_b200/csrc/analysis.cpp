@@ -932,58 +932,76 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
   a->cost_model = o->cost_model;
   int32_t n_slots = 0;
   a->h_cp.clear();
+  a->h_cp_comm.clear();
+  a->h_cp_comp.clear();
   if (o->cost_model == TOAST_COST_CRITICAL_PATH) {
     // finish-time slots: every non-parameter value holds one from its def to
     // its last use (reused greedily); parameters finish at 0 and need none.
-    // Values live for at most CP_SHORT ops take one of CP_SMEM_SLOTS on-chip
-    // slots when one is free (bit 31 set), the rest global scratch slots.
-    std::vector<uint32_t> slot_of(g->values.size(), NO_SLOT), free_slots, free_fast;
-    for (int i = CP_SMEM_SLOTS - 1; i >= 0; --i) free_fast.push_back(CP_FAST | (uint32_t)i);
-    auto push = [&](const void* rec) {
-      const uint32_t* w = reinterpret_cast<const uint32_t*>(rec);
-      a->h_cp.insert(a->h_cp.end(), w, w + 4);
-    };
+    // Edge durations are shared by every edge of the same communication class
+    // (def signature, use materialisation class, use role -> dim map, bytes),
+    // compute times by every op of the same (signature, FLOPs) class: the
+    // kernels evaluate each class once per candidate.
+    std::vector<uint32_t> slot_of(g->values.size(), NO_SLOT), free_slots;
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint64_t>, uint32_t> comm_id;
+    std::map<std::pair<uint32_t, uint64_t>, uint32_t> comp_id;
     for (int32_t t = 0; t < n_ops; ++t) {
       const GOp& op = g->ops[t];
-      KCpOp r{};
-      r.sig = (uint16_t)a->op_sig[t];
-      r.n_uses = (uint8_t)op.operands.size();
-      r.flags = (a->h_ops[t].flags & 1) ? 1 : 0;
-      r.gflops = a->h_gflops[t];
-      r.res_slot = NO_SLOT;
-      if (op.result >= 0 && op.kind != OK_PARAM) {
-        if (last_use[op.result] - t <= CP_SHORT && !free_fast.empty()) {
-          slot_of[op.result] = free_fast.back();
-          free_fast.pop_back();
-        } else {
-          if (free_slots.empty()) free_slots.push_back((uint32_t)n_slots++);
-          slot_of[op.result] = free_slots.back();
-          free_slots.pop_back();
+      uint32_t comp = NO_CLASS;
+      if (a->h_ops[t].flags & 1) {
+        auto it = comp_id.emplace(std::make_pair(a->op_sig[t], a->h_gflops[t]), (uint32_t)a->h_cp_comp.size());
+        if (it.second) {
+          KCpComp c{};
+          c.sig = a->op_sig[t];
+          c.gflops = a->h_gflops[t];
+          a->h_cp_comp.push_back(c);
         }
-        r.res_slot = slot_of[op.result];
+        comp = it.first->second;
       }
-      push(&r);
+      uint32_t res_slot = NO_SLOT;
+      if (op.result >= 0 && op.kind != OK_PARAM) {
+        if (free_slots.empty()) free_slots.push_back((uint32_t)n_slots++);
+        slot_of[op.result] = free_slots.back();
+        free_slots.pop_back();
+        res_slot = slot_of[op.result];
+      }
+      if (op.operands.size() > 0xFFFF || comp > 0xFFFF) { err = "critical-path stream limits"; return TOAST_E_LIMIT; }
+      a->h_cp.push_back(res_slot);
+      a->h_cp.push_back(comp | ((uint32_t)op.operands.size() << 16));
+      const uint32_t umc = (uint32_t)(a->h_sig_mr[a->op_sig[t]] & 0xFFFFFFFFu);
       for (size_t k = 0; k < op.operands.size(); ++k) {
         const int32_t v = op.operands[k];
-        KCpUse u{};
-        u.def_slot = slot_of[v];
         uint32_t um = ~0u;
         for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
           uint32_t rr = OL[t].use_role[k][i];
           um = (um & ~(0xFu << (4 * rr))) | ((uint32_t)i << (4 * rr));
         }
-        u.use_dimof = um;
-        u.gb_sig = a->h_ops[g->values[v].def_op].gbytes | ((uint64_t)a->op_sig[g->values[v].def_op] << 48);
-        push(&u);
+        const int32_t d = g->values[v].def_op;
+        auto it = comm_id.emplace(std::make_tuple((uint32_t)a->op_sig[d], umc, um, a->h_ops[d].gbytes),
+                                  (uint32_t)a->h_cp_comm.size());
+        if (it.second) {
+          KCpComm c{};
+          c.def_sig = (uint16_t)a->op_sig[d];
+          c.use_mc = (uint16_t)umc;
+          c.use_dimof = um;
+          c.gb = a->h_ops[d].gbytes;
+          a->h_cp_comm.push_back(c);
+        }
+        a->h_cp.push_back(slot_of[v]);
+        a->h_cp.push_back(it.first->second);
       }
       // values whose last use is t give their slots back (after t read them)
       for (int32_t dv : deaths[t]) {
         const int32_t val = g->ops[dv].result;
-        if (val >= 0 && slot_of[val] != NO_SLOT) (slot_of[val] & CP_FAST ? free_fast : free_slots).push_back(slot_of[val]);
+        if (val >= 0 && slot_of[val] != NO_SLOT) free_slots.push_back(slot_of[val]);
       }
     }
+    if (getenv("TOAST_DEBUG"))
+      fprintf(stderr, "[toast] critical path: %d finish slots, %zu communication classes, %zu compute classes\n",
+              n_slots, a->h_cp_comm.size(), a->h_cp_comp.size());
   }
   a->dt.n_slots = n_slots;
+  a->dt.n_comm = (int32_t)a->h_cp_comm.size();
+  a->dt.n_comp = (int32_t)a->h_cp_comp.size();
   a->dt.cost_model = o->cost_model;
 
   // ------------------------------------------------------------ baseline (empty sequence)

@@ -72,9 +72,9 @@ __host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
 }
 __host__ __device__ inline int smem_d_bytes(int n_tmpl) { return r16(n_tmpl * 32); }
 __host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl,
-                                                int n_mc, int cp) {
+                                                int n_mc) {
   return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl) +
-         r16(n_sigs * 32) + r16(n_mc * 64) + (cp ? CP_SMEM_SLOTS * 32 * 8 : 0);
+         r16(n_sigs * 32) + r16(n_mc * 64);
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -120,7 +120,6 @@ struct Smem {               // byte offsets into g_smem
   uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
   uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u16)
-  uint32_t cpf;             // R22: [CP_SMEM_SLOTS][32] on-chip finish-time slots (double)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -140,7 +139,6 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
   s.pc = s.tb + smem_d_bytes(T.n_tmpl);
   s.mca = s.pc + r16(T.n_sigs * 32);
-  s.cpf = s.mca + r16(T.n_mc * 64);
   return s;
 }
 
@@ -338,103 +336,111 @@ __device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
 }
 
 // ---------------------------------------------------------------- R22: critical path (NEXT-2)
-// One lane = one candidate: the ops in program order, finish(t) = max over
-// operands, in operand order, of (finish(def) + the edge's collective time)
-// + t's compute time; the finish times of live values sit in this warp's
-// global scratch [slot][32].  The edge's collectives are C11's (reading R20)
-// over its own bytes and their time is C13's ring formula — fixed order,
-// explicit round-to-nearest, bit-identical to the oracle.
+// Per candidate: finish(t) = max over operands, in operand order, of
+// (finish(def) + the edge's collective duration) + t's compute time.  Every
+// edge of one communication class (def signature, use materialisation class,
+// role -> dim map, bytes) has the same duration, every op of one compute
+// class (signature, FLOPs) the same compute time, so the block's warps first
+// evaluate each class once per lane into the block's scratch; warp 0 then
+// walks the op stream, keeping the finish times of live values in the
+// scratch's slots.  The duration is C11's collectives (reading R20) over the
+// edge's bytes timed by C13's ring formula — fixed order, explicit
+// round-to-nearest, bit-identical to the oracle.
 template <int NA, bool P2>
-__device__ __forceinline__ double cp_sweep(const DeviceTables& T, const Smem& S, int lane, double* __restrict__ scr) {
+__device__ __forceinline__ void cp_classes(const DeviceTables& T, const Smem& S, int K, int warp, int lane,
+                                           double* __restrict__ scr) {
   const uint32_t sh = smem_base();
   constexpr uint32_t esz = sizeof(typename Ent<NA>::T);
   const uint32_t ea = sh + S.sig + (uint32_t)lane * esz;
   auto ent = [&](uint32_t sg) { return esz == 2 ? lds_u16(ea + sg * 32 * esz) : lds_u32(ea + sg * 32 * esz); };
+  for (int c = warp; c < T.n_comm; c += K) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(T.cp_comm + c));
+    const uint32_t de = ent(w.x & 0xFFFF);
+    const uint32_t a2r = sp<uint16_t>(S.mca)[(w.x >> 16) * 32 + lane];
+    const uint64_t gb = u64of(w.z, w.w);
+    uint32_t dimU = 0, dimD = 0, P = 0, presD = 0;
+#pragma unroll
+    for (int A = 0; A < NA; ++A) {
+      const uint32_t ru = (a2r >> (4 * A)) & 15;
+      const uint32_t du = ru == 15 ? 15u : (w.y >> (4 * ru)) & 15;
+      const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+      dimU |= du << (4 * A);
+      dimD |= dd << (4 * A);
+      P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
+      presD |= (dd != 15 ? 1u : 0u) << A;
+    }
+    double m = 0.0;
+    if (dimD != dimU || P) {
+      uint64_t ep[NA][4];
+#pragma unroll
+      for (int A = 0; A < NA; ++A) ep[A][0] = ep[A][1] = ep[A][2] = ep[A][3] = 0;
+      uint64_t size = dv<P2>(T, gb, dcode<P2>(T, presD));
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather
+        const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+        if (dd == 15 || du != 15) continue;
+        ep[A][TOAST_AG] += size;
+        size *= (uint64_t)T.sizes[A];
+      }
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
+        const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+        if (dd == 15 || du == 15 || dd == du) continue;
+        ep[A][TOAST_A2A] += size;
+      }
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
+        if (!((P >> A) & 1)) continue;
+        if (((dimU >> (4 * A)) & 15) != 15) {
+          size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
+          ep[A][TOAST_RS] += size;
+        } else {
+          ep[A][TOAST_AR] += size;
+        }
+      }
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {
+        const double n = (double)T.sizes[A];
+        const double n1 = __dsub_rn(n, 1.0);
+        const double ag = __ull2double_rn(ep[A][TOAST_AG]), rs = __ull2double_rn(ep[A][TOAST_RS]);
+        const double ar = __ull2double_rn(ep[A][TOAST_AR]), a2a = __ull2double_rn(ep[A][TOAST_A2A]);
+        const double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
+        const double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
+        m = __dadd_rn(m, __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]));
+      }
+    }
+    scr[(size_t)c * 32 + lane] = m;
+  }
+  for (int c = warp; c < T.n_comp; c += K) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(T.cp_comp + c));
+    const uint32_t a2r = e_a2r16<NA>(ent(w.x));
+    uint32_t opmask = 0;
+#pragma unroll
+    for (int A = 0; A < NA; ++A) opmask |= (((a2r >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
+    scr[(size_t)(T.n_comm + c) * 32 + lane] =
+        __ddiv_rn(__ull2double_rn(dv<P2>(T, u64of(w.z, w.w), dcode<P2>(T, opmask))), T.F);
+  }
+}
+
+__device__ __forceinline__ double cp_sweep(const DeviceTables& T, int lane, const double* __restrict__ cls,
+                                           double* __restrict__ slots) {
   double cp = 0.0;
   uint32_t q = 0;
 #pragma unroll 1
   for (int t = 0; t < T.n_ops; ++t) {
-    const uint4 h = __ldg(T.cp + q++);
-    const uint32_t sig = h.x & 0xFFFF, nu = (h.x >> 16) & 0xFF, fl = h.x >> 24, res_slot = h.y;
-    const uint32_t a2r = e_a2r16<NA>(ent(sig));
+    const uint2 h = __ldg(T.cp + q++);
+    const uint32_t comp = h.y & 0xFFFF, nu = h.y >> 16;
     double ready = 0.0;
 #pragma unroll 2
     for (uint32_t k = 0; k < nu; ++k) {
-      const uint4 u = __ldg(T.cp + q++);
-      double f = 0.0;
-      if (u.x & CP_FAST) {
-        if (u.x != NO_SLOT) f = sp<double>(S.cpf)[(u.x & 0xFFFF) * 32 + lane];
-      } else {
-        f = scr[(size_t)u.x * 32 + lane];
-      }
-      const uint64_t gb = u64of(u.z, u.w & 0xFFFFu);
-      const uint32_t de = ent(u.w >> 16);
-      uint32_t dimU = 0, dimD = 0, P = 0, presD = 0;
-#pragma unroll
-      for (int A = 0; A < NA; ++A) {
-        const uint32_t ru = (a2r >> (4 * A)) & 15;
-        const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
-        const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
-        dimU |= du << (4 * A);
-        dimD |= dd << (4 * A);
-        P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
-        presD |= (dd != 15 ? 1u : 0u) << A;
-      }
-      if (dimD != dimU || P) {
-        uint64_t ep[NA][4];
-#pragma unroll
-        for (int A = 0; A < NA; ++A) ep[A][0] = ep[A][1] = ep[A][2] = ep[A][3] = 0;
-        uint64_t size = dv<P2>(T, gb, dcode<P2>(T, presD));
-#pragma unroll
-        for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather
-          const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
-          if (dd == 15 || du != 15) continue;
-          ep[A][TOAST_AG] += size;
-          size *= (uint64_t)T.sizes[A];
-        }
-#pragma unroll
-        for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
-          const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
-          if (dd == 15 || du == 15 || dd == du) continue;
-          ep[A][TOAST_A2A] += size;
-        }
-#pragma unroll
-        for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
-          if (!((P >> A) & 1)) continue;
-          if (((dimU >> (4 * A)) & 15) != 15) {
-            size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
-            ep[A][TOAST_RS] += size;
-          } else {
-            ep[A][TOAST_AR] += size;
-          }
-        }
-        double m = 0.0;
-#pragma unroll
-        for (int A = 0; A < NA; ++A) {
-          const double n = (double)T.sizes[A];
-          const double n1 = __dsub_rn(n, 1.0);
-          const double ag = __ull2double_rn(ep[A][TOAST_AG]), rs = __ull2double_rn(ep[A][TOAST_RS]);
-          const double ar = __ull2double_rn(ep[A][TOAST_AR]), a2a = __ull2double_rn(ep[A][TOAST_A2A]);
-          const double p1 = __dmul_rn(n1, __dadd_rn(ag, rs));
-          const double p2 = __ddiv_rn(__dmul_rn(n1, __dadd_rn(__dmul_rn(2.0, ar), a2a)), n);
-          m = __dadd_rn(m, __ddiv_rn(__dadd_rn(p1, p2), T.bw[A]));
-        }
-        f = __dadd_rn(f, m);
-      }
+      const uint2 u = __ldg(T.cp + q++);
+      const double fin = u.x == NO_SLOT ? 0.0 : slots[(size_t)u.x * 32 + lane];
+      const double f = __dadd_rn(fin, cls[(size_t)u.y * 32 + lane]);
       ready = f > ready ? f : ready;
     }
-    double ct = 0.0;
-    if (fl & 1) {
-      uint32_t opmask = 0;
-#pragma unroll
-      for (int A = 0; A < NA; ++A) opmask |= (((a2r >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
-      ct = __ddiv_rn(__ull2double_rn(dv<P2>(T, u64of(h.z, h.w), dcode<P2>(T, opmask))), T.F);
-    }
+    const double ct = comp == NO_CLASS ? 0.0 : cls[(size_t)(T.n_comm + comp) * 32 + lane];
     const double ft = __dadd_rn(ready, ct);
-    if (res_slot != NO_SLOT) {
-      if (res_slot & CP_FAST) sp<double>(S.cpf)[(res_slot & 0xFFFF) * 32 + lane] = ft;
-      else scr[(size_t)res_slot * 32 + lane] = ft;
-    }
+    if (h.x != NO_SLOT) slots[(size_t)h.x * 32 + lane] = ft;
     cp = ft > cp ? ft : cp;
   }
   return cp;
@@ -709,6 +715,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     peak = M > peak ? M : peak;
   }
   }
+  if (CP) cp_classes<NA, P2>(T, S, K, warp, lane, T.cp_scratch + (size_t)blockIdx.x * (T.n_comm + T.n_comp + T.n_slots) * 32);
   seg[0 * 32 + lane] = key;
   seg[1 * 32 + lane] = flo;
   seg[2 * 32 + lane] = fhi;
@@ -750,7 +757,10 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
 #pragma unroll
       for (int k = 0; k < 4; ++k) ncoll += cnt[(A * 4 + k) * 32 + lane];
     }
-    if (CP) tt = cp_sweep<NA, P2>(T, S, lane, T.cp_scratch + (size_t)blockIdx.x * T.n_slots * 32);
+    if (CP) {
+      double* scr = T.cp_scratch + (size_t)blockIdx.x * (T.n_comm + T.n_comp + T.n_slots) * 32;
+      tt = cp_sweep(T, lane, scr, scr + (size_t)(T.n_comm + T.n_comp) * 32);
+    }
     const uint64_t pk = pk_all;
     const double RT = __ddiv_rn(tt, T.t0);
     const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
@@ -1045,7 +1055,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl, T.n_mc, T.cost_model) > dev_smem) {
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl, T.n_mc) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -1054,7 +1064,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl, T.n_mc, T.cost_model);
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl, T.n_mc);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
       cudaError_t e = dispatch(T, [&]<int NA, bool P2, bool CP>() {
@@ -1081,10 +1091,15 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) {
     // R22: the critical-path stream and one finish-time scratch [n_slots][32] per resident block
     if ((st = upload(a, a->h_cp, &p, err))) return st;
-    T.cp = reinterpret_cast<const uint4*>(p);
+    T.cp = reinterpret_cast<const uint2*>(p);
+    if ((st = upload(a, a->h_cp_comm, &p, err))) return st;
+    T.cp_comm = reinterpret_cast<const KCpComm*>(p);
+    if ((st = upload(a, a->h_cp_comp, &p, err))) return st;
+    T.cp_comp = reinterpret_cast<const KCpComp*>(p);
     int max_blocks = 0;
     for (int i = 0; i < 4; ++i) max_blocks = std::max(max_blocks, std::max(a->occ_eval[i], a->occ_roll[i]));
-    const size_t bytes = (size_t)max_blocks * sms * (size_t)std::max(T.n_slots, 1) * 32 * sizeof(double);
+    const size_t bytes = (size_t)max_blocks * sms * (size_t)std::max(T.n_comm + T.n_comp + T.n_slots, 1) * 32 *
+                         sizeof(double);
     void* d = nullptr;
     TOAST_CUDA(cudaMalloc(&d, bytes));
     a->dev_allocs.push_back(d);
@@ -1134,7 +1149,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc, a->dt.cost_model);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
@@ -1152,7 +1167,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc, a->dt.cost_model);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T, [&]<int NA, bool P2, bool CP>() {

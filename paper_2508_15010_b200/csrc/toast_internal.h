@@ -142,25 +142,23 @@ struct KSig {
   uint8_t pad;           // bit0: every axis subset divides every shardable role (one-round materialisation)
   uint64_t cls;          // byte r: deselection class of role r (0 = never deselected)
 };
-// critical-path stream (reading R22): per op in program order a KCpOp, then
-// one KCpUse per operand (operand order)
-struct KCpOp {           // 16 B
-  uint16_t sig;
-  uint8_t n_uses;
-  uint8_t flags;         // bit0: matmul-class (has compute time)
-  uint32_t res_slot;     // finish-time slot of the result (NO_SLOT: none)
-  uint64_t gflops;       // global FLOPs of the op (< 2^64)
-};
-struct KCpUse {          // 16 B
-  uint32_t def_slot;     // finish-time slot of the operand (NO_SLOT: a parameter, finish 0)
+// critical-path stream (reading R22), 8-byte records (2 x u32) in program
+// order: per op {result slot, compute class | #operands << 16}, then per
+// operand {its def's finish slot, communication class}
+struct KCpComm {         // 16 B: an edge duration class
+  uint16_t def_sig;
+  uint16_t use_mc;       // the use op's materialisation class
   uint32_t use_dimof;    // nibble r: operand dim held by the op's role r (0xF: none)
-  uint64_t gb_sig;       // def global bytes (bits 0-47) | def signature << 48
+  uint64_t gb;           // def global bytes
 };
-constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
-constexpr uint32_t CP_FAST = 0x80000000u;   // slot flag: an on-chip (shared-memory) finish-time slot
-constexpr int CP_SMEM_SLOTS = 0;            // on-chip slots per warp ([n][32] doubles; 0: all slots in global scratch — measured faster)
-constexpr int CP_SHORT = 96;                // values live for at most this many ops may take one
-static_assert(sizeof(KCpOp) == 16 && sizeof(KCpUse) == 16, "cp records");
+struct KCpComp {         // 16 B: a compute-time class
+  uint32_t sig;
+  uint32_t pad;
+  uint64_t gflops;
+};
+constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;   // a parameter's "slot": finish 0
+constexpr uint32_t NO_CLASS = 0xFFFFu;      // no compute time
+static_assert(sizeof(KCpComm) == 16 && sizeof(KCpComp) == 16, "cp records");
 static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
 
 
@@ -193,8 +191,11 @@ struct DeviceTables {
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
   int32_t n_points, n_mc;
   int32_t cost_model, n_slots;   // R22: critical path; finish-time slots per candidate
-  const uint4* cp = nullptr;     // critical-path stream (KCpOp / KCpUse records)
-  double* cp_scratch = nullptr;  // [resident warps][n_slots][32] finish times
+  int32_t n_comm, n_comp;        // R22: edge-duration and compute-time classes
+  const uint2* cp = nullptr;     // critical-path stream
+  const KCpComm* cp_comm = nullptr;
+  const KCpComp* cp_comp = nullptr;
+  double* cp_scratch = nullptr;  // per resident block: [n_comm + n_comp + n_slots][32] doubles
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -241,7 +242,9 @@ struct toast_analysis {
   // sharing (materialisation classes, class-keyed templates, delta terms):
   // roles over signatures, signature-keyed templates, absolute frontier terms
   int64_t work_sig_roles = 0, work_tmpl = 0, work_terms = 0;
-  std::vector<uint32_t> h_cp;               // critical-path stream (16-B records as 4 x u32)
+  std::vector<uint32_t> h_cp;               // critical-path stream (8-B records as 2 x u32)
+  std::vector<toast::KCpComm> h_cp_comm;
+  std::vector<toast::KCpComp> h_cp_comp;
   int32_t cost_model = 0;
   std::vector<toast::KSig> h_sigs;          // per materialisation class
   std::vector<uint64_t> h_sig_mr;           // per signature: class | resdim << 32
