@@ -94,6 +94,7 @@ toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_anal
     a->graph = std::make_shared<const toast_graph>(*g);
     if (a->device >= 0) {
       st = toast::upload_tables(a, err);
+      if (st == TOAST_OK) st = toast::autotune_k(a, err);
       if (st != TOAST_OK) { toast::free_tables(a); delete a; return fail(st, err); }
     }
   } catch (std::bad_alloc&) {

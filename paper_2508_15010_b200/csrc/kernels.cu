@@ -1178,6 +1178,54 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   return TOAST_OK;
 }
 
+// Throughput K (warps sharing one batch of 32 candidates): measured, not
+// guessed.  Each K with resident blocks runs the rollout kernel on the same
+// multi-wave batch of empty prefixes (CUDA events, best of 2 after a warm-up)
+// and the fastest becomes the analysis' k_throughput.  Results never depend
+// on K — only the speed does.  TOAST_FORCE_K overrides.
+toast_status autotune_k(toast_analysis* a, std::string& err) {
+  // (the critical-path variant keeps the occupancy heuristic: its walk runs on one warp per block)
+  if (getenv("TOAST_FORCE_K") || a->n_sms <= 0 || a->dt.cost_model == TOAST_COST_CRITICAL_PATH) return TOAST_OK;
+  int occ_max = 0;
+  for (int i = 0, K = 1; i < 4; ++i, K *= 2) occ_max = std::max(occ_max, std::min(a->occ_eval[i], a->occ_roll[i]) * K);
+  const int64_t n = 2 * (int64_t)occ_max * a->n_sms * 32;
+  void* buf = nullptr;
+  TOAST_CUDA(cudaMalloc(&buf, (size_t)n * (64 + 64 + sizeof(toast_cost))));
+  TOAST_CUDA(cudaMemset(buf, 0, (size_t)n * 64));
+  uint16_t* d_pre = reinterpret_cast<uint16_t*>(buf);
+  uint16_t* d_seq = d_pre + n * 32;
+  toast_cost* d_out = reinterpret_cast<toast_cost*>(d_seq + n * 32);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int keep = a->k_throughput;
+  int best_k = keep;
+  float best_ms = 1e30f;
+  toast_status st = TOAST_OK;
+  for (int i = 0, K = 1; i < 4 && st == TOAST_OK; ++i, K *= 2) {
+    if (a->occ_eval[i] < 1 || a->occ_roll[i] < 1) continue;
+    a->k_throughput = K;
+    float ms = 1e30f;
+    for (int rep = 0; rep < 3 && st == TOAST_OK; ++rep) {
+      cudaEventRecord(e0, 0);
+      st = launch_rollout(a, d_pre, n, 1, (uint64_t)rep * n, d_seq, d_out, nullptr, err, 1);
+      cudaEventRecord(e1, 0);
+      cudaEventSynchronize(e1);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e0, e1);
+      if (rep) ms = std::min(ms, t);   // rep 0 is the warm-up
+    }
+    if (ms < best_ms) { best_ms = ms; best_k = K; }
+  }
+  a->k_throughput = st == TOAST_OK ? best_k : keep;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  if (st != TOAST_OK) return st;
+  TOAST_CUDA(cudaGetLastError());
+  return TOAST_OK;
+}
+
 toast_status launch_round_reduce(const toast_cost* d_lcost, const uint16_t* d_lpre, const toast_cost* d_cost,
                                  const uint16_t* d_seqs, int L, int R, void* d_out, void* stream, std::string& err) {
   if (L <= 0) return TOAST_OK;

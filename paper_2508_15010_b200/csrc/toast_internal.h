@@ -294,6 +294,7 @@ void host_materialize(const toast_analysis* a, const uint16_t* seq, uint8_t* mas
 toast_status lower_program(const toast_analysis* a, const uint16_t* seq, std::string& out, std::string& err);
 // kernels.cu
 toast_status upload_tables(toast_analysis* a, std::string& err);
+toast_status autotune_k(toast_analysis* a, std::string& err);   // measured throughput K (after upload_tables)
 void free_tables(toast_analysis* a);
 toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, toast_cost* d_out, void* stream,
                          std::string& err);
