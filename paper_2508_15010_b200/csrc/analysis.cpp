@@ -842,11 +842,27 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       lo[0] = hi[0] = prodall;
       for (size_t q = 0; q < NS; ++q) { lo[1 + q] = prodall / dmax[q]; hi[1 + q] = prodall; }
       for (size_t q = 0; q < NT; ++q) { lo[1 + NS + q] = 0; hi[1 + NS + q] = prodall - prodall / dmax[a->h_tmpl[q].def_sig]; }
-      auto geq = [&](const std::vector<int64_t>& x, const std::vector<int64_t>& y) {   // x >= y for every w in the box
-        __int128 m = 0;
-        for (size_t d = 0; d < D; ++d) {
-          const __int128 df = (__int128)x[d] - y[d];
-          m += df * (df > 0 ? lo[d] : hi[d]);
+      // x >= y for every feasible w.  The feasible set is the box plus the
+      // coupling g_tm <= 1 - 1/d_D (a template's growth 1/d_U - 1/d_D never
+      // exceeds 1 - 1/d_D, with d_D its def signature's divisor — the same
+      // weight as that signature's live-byte coordinate).  The minimum over
+      // this set separates per signature s: with B_s = the sum of s's
+      // templates' negative differences (each taking g at its cap) the
+      // signature's coefficient becomes (diff_s - B_s), minimised at an
+      // endpoint of [lo_s, hi_s]; positive template differences take g = 0.
+      std::vector<std::vector<uint32_t>> sig_tmpls(NS);
+      for (size_t q = 0; q < NT; ++q) sig_tmpls[a->h_tmpl[q].def_sig].push_back((uint32_t)q);
+      auto geq = [&](const std::vector<int64_t>& x, const std::vector<int64_t>& y) {
+        __int128 m = (__int128)(x[0] - y[0]) * prodall;
+        for (size_t q = 0; q < NS; ++q) {
+          const __int128 a_s = (__int128)x[1 + q] - y[1 + q];
+          __int128 B = 0;
+          for (uint32_t tm : sig_tmpls[q]) {
+            const __int128 b = (__int128)x[1 + NS + tm] - y[1 + NS + tm];
+            if (b < 0) B += b;
+          }
+          const __int128 coef = a_s - B;
+          m += coef * (coef >= 0 ? lo[1 + q] : hi[1 + q]) + B * prodall;
         }
         return m >= 0;
       };
