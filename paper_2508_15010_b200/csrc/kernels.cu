@@ -446,6 +446,12 @@ __device__ __forceinline__ double cp_sweep(const DeviceTables& T, int lane, cons
   return cp;
 }
 
+// a block of one warp needs only the warp's own ordering
+__device__ __forceinline__ void block_sync(int K) {
+  if (K == 1) __syncwarp();
+  else __syncthreads();
+}
+
 // ---------------------------------------------------------------- one batch of 32 candidates
 // The K warps of the block share the batch: warp 0 decodes, all warps
 // materialise a share of the signatures, warp w sweeps op segment w (its own
@@ -455,7 +461,7 @@ __device__ __forceinline__ double cp_sweep(const DeviceTables& T, int lane, cons
 template <int NA, bool P2, bool CP>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
                                            toast_cost* __restrict__ out) {
-  __syncthreads();
+  block_sync(K);
   if (warp == 0) {
     uint64_t f0, on, ap;
     sp<uint32_t>(S.status)[lane] = decode(T, S, lane, f0, on, ap);
@@ -463,7 +469,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     sp<unsigned long long>(S.on)[lane] = on;
     sp<unsigned long long>(S.axpos)[lane] = ap;
   }
-  __syncthreads();
+  block_sync(K);
   // H2: materialise this warp's share of the signatures; per signature the
   // state-key terms (H7, R14) and the local FLOPs (H3) of all its ops at once
   uint64_t key = 0, flo = 0, fhi = 0;
@@ -478,16 +484,32 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     for (int c = warp; c < T.n_mc; c += K)
       sp<uint16_t>(S.mca)[c * 32 + lane] = (uint16_t)materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
   }
-  __syncthreads();
+  block_sync(K);
   {
     // H2b: per signature the entry (axis -> role | axis -> result dim), the
     // result layout's division code, the state-key terms (H7) and the local
     // FLOPs (H3) of all its ops
+    // (the next signature's table words are loaded one iteration ahead)
+    uint64_t nglo = 0, nghi = 0, nmr = 0;
+    if (warp < T.n_sigs) {
+      nglo = __ldg(T.sig_flops + 2 * warp);
+      nghi = __ldg(T.sig_flops + 2 * warp + 1);
+      nmr = __ldg(T.sig_mr + warp);
+    }
     for (int s = warp; s < T.n_sigs; s += K) {
-      const uint64_t glo = __ldg(T.sig_flops + 2 * s), ghi = __ldg(T.sig_flops + 2 * s + 1);
-      const uint64_t mr = __ldg(T.sig_mr + s);
+      const uint64_t glo = nglo, ghi = nghi, mr = nmr;
+      if (s + K < T.n_sigs) {
+        nglo = __ldg(T.sig_flops + 2 * (s + K));
+        nghi = __ldg(T.sig_flops + 2 * (s + K) + 1);
+        nmr = __ldg(T.sig_mr + s + K);
+      }
       const uint32_t a2r = sp<uint16_t>(S.mca)[(uint32_t)(mr & 0xFFFF) * 32 + lane];
       const uint32_t rdm = (uint32_t)(mr >> 32);
+      // the state-key terms: every axis's load issued at once (role 15 reads a
+      // valid word and is masked out)
+      uint64_t kt[NA];
+#pragma unroll
+      for (int A = 0; A < NA; ++A) kt[A] = __ldg(T.sig_key + (size_t)s * 32 + A * 8 + ((a2r >> (4 * A)) & 7));
       uint32_t dims = 0;
 #pragma unroll
       for (int A = 0; A < 4; ++A) {
@@ -503,11 +525,9 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       uint32_t opmask = 0;
 #pragma unroll
       for (int A = 0; A < NA; ++A) {
-        const uint32_t r = e_role<NA>(e, A);
-        if (r != 15) {
-          key += __ldg(T.sig_key + (size_t)s * 32 + A * 8 + r);
-          opmask |= 1u << A;
-        }
+        const bool on = ((a2r >> (4 * A)) & 15) != 15;
+        key += on ? kt[A] : 0ULL;
+        opmask |= (on ? 1u : 0u) << A;
       }
       if (glo | ghi) {
         const unsigned __int128 f = dv128<P2>(T, ((unsigned __int128)ghi << 64) | glo, opmask);
@@ -517,7 +537,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       }
     }
   }
-  __syncthreads();
+  block_sync(K);
   const uint32_t acc = S.acc + (uint32_t)warp * smem_acc_bytes(NA);
   unsigned long long* pay = sp<unsigned long long>(acc);
   uint32_t* cnt = sp<uint32_t>(acc + NA * 4 * 32 * 8);
@@ -598,7 +618,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   }
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = rp[q]; cnt[q * 32 + lane] = rc[q]; }
-  __syncthreads();
+  block_sync(K);
 
   // H5 (C12, reading R19): peak = max over the kept ops of the peak-memory
   // frontier of M_t = constant + sum_s Live_t[s] / d_s + sum_tm growth_tm(Tmp_t[tm])
@@ -721,7 +741,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   seg[2 * 32 + lane] = fhi;
   seg[3 * 32 + lane] = 0ULL;
   seg[4 * 32 + lane] = peak;
-  __syncthreads();
+  block_sync(K);
   if (warp == 0) {
     // combine the K segments: sums into warp 0's slots, peak by the segment scan
     key = 0; flo = 0; fhi = 0;
@@ -799,7 +819,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       dst[15] = make_uint4(0, 0, 0, 0);
     }
   }
-  __syncthreads();
+  block_sync(K);
 }
 
 __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restrict__ g, int lane, bool valid) {
