@@ -937,6 +937,27 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         a->point_op.push_back(t);
         prev = &p;
       }
+      // compact the frontier's feature ids: only the signatures and templates
+      // a term uses get a per-lane code slot in the kernels' shared memory
+      std::vector<uint32_t> sslot(NS, 0xFFFFu), tslot(NT, 0xFFFFFFFFu);
+      uint32_t nfs = 0, nft = 0;
+      for (const KPoint& kp : a->h_points) {
+        uint64_t* tp = a->h_terms.data() + kp.term_begin + 1;
+        for (uint32_t k = 0; k < kp.n_sig; ++k, ++tp) {
+          const uint32_t f = (uint32_t)(*tp >> 48);
+          if (sslot[f] == 0xFFFFu) sslot[f] = nfs++;
+          *tp = (*tp & ((1ULL << 48) - 1)) | ((uint64_t)sslot[f] << 48);
+        }
+        for (uint32_t k = 0; k < kp.n_tmpl; ++k, ++tp) {
+          const uint32_t f = (uint32_t)(*tp >> 48);
+          if (tslot[f] == 0xFFFFFFFFu) tslot[f] = nft++;
+          *tp = (*tp & ((1ULL << 48) - 1)) | ((uint64_t)tslot[f] << 48);
+        }
+      }
+      for (size_t q = 0; q < NS; ++q) a->h_sig_mr[q] = (a->h_sig_mr[q] & ~0xFFFF0000ULL) | ((uint64_t)sslot[q] << 16);
+      for (size_t q = 0; q < NT; ++q) a->h_tmpl[q].fslot = tslot[q];
+      a->dt.n_fsig = (int32_t)nfs;
+      a->dt.n_ftmpl = (int32_t)nft;
     }
     if (getenv("TOAST_DEBUG"))
       fprintf(stderr, "[toast] ops %d loops %lld signatures %zu templates %zu frontier points %zu terms %zu actions %zu desel classes %zu\n",

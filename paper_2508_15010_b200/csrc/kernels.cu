@@ -60,21 +60,25 @@ __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
 //      the table is written)
 //   B  the per-color event lists [n_acolors][32] (decode/materialise), then,
 //      per warp, the payload/count accumulators and the segment results
-__host__ __device__ inline int smem_c_bytes() { return 32 * (8 + 8 + 4 + 8 + 16); }
+__host__ __device__ inline int smem_c_bytes(int n_axes) { return 32 * (8 + 8 + 4 + 8 + 4 * n_axes); }
 __host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes) {
   int a1 = n_sigs * 32 * sig_entry_bytes(n_axes), a2 = 2048 + n_words * 128;
   return r16(a1 > a2 ? a1 : a2);
 }
-__host__ __device__ inline int smem_acc_bytes(int n_axes) { return n_axes * 4 * 32 * (8 + 4) + 32 * 5 * 8; }
+// per warp: payload/count accumulators, plus the segment results when K > 1
+__host__ __device__ inline int smem_acc_bytes(int n_axes, int K) {
+  return n_axes * 4 * 32 * (8 + 4) + (K > 1 ? 32 * 5 * 8 : 0);
+}
 __host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
-  int b1 = n_ac * 128, b2 = K * smem_acc_bytes(n_axes);
+  int b1 = n_ac * 128, b2 = K * smem_acc_bytes(n_axes, K);
   return r16(b1 > b2 ? b1 : b2);
 }
-__host__ __device__ inline int smem_d_bytes(int n_tmpl) { return r16(n_tmpl * 32); }
-__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_tmpl,
-                                                int n_mc) {
-  return smem_c_bytes() + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) + smem_d_bytes(n_tmpl) +
-         r16(n_sigs * 32) + r16(n_mc * 64);
+__host__ __device__ inline int smem_d_bytes(int n_ftmpl) { return r16(n_ftmpl * 32); }
+// n_ftmpl / n_fsig: the templates / signatures the frontier's terms use
+__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_ftmpl,
+                                                int n_mc, int n_fsig) {
+  return smem_c_bytes(n_axes) + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) +
+         smem_d_bytes(n_ftmpl) + r16(n_fsig * 32) + r16(n_mc * 64);
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -117,8 +121,8 @@ struct Smem {               // byte offsets into g_smem
   uint32_t axpos;           // [32] 2-bit axis of every sequence position (u64)
   uint32_t axb;             // [4][32] per mesh axis: bitmap of the positions whose action uses it
   uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
-  uint32_t tb;              // [n_tmpl][32] per edge template: divU | divD << 4 (equal: no temporary)
-  uint32_t pc;              // [n_sigs][32] per signature: division code of the result layout
+  uint32_t tb;              // [n_ftmpl][32] per frontier template: divU | divD << 4 (equal: no temporary)
+  uint32_t pc;              // [n_fsig][32] per frontier signature: division code of the result layout
   uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u16)
 };
 
@@ -129,7 +133,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.status = 512;
   s.axpos = 640;
   s.axb = 896;
-  const uint32_t a = smem_c_bytes();
+  const uint32_t a = smem_c_bytes(T.n_axes);
   s.sig = a;
   s.seq = a;
   s.legal = a + 2048;
@@ -137,8 +141,8 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.acol = b;
   s.acc = b;
   s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
-  s.pc = s.tb + smem_d_bytes(T.n_tmpl);
-  s.mca = s.pc + r16(T.n_sigs * 32);
+  s.pc = s.tb + smem_d_bytes(T.n_ftmpl);
+  s.mca = s.pc + r16(T.n_fsig * 32);
   return s;
 }
 
@@ -196,8 +200,7 @@ template <int NA> __device__ __forceinline__ uint32_t e_a2r16(uint32_t e) {
 __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
                                            uint64_t& ones, uint64_t& axpos) {
   for (int c = 0; c < T.n_acolors; ++c) sp<uint32_t>(S.acol)[c * 32 + lane] = 0u;
-#pragma unroll
-  for (int A = 0; A < 4; ++A) sp<uint32_t>(S.axb)[A * 32 + lane] = 0u;
+  for (int A = 0; A < T.n_axes; ++A) sp<uint32_t>(S.axb)[A * 32 + lane] = 0u;
   uint32_t status = 0;
   bool stopped = false;
   uint64_t fx = 0, on = 0, ap = 0;
@@ -504,7 +507,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         nmr = __ldg(T.sig_mr + s + K);
       }
       const uint32_t a2r = sp<uint16_t>(S.mca)[(uint32_t)(mr & 0xFFFF) * 32 + lane];
-      const uint32_t rdm = (uint32_t)(mr >> 32);
+      const uint32_t rdm = (uint32_t)(mr >> 32);   // (bits 16-31 of the low word: the frontier slot)
       // the state-key terms: every axis's load issued at once (role 15 reads a
       // valid word and is masked out)
       uint64_t kt[NA];
@@ -521,7 +524,8 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       uint32_t present = 0;
 #pragma unroll
       for (int A = 0; A < NA; ++A) present |= (e_dim<NA>(e, A) != 15 ? 1u : 0u) << A;
-      sp<uint8_t>(S.pc)[s * 32 + lane] = (uint8_t)dcode<P2>(T, present);
+      const uint32_t fslot = (uint32_t)(mr >> 16) & 0xFFFF;
+      if (fslot != 0xFFFF) sp<uint8_t>(S.pc)[fslot * 32 + lane] = (uint8_t)dcode<P2>(T, present);
       uint32_t opmask = 0;
 #pragma unroll
       for (int A = 0; A < NA; ++A) {
@@ -538,7 +542,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     }
   }
   block_sync(K);
-  const uint32_t acc = S.acc + (uint32_t)warp * smem_acc_bytes(NA);
+  const uint32_t acc = S.acc + (uint32_t)warp * smem_acc_bytes(NA, K);
   unsigned long long* pay = sp<unsigned long long>(acc);
   uint32_t* cnt = sp<uint32_t>(acc + NA * 4 * 32 * 8);
   unsigned long long* seg = sp<unsigned long long>(acc + NA * 4 * 32 * 12);
@@ -614,7 +618,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       }
       tbv = (uint8_t)(dcode<P2>(T, presU) | (dcode<P2>(T, presD) << 4));
     }
-    sp<uint8_t>(S.tb)[tix * 32 + lane] = tbv;
+    if (t2.y != 0xFFFFFFFFu) sp<uint8_t>(S.tb)[t2.y * 32 + lane] = tbv;
   }
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = rp[q]; cnt[q * 32 + lane] = rc[q]; }
@@ -736,18 +740,20 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   }
   }
   if (CP) cp_classes<NA, P2>(T, S, K, warp, lane, T.cp_scratch + (size_t)blockIdx.x * (T.n_comm + T.n_comp + T.n_slots) * 32);
-  seg[0 * 32 + lane] = key;
-  seg[1 * 32 + lane] = flo;
-  seg[2 * 32 + lane] = fhi;
-  seg[3 * 32 + lane] = 0ULL;
-  seg[4 * 32 + lane] = peak;
+  if (K > 1) {
+    seg[0 * 32 + lane] = key;
+    seg[1 * 32 + lane] = flo;
+    seg[2 * 32 + lane] = fhi;
+    seg[3 * 32 + lane] = 0ULL;
+    seg[4 * 32 + lane] = peak;
+  }
   block_sync(K);
   if (warp == 0) {
-    // combine the K segments: sums into warp 0's slots, peak by the segment scan
-    key = 0; flo = 0; fhi = 0;
-    unsigned long long pk_all = 0;
-    for (int w = 0; w < K; ++w) {
-      const uint32_t aw = S.acc + (uint32_t)w * smem_acc_bytes(NA);
+    // combine the K warps' sums (into warp 0's slots) and peaks
+    unsigned long long pk_all = peak;
+    if (K > 1) { key = 0; flo = 0; fhi = 0; pk_all = 0; }
+    for (int w = 0; K > 1 && w < K; ++w) {
+      const uint32_t aw = S.acc + (uint32_t)w * smem_acc_bytes(NA, K);
       const unsigned long long* sw = sp<const unsigned long long>(aw + NA * 4 * 32 * 12);
       key += sw[0 * 32 + lane];
       const uint64_t f = sw[1 * 32 + lane];
@@ -1075,7 +1081,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_tmpl, T.n_mc) > dev_smem) {
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_ftmpl, T.n_mc, T.n_fsig) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -1084,7 +1090,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_tmpl, T.n_mc);
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_ftmpl, T.n_mc, T.n_fsig);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
       cudaError_t e = dispatch(T, [&]<int NA, bool P2, bool CP>() {
@@ -1169,7 +1175,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
@@ -1187,7 +1193,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_tmpl, a->dt.n_mc);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig);
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T, [&]<int NA, bool P2, bool CP>() {

@@ -127,7 +127,7 @@ struct KTmpl {           // 24 B
   uint32_t use_dimof;
   uint64_t sum_gbytes;
   uint32_t n_edges;
-  uint32_t pad;
+  uint32_t fslot;        // the template's growth-code slot for the frontier (0xFFFFFFFF: no frontier term uses it)
 };
 // one op signature, 64 B (one warp-uniform 4 x 16-B load): per role its
 // divisibility word, per distinct action color of the signature the roles it
@@ -178,7 +178,7 @@ struct DeviceTables {
   const uint64_t* terms = nullptr;       // per point: constant, then value | feature << 48
   const KUse* spec = nullptr;            // special edges of the points
   const KSig* sigs = nullptr;            // [n_mc] per materialisation class
-  const uint64_t* sig_mr = nullptr;      // [n_sigs] materialisation class | role -> result dim nibbles << 32
+  const uint64_t* sig_mr = nullptr;      // [n_sigs] class | frontier slot << 16 (0xFFFF: none) | result dims << 32
   const uint64_t* sig_key = nullptr;     // [n_sigs][4 axes][8 roles] summed state-key terms (R14)
   const uint64_t* sig_flops = nullptr;   // [n_sigs][2] summed global FLOPs of matmul-class ops (lo, hi)
   const KTmpl* tmpl = nullptr;           // [n_tmpl]
@@ -190,6 +190,7 @@ struct DeviceTables {
   int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
   int32_t n_points, n_mc;
+  int32_t n_fsig, n_ftmpl;  // signatures / templates the frontier terms use (their per-lane code tables)
   int32_t cost_model, n_slots;   // R22: critical path; finish-time slots per candidate
   int32_t n_comm, n_comp;        // R22: edge-duration and compute-time classes
   const uint2* cp = nullptr;     // critical-path stream
