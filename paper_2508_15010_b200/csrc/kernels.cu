@@ -1158,6 +1158,7 @@ void free_tables(toast_analysis* a) {
 // K (warps sweeping one batch): big batches keep K = 1 (throughput); a batch
 // count below one wave spreads each batch over more warps (latency)
 static inline int pick_k(const toast_analysis* a, int64_t batches, const int32_t* occ) {
+  if (a->k_force) return a->k_force;
   const char* fk = getenv("TOAST_FORCE_K");
   int K = a->k_throughput;
   if (!fk && batches < (int64_t)occ[0] * a->n_sms) {
@@ -1212,9 +1213,11 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
 toast_status autotune_k(toast_analysis* a, std::string& err) {
   // (the critical-path variant keeps the occupancy heuristic: its walk runs on one warp per block)
   if (getenv("TOAST_FORCE_K") || a->n_sms <= 0 || a->dt.cost_model == TOAST_COST_CRITICAL_PATH) return TOAST_OK;
+  // each K runs three of its own whole waves (no partial tail), compared by candidates per second
   int occ_max = 0;
-  for (int i = 0, K = 1; i < 4; ++i, K *= 2) occ_max = std::max(occ_max, std::min(a->occ_eval[i], a->occ_roll[i]) * K);
-  const int64_t n = 2 * (int64_t)occ_max * a->n_sms * 32;
+  for (int i = 0, K = 1; i < 4; ++i, K *= 2) occ_max = std::max(occ_max, std::min(a->occ_eval[i], a->occ_roll[i]));
+  const int64_t n_alloc = 3 * (int64_t)occ_max * a->n_sms * 32;
+  const int64_t n = n_alloc;
   void* buf = nullptr;
   TOAST_CUDA(cudaMalloc(&buf, (size_t)n * (64 + 64 + sizeof(toast_cost))));
   TOAST_CUDA(cudaMemset(buf, 0, (size_t)n * 64));
@@ -1230,19 +1233,22 @@ toast_status autotune_k(toast_analysis* a, std::string& err) {
   toast_status st = TOAST_OK;
   for (int i = 0, K = 1; i < 4 && st == TOAST_OK; ++i, K *= 2) {
     if (a->occ_eval[i] < 1 || a->occ_roll[i] < 1) continue;
-    a->k_throughput = K;
+    a->k_force = K;
+    const int64_t nk = 3 * (int64_t)std::min(a->occ_eval[i], a->occ_roll[i]) * a->n_sms * 32;
     float ms = 1e30f;
     for (int rep = 0; rep < 3 && st == TOAST_OK; ++rep) {
       cudaEventRecord(e0, 0);
-      st = launch_rollout(a, d_pre, n, 1, (uint64_t)rep * n, d_seq, d_out, nullptr, err, 1);
+      st = launch_rollout(a, d_pre, nk, 1, (uint64_t)rep * nk, d_seq, d_out, nullptr, err, 1);
       cudaEventRecord(e1, 0);
       cudaEventSynchronize(e1);
       float t = 0.f;
       cudaEventElapsedTime(&t, e0, e1);
       if (rep) ms = std::min(ms, t);   // rep 0 is the warm-up
     }
-    if (ms < best_ms) { best_ms = ms; best_k = K; }
+    const float per = ms / (float)nk;   // time per candidate
+    if (per < best_ms) { best_ms = per; best_k = K; }
   }
+  a->k_force = 0;
   a->k_throughput = st == TOAST_OK ? best_k : keep;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

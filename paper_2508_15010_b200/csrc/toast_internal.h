@@ -270,6 +270,7 @@ struct toast_analysis {
   int32_t eval_blocks = 0, rollout_blocks = 0;
   int32_t occ_eval[4] = {0, 0, 0, 0}, occ_roll[4] = {0, 0, 0, 0};   // blocks per SM for K = 1, 2, 4, 8
   int32_t n_sms = 0, k_throughput = 1;
+  int32_t k_force = 0;   // autotune: every launch uses this K (0: pick)
   void* pipe_stream[2] = {nullptr, nullptr};   // host-buffer path: chunked H2D / kernel / D2H overlap
   // search buffers, kept between searches (a search that finds them in use allocates its own)
   struct SearchPool {
