@@ -728,6 +728,20 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       a->h_sig_flops[q * 2] = (uint64_t)f;
       a->h_sig_flops[q * 2 + 1] = (uint64_t)(f >> 64);
     }
+    // per materialisation class: the signatures share one axis -> role map, so
+    // their state-key terms add per (axis, role) and their FLOP sums share one
+    // exact divisor (every op's FLOPs divide exactly) — the kernels take both
+    // once per class
+    a->h_mc_key.assign(a->h_sigs.size() * 32, 0);
+    a->h_mc_flops.assign(a->h_sigs.size() * 2, 0);
+    for (size_t q = 0; q < NS; ++q) {
+      const size_t c = (size_t)(a->h_sig_mr[q] & 0xFFFF);
+      for (int i = 0; i < 32; ++i) a->h_mc_key[c * 32 + i] += a->h_sig_key[q * 32 + i];
+      unsigned __int128 f = ((unsigned __int128)a->h_mc_flops[c * 2 + 1] << 64) | a->h_mc_flops[c * 2];
+      f += ((unsigned __int128)a->h_sig_flops[q * 2 + 1] << 64) | a->h_sig_flops[q * 2];
+      a->h_mc_flops[c * 2] = (uint64_t)f;
+      a->h_mc_flops[c * 2 + 1] = (uint64_t)(f >> 64);
+    }
     // edge templates (C11): use edges with the same (def signature, use
     // signature, use role->dim map) communicate identically for a candidate;
     // a value used more than once by one op is a "special" edge group, costed

@@ -484,35 +484,41 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     for (int A = 0; A < NA; ++A) axb[A] = sp<uint32_t>(S.axb)[A * 32 + lane];
     // H2a: one materialisation per class (signatures that differ only in
     // their result dims share it): the axis -> role map
-    for (int c = warp; c < T.n_mc; c += K)
-      sp<uint16_t>(S.mca)[c * 32 + lane] = (uint16_t)materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
+    for (int c = warp; c < T.n_mc; c += K) {
+      const uint64_t glo = __ldg(T.mc_flops + 2 * c), ghi = __ldg(T.mc_flops + 2 * c + 1);
+      const uint32_t a2r = materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
+      sp<uint16_t>(S.mca)[c * 32 + lane] = (uint16_t)a2r;
+      // the class's state-key terms (H7, R14; every axis's load issued at once,
+      // role 15 reads a valid word and is masked out) and local FLOPs (H3)
+      uint64_t kt[NA];
+#pragma unroll
+      for (int A = 0; A < NA; ++A) kt[A] = __ldg(T.mc_key + (size_t)c * 32 + A * 8 + ((a2r >> (4 * A)) & 7));
+      uint32_t opmask = 0;
+#pragma unroll
+      for (int A = 0; A < NA; ++A) {
+        const bool on_ = ((a2r >> (4 * A)) & 15) != 15;
+        key += on_ ? kt[A] : 0ULL;
+        opmask |= (on_ ? 1u : 0u) << A;
+      }
+      if (glo | ghi) {
+        const unsigned __int128 f = dv128<P2>(T, ((unsigned __int128)ghi << 64) | glo, opmask);
+        const uint64_t l = (uint64_t)f;
+        flo += l;
+        fhi += (uint64_t)(f >> 64) + ((flo < l) ? 1 : 0);
+      }
+    }
   }
   block_sync(K);
   {
-    // H2b: per signature the entry (axis -> role | axis -> result dim), the
-    // result layout's division code, the state-key terms (H7) and the local
-    // FLOPs (H3) of all its ops
-    // (the next signature's table words are loaded one iteration ahead)
-    uint64_t nglo = 0, nghi = 0, nmr = 0;
-    if (warp < T.n_sigs) {
-      nglo = __ldg(T.sig_flops + 2 * warp);
-      nghi = __ldg(T.sig_flops + 2 * warp + 1);
-      nmr = __ldg(T.sig_mr + warp);
-    }
+    // H2b: per signature the entry (axis -> role | axis -> result dim) and,
+    // for the frontier's signatures, the result layout's division code
+    // (the next signature's table word is loaded one iteration ahead)
+    uint64_t nmr = warp < T.n_sigs ? __ldg(T.sig_mr + warp) : 0;
     for (int s = warp; s < T.n_sigs; s += K) {
-      const uint64_t glo = nglo, ghi = nghi, mr = nmr;
-      if (s + K < T.n_sigs) {
-        nglo = __ldg(T.sig_flops + 2 * (s + K));
-        nghi = __ldg(T.sig_flops + 2 * (s + K) + 1);
-        nmr = __ldg(T.sig_mr + s + K);
-      }
+      const uint64_t mr = nmr;
+      if (s + K < T.n_sigs) nmr = __ldg(T.sig_mr + s + K);
       const uint32_t a2r = sp<uint16_t>(S.mca)[(uint32_t)(mr & 0xFFFF) * 32 + lane];
       const uint32_t rdm = (uint32_t)(mr >> 32);   // (bits 16-31 of the low word: the frontier slot)
-      // the state-key terms: every axis's load issued at once (role 15 reads a
-      // valid word and is masked out)
-      uint64_t kt[NA];
-#pragma unroll
-      for (int A = 0; A < NA; ++A) kt[A] = __ldg(T.sig_key + (size_t)s * 32 + A * 8 + ((a2r >> (4 * A)) & 7));
       uint32_t dims = 0;
 #pragma unroll
       for (int A = 0; A < 4; ++A) {
@@ -521,23 +527,12 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       }
       const uint32_t e = pack_entry<NA>(a2r | (dims << 16));
       ent_store<NA>(S, s, lane, e);
-      uint32_t present = 0;
-#pragma unroll
-      for (int A = 0; A < NA; ++A) present |= (e_dim<NA>(e, A) != 15 ? 1u : 0u) << A;
       const uint32_t fslot = (uint32_t)(mr >> 16) & 0xFFFF;
-      if (fslot != 0xFFFF) sp<uint8_t>(S.pc)[fslot * 32 + lane] = (uint8_t)dcode<P2>(T, present);
-      uint32_t opmask = 0;
+      if (fslot != 0xFFFF) {
+        uint32_t present = 0;
 #pragma unroll
-      for (int A = 0; A < NA; ++A) {
-        const bool on = ((a2r >> (4 * A)) & 15) != 15;
-        key += on ? kt[A] : 0ULL;
-        opmask |= (on ? 1u : 0u) << A;
-      }
-      if (glo | ghi) {
-        const unsigned __int128 f = dv128<P2>(T, ((unsigned __int128)ghi << 64) | glo, opmask);
-        const uint64_t l = (uint64_t)f;
-        flo += l;
-        fhi += (uint64_t)(f >> 64) + ((flo < l) ? 1 : 0);
+        for (int A = 0; A < NA; ++A) present |= (e_dim<NA>(e, A) != 15 ? 1u : 0u) << A;
+        sp<uint8_t>(S.pc)[fslot * 32 + lane] = (uint8_t)dcode<P2>(T, present);
       }
     }
   }
@@ -1063,10 +1058,10 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   T.sigs = reinterpret_cast<const KSig*>(p);
   if ((st = upload(a, a->h_sig_mr, &p, err))) return st;
   T.sig_mr = reinterpret_cast<const uint64_t*>(p);
-  if ((st = upload(a, a->h_sig_key, &p, err))) return st;
-  T.sig_key = reinterpret_cast<const uint64_t*>(p);
-  if ((st = upload(a, a->h_sig_flops, &p, err))) return st;
-  T.sig_flops = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_mc_key, &p, err))) return st;
+  T.mc_key = reinterpret_cast<const uint64_t*>(p);
+  if ((st = upload(a, a->h_mc_flops, &p, err))) return st;
+  T.mc_flops = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_tmpl, &p, err))) return st;
   T.tmpl = reinterpret_cast<const KTmpl*>(p);
   if ((st = upload(a, a->h_desel_cls, &p, err))) return st;
@@ -1207,16 +1202,17 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
 
 // Throughput K (warps sharing one batch of 32 candidates): measured, not
 // guessed.  Each K with resident blocks runs the rollout kernel on the same
-// multi-wave batch of empty prefixes (CUDA events, best of 2 after a warm-up)
+// multi-wave batch of empty prefixes (CUDA events, best of 5 after a warm-up)
 // and the fastest becomes the analysis' k_throughput.  Results never depend
 // on K — only the speed does.  TOAST_FORCE_K overrides.
 toast_status autotune_k(toast_analysis* a, std::string& err) {
   // (the critical-path variant keeps the occupancy heuristic: its walk runs on one warp per block)
   if (getenv("TOAST_FORCE_K") || a->n_sms <= 0 || a->dt.cost_model == TOAST_COST_CRITICAL_PATH) return TOAST_OK;
-  // each K runs three of its own whole waves (no partial tail), compared by candidates per second
+  // each K runs eight of its own whole waves (no partial tail; about the
+  // bench's 2^18 rollouts), compared by candidates per second
   int occ_max = 0;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) occ_max = std::max(occ_max, std::min(a->occ_eval[i], a->occ_roll[i]));
-  const int64_t n_alloc = 3 * (int64_t)occ_max * a->n_sms * 32;
+  const int64_t n_alloc = 8 * (int64_t)occ_max * a->n_sms * 32;
   const int64_t n = n_alloc;
   void* buf = nullptr;
   TOAST_CUDA(cudaMalloc(&buf, (size_t)n * (64 + 64 + sizeof(toast_cost))));
@@ -1234,9 +1230,9 @@ toast_status autotune_k(toast_analysis* a, std::string& err) {
   for (int i = 0, K = 1; i < 4 && st == TOAST_OK; ++i, K *= 2) {
     if (a->occ_eval[i] < 1 || a->occ_roll[i] < 1) continue;
     a->k_force = K;
-    const int64_t nk = 3 * (int64_t)std::min(a->occ_eval[i], a->occ_roll[i]) * a->n_sms * 32;
+    const int64_t nk = 8 * (int64_t)std::min(a->occ_eval[i], a->occ_roll[i]) * a->n_sms * 32;
     float ms = 1e30f;
-    for (int rep = 0; rep < 3 && st == TOAST_OK; ++rep) {
+    for (int rep = 0; rep < 6 && st == TOAST_OK; ++rep) {
       cudaEventRecord(e0, 0);
       st = launch_rollout(a, d_pre, nk, 1, (uint64_t)rep * nk, d_seq, d_out, nullptr, err, 1);
       cudaEventRecord(e1, 0);

@@ -179,8 +179,8 @@ struct DeviceTables {
   const KUse* spec = nullptr;            // special edges of the points
   const KSig* sigs = nullptr;            // [n_mc] per materialisation class
   const uint64_t* sig_mr = nullptr;      // [n_sigs] class | frontier slot << 16 (0xFFFF: none) | result dims << 32
-  const uint64_t* sig_key = nullptr;     // [n_sigs][4 axes][8 roles] summed state-key terms (R14)
-  const uint64_t* sig_flops = nullptr;   // [n_sigs][2] summed global FLOPs of matmul-class ops (lo, hi)
+  const uint64_t* mc_key = nullptr;      // [n_mc][4 axes][8 roles] summed state-key terms (R14)
+  const uint64_t* mc_flops = nullptr;    // [n_mc][2] summed global FLOPs of matmul-class ops (lo, hi)
   const KTmpl* tmpl = nullptr;           // [n_tmpl]
   const uint64_t* desel = nullptr;       // [class][2] = need0, need1 (class 0 = none)
   const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
@@ -253,6 +253,7 @@ struct toast_analysis {
   std::vector<uint8_t> h_sig_nroles;
   std::vector<uint32_t> h_sig_resdim;
   std::vector<uint64_t> h_sig_key, h_sig_flops;
+  std::vector<uint64_t> h_mc_key, h_mc_flops;   // the same summed per materialisation class (uploaded)
   std::vector<toast::KTmpl> h_tmpl;
   std::vector<uint32_t> op_sig;
   std::vector<int32_t> axis_size;
