@@ -331,6 +331,20 @@ def variant_cp(args, cfg, local, stream, flush):
             "cost_model": "critical path (DESIGN.md reading R22)", "finish_slots": a.kernel_tables().get("n_slots")}
 
 
+def issue_view(prof, n, ms, sm_max_mhz):
+    """The instruction-issue view of the same launch: warp instructions per
+    evaluation from the committed ncu capture (same config, same launch size
+    and K) x this run's evaluations/s, against 148 SMs x 4 schedulers x 1
+    warp-instruction per clock."""
+    if not prof or not prof.get("warp_inst_executed") or not prof.get("evals_per_launch"):
+        return None
+    per_eval = prof["warp_inst_executed"] / prof["evals_per_launch"]
+    achieved = per_eval * n / (ms / 1000.0) / 1e9
+    peak = 148 * 4 * sm_max_mhz * 1e6 / 1e9
+    return {"warp_inst_per_eval": per_eval, "achieved": achieved, "peak": peak, "unit": "G warp-inst/s",
+            "frac": achieved / peak, "ncu_issue_active_pct": prof.get("issue_active_pct")}
+
+
 def run_toast(args, cfg, rank, world, local):
     import numpy as np
     import torch
@@ -432,6 +446,7 @@ def run_toast(args, cfg, rank, world, local):
                                  "peak_gbs": float(peaks.get("hbm_gbs", 6450.0)),
                                  "frac": 384 * (N / (ms_local / 1000.0)) / 1e9 / float(peaks.get("hbm_gbs", 6450.0))},
                          "ncu": prof,
+                         "issue": issue_view(prof, N, ms_local, sm_max),
                          "note": f"{ops} algorithmic int ops/eval (DESIGN.md Roofline); peak = 148 SMs x 128 INT32 "
                                  f"lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz); traffic = ncu dram bytes of "
                                  f"one launch of this size (profiles/ncu_summary.json)"},

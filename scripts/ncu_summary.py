@@ -44,6 +44,16 @@ out.update({
     "smem_wavefronts": float(M["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][0].replace(",", "")),
     "report": os.path.basename(rep), "round": tag,
 })
+# evaluations in the captured launch: the bench line of the same run (plain_<cfg>.log)
+try:
+    plain = os.path.join(os.path.dirname(rep), f"plain_forced_{cfg}.log")
+    if not os.path.exists(plain):
+        plain = os.path.join(os.path.dirname(rep), f"plain_{cfg}.log")
+    line = json.loads(open(plain).read().strip().splitlines()[-1])
+    out["evals_per_launch"] = line["config"]["rollouts_per_step_per_gpu"]
+    out["warps_per_batch"] = line["config"].get("warps_per_batch")
+except Exception:
+    pass
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 p = os.path.join(ROOT, "profiles", "ncu_summary.json")
 allp = json.load(open(p)) if os.path.exists(p) else {}
