@@ -78,7 +78,7 @@ __host__ __device__ inline int smem_d_bytes(int n_ftmpl) { return r16(n_ftmpl * 
 __host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_ftmpl,
                                                 int n_mc, int n_fsig) {
   return smem_c_bytes(n_axes) + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) +
-         smem_d_bytes(n_ftmpl) + r16(n_fsig * 32) + r16(n_mc * 64);
+         smem_d_bytes(n_ftmpl) + r16(n_fsig * 32) + r16(n_mc * 32 * (n_axes <= 2 ? 1 : 2));
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -123,7 +123,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
   uint32_t tb;              // [n_ftmpl][32] per frontier template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_fsig][32] per frontier signature: division code of the result layout
-  uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u16)
+  uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u8 for <= 2 axes, else u16)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -185,6 +185,18 @@ __device__ __forceinline__ uint32_t ent_load(const Smem& S, uint32_t sig, int la
 template <int NA>
 __device__ __forceinline__ void ent_store(const Smem& S, uint32_t sig, int lane, uint32_t e) {
   sp<typename Ent<NA>::T>(S.sig)[sig * 32 + lane] = (typename Ent<NA>::T)e;
+}
+// a materialisation class's axis -> role map per lane: one byte for meshes of
+// <= 2 axes (the nibbles of absent axes read back as 0xF), else 16 bits
+template <int NA>
+__device__ __forceinline__ uint32_t mca_load(const Smem& S, uint32_t c, int lane) {
+  if (NA <= 2) return 0xFF00u | sp<const uint8_t>(S.mca)[c * 32 + lane];
+  return sp<const uint16_t>(S.mca)[c * 32 + lane];
+}
+template <int NA>
+__device__ __forceinline__ void mca_store(const Smem& S, uint32_t c, int lane, uint32_t a2r) {
+  if (NA <= 2) sp<uint8_t>(S.mca)[c * 32 + lane] = (uint8_t)a2r;
+  else sp<uint16_t>(S.mca)[c * 32 + lane] = (uint16_t)a2r;
 }
 // axis A's role / result dim in an entry (15 = none)
 template <int NA> __device__ __forceinline__ uint32_t e_role(uint32_t e, int A) { return (e >> (4 * A)) & 15; }
@@ -359,7 +371,7 @@ __device__ __forceinline__ void cp_classes(const DeviceTables& T, const Smem& S,
   for (int c = warp; c < T.n_comm; c += K) {
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(T.cp_comm + c));
     const uint32_t de = ent(w.x & 0xFFFF);
-    const uint32_t a2r = sp<uint16_t>(S.mca)[(w.x >> 16) * 32 + lane];
+    const uint32_t a2r = mca_load<NA>(S, w.x >> 16, lane);
     const uint64_t gb = u64of(w.z, w.w);
     uint32_t dimU = 0, dimD = 0, P = 0, presD = 0;
 #pragma unroll
@@ -487,7 +499,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     for (int c = warp; c < T.n_mc; c += K) {
       const uint64_t glo = __ldg(T.mc_flops + 2 * c), ghi = __ldg(T.mc_flops + 2 * c + 1);
       const uint32_t a2r = materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
-      sp<uint16_t>(S.mca)[c * 32 + lane] = (uint16_t)a2r;
+      mca_store<NA>(S, c, lane, a2r);
       // the class's state-key terms (H7, R14; every axis's load issued at once,
       // role 15 reads a valid word and is masked out) and local FLOPs (H3)
       uint64_t kt[NA];
@@ -517,7 +529,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     for (int s = warp; s < T.n_sigs; s += K) {
       const uint64_t mr = nmr;
       if (s + K < T.n_sigs) nmr = __ldg(T.sig_mr + s + K);
-      const uint32_t a2r = sp<uint16_t>(S.mca)[(uint32_t)(mr & 0xFFFF) * 32 + lane];
+      const uint32_t a2r = mca_load<NA>(S, (uint32_t)(mr & 0xFFFF), lane);
       const uint32_t rdm = (uint32_t)(mr >> 32);   // (bits 16-31 of the low word: the frontier slot)
       uint32_t dims = 0;
 #pragma unroll
@@ -565,7 +577,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       n2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K) + 2);
     }
     const uint32_t de = ent_load<NA>(S, t0.x & 0xFFFF, lane);
-    const uint32_t ue = sp<uint16_t>(S.mca)[(t0.x >> 16) * 32 + lane];   // the use class's axis -> role map
+    const uint32_t ue = mca_load<NA>(S, t0.x >> 16, lane);   // the use class's axis -> role map
     const uint32_t use_dimof = t0.y;
     uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
