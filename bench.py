@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--R", type=int, default=256, help="search rollouts per leaf")
     p.add_argument("--cost-model", default="sum", choices=["sum", "cp"],
                    help="runtime model of the timed arm: straight-line sum (G14) or critical path (R22)")
-    p.add_argument("--no-variants", action="store_true", help="skip the critical-path variant measurement")
+    p.add_argument("--no-variants", action="store_true", help="skip the variant measurements (critical path, contraction)")
     return p.parse_args()
 
 
@@ -301,13 +301,10 @@ def profile_summary(config: str):
     return d
 
 
-def variant_cp(args, cfg, local, stream, flush):
-    """SURVEY §8(f) NEXT-2: the same rollout step under the critical-path cost
-    model (reading R22), timed the same way on this GPU (10 steps)."""
+def _variant_rate(args, a, local, stream, flush):
+    """One variant analysis' rollout step, timed like the main line (10 steps, L2 flushed)."""
     import torch
     from paper_2508_15010_b200 import toast as T
-    a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
-                         cuda_device=local, cost_model=T.COST_CRITICAL_PATH)
     wave = a.preferred_batch()
     N = max(wave, (args.n // wave) * wave)
     dev = torch.device("cuda", local)
@@ -327,8 +324,44 @@ def variant_cp(args, cfg, local, stream, flush):
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
     m = statistics.mean(ms)
-    return {"metric": METRIC, "value": N / (m / 1000.0), "unit": UNIT, "ms_per_step": m, "rollouts_per_step": N,
-            "cost_model": "critical path (DESIGN.md reading R22)", "finish_slots": a.kernel_tables().get("n_slots")}
+    return {"metric": METRIC, "value": N / (m / 1000.0), "unit": UNIT, "ms_per_step": m, "rollouts_per_step": N}
+
+
+def variant_cp(args, cfg, local, stream, flush):
+    """SURVEY §8(f) NEXT-2: the same rollout step under the critical-path cost
+    model (reading R22), timed the same way on this GPU (10 steps)."""
+    from paper_2508_15010_b200 import toast as T
+    a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
+                         cuda_device=local, cost_model=T.COST_CRITICAL_PATH)
+    r = _variant_rate(args, a, local, stream, flush)
+    r.update({"cost_model": "critical path (DESIGN.md reading R22)", "finish_slots": a.kernel_tables().get("n_slots")})
+    return r
+
+
+def variant_contraction(args, cfg, local, stream, flush):
+    """conflicts grouped by the graph-contraction heuristic
+    (reading R23) instead of compatibility sets: H0 time, the resulting sets /
+    SetGroups / actions, the rollout step timed the same way, and the best score
+    a single-GPU search reaches with the main line's search budget (seed 0) —
+    the paper's "not produce results that differ significantly"."""
+    from paper_2508_15010_b200 import toast as T
+    t = time.perf_counter()
+    a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
+                         cuda_device=local, grouping=T.GROUP_CONTRACTION)
+    nda_s = time.perf_counter() - t
+    d = a.dump()
+    r = _variant_rate(args, a, local, stream, flush)
+    r.update({"grouping": "graph contraction (DESIGN.md reading R23)", "nda_s": nda_s,
+              "contracted_edges": d["contracted"], "skipped_edges": d["contract_rejected"],
+              "sets": len(d["set_group"]), "setgroups": d["n_groups"], "actions": len(d["actions"]) + 1})
+    if not args.no_search:
+        never = 1 << 30
+        g = T.search(a, T.SearchOptions(seed=0, max_evals=args.search_budget, leaves_per_round=args.L,
+                                        rollouts_per_leaf=args.R, patience=never), stream=stream)
+        r["search_best_score"] = float(g["best"]["score"])
+        r["search_best_seq"] = [int(x) for x in g["best_seq"] if x]
+        r["search_evals"] = int(g["evals"])
+    return r
 
 
 def issue_view(prof, n, ms, sm_max_mhz):
@@ -455,12 +488,16 @@ def run_toast(args, cfg, rank, world, local):
                     "d2h_bytes_per_step": N * (64 + 256)},
         }
     if rank == 0 and not args.no_variants and args.cost_model == "sum":
-        line["variants"] = {"critical_path": variant_cp(args, cfg, local, stream, flush)}
+        line["variants"] = {"critical_path": variant_cp(args, cfg, local, stream, flush),
+                            "contraction": variant_contraction(args, cfg, local, stream, flush)}
     ttb = None
     if not args.no_search:
         ttb = time_to_best_gpu(a, args, rank, world, stream)
         if rank == 0:
             line["time_to_best"] = ttb
+            vc = line.get("variants", {}).get("contraction")
+            if vc and "search_best_score" in vc:
+                vc["compat_sets_best_score"] = ttb["target_score"]   # same budget, seed 0, compatibility sets
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
         if ttb is not None:

@@ -88,13 +88,22 @@ typedef struct {
    G14: compute + every collective, straight-line) or TOAST_COST_CRITICAL_PATH
    (1, reading R22: the latest finish over the op DAG, finish(t) = max over
    operands of (finish(def) + the edge's collective time) + t's compute time).
-   Every other record field is the same under both. */
+   Every other record field is the same under both.
+   conflict_grouping: how conflicts are grouped into sets whose resolution is
+   decided together — TOAST_GROUP_COMPAT (0, §3.5: the closure of
+   the "compatible conflicts" box relation) or
+   TOAST_GROUP_CONTRACTION (1, the dimension-graph contraction heuristic of
+   the [comment] block P:1346-1357, reading R23: eagerly contract
+   M edges unless a directed path would join the two endpoints of a
+   conflict; conflicts on the same pair of contracted nodes form one set).
+   Any other value: TOAST_E_INVALID_ARG. */
 enum { TOAST_COST_SUM = 0, TOAST_COST_CRITICAL_PATH = 1 };
+enum { TOAST_GROUP_COMPAT = 0, TOAST_GROUP_CONTRACTION = 1 };
 typedef struct {
   int32_t min_unique_dims;
   int32_t max_depth;
   int32_t cost_model;
-  int32_t reserved;      /* 0 */
+  int32_t conflict_grouping;
 } toast_nda_opts;
 
 typedef struct toast_graph toast_graph;        /* opaque, library-owned */

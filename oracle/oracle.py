@@ -58,7 +58,7 @@ def lib():
         L = _lib
         L.orc_new.restype = ctypes.c_void_p
         L.orc_new.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_double, ctypes.c_uint64,
-                              ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+                              ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.orc_last_error.restype = ctypes.c_char_p
         L.orc_free.argtypes = [ctypes.c_void_p]
         for f in ("orc_n_actions", "orc_n_loops", "orc_n_ops"):
@@ -81,6 +81,7 @@ def lib():
         L.orc_def_loop.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         for f in ("orc_n_names", "orc_n_identities", "orc_n_map"):
             getattr(L, f).argtypes = [ctypes.c_void_p]
+        L.orc_edges.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         L.orc_search.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_double,
                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
@@ -100,13 +101,14 @@ def mesh_spec(axes) -> str:
 
 class Oracle:
     def __init__(self, ir: str, axes, flops_per_sec: float, dm: int, penalty_c: float = 100.0,
-                 min_dims: int = 10, max_depth: int = 30, cost_model: int = 0):
-        """cost_model: 0 = straight-line sum (reading G14), 1 = critical path (reading R22)."""
+                 min_dims: int = 10, max_depth: int = 30, cost_model: int = 0, grouping: int = 0):
+        """cost_model: 0 = straight-line sum (reading G14), 1 = critical path (reading R22).
+        grouping: 0 = compatibility sets (C4/C5), 1 = graph contraction heuristic (reading R23)."""
         L = lib()
         self.axes = list(axes)
         self.max_depth = max_depth
         h = L.orc_new(ir.encode(), mesh_spec(axes).encode(), float(flops_per_sec), int(dm),
-                      float(penalty_c), int(min_dims), int(max_depth), int(cost_model))
+                      float(penalty_c), int(min_dims), int(max_depth), int(cost_model), int(grouping))
         if not h:
             raise OracleError(L.orc_last_error().decode())
         self.h = ctypes.c_void_p(h)
@@ -133,6 +135,14 @@ class Oracle:
 
     def def_loop(self, t: int, i: int) -> int:
         return lib().orc_def_loop(self.h, t, i)
+
+    def edges(self) -> np.ndarray:
+        """The deduplicated M edges over loops (C1): int32[n][2] (def loop, use loop)."""
+        L = lib()
+        n = L.orc_edges(self.h, None, 0)
+        e = np.zeros((max(n, 1), 2), np.int32)
+        L.orc_edges(self.h, e.ctypes.data, n)
+        return e[:n]
 
     def nda_sizes(self):
         L = lib()

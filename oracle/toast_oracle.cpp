@@ -14,7 +14,10 @@
 //   C1–C5, C9–C14 pinned by paper worked examples / closed forms / invariants /
 //   brute force; C15 pinned by Philox KAT vectors; C6 (WL signatures), C7
 //   (argument keys) and C8 (action table order) are "parity unpinned" beyond
-//   the structural invariants in tests/test_oracle_pins.py.
+//   the structural invariants in tests/test_oracle_pins.py.  The contraction
+//   heuristic (reading R23, NEXT-4) is pinned by the paper's box / incompatible
+//   listings, by "all conflicts of the attention layer
+//   compatible" and by brute-force path checks on random programs.
 //
 // Build: g++ -O2 -std=c++17 -ffp-contract=off -fPIC -shared -pthread
 // =============================================================================
@@ -692,6 +695,7 @@ struct Oracle {
   double F = 1e12; u64 DM = 0; double C = 100.0;
   int min_dims = 10, max_depth = 30;
   int cost_model = 0;   // 0: straight-line sum (G14); 1: critical path (reading R22)
+  int grouping = 0;     // 0: compatibility sets (C4/C5); 1: graph contraction heuristic (reading R23)
 
   std::vector<Loop> loops;
   std::vector<int> op_loop_begin;                       // loops of op t: [begin[t], begin[t+1])
@@ -704,6 +708,8 @@ struct Oracle {
   std::vector<Box> boxes;                               // candidate boxes in canonical order
   std::vector<int> box_accepted;
   int dropped_boxes = 0;
+  std::vector<int> cnode;                               // R23: contracted node of each loop (smallest member)
+  int contracted = 0, contract_rejected = 0;            // R23: edges contracted / skipped
   std::vector<int> conf_set, conf_side0;
   std::vector<int> set_root;                            // smallest conflict per set
   std::vector<u64> set_sig;
@@ -763,8 +769,12 @@ struct Oracle {
     comp.resize(loops.size());
     for (size_t l = 0; l < loops.size(); l++) comp[l] = cu.find((int)l);   // smallest member (unite keeps min root)
     find_conflicts();
-    find_boxes();
-    build_sets();
+    if (grouping == 0) {
+      find_boxes();
+      build_sets();
+    } else {
+      build_sets_contraction();
+    }
     build_groups();
     build_supercolors();
     build_actions();
@@ -904,6 +914,73 @@ struct Oracle {
     }
   }
 
+  // NEXT-4 (reading R23): the dimension-graph contraction heuristic
+  // ([comment] §3.5): "Eagerly contract edges in the dimension
+  // graph unless this produces a (directed) path between two nodes that
+  // participate in a conflict."  Edges are taken once each in canonical
+  // (def loop, use loop) order (contraction only adds paths, so a skipped edge
+  // stays skipped and one pass is the fixpoint).  A contraction is skipped when,
+  // in the contracted graph, the two endpoints of some conflict would share a
+  // node or one would reach the other.  "Both vertical edges will be
+  // contracted, which amounts to identifying the conflicts at the top and
+  // bottom of the box as compatible": conflicts whose endpoints
+  // land on the same pair of contracted nodes form one set; side 0 of a
+  // conflict is its endpoint in the node of the set's smallest conflict's u.
+  // Contraction never joins components, so a conflict can only acquire a path
+  // through an edge of its own component: only those conflicts are checked.
+  bool contracted_conflict_path(UF& t, int component) {
+    std::map<int, std::set<int>> adj;   // contracted graph of the component
+    for (auto& e : edges) {
+      if (comp[e.first] != component) continue;
+      int a = t.find(e.first), b = t.find(e.second);
+      if (a != b) adj[a].insert(b);
+    }
+    for (auto& c : conflicts) {
+      if (comp[c.u] != component) continue;
+      int U = t.find(c.u), V = t.find(c.v);
+      if (U == V) return true;
+      for (int dir = 0; dir < 2; dir++) {   // U ~> V, then V ~> U (breadth-first)
+        int src = dir == 0 ? U : V, dst = dir == 0 ? V : U;
+        std::set<int> seen{src};
+        std::deque<int> q{src};
+        while (!q.empty()) {
+          int x = q.front(); q.pop_front();
+          if (x == dst) return true;
+          for (int y : adj[x]) if (seen.insert(y).second) q.push_back(y);
+        }
+      }
+    }
+    return false;
+  }
+  void build_sets_contraction() {
+    UF g((int)loops.size());
+    for (auto& e : edges) {                 // std::set order: (def loop, use loop) ascending
+      if (g.find(e.first) == g.find(e.second)) continue;
+      UF trial = g;
+      trial.unite(e.first, e.second);
+      if (contracted_conflict_path(trial, comp[e.first])) { contract_rejected++; continue; }
+      g = trial;
+      contracted++;
+    }
+    cnode.resize(loops.size());
+    for (size_t l = 0; l < loops.size(); l++) cnode[l] = g.find((int)l);   // unite keeps the smallest member
+    // sets: conflicts on the same unordered pair of contracted nodes, numbered by smallest conflict
+    int n = (int)conflicts.size();
+    std::map<std::pair<int, int>, int> pair_set;
+    conf_set.assign(n, -1); conf_side0.assign(n, -1);
+    for (int i = 0; i < n; i++) {
+      int U = cnode[conflicts[i].u], V = cnode[conflicts[i].v];
+      std::pair<int, int> key{std::min(U, V), std::max(U, V)};
+      if (!pair_set.count(key)) {
+        pair_set[key] = (int)set_root.size();
+        set_root.push_back(i);
+      }
+      conf_set[i] = pair_set[key];
+      int root_u = cnode[conflicts[set_root[conf_set[i]]].u];
+      conf_side0[i] = cnode[conflicts[i].u] == root_u ? conflicts[i].u : conflicts[i].v;
+    }
+  }
+
   // C6: SetGroups — isomorphic sets across layers (§3.6), 3-round WL
   void build_groups() {
     int ns = (int)set_root.size();
@@ -925,9 +1002,16 @@ struct Oracle {
         conf_edges.insert({cf.u, cf.v});
       }
       std::set<std::pair<int, int>> m_edges;
-      for (int bi : set_boxes[s]) {
-        m_edges.insert({boxes[bi].N, boxes[bi].L});
-        m_edges.insert({boxes[bi].O, boxes[bi].R});
+      if (grouping == 0) {
+        for (int bi : set_boxes[s]) {
+          m_edges.insert({boxes[bi].N, boxes[bi].L});
+          m_edges.insert({boxes[bi].O, boxes[bi].R});
+        }
+      } else {
+        // R23: the contracted M edges between the set's endpoints (the analogue of its boxes' vertical edges)
+        for (auto& e : edges)
+          if (sidemask.count(e.first) && sidemask.count(e.second) && cnode[e.first] == cnode[e.second])
+            m_edges.insert(e);
       }
       std::map<int, u64> label;
       for (auto& kv : sidemask) {
@@ -1464,7 +1548,7 @@ const char* orc_last_error() { return g_err.c_str(); }
 
 // axes: "name=size:bw,name=size:bw"
 void* orc_new(const char* ir, const char* mesh, double F, uint64_t DM, double C, int min_dims, int max_depth,
-              int cost_model) {
+              int cost_model, int grouping) {
   try {
     auto* O = new Oracle();
     std::string ms(mesh);
@@ -1486,6 +1570,8 @@ void* orc_new(const char* ir, const char* mesh, double F, uint64_t DM, double C,
     O->F = F; O->DM = DM; O->C = C; O->min_dims = min_dims; O->max_depth = max_depth;
     if (cost_model != 0 && cost_model != 1) throw OracleError("E_INVALID_ARG", "cost_model must be 0 or 1");
     O->cost_model = cost_model;
+    if (grouping != 0 && grouping != 1) throw OracleError("E_INVALID_ARG", "grouping must be 0 or 1");
+    O->grouping = grouping;
     O->M = parse_module(ir);
     O->build();
     return O;
@@ -1559,6 +1645,16 @@ int orc_def_loop(void* h, int t, int i) { Oracle* O = (Oracle*)h; return O->def_
 int orc_n_names(void* h) { return ((Oracle*)h)->nda.n_names; }
 int orc_n_identities(void* h) { return (int)((Oracle*)h)->nda.I.size(); }
 int orc_n_map(void* h) { return (int)((Oracle*)h)->nda.M.size(); }
+// the deduplicated M edges over loops (C1), as (def loop, use loop) pairs in canonical order; returns the count
+int orc_edges(void* h, int* out, int cap) {
+  Oracle* O = (Oracle*)h;
+  int n = 0;
+  for (auto& e : O->edges) {
+    if (n < cap) { out[2 * n] = e.first; out[2 * n + 1] = e.second; }
+    n++;
+  }
+  return n;
+}
 
 void orc_philox(const uint32_t* ctr, const uint32_t* key, uint32_t* out) { philox4x32_10(ctr, key, out); }
 
@@ -1587,6 +1683,12 @@ int64_t orc_dump(void* h, char* buf, int64_t cap) {
     s += "[" + num(C.op) + "," + num(C.u) + "," + num(C.v) + "," + num(O->conf_set[c]) + "," + num(O->conf_side0[c]) + "]";
   }
   s += "],\"n_boxes\":" + num(O->boxes.size()) + ",\"dropped_boxes\":" + num(O->dropped_boxes);
+  s += ",\"contracted\":" + num(O->contracted) + ",\"contract_rejected\":" + num(O->contract_rejected);
+  if (O->grouping == 1) {
+    s += ",\"cnode\":[";
+    for (size_t l = 0; l < O->cnode.size(); l++) { if (l) s += ","; s += num(O->cnode[l]); }
+    s += "]";
+  }
   s += ",\"set_group\":[";
   for (size_t i = 0; i < O->set_group.size(); i++) { if (i) s += ","; s += num(O->set_group[i]); }
   s += "],\"set_sig\":[";

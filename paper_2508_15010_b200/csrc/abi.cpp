@@ -84,6 +84,8 @@ toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_anal
     return fail(TOAST_E_INVALID_ARG, "min_unique_dims must be >= 0 and max_depth in [1, 32]");
   if (o->cost_model != TOAST_COST_SUM && o->cost_model != TOAST_COST_CRITICAL_PATH)
     return fail(TOAST_E_INVALID_ARG, "cost_model must be TOAST_COST_SUM or TOAST_COST_CRITICAL_PATH");
+  if (o->conflict_grouping != TOAST_GROUP_COMPAT && o->conflict_grouping != TOAST_GROUP_CONTRACTION)
+    return fail(TOAST_E_INVALID_ARG, "conflict_grouping must be TOAST_GROUP_COMPAT or TOAST_GROUP_CONTRACTION");
   toast_analysis* a = new (std::nothrow) toast_analysis();
   if (!a) return fail(TOAST_E_OOM, "out of host memory");
   std::string err;

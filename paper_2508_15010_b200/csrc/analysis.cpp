@@ -180,6 +180,148 @@ OpLoops loops_of(const toast_graph* g, const GOp& op) {
 
 inline bool is_matmul_class(OpKind k) { return k == OK_MATMUL || k == OK_DOT || k == OK_CONV || k == OK_CONV_BI || k == OK_CONV_BF; }
 
+
+// NEXT-4, reading R23: the dimension-graph contraction heuristic
+// ([comment] §3.5) — "eagerly contract edges in the dimension graph
+// unless this produces a (directed) path between two nodes that participate in
+// a conflict".  M edges are taken once each in (def loop, use loop) order.
+// Per contracted node of a component with conflicts, bitsets over the conflict
+// endpoints: A = endpoints reaching it, D = endpoints it reaches (both including
+// its own members), PA = the conflict partners of A.  Merging X and Y creates
+// exactly the new paths through the merged node, so it joins a conflict iff
+// (PA(X) | PA(Y)) & (D(X) | D(Y)) != 0.  After a merge the merged A / D are
+// pushed to the node's descendants / ancestors; a node that already contains
+// them stops the push (A only grows along edges, D only against them).
+// Conflicts on the same unordered pair of contracted nodes form one set
+// (contracting both vertical edges of a box identifies its
+// conflicts as compatible), side 0 = the endpoint in the node of the set's
+// smallest conflict's u.  The WL hash (C6) sees the contracted M edges between
+// the set's endpoints.
+static void build_contraction_sets(toast_analysis* a, int64_t NL, const std::vector<uint64_t>& ekeys,
+                                   const std::vector<int64_t>& out_off, const std::vector<int32_t>& out_dst,
+                                   const std::vector<int32_t>& ep_index, int32_t NE, const std::vector<uint64_t>& reach,
+                                   const std::vector<int64_t>& reach_off, int32_t& n_sets,
+                                   std::vector<std::vector<std::pair<int32_t, int32_t>>>& set_medges) {
+  const size_t W = (size_t)(NE + 63) / 64;
+  const int32_t NC = (int32_t)a->conflicts.size();
+  auto bit = [](uint64_t* b, int32_t i) { b[i >> 6] |= 1ULL << (i & 63); };
+  std::vector<uint64_t> partner((size_t)NE * W, 0);
+  for (const auto& c : a->conflicts) {
+    bit(&partner[(size_t)ep_index[c.u] * W], ep_index[c.v]);
+    bit(&partner[(size_t)ep_index[c.v] * W], ep_index[c.u]);
+  }
+  int64_t nreach = 0;
+  for (int64_t l = 0; l < NL; ++l) if (reach_off[l] >= 0) nreach = std::max(nreach, reach_off[l] + 1);
+  std::vector<uint64_t> A((size_t)nreach * W, 0), D((size_t)nreach * W, 0), PA((size_t)nreach * W, 0);
+  auto row = [&](std::vector<uint64_t>& v, int32_t l) { return &v[(size_t)reach_off[l] * W]; };
+  // contracted adjacency (loop ids, resolved through the DSU when read)
+  std::vector<std::vector<int32_t>> gout(NL), gin(NL);
+  for (uint64_t e : ekeys) {
+    const int32_t x = (int32_t)(e >> 32), y = (int32_t)(uint32_t)e;
+    if (reach_off[x] < 0) continue;
+    gout[x].push_back(y);
+    gin[y].push_back(x);
+  }
+  // initial A / PA in loop order (every M edge goes from a lower to a higher loop id), D = reach + itself
+  for (int64_t l = 0; l < NL; ++l) {
+    if (reach_off[l] < 0) continue;
+    uint64_t *al = row(A, (int32_t)l), *pl = row(PA, (int32_t)l), *dl = row(D, (int32_t)l);
+    const uint64_t* rl = &reach[(size_t)reach_off[l] * W];
+    for (size_t w = 0; w < W; ++w) dl[w] = rl[w];
+    if (ep_index[l] >= 0) {
+      bit(al, ep_index[l]);
+      bit(dl, ep_index[l]);
+      const uint64_t* pp = &partner[(size_t)ep_index[l] * W];
+      for (size_t w = 0; w < W; ++w) pl[w] |= pp[w];
+    }
+    for (int32_t p : gin[l]) {
+      const uint64_t *ap = row(A, p), *ppa = row(PA, p);
+      for (size_t w = 0; w < W; ++w) { al[w] |= ap[w]; pl[w] |= ppa[w]; }
+    }
+  }
+  DSU cg(NL);
+  std::vector<int32_t> stack;
+  auto merge_adj = [&](std::vector<int32_t>& into, std::vector<int32_t>& from, int32_t z) {
+    for (int32_t v : from) into.push_back(v);
+    std::vector<int32_t>().swap(from);
+    for (int32_t& v : into) v = cg.root(v);
+    std::sort(into.begin(), into.end());
+    into.erase(std::unique(into.begin(), into.end()), into.end());
+    into.erase(std::remove(into.begin(), into.end(), z), into.end());
+  };
+  auto push = [&](std::vector<uint64_t>& S, std::vector<uint64_t>* S2, std::vector<std::vector<int32_t>>& adj, int32_t z) {
+    const uint64_t* sz = row(S, z);
+    const uint64_t* sz2 = S2 ? row(*S2, z) : nullptr;
+    stack.assign(adj[z].begin(), adj[z].end());
+    while (!stack.empty()) {
+      const int32_t w = cg.root(stack.back());
+      stack.pop_back();
+      if (w == z) continue;
+      uint64_t* sw = row(S, w);
+      bool sub = true;
+      for (size_t q = 0; q < W && sub; ++q) sub = (sz[q] & ~sw[q]) == 0;
+      if (sub) continue;
+      for (size_t q = 0; q < W; ++q) sw[q] |= sz[q];
+      if (S2) { uint64_t* s2 = row(*S2, w); for (size_t q = 0; q < W; ++q) s2[q] |= sz2[q]; }
+      for (int32_t v : adj[w]) stack.push_back(v);
+    }
+  };
+  for (uint64_t e : ekeys) {
+    const int32_t x0 = (int32_t)(e >> 32), y0 = (int32_t)(uint32_t)e;
+    const int32_t x = cg.root(x0), y = cg.root(y0);
+    if (x == y) continue;
+    if (reach_off[x0] < 0) { cg.join(x, y); a->contracted++; continue; }   // no conflict in this component
+    {
+      const uint64_t *ax = row(PA, x), *ay = row(PA, y), *dx = row(D, x), *dy = row(D, y);
+      bool joins = false;
+      for (size_t q = 0; q < W && !joins; ++q) joins = ((ax[q] | ay[q]) & (dx[q] | dy[q])) != 0;
+      if (joins) { a->contract_rejected++; continue; }
+    }
+    const int32_t z = std::min(x, y), o2 = std::max(x, y);
+    cg.join(x, y);
+    a->contracted++;
+    {
+      uint64_t *az = row(A, z), *dz = row(D, z), *pz = row(PA, z);
+      const uint64_t *ao = row(A, o2), *dox = row(D, o2), *po = row(PA, o2);
+      for (size_t q = 0; q < W; ++q) { az[q] |= ao[q]; dz[q] |= dox[q]; pz[q] |= po[q]; }
+    }
+    merge_adj(gout[z], gout[o2], z);
+    merge_adj(gin[z], gin[o2], z);
+    push(A, &PA, gout, z);   // descendants are now reached by A(z)
+    push(D, nullptr, gin, z);   // ancestors now reach D(z)
+  }
+  a->cnode.resize(NL);
+  for (int64_t l = 0; l < NL; ++l) a->cnode[l] = cg.root((int32_t)l);
+  // sets
+  std::map<std::pair<int32_t, int32_t>, int32_t> pair_set;
+  std::vector<int32_t> set_first;
+  for (int32_t i = 0; i < NC; ++i) {
+    auto& c = a->conflicts[i];
+    const int32_t U = a->cnode[c.u], V = a->cnode[c.v];
+    auto it = pair_set.emplace(std::make_pair(std::min(U, V), std::max(U, V)), (int32_t)set_first.size());
+    if (it.second) set_first.push_back(i);
+    c.set = it.first->second;
+    c.side0 = U == a->cnode[a->conflicts[set_first[c.set]].u] ? c.u : c.v;
+  }
+  n_sets = (int32_t)set_first.size();
+  set_medges.assign(n_sets, {});
+  std::vector<std::vector<int32_t>> ep_sets(NE);
+  for (int32_t i = 0; i < NC; ++i) {
+    const auto& c = a->conflicts[i];
+    for (int32_t l : {c.u, c.v}) {
+      auto& v = ep_sets[ep_index[l]];
+      if (std::find(v.begin(), v.end(), c.set) == v.end()) v.push_back(c.set);
+    }
+  }
+  for (uint64_t e : ekeys) {
+    const int32_t x = (int32_t)(e >> 32), y = (int32_t)(uint32_t)e;
+    if (ep_index[x] < 0 || ep_index[y] < 0 || a->cnode[x] != a->cnode[y]) continue;
+    for (int32_t sx : ep_sets[ep_index[x]])
+      for (int32_t sy : ep_sets[ep_index[y]])
+        if (sx == sy) set_medges[sx].push_back({x, y});
+  }
+}
+
 }  // namespace
 
 toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast_analysis* a, std::string& err) {
@@ -290,6 +432,12 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     int32_t e = ep_index[to];
     return (reach[(size_t)reach_off[from] * W + (e >> 6)] >> (e & 63)) & 1;
   };
+  a->grouping = o->conflict_grouping;
+  int32_t n_sets = 0;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> set_medges;   // per set: the M edges its WL hash sees (C6)
+  if (o->conflict_grouping == TOAST_GROUP_CONTRACTION) {
+    build_contraction_sets(a, NL, ekeys, out_off, out_dst, ep_index, NE, reach, reach_off, n_sets, set_medges);
+  } else {
   struct BoxRec { int32_t c1, c2, N, O, L, R, parity; };
   std::vector<BoxRec> boxes;
   for (int32_t ci = 0; ci < NC; ++ci) {
@@ -353,7 +501,6 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     if (root_first[croot[i]] < 0) root_first[croot[i]] = i;
   }
   std::vector<int32_t> set_of_root(NC, -1);
-  int32_t n_sets = 0;
   for (int32_t i = 0; i < NC; ++i)
     if (root_first[croot[i]] == i) set_of_root[croot[i]] = n_sets++;
   for (int32_t i = 0; i < NC; ++i) {
@@ -363,18 +510,20 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     c.side0 = (cpar[i] ^ cpar[first]) ? c.v : c.u;
   }
 
+  set_medges.assign(n_sets, {});
+  for (size_t b = 0; b < boxes.size(); ++b) {
+    if (!box_ok[b]) continue;
+    auto& E = set_medges[a->conflicts[boxes[b].c1].set];
+    E.push_back({boxes[b].N, boxes[b].L});
+    E.push_back({boxes[b].O, boxes[b].R});
+  }
+  }   // compatibility sets
+
   // ------------------------------------------------------------ C6 SetGroups (3-round WL)
   a->set_sig.assign(n_sets, 0);
   {
     std::vector<std::vector<int32_t>> set_conf(n_sets);
     for (int32_t i = 0; i < NC; ++i) set_conf[a->conflicts[i].set].push_back(i);
-    std::vector<std::vector<std::pair<int32_t, int32_t>>> set_medges(n_sets);
-    for (size_t b = 0; b < boxes.size(); ++b) {
-      if (!box_ok[b]) continue;
-      auto& E = set_medges[a->conflicts[boxes[b].c1].set];
-      E.push_back({boxes[b].N, boxes[b].L});
-      E.push_back({boxes[b].O, boxes[b].R});
-    }
     for (int32_t s = 0; s < n_sets; ++s) {
       std::map<int32_t, int> side;   // node -> side mask
       std::vector<std::pair<int32_t, int32_t>> cedges;
@@ -1231,7 +1380,14 @@ std::string dump_json(const toast_analysis* a) {
     for (size_t q = 0; q < a->point_op.size(); ++q) { if (q) s += ','; s += I(a->point_op[q]); }
     s += "]}";
   }
-  s += ",\"n_boxes\":" + I(a->n_boxes) + ",\"dropped_boxes\":" + I(a->dropped_boxes) + ",\"set_group\":[";
+  s += ",\"n_boxes\":" + I(a->n_boxes) + ",\"dropped_boxes\":" + I(a->dropped_boxes);
+  s += ",\"contracted\":" + I(a->contracted) + ",\"contract_rejected\":" + I(a->contract_rejected);
+  if (a->grouping == TOAST_GROUP_CONTRACTION) {
+    s += ",\"cnode\":[";
+    for (size_t l = 0; l < a->cnode.size(); ++l) { if (l) s += ','; s += I(a->cnode[l]); }
+    s += "]";
+  }
+  s += ",\"set_group\":[";
   for (size_t i = 0; i < a->set_group.size(); ++i) { if (i) s += ','; s += I(a->set_group[i]); }
   s += "],\"set_sig\":[";
   for (size_t i = 0; i < a->set_sig.size(); ++i) {

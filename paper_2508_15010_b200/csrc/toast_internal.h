@@ -218,6 +218,9 @@ struct toast_analysis {
   struct Conf { int32_t op, u, v, set, side0; };
   std::vector<Conf> conflicts;
   int64_t n_boxes = 0, dropped_boxes = 0;
+  int32_t grouping = 0;                      // TOAST_GROUP_COMPAT / TOAST_GROUP_CONTRACTION (reading R23)
+  int64_t contracted = 0, contract_rejected = 0;
+  std::vector<int32_t> cnode;                // R23: contracted node (smallest member loop) per loop
   std::vector<int32_t> set_group;
   std::vector<uint64_t> set_sig;
   int32_t n_groups = 0;

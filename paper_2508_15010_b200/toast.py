@@ -58,10 +58,11 @@ class _Machine(ctypes.Structure):
 
 class _NdaOpts(ctypes.Structure):
     _fields_ = [("min_unique_dims", ctypes.c_int32), ("max_depth", ctypes.c_int32), ("cost_model", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("conflict_grouping", ctypes.c_int32)]
 
 
 COST_SUM, COST_CRITICAL_PATH = 0, 1
+GROUP_COMPAT, GROUP_CONTRACTION = 0, 1
 
 
 class _ActionInfo(ctypes.Structure):
@@ -238,18 +239,19 @@ class Analysis:
         return self._dump_all()["kernel_tables"]
 
 
-def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30, cost_model: int = COST_SUM) -> Analysis:
-    """toast_nda (H0)."""
-    o = _NdaOpts(int(min_unique_dims), int(max_depth), int(cost_model), 0)
+def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30, cost_model: int = COST_SUM,
+        grouping: int = GROUP_COMPAT) -> Analysis:
+    """toast_nda (H0).  grouping: GROUP_COMPAT (C4/C5) or GROUP_CONTRACTION (reading R23)."""
+    o = _NdaOpts(int(min_unique_dims), int(max_depth), int(cost_model), int(grouping))
     h = _P()
     _check(_lib.toast_nda(graph._h, ctypes.byref(o), ctypes.byref(h)))
     return Analysis(h, None)
 
 
 def build_analysis(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c=100.0, min_unique_dims=10,
-                   max_depth=30, cuda_device=0, cost_model=COST_SUM) -> Analysis:
+                   max_depth=30, cuda_device=0, cost_model=COST_SUM, grouping=GROUP_COMPAT) -> Analysis:
     g = load_graph(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c, cuda_device)
-    a = nda(g, min_unique_dims, max_depth, cost_model)
+    a = nda(g, min_unique_dims, max_depth, cost_model, grouping)
     a.axes = list(axes)
     return a
 
