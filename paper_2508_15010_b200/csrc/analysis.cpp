@@ -1135,18 +1135,84 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
   a->h_cp_comm.clear();
   a->h_cp_comp.clear();
   if (o->cost_model == TOAST_COST_CRITICAL_PATH) {
-    // finish-time slots: every non-parameter value holds one from its def to
-    // its last use (reused greedily); parameters finish at 0 and need none.
     // Edge durations are shared by every edge of the same communication class
     // (def signature, use materialisation class, use role -> dim map, bytes),
     // compute times by every op of the same (signature, FLOPs) class: the
     // kernels evaluate each class once per candidate.
-    std::vector<uint32_t> slot_of(g->values.size(), NO_SLOT), free_slots;
-    std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint64_t>, uint32_t> comm_id;
-    std::map<std::pair<uint32_t, uint64_t>, uint32_t> comp_id;
+    //
+    // Exact reductions of the max-plus walk (every finish time is >= +0, so
+    // x + 0.0 == x bit for bit):
+    //  * an edge whose def and use ops are of one materialisation class and
+    //    whose every shardable role is the same result / operand dim, with no
+    //    shardable role off the result (no partial sum), never communicates:
+    //    its duration is 0 for every candidate, the walk takes the def's
+    //    finish as is (ZERO_COMM, no class, no add);
+    //  * an op without compute time whose single operand edge is such an edge
+    //    finishes exactly when its operand does: it is elided and its result
+    //    shares the operand's finish (an alias), so it costs nothing per
+    //    candidate and the latest finish is unchanged.
+    // Finish-time slots are then held per alias class, from the def of its
+    // first value to the last use of any of its values (reused greedily);
+    // parameters finish at 0 and need none.
+    auto shardable_roles = [&](uint32_t sig) {
+      uint32_t m = 0;
+      for (int r = 0; r < 8; ++r)
+        if ((a->h_sig_roles[(size_t)sig * 8 + r] & 0x3FF) != NO_ACOLOR) m |= 1u << r;
+      return m;
+    };
+    auto use_dimof = [&](int32_t t, size_t k) {
+      uint32_t um = ~0u;
+      for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
+        uint32_t rr = OL[t].use_role[k][i];
+        um = (um & ~(0xFu << (4 * rr))) | ((uint32_t)i << (4 * rr));
+      }
+      return um;
+    };
+    auto zero_edge = [&](int32_t t, size_t k) {
+      const int32_t d = g->values[g->ops[t].operands[k]].def_op;
+      const uint32_t sd = a->op_sig[d], su = a->op_sig[t];
+      if ((a->h_sig_mr[sd] & 0xFFFF) != (a->h_sig_mr[su] & 0xFFFF)) return false;
+      const uint32_t rd = a->h_sig_resdim[sd], um = use_dimof(t, k), sh = shardable_roles(sd);
+      for (int r = 0; r < 8; ++r) {
+        if (!((sh >> r) & 1)) continue;
+        const uint32_t dd = (rd >> (4 * r)) & 15, du = (um >> (4 * r)) & 15;
+        if (dd == 15 || dd != du) return false;
+      }
+      return true;
+    };
+    const size_t NV = g->values.size();
+    std::vector<int32_t> fid(NV);                 // alias class of each value's finish (a value id)
+    std::iota(fid.begin(), fid.end(), 0);
+    std::vector<char> elided(n_ops, 0);
+    std::vector<uint32_t> zero_bits(n_ops, 0);    // bit k: operand k's edge never communicates
     for (int32_t t = 0; t < n_ops; ++t) {
       const GOp& op = g->ops[t];
-      uint32_t comp = NO_CLASS;
+      for (size_t k = 0; k < op.operands.size(); ++k)
+        if (zero_edge(t, k)) zero_bits[t] |= 1u << k;
+      if (op.kind != OK_PARAM && !(a->h_ops[t].flags & 1) && op.operands.size() == 1 && (zero_bits[t] & 1)) {
+        elided[t] = 1;
+        if (op.result >= 0) fid[op.result] = fid[op.operands[0]];
+      }
+    }
+    // The walk runs in BUNDLES of at most CP_EMAX operand edges whose ops read
+    // no finish produced inside the same bundle: the kernel issues all of a
+    // bundle's loads before it combines them, so a bundle costs one memory
+    // round trip instead of one per op.  Any topological order gives the same
+    // finish times (each is a function of its operands', in operand order) and
+    // the same latest finish (max is exact), so the schedule is free: ops are
+    // taken greedily in program order from a window of CP_WINDOW ops past the
+    // first unscheduled one (the window bounds how far liveness can stretch).
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint64_t>, uint32_t> comm_id;
+    std::map<std::pair<uint32_t, uint64_t>, uint32_t> comp_id;
+    struct WOp { int32_t t; uint32_t comp; int32_t e0, ne; };
+    struct WEdge { int32_t cls_val; uint32_t comm; };   // alias class of the operand (value id), class / ZERO_COMM
+    std::vector<WOp> wops;
+    std::vector<WEdge> wedges;
+    std::vector<int32_t> producer(NV, -1);   // walked op index producing an alias class
+    for (int32_t t = 0; t < n_ops; ++t) {
+      const GOp& op = g->ops[t];
+      if (elided[t] || op.kind == OK_PARAM) continue;   // parameters finish at 0 and hold no slot
+      WOp w{t, NO_CLASS, (int32_t)wedges.size(), 0};
       if (a->h_ops[t].flags & 1) {
         auto it = comp_id.emplace(std::make_pair(a->op_sig[t], a->h_gflops[t]), (uint32_t)a->h_cp_comp.size());
         if (it.second) {
@@ -1155,49 +1221,117 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
           c.gflops = a->h_gflops[t];
           a->h_cp_comp.push_back(c);
         }
-        comp = it.first->second;
+        w.comp = it.first->second;
       }
-      uint32_t res_slot = NO_SLOT;
-      if (op.result >= 0 && op.kind != OK_PARAM) {
-        if (free_slots.empty()) free_slots.push_back((uint32_t)n_slots++);
-        slot_of[op.result] = free_slots.back();
-        free_slots.pop_back();
-        res_slot = slot_of[op.result];
-      }
-      if (op.operands.size() > 0xFFFF || comp > 0xFFFF) { err = "critical-path stream limits"; return TOAST_E_LIMIT; }
-      a->h_cp.push_back(res_slot);
-      a->h_cp.push_back(comp | ((uint32_t)op.operands.size() << 16));
       const uint32_t umc = (uint32_t)(a->h_sig_mr[a->op_sig[t]] & 0xFFFFFFFFu);
       for (size_t k = 0; k < op.operands.size(); ++k) {
         const int32_t v = op.operands[k];
-        uint32_t um = ~0u;
-        for (size_t i = 0; i < OL[t].use_role[k].size(); ++i) {
-          uint32_t rr = OL[t].use_role[k][i];
-          um = (um & ~(0xFu << (4 * rr))) | ((uint32_t)i << (4 * rr));
-        }
         const int32_t d = g->values[v].def_op;
-        auto it = comm_id.emplace(std::make_tuple((uint32_t)a->op_sig[d], umc, um, a->h_ops[d].gbytes),
-                                  (uint32_t)a->h_cp_comm.size());
-        if (it.second) {
-          KCpComm c{};
-          c.def_sig = (uint16_t)a->op_sig[d];
-          c.use_mc = (uint16_t)umc;
-          c.use_dimof = um;
-          c.gb = a->h_ops[d].gbytes;
-          a->h_cp_comm.push_back(c);
+        uint32_t cls = ZERO_COMM;
+        if (!((zero_bits[t] >> k) & 1)) {
+          const uint32_t um = use_dimof(t, k);
+          auto it = comm_id.emplace(std::make_tuple((uint32_t)a->op_sig[d], umc, um, a->h_ops[d].gbytes),
+                                    (uint32_t)a->h_cp_comm.size());
+          if (it.second) {
+            KCpComm c{};
+            c.def_sig = (uint16_t)a->op_sig[d];
+            c.use_mc = (uint16_t)umc;
+            c.use_dimof = um;
+            c.gb = a->h_ops[d].gbytes;
+            a->h_cp_comm.push_back(c);
+          }
+          cls = it.first->second;
         }
-        a->h_cp.push_back(slot_of[v]);
-        a->h_cp.push_back(it.first->second);
+        wedges.push_back({fid[v], cls});
       }
-      // values whose last use is t give their slots back (after t read them)
-      for (int32_t dv : deaths[t]) {
-        const int32_t val = g->ops[dv].result;
-        if (val >= 0 && slot_of[val] != NO_SLOT) free_slots.push_back(slot_of[val]);
+      if (op.operands.empty()) wedges.push_back({-1, ZERO_COMM});   // finish = its own compute time
+      w.ne = (int32_t)wedges.size() - w.e0;
+      if (op.result >= 0) producer[op.result] = (int32_t)wops.size();
+      wops.push_back(w);
+    }
+    const int32_t NW = (int32_t)wops.size();
+    // bundles
+    std::vector<int32_t> bundle_of(NW, -1), order;
+    std::vector<uint8_t> bsize;
+    {
+      int32_t lo = 0, nb = 0;
+      while (lo < NW) {
+        int32_t used = 0;
+        for (int32_t i = lo; i < NW && i < lo + CP_WINDOW; ++i) {
+          if (bundle_of[i] >= 0 || used + wops[i].ne > CP_EMAX) continue;
+          bool ready = true;
+          for (int32_t e = wops[i].e0; e < wops[i].e0 + wops[i].ne && ready; ++e) {
+            const int32_t cv = wedges[e].cls_val;
+            const int32_t pr = cv >= 0 ? producer[cv] : -1;
+            if (pr >= 0 && (bundle_of[pr] < 0 || bundle_of[pr] == nb)) ready = false;
+          }
+          if (!ready) continue;
+          bundle_of[i] = nb;
+          order.push_back(i);
+          used += wops[i].ne;
+        }
+        bsize.push_back((uint8_t)used);
+        ++nb;
+        while (lo < NW && bundle_of[lo] >= 0) ++lo;
       }
     }
+    const int32_t NB = (int32_t)bsize.size();
+    // finish slots per alias class, held from its producer's bundle to the last bundle reading it
+    std::vector<int32_t> last_b(NV, -1);
+    for (int32_t i = 0; i < NW; ++i)
+      if (g->ops[wops[i].t].result >= 0) last_b[g->ops[wops[i].t].result] = bundle_of[i];
+    for (int32_t i = 0; i < NW; ++i)
+      for (int32_t e = wops[i].e0; e < wops[i].e0 + wops[i].ne; ++e)
+        if (wedges[e].cls_val >= 0 && producer[wedges[e].cls_val] >= 0)
+          last_b[wedges[e].cls_val] = std::max(last_b[wedges[e].cls_val], bundle_of[i]);
+    std::vector<std::vector<int32_t>> b_deaths(NB);
+    for (size_t v = 0; v < NV; ++v) if (last_b[v] >= 0) b_deaths[last_b[v]].push_back((int32_t)v);
+    std::vector<uint32_t> slot_of(NV, NO_SLOT), free_slots;
+    std::vector<int32_t> recs;   // walked ops in bundle order
+    size_t oi = 0;
+    for (int32_t b = 0; b < NB; ++b) {
+      const size_t ob = oi;
+      for (; oi < order.size() && bundle_of[order[oi]] == b; ++oi) {
+        const int32_t res = g->ops[wops[order[oi]].t].result;
+        if (res >= 0) {
+          if (free_slots.empty()) free_slots.push_back((uint32_t)n_slots++);
+          slot_of[res] = free_slots.back();
+          free_slots.pop_back();
+        }
+      }
+      for (size_t q = ob; q < oi; ++q) recs.push_back((int32_t)order[q]);
+      for (int32_t c : b_deaths[b])
+        if (slot_of[c] != NO_SLOT) free_slots.push_back(slot_of[c]);
+    }
+    if (n_slots + 2 > 0x7FFF || a->h_cp_comm.size() + a->h_cp_comp.size() + 1 > 0x7FFF) {
+      err = "critical-path stream limits (32765 finish slots, 32766 duration classes)";
+      return TOAST_E_LIMIT;
+    }
+    // records in bundle order; indices into the block's scratch (kernels.cu cp_stride):
+    // classes [communication | compute | zero], slots [finish slots | zero | trash]
+    const uint32_t zero_cls = (uint32_t)(a->h_cp_comm.size() + a->h_cp_comp.size());
+    const uint32_t zero_slot = (uint32_t)n_slots, trash_slot = (uint32_t)n_slots + 1;
+    for (int32_t wi : recs) {
+      const WOp& w = wops[wi];
+      const int32_t res = g->ops[w.t].result;
+      const uint32_t rs = res >= 0 ? slot_of[res] : trash_slot;
+      const uint32_t ct = w.comp == NO_CLASS ? zero_cls : (uint32_t)a->h_cp_comm.size() + w.comp;
+      for (int32_t e = w.e0; e < w.e0 + w.ne; ++e) {
+        const int32_t cv = wedges[e].cls_val;
+        const uint32_t fs = (cv >= 0 && producer[cv] >= 0) ? slot_of[cv] : zero_slot;
+        const uint32_t dur = wedges[e].comm == ZERO_COMM ? zero_cls : wedges[e].comm;
+        const uint32_t first = e == w.e0, last = e == w.e0 + w.ne - 1;
+        a->h_cp.push_back(fs | dur << 16 | first << 31);
+        a->h_cp.push_back((last ? rs : trash_slot) | (last ? ct : zero_cls) << 16 | last << 31);
+      }
+    }
+    a->h_cp_bsize = bsize;
+    a->cp_walked_ops = NW;
+    a->cp_walked_edges = (int32_t)wedges.size();
     if (getenv("TOAST_DEBUG"))
-      fprintf(stderr, "[toast] critical path: %d finish slots, %zu communication classes, %zu compute classes\n",
-              n_slots, a->h_cp_comm.size(), a->h_cp_comp.size());
+      fprintf(stderr, "[toast] critical path: %d of %d ops walked (%zu edges) in %d bundles, %d finish slots, "
+              "%zu communication classes, %zu compute classes\n", NW, n_ops, wedges.size(), NB, n_slots,
+              a->h_cp_comm.size(), a->h_cp_comp.size());
   }
   a->dt.n_slots = n_slots;
   a->dt.n_comm = (int32_t)a->h_cp_comm.size();
@@ -1374,7 +1508,8 @@ std::string dump_json(const toast_analysis* a) {
          I((int64_t)a->h_sigs.size()) + ",\"sig_roles\":" + I(roles) +
          ",\"sig_colors\":" + I(cols) + ",\"n_tmpl\":" + I((int64_t)a->h_tmpl.size()) + ",\"n_points\":" +
          I((int64_t)a->h_points.size()) + ",\"n_terms\":" + I((int64_t)a->h_terms.size()) + ",\"n_spec\":" +
-         I((int64_t)a->h_spec.size()) + ",\"n_slots\":" + I((int64_t)a->dt.n_slots) + ",\"warps_per_batch\":" +
+         I((int64_t)a->h_spec.size()) + ",\"n_slots\":" + I((int64_t)a->dt.n_slots) + ",\"cp_walked_ops\":" +
+         I((int64_t)a->cp_walked_ops) + ",\"cp_walked_edges\":" + I((int64_t)a->cp_walked_edges) + ",\"cp_bundles\":" + I((int64_t)a->h_cp_bsize.size()) + ",\"warps_per_batch\":" +
          I((int64_t)a->k_throughput) + ",\"work\":{\"sig_roles\":" + I(a->work_sig_roles) + ",\"n_tmpl\":" +
          I(a->work_tmpl) + ",\"n_terms\":" + I(a->work_terms) + "},\"frontier_ops\":[";
     for (size_t q = 0; q < a->point_op.size(); ++q) { if (q) s += ','; s += I(a->point_op[q]); }

@@ -426,6 +426,7 @@ __device__ __forceinline__ void cp_classes(const DeviceTables& T, const Smem& S,
     }
     scr[(size_t)c * 32 + lane] = m;
   }
+  if (warp == 0) scr[(size_t)(T.n_comm + T.n_comp) * 32 + lane] = 0.0;   // the "no class" duration
   for (int c = warp; c < T.n_comp; c += K) {
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(T.cp_comp + c));
     const uint32_t a2r = e_a2r16<NA>(ent(w.x));
@@ -437,26 +438,66 @@ __device__ __forceinline__ void cp_classes(const DeviceTables& T, const Smem& S,
   }
 }
 
+// one bundle of exactly W edges (toast_internal.h): every load of the bundle
+// is issued before any is used, then the edges are combined in order — per op
+// the max over its operands of (def finish + edge duration), plus its compute
+// time — and each op's finish is stored.  Bit-identical to the per-op
+// recurrence: the same IEEE adds in the same order, max is exact, and the
+// "no slot / no class" indices read a 0.0 (every finish is >= +0, x + 0.0 == x).
+// per-block scratch of the critical-path walk, in [x][32] doubles: the
+// duration classes (communication, compute, then one 0.0 "no class"), then the
+// finish slots (then the 0.0 "finishes at 0" slot and a trash slot)
+__host__ __device__ __forceinline__ size_t cp_stride(const DeviceTables& T) {
+  return (size_t)(T.n_comm + T.n_comp + 1) + (size_t)(T.n_slots + 2);
+}
+
+template <int W>
+__device__ __forceinline__ void cp_bundle(const uint2* __restrict__ rec, const double* __restrict__ cls,
+                                          double* __restrict__ slots, int lane, double& cp, uint32_t zs, uint32_t zc) {
+  uint2 r[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) r[e] = __ldg(rec + e);
+  double fin[W], dur[W], ct[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) {   // the 0.0 entries are not read (the loads are predicated off)
+    const uint32_t fs = r[e].x & 0x7FFF, dc = (r[e].x >> 16) & 0x7FFF, cc = (r[e].y >> 16) & 0x7FFF;
+    fin[e] = fs == zs ? 0.0 : slots[(size_t)fs * 32 + lane];
+    dur[e] = dc == zc ? 0.0 : cls[(size_t)dc * 32 + lane];
+    ct[e] = cc == zc ? 0.0 : cls[(size_t)cc * 32 + lane];
+  }
+  double ready = 0.0;
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const double f = __dadd_rn(fin[e], dur[e]);
+    ready = (r[e].x >> 31) ? f : (f > ready ? f : ready);
+    if (r[e].y >> 31) {
+      const double ft = __dadd_rn(ready, ct[e]);
+      slots[(size_t)(r[e].y & 0x7FFF) * 32 + lane] = ft;
+      cp = ft > cp ? ft : cp;
+    }
+  }
+}
+
 __device__ __forceinline__ double cp_sweep(const DeviceTables& T, int lane, const double* __restrict__ cls,
                                            double* __restrict__ slots) {
   double cp = 0.0;
-  uint32_t q = 0;
+  slots[(size_t)T.n_slots * 32 + lane] = 0.0;   // the "finishes at 0" slot (parameters)
+  const uint2* rec = T.cp;
+  const uint32_t zs = (uint32_t)T.n_slots, zc = (uint32_t)(T.n_comm + T.n_comp);
 #pragma unroll 1
-  for (int t = 0; t < T.n_ops; ++t) {
-    const uint2 h = __ldg(T.cp + q++);
-    const uint32_t comp = h.y & 0xFFFF, nu = h.y >> 16;
-    double ready = 0.0;
-#pragma unroll 2
-    for (uint32_t k = 0; k < nu; ++k) {
-      const uint2 u = __ldg(T.cp + q++);
-      const double fin = u.x == NO_SLOT ? 0.0 : slots[(size_t)u.x * 32 + lane];
-      const double f = __dadd_rn(fin, cls[(size_t)u.y * 32 + lane]);
-      ready = f > ready ? f : ready;
+  for (int b = 0; b < T.n_bundles; ++b) {
+    const uint32_t ne = __ldg(T.cp_bsize + b);
+    switch (ne) {   // warp-uniform
+      case 1: cp_bundle<1>(rec, cls, slots, lane, cp, zs, zc); break;
+      case 2: cp_bundle<2>(rec, cls, slots, lane, cp, zs, zc); break;
+      case 3: cp_bundle<3>(rec, cls, slots, lane, cp, zs, zc); break;
+      case 4: cp_bundle<4>(rec, cls, slots, lane, cp, zs, zc); break;
+      case 5: cp_bundle<5>(rec, cls, slots, lane, cp, zs, zc); break;
+      case 6: cp_bundle<6>(rec, cls, slots, lane, cp, zs, zc); break;
+      case 7: cp_bundle<7>(rec, cls, slots, lane, cp, zs, zc); break;
+      default: cp_bundle<8>(rec, cls, slots, lane, cp, zs, zc); break;
     }
-    const double ct = comp == NO_CLASS ? 0.0 : cls[(size_t)(T.n_comm + comp) * 32 + lane];
-    const double ft = __dadd_rn(ready, ct);
-    if (h.x != NO_SLOT) slots[(size_t)h.x * 32 + lane] = ft;
-    cp = ft > cp ? ft : cp;
+    rec += ne;
   }
   return cp;
 }
@@ -746,7 +787,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     peak = M > peak ? M : peak;
   }
   }
-  if (CP) cp_classes<NA, P2>(T, S, K, warp, lane, T.cp_scratch + (size_t)blockIdx.x * (T.n_comm + T.n_comp + T.n_slots) * 32);
+  if (CP) cp_classes<NA, P2>(T, S, K, warp, lane, T.cp_scratch + (size_t)blockIdx.x * cp_stride(T) * 32);
   if (K > 1) {
     seg[0 * 32 + lane] = key;
     seg[1 * 32 + lane] = flo;
@@ -791,8 +832,8 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       for (int k = 0; k < 4; ++k) ncoll += cnt[(A * 4 + k) * 32 + lane];
     }
     if (CP) {
-      double* scr = T.cp_scratch + (size_t)blockIdx.x * (T.n_comm + T.n_comp + T.n_slots) * 32;
-      tt = cp_sweep(T, lane, scr, scr + (size_t)(T.n_comm + T.n_comp) * 32);
+      double* scr = T.cp_scratch + (size_t)blockIdx.x * cp_stride(T) * 32;
+      tt = cp_sweep(T, lane, scr, scr + (size_t)(T.n_comm + T.n_comp + 1) * 32);
     }
     const uint64_t pk = pk_all;
     const double RT = __ddiv_rn(tt, T.t0);
@@ -852,7 +893,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? 2 : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
@@ -881,7 +922,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? 2 : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
                                                             toast_cost* __restrict__ out, int64_t rep) {
@@ -1125,13 +1166,16 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     // R22: the critical-path stream and one finish-time scratch [n_slots][32] per resident block
     if ((st = upload(a, a->h_cp, &p, err))) return st;
     T.cp = reinterpret_cast<const uint2*>(p);
+    if ((st = upload(a, a->h_cp_bsize, &p, err))) return st;
+    T.cp_bsize = reinterpret_cast<const uint8_t*>(p);
+    T.n_bundles = (int32_t)a->h_cp_bsize.size();
     if ((st = upload(a, a->h_cp_comm, &p, err))) return st;
     T.cp_comm = reinterpret_cast<const KCpComm*>(p);
     if ((st = upload(a, a->h_cp_comp, &p, err))) return st;
     T.cp_comp = reinterpret_cast<const KCpComp*>(p);
     int max_blocks = 0;
     for (int i = 0; i < 4; ++i) max_blocks = std::max(max_blocks, std::max(a->occ_eval[i], a->occ_roll[i]));
-    const size_t bytes = (size_t)max_blocks * sms * (size_t)std::max(T.n_comm + T.n_comp + T.n_slots, 1) * 32 *
+    const size_t bytes = (size_t)max_blocks * sms * (size_t)cp_stride(T) * 32 *
                          sizeof(double);
     void* d = nullptr;
     TOAST_CUDA(cudaMalloc(&d, bytes));

@@ -158,6 +158,15 @@ struct KCpComp {         // 16 B: a compute-time class
 };
 constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;   // a parameter's "slot": finish 0
 constexpr uint32_t NO_CLASS = 0xFFFFu;      // no compute time
+constexpr uint32_t ZERO_COMM = 0xFFFFFFFFu; // an edge that never communicates: the def's finish as is
+// The walk is a sequence of bundles of <= CP_EMAX operand edges (8-B records:
+// x = the operand's finish slot | duration class << 16 | first edge of its op
+// << 31; y = the op's result slot | compute-time class << 16 | last edge << 31,
+// indices into the block's scratch, kernels.cu cp_stride; "none" indices name
+// a 0.0 entry, a non-last edge names the trash slot); no edge of a bundle
+// reads a slot its bundle writes.
+constexpr int CP_EMAX = 8;
+constexpr int CP_WINDOW = 96;
 static_assert(sizeof(KCpComm) == 16 && sizeof(KCpComp) == 16, "cp records");
 static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
 
@@ -194,6 +203,8 @@ struct DeviceTables {
   int32_t cost_model, n_slots;   // R22: critical path; finish-time slots per candidate
   int32_t n_comm, n_comp;        // R22: edge-duration and compute-time classes
   const uint2* cp = nullptr;     // critical-path stream
+  const uint8_t* cp_bsize = nullptr;   // edges per bundle
+  int32_t n_bundles = 0;
   const KCpComm* cp_comm = nullptr;
   const KCpComp* cp_comp = nullptr;
   double* cp_scratch = nullptr;  // per resident block: [n_comm + n_comp + n_slots][32] doubles
@@ -247,9 +258,11 @@ struct toast_analysis {
   // roles over signatures, signature-keyed templates, absolute frontier terms
   int64_t work_sig_roles = 0, work_tmpl = 0, work_terms = 0;
   std::vector<uint32_t> h_cp;               // critical-path stream (8-B records as 2 x u32)
+  std::vector<uint8_t> h_cp_bsize;          // edges per bundle of the stream
   std::vector<toast::KCpComm> h_cp_comm;
   std::vector<toast::KCpComp> h_cp_comp;
   int32_t cost_model = 0;
+  int32_t cp_walked_ops = 0, cp_walked_edges = 0;   // R22 walk after the exact reductions
   std::vector<toast::KSig> h_sigs;          // per materialisation class
   std::vector<uint64_t> h_sig_mr;           // per signature: class | resdim << 32
   std::vector<uint64_t> h_sig_roles, h_desel_cls;
