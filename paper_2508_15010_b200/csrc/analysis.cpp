@@ -1185,13 +1185,76 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     std::iota(fid.begin(), fid.end(), 0);
     std::vector<char> elided(n_ops, 0);
     std::vector<uint32_t> zero_bits(n_ops, 0);    // bit k: operand k's edge never communicates
+    for (int32_t t = 0; t < n_ops; ++t)
+      for (size_t k = 0; k < g->ops[t].operands.size(); ++k)
+        if (zero_edge(t, k)) zero_bits[t] |= 1u << k;
+    // Dominated edges.  A finish is never below the finish of anything that
+    // reaches it (every term is >= 0 and rounding is monotone), so an edge from
+    // x into t can never win t's max over another operand edge from y when x
+    // reaches y (or x is a parameter, finish 0) and the x edge's duration is
+    // never larger: it never communicates (term finish(x) <= finish(y) <=
+    // finish(y) + d), or both edges are of one duration class (finish(x) + d <=
+    // finish(y) + d, rounding is monotone).  Such edges are dropped.  Among
+    // edges from one value with one duration the first is kept; an operand
+    // that reaches no other operand always keeps an edge.
+    auto edge_class_key = [&](int32_t t, size_t k) {
+      const int32_t d = g->values[g->ops[t].operands[k]].def_op;
+      return std::make_tuple((uint32_t)a->op_sig[d], (uint32_t)(a->h_sig_mr[a->op_sig[t]] & 0xFFFFFFFFu),
+                             use_dimof(t, k), a->h_ops[d].gbytes);
+    };
+    std::vector<uint32_t> drop_bits(n_ops, 0);
+    {
+      std::vector<int32_t> src_of(n_ops, -1);   // source index of non-parameter defs feeding multi-operand ops
+      int32_t NSRC = 0;
+      for (int32_t t = 0; t < n_ops; ++t) {
+        const GOp& op = g->ops[t];
+        if (op.operands.size() < 2) continue;
+        for (int32_t v : op.operands) {
+          const int32_t d = g->values[v].def_op;
+          if (g->ops[d].kind != OK_PARAM && src_of[d] < 0) src_of[d] = NSRC++;
+        }
+      }
+      const size_t WS = (size_t)(NSRC + 63) / 64;
+      std::vector<uint64_t> R((size_t)n_ops * WS, 0);   // R[op]: sources reaching op (itself included)
+      for (int32_t t = 0; t < n_ops && WS; ++t) {
+        uint64_t* rt = &R[(size_t)t * WS];
+        for (int32_t v : g->ops[t].operands) {
+          const uint64_t* rd = &R[(size_t)g->values[v].def_op * WS];
+          for (size_t w = 0; w < WS; ++w) rt[w] |= rd[w];
+        }
+        if (src_of[t] >= 0) rt[src_of[t] >> 6] |= 1ULL << (src_of[t] & 63);
+      }
+      for (int32_t t = 0; t < n_ops; ++t) {
+        const GOp& op = g->ops[t];
+        const size_t nk = op.operands.size();
+        if (nk < 2) continue;
+        for (size_t k = 0; k < nk; ++k) {
+          const bool zk = (zero_bits[t] >> k) & 1;
+          const int32_t xk = op.operands[k], dk = g->values[xk].def_op;
+          bool dom = false;
+          for (size_t j = 0; j < nk && !dom; ++j) {
+            if (j == k) continue;
+            const bool zj = (zero_bits[t] >> j) & 1;
+            const bool no_longer = zk || (!zj && edge_class_key(t, k) == edge_class_key(t, j));
+            if (!no_longer) continue;
+            const int32_t xj = op.operands[j], dj = g->values[xj].def_op;
+            if (xj == xk) dom = zk == zj ? j < k : zk;   // same value: keep the first of equal durations
+            else if (g->ops[dk].kind == OK_PARAM) dom = true;
+            else dom = (R[(size_t)dj * WS + (src_of[dk] >> 6)] >> (src_of[dk] & 63)) & 1;
+          }
+          if (dom) drop_bits[t] |= 1u << k;
+        }
+      }
+    }
     for (int32_t t = 0; t < n_ops; ++t) {
       const GOp& op = g->ops[t];
+      if (op.kind == OK_PARAM || (a->h_ops[t].flags & 1)) continue;
+      int32_t kept = -1, n_kept = 0;
       for (size_t k = 0; k < op.operands.size(); ++k)
-        if (zero_edge(t, k)) zero_bits[t] |= 1u << k;
-      if (op.kind != OK_PARAM && !(a->h_ops[t].flags & 1) && op.operands.size() == 1 && (zero_bits[t] & 1)) {
+        if (!((drop_bits[t] >> k) & 1)) { kept = (int32_t)k; ++n_kept; }
+      if (n_kept == 1 && ((zero_bits[t] >> kept) & 1)) {
         elided[t] = 1;
-        if (op.result >= 0) fid[op.result] = fid[op.operands[0]];
+        if (op.result >= 0) fid[op.result] = fid[op.operands[kept]];
       }
     }
     // The walk runs in BUNDLES of at most CP_EMAX operand edges whose ops read
@@ -1225,6 +1288,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       }
       const uint32_t umc = (uint32_t)(a->h_sig_mr[a->op_sig[t]] & 0xFFFFFFFFu);
       for (size_t k = 0; k < op.operands.size(); ++k) {
+        if ((drop_bits[t] >> k) & 1) continue;
         const int32_t v = op.operands[k];
         const int32_t d = g->values[v].def_op;
         uint32_t cls = ZERO_COMM;
@@ -1255,10 +1319,12 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     std::vector<uint8_t> bsize;
     {
       int32_t lo = 0, nb = 0;
+      const char* em = getenv("TOAST_CP_EMAX");   // bundle width experiments (<= CP_EMAX)
+      const int32_t emax = em ? std::max(1, std::min(CP_EMAX, atoi(em))) : CP_EMAX;
       while (lo < NW) {
         int32_t used = 0;
         for (int32_t i = lo; i < NW && i < lo + CP_WINDOW; ++i) {
-          if (bundle_of[i] >= 0 || used + wops[i].ne > CP_EMAX) continue;
+          if (bundle_of[i] >= 0 || (used + wops[i].ne > emax && used > 0)) continue;
           bool ready = true;
           for (int32_t e = wops[i].e0; e < wops[i].e0 + wops[i].ne && ready; ++e) {
             const int32_t cv = wedges[e].cls_val;

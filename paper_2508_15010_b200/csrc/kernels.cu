@@ -34,6 +34,9 @@
 #ifndef TOAST_MAX_THREADS
 #define TOAST_MAX_THREADS 256
 #endif
+#ifndef TOAST_CP_MIN_BLOCKS
+#define TOAST_CP_MIN_BLOCKS 2   // critical-path instantiations (register-heavier bundled walk)
+#endif
 #ifndef TOAST_MIN_BLOCKS
 #define TOAST_MIN_BLOCKS 3
 #endif
@@ -893,7 +896,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? 2 : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, toast_cost* __restrict__ out) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
@@ -922,7 +925,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? 2 : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
                                                             toast_cost* __restrict__ out, int64_t rep) {
