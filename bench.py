@@ -343,7 +343,7 @@ def variant_contraction(args, cfg, local, stream, flush):
     (reading R23) instead of compatibility sets: H0 time, the resulting sets /
     SetGroups / actions, the rollout step timed the same way, and the best score
     a single-GPU search reaches with the main line's search budget (seed 0) —
-    the paper's "not produce results that differ significantly" (P:1355-1356)."""
+    the paper's "not produce results that differ significantly" (P:1357)."""
     from paper_2508_15010_b200 import toast as T
     t = time.perf_counter()
     a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,

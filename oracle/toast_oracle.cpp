@@ -16,8 +16,8 @@
 //   (argument keys) and C8 (action table order) are "parity unpinned" beyond
 //   the structural invariants in tests/test_oracle_pins.py.  The contraction
 //   heuristic (reading R23, NEXT-4) is pinned by the paper's box / incompatible
-//   listings (P:1306-1316, P:1349-1351), by "all conflicts of the attention layer
-//   compatible" (P:1333) and by brute-force path checks on random programs.
+//   listings (P:1306-1316, P:1350-1352), by "all conflicts of the attention layer
+//   compatible" (P:1336) and by brute-force path checks on random programs.
 //
 // Build: g++ -O2 -std=c++17 -ffp-contract=off -fPIC -shared -pthread
 // =============================================================================
@@ -923,7 +923,7 @@ struct Oracle {
   // in the contracted graph, the two endpoints of some conflict would share a
   // node or one would reach the other.  "Both vertical edges will be
   // contracted, which amounts to identifying the conflicts at the top and
-  // bottom of the box as compatible" (P:1349–1350): conflicts whose endpoints
+  // bottom of the box as compatible" (P:1350): conflicts whose endpoints
   // land on the same pair of contracted nodes form one set; side 0 of a
   // conflict is its endpoint in the node of the set's smallest conflict's u.
   // Contraction never joins components, so a conflict can only acquire a path

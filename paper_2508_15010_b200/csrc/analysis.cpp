@@ -193,7 +193,7 @@ inline bool is_matmul_class(OpKind k) { return k == OK_MATMUL || k == OK_DOT || 
 // pushed to the node's descendants / ancestors; a node that already contains
 // them stops the push (A only grows along edges, D only against them).
 // Conflicts on the same unordered pair of contracted nodes form one set
-// (P:1349-1350: contracting both vertical edges of a box identifies its
+// (P:1350: contracting both vertical edges of a box identifies its
 // conflicts as compatible), side 0 = the endpoint in the node of the set's
 // smallest conflict's u.  The WL hash (C6) sees the contracted M edges between
 // the set's endpoints.

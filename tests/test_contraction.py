@@ -2,7 +2,7 @@
 [comment] §3.5) as an alternative to compatibility sets.
 
 Pins of the oracle (no GPU): the paper's listings — the attention layer's
-conflicts all identified as compatible (P:1333) and the "paths going across"
+conflicts all identified as compatible (P:1336) and the "paths going across"
 listing whose vertical edges are not all contracted
  — and the definition itself, checked by brute force on small
 programs from the contracted graph the oracle reports: no conflict's endpoints
@@ -113,7 +113,7 @@ def check_definition(o: Oracle):
 
 
 def test_attention_conflicts_all_identified_compatible():
-    """P:1333 "(correctly) identify all conflicts in the forward attention layer as
+    """P:1336 "(correctly) identify all conflicts in the forward attention layer as
     compatible": the five conflicts of Fig. 5 form one set whose two
     resolutions are the compatibility-set ones."""
     o1 = _oracle(open(os.path.join(GOLD, "attn_fig5.ir")).read())
@@ -143,7 +143,7 @@ def test_paths_going_across_are_not_contracted():
 
 
 def test_mlp_box_contracted():
-    """P:1349-1350 on the M1 pattern (SURVEY §8(c) MLP-c): the w1-def conflict and the
+    """P:1350 on the M1 pattern (SURVEY §8(c) MLP-c): the w1-def conflict and the
     matmul's (j, k) conflict form a box with no path across; both vertical edges
     are contracted and the two conflicts share one set, as with compatibility sets."""
     c = configs.get("mlp_c")
