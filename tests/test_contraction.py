@@ -259,3 +259,46 @@ def test_gpu_rollout_and_eval_parity(name):
     assert np.array_equal(g_seqs, o_seqs)
     assert T.as_costs(out).tobytes() == oc.tobytes()
     assert T.as_costs(out2).tobytes() == oc.tobytes()
+
+
+@pytest.mark.gpu
+def test_gpu_critical_path_under_contraction():
+    """Both analysis options together (R22 cost model, R23 grouping): rollouts and
+    evals bit-identical to the oracle's."""
+    import torch
+    T = _T()
+    c = configs.get("gpt2")
+    a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0,
+                         cost_model=T.COST_CRITICAL_PATH, grouping=T.GROUP_CONTRACTION)
+    o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cost_model=1,
+               grouping=CONTRACTION)
+    n = 2048
+    pre = torch.zeros((n, 32), dtype=torch.int16, device="cuda")
+    seqs = torch.empty_like(pre)
+    out = torch.empty((n, 256), dtype=torch.uint8, device="cuda")
+    T.rollout_batch(a, pre, 11, 3, seqs, out)
+    torch.cuda.synchronize()
+    o_seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=11, id_base=3)
+    assert np.array_equal(seqs.cpu().numpy().view(np.uint16), o_seqs)
+    assert T.as_costs(out).tobytes() == oc.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy"])
+def test_gpu_search_under_contraction_finds_bruteforce_optimum(name):
+    """C16/C17 under R23: the GPU search reaches the oracle's exhaustive optimum
+    over the heuristic's action space, and the search trace equals the oracle's."""
+    T = _T()
+    c = configs.get(name)
+    dm = 700 if name == "attn_toy" else c.dm
+    a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0,
+                         grouping=T.GROUP_CONTRACTION)
+    o = Oracle(c.ir, c.axes, c.flops_per_sec, dm, c.penalty_c, c.min_dims, c.max_depth, grouping=CONTRACTION)
+    _, _best, bc = o.bruteforce()
+    r = T.search(a, T.SearchOptions(seed=0, max_evals=20000, leaves_per_round=8, rollouts_per_leaf=32, patience=4))
+    assert r["best"]["score"] == bc["score"]
+    opts = T.SearchOptions(seed=3, max_evals=3000, leaves_per_round=4, rollouts_per_leaf=8, patience=3)
+    r = T.search(a, opts)
+    ro, _ = o.search(seed=3, max_evals=3000, L=4, R=8, patience=3)
+    assert int(r["rounds"]) == int(ro["rounds"]) and int(r["evals"]) == int(ro["evals"])
+    assert np.array_equal(r["best_seq"], ro["best_seq"]) and r["best"]["score"] == ro["best"]["score"]
