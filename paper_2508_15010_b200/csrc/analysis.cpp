@@ -895,6 +895,23 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     // signature, use role->dim map) communicate identically for a candidate;
     // a value used more than once by one op is a "special" edge group, costed
     // edge by edge (within-op dedup, G26)
+    // An edge whose def and use ops are of one materialisation class (the same
+    // axis -> role map for every candidate) and whose every shardable role is
+    // the same result dim and operand dim (none off the result: no partial sum)
+    // has D == U and P empty for every candidate: it never communicates and
+    // never grows a temporary, so it is left out of the tables altogether.
+    auto never_communicates = [&](int32_t d, int32_t t, uint32_t um) {
+      const uint32_t sd = a->op_sig[d], su = a->op_sig[t];
+      if ((a->h_sig_mr[sd] & 0xFFFF) != (a->h_sig_mr[su] & 0xFFFF)) return false;
+      const uint32_t rd = a->h_sig_resdim[sd];
+      for (int r = 0; r < 8; ++r) {
+        if ((a->h_sig_roles[(size_t)sd * 8 + r] & 0x3FF) == NO_ACOLOR) continue;
+        const uint32_t dd = (rd >> (4 * r)) & 15, du = (um >> (4 * r)) & 15;
+        if (dd == 15 || dd != du) return false;
+      }
+      return true;
+    };
+    int64_t n_silent = 0;
     std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint32_t> tmpl_id;
     std::set<std::tuple<uint32_t, uint32_t, uint32_t>> sig_tmpl;   // templates keyed by signatures (work count)
     a->h_tmpl.clear();
@@ -919,6 +936,10 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
         }
         const uint64_t gb = a->h_ops[v].gbytes;
         if (gb >> 48) { err = "a value larger than 2^48 bytes"; return TOAST_E_LIMIT; }
+        if (first && last && never_communicates(v, t, um)) {
+          ++n_silent;   // the same layout for every candidate: no collective, no growth (frontier weight 0)
+          continue;
+        }
         if (first && last) {   // the value is used once here: cost it through its template
           // keyed by the use op's materialisation class: only its axis -> role
           // map and this edge's role -> operand dim map decide the use layout
@@ -950,6 +971,8 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       }
     }
     if (a->h_tmpl.size() >= NO_TMPL) { err = "more than 65534 edge templates"; return TOAST_E_LIMIT; }
+    if (getenv("TOAST_DEBUG"))
+      fprintf(stderr, "[toast] %lld single use edges never communicate (no template)\n", (long long)n_silent);
     a->work_tmpl = (int64_t)sig_tmpl.size();
     a->work_sig_roles = 0;
     for (auto& w : sig_words) a->work_sig_roles += (int64_t)w.size();
