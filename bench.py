@@ -218,6 +218,7 @@ def time_to_best_gpu(a, args, rank, world, stream):
             g = T.search(a, opts, stream=stream)
         else:
             from paper_2508_15010_b200 import parallel as P
+            barrier(world)   # every rank starts the race together (rank 0 may have run the variants)
             g = P.search_root_parallel(a, opts, stream=stream)
         per_seed.append((float(g["time_to_target_s"]) if g["hit_target"] else None, int(g["evals"]), int(g["rounds"])))
         if seed == 0:
