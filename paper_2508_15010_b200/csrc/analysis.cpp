@@ -1339,11 +1339,13 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     const int32_t NW = (int32_t)wops.size();
     // bundles
     std::vector<int32_t> bundle_of(NW, -1), order;
-    std::vector<uint8_t> bsize;
+    std::vector<uint32_t> bsize;
     {
       int32_t lo = 0, nb = 0;
       const char* em = getenv("TOAST_CP_EMAX");   // bundle width experiments (<= CP_EMAX)
       const int32_t emax = em ? std::max(1, std::min(CP_EMAX, atoi(em))) : CP_EMAX;
+      const char* fw = getenv("TOAST_CP_FWD");    // 0: no in-bundle forwarding (experiments)
+      const bool fwd = !fw || atoi(fw) != 0;
       while (lo < NW) {
         int32_t used = 0;
         for (int32_t i = lo; i < NW && i < lo + CP_WINDOW; ++i) {
@@ -1352,27 +1354,47 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
           for (int32_t e = wops[i].e0; e < wops[i].e0 + wops[i].ne && ready; ++e) {
             const int32_t cv = wedges[e].cls_val;
             const int32_t pr = cv >= 0 ? producer[cv] : -1;
-            if (pr >= 0 && (bundle_of[pr] < 0 || bundle_of[pr] == nb)) ready = false;
+            // a producer in this bundle hands its finish over in a register
+            if (pr >= 0 && (bundle_of[pr] < 0 || (!fwd && bundle_of[pr] == nb))) ready = false;
           }
           if (!ready) continue;
           bundle_of[i] = nb;
           order.push_back(i);
           used += wops[i].ne;
         }
-        bsize.push_back((uint8_t)used);
+        bsize.push_back((uint32_t)used);
         ++nb;
         while (lo < NW && bundle_of[lo] >= 0) ++lo;
       }
     }
     const int32_t NB = (int32_t)bsize.size();
-    // finish slots per alias class, held from its producer's bundle to the last bundle reading it
+    if (getenv("TOAST_DEBUG")) {   // the walked DAG's depth: no schedule needs fewer bundles
+      std::vector<int32_t> lvl(NW, 0);
+      int32_t depth = 0;
+      for (int32_t i = 0; i < NW; ++i) {
+        for (int32_t e = wops[i].e0; e < wops[i].e0 + wops[i].ne; ++e) {
+          const int32_t cv = wedges[e].cls_val;
+          const int32_t pr = cv >= 0 ? producer[cv] : -1;
+          if (pr >= 0) lvl[i] = std::max(lvl[i], lvl[pr] + 1);
+        }
+        depth = std::max(depth, lvl[i] + 1);
+      }
+      fprintf(stderr, "[toast] critical path: walked DAG depth %d, %d bundles\n", depth, NB);
+    }
+    // finish slots per alias class, held from its producer's bundle to the last
+    // bundle reading it; a class read only inside its producer's bundle (in
+    // registers) needs none
     std::vector<int32_t> last_b(NV, -1);
+    std::vector<char> needs_slot(NV, 0);
     for (int32_t i = 0; i < NW; ++i)
       if (g->ops[wops[i].t].result >= 0) last_b[g->ops[wops[i].t].result] = bundle_of[i];
     for (int32_t i = 0; i < NW; ++i)
-      for (int32_t e = wops[i].e0; e < wops[i].e0 + wops[i].ne; ++e)
-        if (wedges[e].cls_val >= 0 && producer[wedges[e].cls_val] >= 0)
-          last_b[wedges[e].cls_val] = std::max(last_b[wedges[e].cls_val], bundle_of[i]);
+      for (int32_t e = wops[i].e0; e < wops[i].e0 + wops[i].ne; ++e) {
+        const int32_t cv = wedges[e].cls_val;
+        if (cv < 0 || producer[cv] < 0) continue;
+        last_b[cv] = std::max(last_b[cv], bundle_of[i]);
+        if (bundle_of[producer[cv]] != bundle_of[i]) needs_slot[cv] = 1;
+      }
     std::vector<std::vector<int32_t>> b_deaths(NB);
     for (size_t v = 0; v < NV; ++v) if (last_b[v] >= 0) b_deaths[last_b[v]].push_back((int32_t)v);
     std::vector<uint32_t> slot_of(NV, NO_SLOT), free_slots;
@@ -1382,7 +1404,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
       const size_t ob = oi;
       for (; oi < order.size() && bundle_of[order[oi]] == b; ++oi) {
         const int32_t res = g->ops[wops[order[oi]].t].result;
-        if (res >= 0) {
+        if (res >= 0 && needs_slot[res]) {
           if (free_slots.empty()) free_slots.push_back((uint32_t)n_slots++);
           slot_of[res] = free_slots.back();
           free_slots.pop_back();
@@ -1400,19 +1422,52 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     // classes [communication | compute | zero], slots [finish slots | zero | trash]
     const uint32_t zero_cls = (uint32_t)(a->h_cp_comm.size() + a->h_cp_comp.size());
     const uint32_t zero_slot = (uint32_t)n_slots, trash_slot = (uint32_t)n_slots + 1;
-    for (int32_t wi : recs) {
-      const WOp& w = wops[wi];
-      const int32_t res = g->ops[w.t].result;
-      const uint32_t rs = res >= 0 ? slot_of[res] : trash_slot;
-      const uint32_t ct = w.comp == NO_CLASS ? zero_cls : (uint32_t)a->h_cp_comm.size() + w.comp;
-      for (int32_t e = w.e0; e < w.e0 + w.ne; ++e) {
-        const int32_t cv = wedges[e].cls_val;
-        const uint32_t fs = (cv >= 0 && producer[cv] >= 0) ? slot_of[cv] : zero_slot;
-        const uint32_t dur = wedges[e].comm == ZERO_COMM ? zero_cls : wedges[e].comm;
-        const uint32_t first = e == w.e0, last = e == w.e0 + w.ne - 1;
-        a->h_cp.push_back(fs | dur << 16 | first << 31);
-        a->h_cp.push_back((last ? rs : trash_slot) | (last ? ct : zero_cls) << 16 | last << 31);
+    std::vector<int32_t> last_pos(NW, -1);   // position of an op's last edge inside its bundle
+    {
+      int32_t cur_b = -1, pos = 0;
+      for (int32_t wi : recs) {
+        const WOp& w = wops[wi];
+        if (bundle_of[wi] != cur_b) { cur_b = bundle_of[wi]; pos = 0; }
+        const int32_t res = g->ops[w.t].result;
+        const uint32_t rs = (res >= 0 && slot_of[res] != NO_SLOT) ? slot_of[res] : trash_slot;
+        const uint32_t ct = w.comp == NO_CLASS ? zero_cls : (uint32_t)a->h_cp_comm.size() + w.comp;
+        for (int32_t e = w.e0; e < w.e0 + w.ne; ++e, ++pos) {
+          const int32_t cv = wedges[e].cls_val;
+          const int32_t pr = (cv >= 0) ? producer[cv] : -1;
+          const bool fwd_e = pr >= 0 && bundle_of[pr] == cur_b;   // x bit 15: the finish of edge fs of this bundle
+          const uint32_t fs = fwd_e ? (uint32_t)last_pos[pr] : pr >= 0 ? slot_of[cv] : zero_slot;
+          const uint32_t dur = wedges[e].comm == ZERO_COMM ? zero_cls : wedges[e].comm;
+          const uint32_t first = e == w.e0, last = e == w.e0 + w.ne - 1;
+          a->h_cp.push_back(fs | (uint32_t)fwd_e << 15 | dur << 16 | first << 31);
+          a->h_cp.push_back((last ? rs : trash_slot) | (last ? ct : zero_cls) << 16 | last << 31);
+        }
+        last_pos[wi] = pos - 1;
       }
+    }
+    // Prefetch hints: a finish read long after it was written (a forward
+    // activation read by the backward pass) has left the L2 by then; the bundle
+    // PF_DIST bundles before the read prefetches it into L2 (two hints per
+    // bundle header; a read with no free header slot in reach goes without).
+    {
+      const char* pd = getenv("TOAST_CP_PF_DIST");
+      const char* pc = getenv("TOAST_CP_PF_COLD");
+      const int32_t dist = pd ? atoi(pd) : 6, cold = pc ? atoi(pc) : 16;
+      std::vector<uint32_t> pf(NB * 2, 0x3FFF);
+      for (int32_t wi : recs) {
+        const int32_t b = bundle_of[wi];
+        const WOp& w = wops[wi];
+        for (int32_t e = w.e0; e < w.e0 + w.ne && dist > 0 && n_slots < 0x3FFF; ++e) {
+          const int32_t cv = wedges[e].cls_val;
+          if (cv < 0 || producer[cv] < 0 || slot_of[cv] == NO_SLOT) continue;
+          const int32_t pb = bundle_of[producer[cv]];
+          if (b - pb <= cold) continue;
+          for (int32_t t = std::max(pb + 1, b - dist); t >= pb + 1 && t >= b - 4 * dist; --t) {
+            if (pf[2 * t] == 0x3FFF) { pf[2 * t] = slot_of[cv]; break; }
+            if (pf[2 * t + 1] == 0x3FFF) { pf[2 * t + 1] = slot_of[cv]; break; }
+          }
+        }
+      }
+      for (int32_t i = 0; i < NB; ++i) bsize[i] |= pf[2 * i] << 4 | pf[2 * i + 1] << 18;
     }
     a->h_cp_bsize = bsize;
     a->cp_walked_ops = NW;

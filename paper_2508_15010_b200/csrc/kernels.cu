@@ -447,6 +447,8 @@ __device__ __forceinline__ void cp_classes(const DeviceTables& T, const Smem& S,
 // time — and each op's finish is stored.  Bit-identical to the per-op
 // recurrence: the same IEEE adds in the same order, max is exact, and the
 // "no slot / no class" indices read a 0.0 (every finish is >= +0, x + 0.0 == x).
+__device__ __forceinline__ void prefetch_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // per-block scratch of the critical-path walk, in [x][32] doubles: the
 // duration classes (communication, compute, then one 0.0 "no class"), then the
 // finish slots (then the 0.0 "finishes at 0" slot and a trash slot)
@@ -462,19 +464,28 @@ __device__ __forceinline__ void cp_bundle(const uint2* __restrict__ rec, const d
   for (int e = 0; e < W; ++e) r[e] = __ldg(rec + e);
   double fin[W], dur[W], ct[W];
 #pragma unroll
-  for (int e = 0; e < W; ++e) {   // the 0.0 entries are not read (the loads are predicated off)
+  for (int e = 0; e < W; ++e) {   // the 0.0 entries and forwarded finishes are not read (predicated off)
     const uint32_t fs = r[e].x & 0x7FFF, dc = (r[e].x >> 16) & 0x7FFF, cc = (r[e].y >> 16) & 0x7FFF;
-    fin[e] = fs == zs ? 0.0 : slots[(size_t)fs * 32 + lane];
+    fin[e] = (fs == zs || ((r[e].x >> 15) & 1)) ? 0.0 : slots[(size_t)fs * 32 + lane];
     dur[e] = dc == zc ? 0.0 : cls[(size_t)dc * 32 + lane];
     ct[e] = cc == zc ? 0.0 : cls[(size_t)cc * 32 + lane];
   }
-  double ready = 0.0;
+  double ready = 0.0, ftv[W];
 #pragma unroll
   for (int e = 0; e < W; ++e) {
-    const double f = __dadd_rn(fin[e], dur[e]);
+    double x = fin[e];
+    if (e > 0 && ((r[e].x >> 15) & 1)) {   // produced by an op earlier in this bundle: its register
+      const uint32_t j = r[e].x & 7;
+      x = ftv[0];
+#pragma unroll
+      for (int k = 1; k < e; ++k) x = j == (uint32_t)k ? ftv[k] : x;
+    }
+    const double f = __dadd_rn(x, dur[e]);
     ready = (r[e].x >> 31) ? f : (f > ready ? f : ready);
+    ftv[e] = 0.0;
     if (r[e].y >> 31) {
       const double ft = __dadd_rn(ready, ct[e]);
+      ftv[e] = ft;
       slots[(size_t)(r[e].y & 0x7FFF) * 32 + lane] = ft;
       cp = ft > cp ? ft : cp;
     }
@@ -489,7 +500,9 @@ __device__ __forceinline__ double cp_sweep(const DeviceTables& T, int lane, cons
   const uint32_t zs = (uint32_t)T.n_slots, zc = (uint32_t)(T.n_comm + T.n_comp);
 #pragma unroll 1
   for (int b = 0; b < T.n_bundles; ++b) {
-    const uint32_t ne = __ldg(T.cp_bsize + b);
+    const uint32_t hdr = __ldg(T.cp_bsize + b), ne = hdr & 15, p0 = (hdr >> 4) & 0x3FFF, p1 = hdr >> 18;
+    if (p0 != 0x3FFFu) prefetch_l2(slots + (size_t)p0 * 32 + lane);   // a finish read a few bundles from now
+    if (p1 != 0x3FFFu) prefetch_l2(slots + (size_t)p1 * 32 + lane);
     switch (ne) {   // warp-uniform
       case 1: cp_bundle<1>(rec, cls, slots, lane, cp, zs, zc); break;
       case 2: cp_bundle<2>(rec, cls, slots, lane, cp, zs, zc); break;
@@ -1170,7 +1183,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     if ((st = upload(a, a->h_cp, &p, err))) return st;
     T.cp = reinterpret_cast<const uint2*>(p);
     if ((st = upload(a, a->h_cp_bsize, &p, err))) return st;
-    T.cp_bsize = reinterpret_cast<const uint8_t*>(p);
+    T.cp_bsize = reinterpret_cast<const uint32_t*>(p);
     T.n_bundles = (int32_t)a->h_cp_bsize.size();
     if ((st = upload(a, a->h_cp_comm, &p, err))) return st;
     T.cp_comm = reinterpret_cast<const KCpComm*>(p);

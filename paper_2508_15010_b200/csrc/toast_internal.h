@@ -203,7 +203,7 @@ struct DeviceTables {
   int32_t cost_model, n_slots;   // R22: critical path; finish-time slots per candidate
   int32_t n_comm, n_comp;        // R22: edge-duration and compute-time classes
   const uint2* cp = nullptr;     // critical-path stream
-  const uint8_t* cp_bsize = nullptr;   // edges per bundle
+  const uint32_t* cp_bsize = nullptr;  // per bundle: edges | prefetch slot << 4 | prefetch slot << 18 (0x3FFF: none)
   int32_t n_bundles = 0;
   const KCpComm* cp_comm = nullptr;
   const KCpComp* cp_comp = nullptr;
@@ -258,7 +258,7 @@ struct toast_analysis {
   // roles over signatures, signature-keyed templates, absolute frontier terms
   int64_t work_sig_roles = 0, work_tmpl = 0, work_terms = 0;
   std::vector<uint32_t> h_cp;               // critical-path stream (8-B records as 2 x u32)
-  std::vector<uint8_t> h_cp_bsize;          // edges per bundle of the stream
+  std::vector<uint32_t> h_cp_bsize;         // per bundle of the stream: edges | two prefetch hints
   std::vector<toast::KCpComm> h_cp_comm;
   std::vector<toast::KCpComp> h_cp_comp;
   int32_t cost_model = 0;
