@@ -430,20 +430,30 @@ def run_toast(args, cfg, rank, world, local):
     st = T.as_costs(out[:4096])
     assert (st["status"] == 0).all()
 
-    # e2e through the public API with host (pinned) buffers: H2D + kernel + D2H
+    # e2e through the public API with host (pinned) buffers: H2D + kernel + D2H.
+    # The search-facing call (toast_rollout_scores: the sequence + 16-B score/state
+    # key per candidate) is the headline; the full 256-B records are timed beside it.
     h_pre = torch.zeros((N, 32), dtype=torch.int16).pin_memory()
     h_seqs = torch.empty_like(h_pre).pin_memory()
     h_out = torch.empty((N, 256), dtype=torch.uint8).pin_memory()
-    T.rollout_batch(a, h_pre, args.seed, base, h_seqs, h_out, stream=stream)   # warm (scratch alloc)
-    e2e_ms = []
-    for s in range(max(3, min(args.steps, 10))):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        T.rollout_batch(a, h_pre, args.seed, base + s * N, h_seqs, h_out, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-    e2e = allreduce_max(statistics.mean(e2e_ms), world)
+    h_sc = torch.empty((N, 16), dtype=torch.uint8).pin_memory()
+
+    def timed_host(call):
+        call(0)   # warm (scratch allocation)
+        t = []
+        for s in range(max(3, min(args.steps, 10))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            call(s)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t.append(e0.elapsed_time(e1))
+        return allreduce_max(statistics.mean(t), world)
+
+    e2e = timed_host(lambda s: T.rollout_scores(a, h_pre, args.seed, base + s * N, h_seqs, h_sc, stream=stream))
+    e2e_full = timed_host(lambda s: T.rollout_batch(a, h_pre, args.seed, base + s * N, h_seqs, h_out, stream=stream))
+    sc = T.as_scores(h_sc[:4096])
+    assert not np.isnan(sc["score"]).any()
 
     line = None
     if rank == 0:
@@ -486,7 +496,11 @@ def run_toast(args, cfg, rank, world, local):
                                  f"one launch of this size (profiles/ncu_summary.json)"},
             "clocks": clk,
             "e2e": {"value": N * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": N * 64,
-                    "d2h_bytes_per_step": N * (64 + 256)},
+                    "d2h_bytes_per_step": N * (64 + 16),
+                    "call": "toast_rollout_scores (sequence + 16-B score/state key per candidate), pinned host buffers",
+                    "full_records": {"value": N * world / (e2e_full / 1000.0), "unit": UNIT,
+                                     "h2d_bytes_per_step": N * 64, "d2h_bytes_per_step": N * (64 + 256),
+                                     "call": "toast_rollout_batch (256-B toast_cost records)"}},
         }
     if rank == 0 and not args.no_variants and args.cost_model == "sum":
         line["variants"] = {"critical_path": variant_cp(args, cfg, local, stream, flush),

@@ -177,6 +177,27 @@ toast_status toast_eval_batch(const toast_analysis* a, const uint16_t* seqs, int
 toast_status toast_rollout_batch(const toast_analysis* a, const uint16_t* prefixes, int64_t n, uint64_t seed,
                                  uint64_t id_base, uint16_t* out_seqs, toast_cost* out, void* cuda_stream);
 
+/* The search-facing result of one candidate, 16 B: the score C(s) = RT(s) +
+ * MP(s) and the state key (reading R14) — what the
+ * tree backs up and identifies states by.  Bit-identical to the `score` and
+ * `state_key` of the full toast_cost record; a candidate whose record would
+ * carry a nonzero status has score = NaN (0x7FF8000000000000) and state_key =
+ * that status.  For callers that do not need the payload breakdown: a 16-B
+ * record moves 1/16 of the bytes of toast_cost across PCIe on the host path. */
+typedef struct {
+  double score;
+  uint64_t state_key;
+} toast_score;
+
+/* toast_eval_scores / toast_rollout_scores — toast_eval_batch /
+ * toast_rollout_batch with toast_score[n] results (same computation, same
+ * memory rules: all buffers host or all device; device pointers run
+ * asynchronously on cuda_stream, host pointers synchronously). */
+toast_status toast_eval_scores(const toast_analysis* a, const uint16_t* seqs, int64_t n, toast_score* out,
+                               void* cuda_stream);
+toast_status toast_rollout_scores(const toast_analysis* a, const uint16_t* prefixes, int64_t n, uint64_t seed,
+                                  uint64_t id_base, uint16_t* out_seqs, toast_score* out, void* cuda_stream);
+
 /* per-loop axis masks of one sequence (debug / tests; NEXT-1 lowering).
  * masks: uint8[cap]; *n = number of loops. seq is a host pointer. */
 toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], uint8_t* masks, int64_t cap,

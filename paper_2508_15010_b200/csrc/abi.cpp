@@ -172,6 +172,36 @@ toast_status toast_rollout_batch(const toast_analysis* a, const uint16_t* prefix
   return ret(st, err);
 }
 
+toast_status toast_eval_scores(const toast_analysis* a, const uint16_t* seqs, int64_t n, toast_score* out,
+                               void* cuda_stream) {
+  if (!a || n < 0 || (n > 0 && (!seqs || !out))) return fail(TOAST_E_INVALID_ARG, "bad argument");
+  if (!has_device(a)) return fail(TOAST_E_CUDA, "the analysis has no device tables (cuda_device = -1 or no GPU)");
+  if (n == 0) return ret(TOAST_OK, "");
+  std::string err;
+  cudaSetDevice(a->device);
+  bool dev_in = toast::is_device_pointer(seqs), dev_out = toast::is_device_pointer(out);
+  if (dev_in != dev_out) return fail(TOAST_E_INVALID_ARG, "seqs and out must both be host or both be device memory");
+  toast_status st = dev_in ? toast::launch_eval(a, seqs, n, out, cuda_stream, err, true)
+                           : toast::run_host_buffers(const_cast<toast_analysis*>(a), false, seqs, n, 0, 0, nullptr, out,
+                                                     cuda_stream, err, true);
+  return ret(st, err);
+}
+
+toast_status toast_rollout_scores(const toast_analysis* a, const uint16_t* prefixes, int64_t n, uint64_t seed,
+                                  uint64_t id_base, uint16_t* out_seqs, toast_score* out, void* cuda_stream) {
+  if (!a || n < 0 || (n > 0 && (!prefixes || !out || !out_seqs))) return fail(TOAST_E_INVALID_ARG, "bad argument");
+  if (!has_device(a)) return fail(TOAST_E_CUDA, "the analysis has no device tables (cuda_device = -1 or no GPU)");
+  if (n == 0) return ret(TOAST_OK, "");
+  std::string err;
+  cudaSetDevice(a->device);
+  bool d1 = toast::is_device_pointer(prefixes), d2 = toast::is_device_pointer(out_seqs), d3 = toast::is_device_pointer(out);
+  if (d1 != d2 || d1 != d3) return fail(TOAST_E_INVALID_ARG, "buffers must all be host or all be device memory");
+  toast_status st = d1 ? toast::launch_rollout(a, prefixes, n, seed, id_base, out_seqs, out, cuda_stream, err, 1, true)
+                       : toast::run_host_buffers(const_cast<toast_analysis*>(a), true, prefixes, n, seed, id_base,
+                                                 out_seqs, out, cuda_stream, err, true);
+  return ret(st, err);
+}
+
 toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], uint8_t* masks, int64_t cap, int64_t* n) {
   if (!a || !seq || !n) return fail(TOAST_E_INVALID_ARG, "NULL argument");
   *n = a->n_loops;

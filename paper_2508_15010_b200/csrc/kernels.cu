@@ -532,7 +532,7 @@ __device__ __forceinline__ void block_sync(int K) {
 // scores and writes the records.  S.seq holds the candidates on entry.
 template <int NA, bool P2, bool CP>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
-                                           toast_cost* __restrict__ out) {
+                                           void* __restrict__ out, int64_t idx, bool compact) {
   block_sync(K);
   if (warp == 0) {
     uint64_t f0, on, ap;
@@ -854,9 +854,15 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     const uint64_t pk = pk_all;
     const double RT = __ddiv_rn(tt, T.t0);
     const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
-    if (valid) {
+    if (valid && compact) {
+      // toast_score (include/toast.h): score | state key, or NaN | status
+      const bool ok = status == 0;
+      const unsigned long long w0 = ok ? (unsigned long long)__double_as_longlong(__dadd_rn(RT, MP)) : 0x7FF8000000000000ULL;
+      const unsigned long long w1 = ok ? key : (unsigned long long)status;
+      reinterpret_cast<uint4*>(out)[idx] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+    } else if (valid) {
       // record layout = toast_cost (include/toast.h), written as 16 x 16 B
-      uint4* dst = reinterpret_cast<uint4*>(out);
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<toast_cost*>(out) + idx);
       const bool ok = status == 0;
       auto d2 = [](double x) { return (unsigned long long)__double_as_longlong(x); };
       const unsigned long long w0 = ok ? d2(tt) : 0ULL, w1 = ok ? d2(__dadd_rn(RT, MP)) : 0ULL;
@@ -910,7 +916,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
 
 template <int NA, bool P2, bool CP>
 __global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
-                                                         int64_t n, toast_cost* __restrict__ out) {
+                                                         int64_t n, void* __restrict__ out, bool compact) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
   const int64_t nbatch = (n + 31) / 32;
@@ -918,7 +924,7 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS :
     const int64_t i = b * 32 + lane;
     const bool valid = i < n;
     if (warp == 0) load_seq(S, seqs + i * 32, lane, valid);
-    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out + i);
+    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, i, compact);
   }
 }
 
@@ -941,7 +947,7 @@ template <int NA, bool P2, bool CP>
 __global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
-                                                            toast_cost* __restrict__ out, int64_t rep) {
+                                                            void* __restrict__ out, int64_t rep, bool compact) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
   const int64_t nbatch = (n + 31) / 32;
@@ -1012,7 +1018,7 @@ __global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS :
                             sp<uint32_t>(S.seq)[(4 * k + 3) * 32 + lane]);
     }
     }   // warp 0
-    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out + i);
+    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, i, compact);
   }
 }
 
@@ -1206,10 +1212,10 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
 
 void free_tables(toast_analysis* a) {
   if (a->device >= 0) cudaSetDevice(a->device);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < PIPE_STREAMS; ++i)
     if (a->pipe_stream[i]) cudaStreamDestroy((cudaStream_t)a->pipe_stream[i]);
   if (a->pipe_event) cudaEventDestroy((cudaEvent_t)a->pipe_event);
-  a->pipe_stream[0] = a->pipe_stream[1] = nullptr;
+  for (int i = 0; i < PIPE_STREAMS; ++i) a->pipe_stream[i] = nullptr;
   a->pipe_event = nullptr;
   if (a->spool.d) cudaFree(a->spool.d);
   if (a->spool.h_pre) cudaFreeHost(a->spool.h_pre);
@@ -1236,8 +1242,8 @@ static inline int pick_k(const toast_analysis* a, int64_t batches, const int32_t
 }
 static inline int kidx(int K) { return K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0; }
 
-toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, toast_cost* d_out, void* stream,
-                         std::string& err) {
+toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, void* d_out, void* stream,
+                         std::string& err, bool compact) {
   if (n <= 0) return TOAST_OK;
   const int64_t batches = (n + 31) / 32;
   const int K = pick_k(a, batches, a->occ_eval);
@@ -1247,7 +1253,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
-    toast_eval_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_seqs, n, d_out);
+    toast_eval_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_seqs, n, d_out, compact);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());
@@ -1255,7 +1261,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
 }
 
 toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
-                            uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err, int64_t rep) {
+                            uint16_t* d_seqs, void* d_out, void* stream, std::string& err, int64_t rep, bool compact) {
   if (n <= 0) return TOAST_OK;
   const int64_t batches = (n + 31) / 32;
   const int K = pick_k(a, batches, a->occ_roll);
@@ -1265,7 +1271,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   cudaStream_t st = (cudaStream_t)stream;
   const DeviceTables& T = a->dt;
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
-    toast_rollout_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep);
+    toast_rollout_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep, compact);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());
@@ -1349,10 +1355,12 @@ static bool is_pinned(const void* p) {
 // buffers are pipelined in chunks on two internal streams (after the caller's
 // stream's prior work) so PCIe transfers overlap the kernels.
 toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h_in, int64_t n, uint64_t seed,
-                              uint64_t id_base, uint16_t* h_seqs, toast_cost* h_out, void* stream, std::string& err) {
+                              uint64_t id_base, uint16_t* h_seqs, void* h_out, void* stream, std::string& err,
+                              bool compact) {
   if (n <= 0) return TOAST_OK;
   std::lock_guard<std::mutex> lk(a->scratch_mu);
-  const size_t in_b = (size_t)n * 64, out_b = (size_t)n * sizeof(toast_cost);
+  const size_t rec = compact ? sizeof(toast_score) : sizeof(toast_cost);
+  const size_t in_b = (size_t)n * 64, out_b = (size_t)n * rec;
   const size_t need = out_b + in_b + (rollout ? in_b : 0);
   if (a->scratch_bytes < need) {
     if (a->scratch) cudaFree(a->scratch);
@@ -1362,7 +1370,8 @@ toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h
     a->scratch_bytes = need;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  toast_cost* d_out = reinterpret_cast<toast_cost*>(a->scratch);
+  char* d_out = reinterpret_cast<char*>(a->scratch);
+  char* h_outc = reinterpret_cast<char*>(h_out);
   uint16_t* d_in = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(a->scratch) + out_b);
   uint16_t* d_seqs = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(a->scratch) + out_b + in_b);
   const int64_t wave = (int64_t)std::min(a->occ_eval[0], a->occ_roll[0]) * a->n_sms * 32;
@@ -1370,8 +1379,8 @@ toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h
                          (!rollout || is_pinned(h_seqs));
   if (!pipelined) {
     TOAST_CUDA(cudaMemcpyAsync(d_in, h_in, in_b, cudaMemcpyHostToDevice, s));
-    toast_status st = rollout ? launch_rollout(a, d_in, n, seed, id_base, d_seqs, d_out, stream, err, 1)
-                              : launch_eval(a, d_in, n, d_out, stream, err);
+    toast_status st = rollout ? launch_rollout(a, d_in, n, seed, id_base, d_seqs, d_out, stream, err, 1, compact)
+                              : launch_eval(a, d_in, n, d_out, stream, err, compact);
     if (st) return st;
     TOAST_CUDA(cudaMemcpyAsync(h_out, d_out, out_b, cudaMemcpyDeviceToHost, s));
     if (rollout) TOAST_CUDA(cudaMemcpyAsync(h_seqs, d_seqs, in_b, cudaMemcpyDeviceToHost, s));
@@ -1379,25 +1388,32 @@ toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h
     return TOAST_OK;
   }
   if (!a->pipe_stream[0]) {
-    for (int i = 0; i < 2; ++i) TOAST_CUDA(cudaStreamCreateWithFlags((cudaStream_t*)&a->pipe_stream[i], cudaStreamNonBlocking));
+    for (int i = 0; i < PIPE_STREAMS; ++i) TOAST_CUDA(cudaStreamCreateWithFlags((cudaStream_t*)&a->pipe_stream[i], cudaStreamNonBlocking));
     TOAST_CUDA(cudaEventCreateWithFlags((cudaEvent_t*)&a->pipe_event, cudaEventDisableTiming));
   }
   TOAST_CUDA(cudaEventRecord((cudaEvent_t)a->pipe_event, s));
-  for (int i = 0; i < 2; ++i) TOAST_CUDA(cudaStreamWaitEvent((cudaStream_t)a->pipe_stream[i], (cudaEvent_t)a->pipe_event, 0));
-  const int64_t chunk = std::max<int64_t>(wave / 2, 32);
+  // chunks round-robin over PIPE_STREAMS streams: a stream's next H2D waits only
+  // for its own previous chunk's D2H, so copies in both directions and kernels overlap
+  const char* ps_env = getenv("TOAST_PIPE_STREAMS");
+  const char* cd_env = getenv("TOAST_PIPE_CHUNK_DIV");
+  const int nps = ps_env ? std::max(1, std::min(PIPE_STREAMS, atoi(ps_env))) : 4;
+  const int64_t cdiv = cd_env ? std::max(1, atoi(cd_env)) : 2;
+  for (int i = 0; i < nps; ++i) TOAST_CUDA(cudaStreamWaitEvent((cudaStream_t)a->pipe_stream[i], (cudaEvent_t)a->pipe_event, 0));
+  const int64_t chunk = std::max<int64_t>(wave / cdiv, 32);
   int c = 0;
   for (int64_t o = 0; o < n; o += chunk, ++c) {
     const int64_t m = std::min(chunk, n - o);
-    cudaStream_t ps = (cudaStream_t)a->pipe_stream[c & 1];
+    cudaStream_t ps = (cudaStream_t)a->pipe_stream[c % nps];
     TOAST_CUDA(cudaMemcpyAsync(d_in + o * 32, h_in + o * 32, (size_t)m * 64, cudaMemcpyHostToDevice, ps));
     toast_status st = rollout ? launch_rollout(a, d_in + o * 32, m, seed, id_base + (uint64_t)o, d_seqs + o * 32,
-                                               d_out + o, ps, err, 1)
-                              : launch_eval(a, d_in + o * 32, m, d_out + o, ps, err);
+                                               d_out + (size_t)o * rec, ps, err, 1, compact)
+                              : launch_eval(a, d_in + o * 32, m, d_out + (size_t)o * rec, ps, err, compact);
     if (st) return st;
-    TOAST_CUDA(cudaMemcpyAsync(h_out + o, d_out + o, (size_t)m * sizeof(toast_cost), cudaMemcpyDeviceToHost, ps));
+    TOAST_CUDA(cudaMemcpyAsync(h_outc + (size_t)o * rec, d_out + (size_t)o * rec, (size_t)m * rec,
+                               cudaMemcpyDeviceToHost, ps));
     if (rollout) TOAST_CUDA(cudaMemcpyAsync(h_seqs + o * 32, d_seqs + o * 32, (size_t)m * 64, cudaMemcpyDeviceToHost, ps));
   }
-  for (int i = 0; i < 2; ++i) TOAST_CUDA(cudaStreamSynchronize((cudaStream_t)a->pipe_stream[i]));
+  for (int i = 0; i < nps; ++i) TOAST_CUDA(cudaStreamSynchronize((cudaStream_t)a->pipe_stream[i]));
   return TOAST_OK;
 }
 

@@ -166,6 +166,7 @@ constexpr uint32_t ZERO_COMM = 0xFFFFFFFFu; // an edge that never communicates: 
 // a 0.0 entry, a non-last edge names the trash slot); no edge of a bundle
 // reads a slot its bundle writes.
 constexpr int CP_EMAX = 8;
+constexpr int PIPE_STREAMS = 8;   // host-buffer pipeline streams (at most)
 constexpr int CP_WINDOW = 96;
 static_assert(sizeof(KCpComm) == 16 && sizeof(KCpComp) == 16, "cp records");
 static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
@@ -288,7 +289,7 @@ struct toast_analysis {
   int32_t occ_eval[4] = {0, 0, 0, 0}, occ_roll[4] = {0, 0, 0, 0};   // blocks per SM for K = 1, 2, 4, 8
   int32_t n_sms = 0, k_throughput = 1;
   int32_t k_force = 0;   // autotune: every launch uses this K (0: pick)
-  void* pipe_stream[2] = {nullptr, nullptr};   // host-buffer path: chunked H2D / kernel / D2H overlap
+  void* pipe_stream[toast::PIPE_STREAMS] = {};      // host-buffer path: chunked H2D / kernel / D2H overlap
   // search buffers, kept between searches (a search that finds them in use allocates its own)
   struct SearchPool {
     void* d = nullptr;
@@ -315,15 +316,18 @@ toast_status lower_program(const toast_analysis* a, const uint16_t* seq, std::st
 toast_status upload_tables(toast_analysis* a, std::string& err);
 toast_status autotune_k(toast_analysis* a, std::string& err);   // measured throughput K (after upload_tables)
 void free_tables(toast_analysis* a);
-toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, toast_cost* d_out, void* stream,
-                         std::string& err);
+// d_out: toast_cost[n], or toast_score[n] when compact
+toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, void* d_out, void* stream,
+                         std::string& err, bool compact = false);
 toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
-                            uint16_t* d_seqs, toast_cost* d_out, void* stream, std::string& err, int64_t rep = 1);
+                            uint16_t* d_seqs, void* d_out, void* stream, std::string& err, int64_t rep = 1,
+                            bool compact = false);
 // search round reduction (K3): per leaf, reward sum + best candidate; d_out = [L] records of leaf_red_bytes()
 toast_status launch_round_reduce(const toast_cost* d_lcost, const uint16_t* d_lpre, const toast_cost* d_cost,
                                  const uint16_t* d_seqs, int L, int R, void* d_out, void* stream, std::string& err);
 size_t leaf_red_bytes();
 toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h_in, int64_t n, uint64_t seed,
-                              uint64_t id_base, uint16_t* h_seqs, toast_cost* h_out, void* stream, std::string& err);
+                              uint64_t id_base, uint16_t* h_seqs, void* h_out, void* stream, std::string& err,
+                              bool compact = false);
 bool is_device_pointer(const void* p);
 }  // namespace toast

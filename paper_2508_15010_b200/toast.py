@@ -83,6 +83,10 @@ SEARCH_RESULT_DTYPE = np.dtype([
 
 ROOT_STAT_DTYPE = np.dtype([("visits", "<i8"), ("value_sum", "<f8")])
 
+# toast_score (include/toast.h): score, or NaN with the status in state_key
+SCORE_DTYPE = np.dtype([("score", "<f8"), ("state_key", "<u8")])
+assert SCORE_DTYPE.itemsize == 16
+
 _P = ctypes.c_void_p
 _sigs = {
     "toast_load_graph": [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(_Axis), ctypes.c_int32,
@@ -95,6 +99,8 @@ _sigs = {
     "toast_dump_analysis": [_P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
     "toast_eval_batch": [_P, _P, ctypes.c_int64, _P, _P],
     "toast_rollout_batch": [_P, _P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _P, _P, _P],
+    "toast_eval_scores": [_P, _P, ctypes.c_int64, _P, _P],
+    "toast_rollout_scores": [_P, _P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _P, _P, _P],
     "toast_materialize": [_P, _P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
     "toast_lower": [_P, _P, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
     "toast_search_root_stats": [_P, _P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
@@ -271,6 +277,30 @@ def rollout_batch(a: Analysis, prefixes, seed: int, id_base: int, out_seqs, out,
     _check(_lib.toast_rollout_batch(a._h, _ptr(prefixes), int(n), int(seed), int(id_base), _ptr(out_seqs),
                                     _ptr(out), _stream(stream)))
     return out_seqs, out
+
+
+def eval_scores(a: Analysis, seqs, out, stream=None, n: int | None = None):
+    """toast_eval_scores: seqs uint16[n][32] -> out 16-B toast_score records (same memory kind)."""
+    n = _len(seqs, 64) if n is None else n
+    assert _len(out, 16) >= n
+    _check(_lib.toast_eval_scores(a._h, _ptr(seqs), int(n), _ptr(out), _stream(stream)))
+    return out
+
+
+def rollout_scores(a: Analysis, prefixes, seed: int, id_base: int, out_seqs, out, stream=None, n: int | None = None):
+    """toast_rollout_scores: toast_rollout_batch with 16-B toast_score results."""
+    n = _len(prefixes, 64) if n is None else n
+    assert _len(out, 16) >= n
+    _check(_lib.toast_rollout_scores(a._h, _ptr(prefixes), int(n), int(seed), int(id_base), _ptr(out_seqs),
+                                     _ptr(out), _stream(stream)))
+    return out_seqs, out
+
+
+def as_scores(out) -> np.ndarray:
+    """View a torch uint8[n,16] / numpy buffer of toast_score records as SCORE_DTYPE."""
+    if hasattr(out, "data_ptr"):
+        out = out.detach().cpu().contiguous().numpy()
+    return np.ascontiguousarray(out).view(SCORE_DTYPE).reshape(-1)
 
 
 def materialize(a: Analysis, seq) -> np.ndarray:

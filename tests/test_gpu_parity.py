@@ -385,3 +385,38 @@ def test_critical_path_random_programs():
         assert_same(gc, oc, ir)
         ran += 1
     assert ran >= 15
+
+
+@pytest.mark.parametrize("name", ["mlp_c", "gpt2", "gpt2_4ax_np2", "unet"])
+def test_compact_scores_equal_full_records(name):
+    """toast_eval_scores / toast_rollout_scores: the 16-B results are the full
+    records' score and state key bit for bit (NaN | status for a bad candidate),
+    on device pointers and through the pinned host-buffer pipeline."""
+    import torch
+    T = _T()
+    a, o = setup(name)
+    n = 4096 if name != "unet" else 1024
+    seqs = candidates.uniform(n, o.n_actions + 2, seed=3, bad_frac=0.05)
+    full = gpu_eval(a, seqs)
+    d_seqs = torch.from_numpy(np.ascontiguousarray(seqs).view(np.int16)).cuda()
+    d_sc = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
+    T.eval_scores(a, d_seqs, d_sc)
+    torch.cuda.synchronize()
+    sc = T.as_scores(d_sc)
+    ok = full["status"] == 0
+    assert ok.any() and (~ok).any()
+    assert (sc["score"][ok].view(np.uint64) == full["score"][ok].view(np.uint64)).all()
+    assert (sc["state_key"][ok] == full["state_key"][ok]).all()
+    assert np.isnan(sc["score"][~ok]).all() and (sc["state_key"][~ok] == full["status"][~ok]).all()
+    # rollouts, device and pinned host buffers (large enough for the chunked pipeline)
+    m = max(2 * a.preferred_batch() + 77, 4096)
+    pre = np.zeros((m, 32), np.uint16)
+    gs, gc = gpu_rollout(a, pre, 21, 9)
+    h_pre = torch.zeros((m, 32), dtype=torch.int16).pin_memory()
+    h_seq = torch.empty_like(h_pre).pin_memory()
+    h_sc = torch.empty((m, 16), dtype=torch.uint8).pin_memory()
+    T.rollout_scores(a, h_pre, 21, 9, h_seq, h_sc)
+    hs = T.as_scores(h_sc)
+    assert np.array_equal(h_seq.numpy().view(np.uint16), gs)
+    assert (hs["score"].view(np.uint64) == gc["score"].view(np.uint64)).all()
+    assert (hs["state_key"] == gc["state_key"]).all()
