@@ -302,3 +302,49 @@ def test_gpu_search_under_contraction_finds_bruteforce_optimum(name):
     ro, _ = o.search(seed=3, max_evals=3000, L=4, R=8, patience=3)
     assert int(r["rounds"]) == int(ro["rounds"]) and int(r["evals"]) == int(ro["evals"])
     assert np.array_equal(r["best_seq"], ro["best_seq"]) and r["best"]["score"] == ro["best"]["score"]
+
+
+@pytest.mark.parametrize("name", ["gpt24", "unet"])
+def test_library_contraction_definition_at_full_size(name):
+    """The library's contraction of the full-size configs checked against the
+    definition directly: no conflict joined by the contracted graph, and
+    every uncontracted edge would join one (maximal) — the latter through the
+    merged node only, since a merge creates exactly the paths through it.  The M
+    edges come from the oracle's loop table (equal to the library's, pinned by
+    test_library_host.py::test_h0_analysis_equals_oracle)."""
+    T = _T()
+    c = configs.get(name)
+    a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=-1,
+                         grouping=T.GROUP_CONTRACTION)
+    d = a.dump()
+    o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth)
+    assert d["loops"] == o.dump()["loops"]
+    edges = [tuple(e) for e in o.edges()]
+    cn = d["cnode"]
+    conf = d["conflicts"]
+    adj, radj = _adj(edges, cn), defaultdict(set)
+    for x, ys in list(adj.items()):
+        for y in ys:
+            radj[y].add(x)
+    partners = defaultdict(set)
+    for _op, u, v, _s, _s0 in conf:
+        partners[cn[u]].add(cn[v])
+        partners[cn[v]].add(cn[u])
+    # no conflict joined: for every node with conflict endpoints, no partner node is reachable from it
+    for U, ps in partners.items():
+        assert U not in ps
+        assert not (ps & _reach(adj, U)), U
+    # maximal: merging the two nodes of any split edge joins a conflict through the merged node
+    split = {(cn[a_], cn[b]) for a_, b in edges if cn[a_] != cn[b]}
+    assert len(split) > 0 and d["contract_rejected"] >= len(split)
+    for X, Y in split:
+        fwd = _reach(adj, X) | _reach(adj, Y)
+        bwd = _reach(radj, X) | _reach(radj, Y)
+        joined = any(partners[p] & fwd for p in bwd if p in partners)
+        assert joined, (X, Y)
+    # sets = unordered node pairs
+    key_set = {}
+    for _op, u, v, s, _s0 in conf:
+        k = tuple(sorted((cn[u], cn[v])))
+        assert key_set.setdefault(k, s) == s
+    assert len(set(key_set.values())) == len(key_set)
