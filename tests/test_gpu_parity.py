@@ -365,26 +365,30 @@ def test_critical_path_full_size_sampled():
         assert_same(gc[i:i + 1], c1, f"row {i}")
 
 
-def test_critical_path_random_programs():
-    """R22 on random programs (repeated operands, a size-3 axis)."""
+@pytest.mark.parametrize("grouping", [0, 1])
+def test_critical_path_random_programs(grouping):
+    """R22 on random programs (unary chains, diamonds and repeated operands —
+    the walk's aliases, never-communicating and dominated edges, in-bundle
+    forwarding — and a size-3 axis), under both conflict groupings."""
     T = _T()
     from workloads import models
     ran = 0
-    for seed in range(30):
-        ir = models.random_program(seed, n_ops=20, max_ext=8)
+    for seed in range(60):
+        ir = models.random_program(seed, n_ops=20 + seed % 3 * 10, max_ext=8)
         axes = [("a", 2, 1e10), ("b", 3, 1e11)] if seed % 2 else [("a", 2, 1e10), ("b", 4, 1e11)]
         try:
-            a = T.build_analysis(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cuda_device=0, cost_model=T.COST_CRITICAL_PATH)
+            a = T.build_analysis(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cuda_device=0, cost_model=T.COST_CRITICAL_PATH,
+                                 grouping=grouping)
         except T.ToastError:
             continue
-        o = Oracle(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cost_model=1)
+        o = Oracle(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cost_model=1, grouping=grouping)
         pre = np.zeros((256, 32), np.uint16)
         os_, oc = o.rollout(pre, seed=seed)
         gs, gc = gpu_rollout(a, pre, seed, 0)
         assert np.array_equal(gs, os_)
         assert_same(gc, oc, ir)
         ran += 1
-    assert ran >= 15
+    assert ran >= 30
 
 
 @pytest.mark.parametrize("name", ["mlp_c", "gpt2", "gpt2_4ax_np2", "unet"])
