@@ -60,3 +60,43 @@ def search_root_parallel(a: "T.Analysis", opts: "T.SearchOptions", group=None, s
 def rank_id_base(rank: int, per_rank: int) -> int:
     """Disjoint Philox counter ranges per rank for weak-scaled rollouts."""
     return rank << 40
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple:
+    """The contiguous rows [lo, hi) of an n-row batch that rank evaluates:
+    the first n % world ranks take one row more."""
+    q, r = divmod(n, world)
+    lo = rank * q + min(rank, r)
+    return lo, lo + q + (1 if rank < r else 0)
+
+
+def eval_sharded(a: "T.Analysis", seqs, group=None, stream=None, compact: bool = False, _evaluate=None):
+    """Data-parallel toast_eval_batch over the ranks of `group`:
+    every rank holds the same global batch seqs (uint16[n][32], device tensor on
+    NCCL), evaluates its contiguous rows [lo, hi) with the library, and one
+    all_gather_into_tensor of the fixed-size result records (the last ranks'
+    slices padded to the largest) gives every rank all n results in batch
+    order.  Returns a uint8 [n, record bytes] tensor (256-B toast_cost, or 16-B
+    toast_score when compact).  There is no exchange inside the evaluation:
+    candidates are independent.  _evaluate(seqs_slice, out_slice) replaces the
+    library call in host-logic tests only."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n = int(seqs.shape[0])
+    rec = 16 if compact else 256
+    lo, hi = shard_range(n, rank, world)
+    width = shard_range(n, 0, world)[1]            # the largest slice
+    local = torch.zeros((width, rec), dtype=torch.uint8, device=seqs.device)
+    if hi > lo:
+        if _evaluate is not None:
+            _evaluate(seqs[lo:hi], local[: hi - lo])
+        elif compact:
+            T.eval_scores(a, seqs[lo:hi], local[: hi - lo], stream=stream)
+        else:
+            T.eval_batch(a, seqs[lo:hi], local[: hi - lo], stream=stream)
+    gathered = torch.empty((world * width, rec), dtype=torch.uint8, device=seqs.device)
+    dist.all_gather_into_tensor(gathered, local, group=group)
+    parts = [gathered[r * width: r * width + (shard_range(n, r, world)[1] - shard_range(n, r, world)[0])]
+             for r in range(world)]
+    return torch.cat(parts, dim=0)

@@ -270,6 +270,35 @@ def test_root_parallel_search_nccl_single_rank():
     assert len(trace) == int(r["rounds"]) and trace[-1] == r["best"]["score"]
 
 
+def test_eval_sharded_nccl_single_rank():
+    """parallel.eval_sharded over NCCL at world size 1: the
+    gathered records equal toast_eval_batch's, full and compact."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    T = _T()
+    from paper_2508_15010_b200 import parallel as P
+    a, o = setup("gpt2")
+    seqs, oc = o.rollout(np.zeros((1000, 32), np.uint16), seed=8)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        d = torch.from_numpy(np.ascontiguousarray(seqs).view(np.int16)).cuda()
+        full = P.eval_sharded(a, d)
+        comp = P.eval_sharded(a, d, compact=True)
+    finally:
+        dist.destroy_process_group()
+    assert T.as_costs(full).tobytes() == oc.tobytes()
+    sc = T.as_scores(comp)
+    assert (sc["score"].view(np.uint64) == oc["score"].view(np.uint64)).all() and (sc["state_key"] == oc["state_key"]).all()
+
+
 def test_random_programs_parity_including_repeated_operands():
     """Random programs (repeated operands such as mul(x, x) / matmul(x, x) take
     the per-edge path; the rest go through edge templates), two meshes, oracle

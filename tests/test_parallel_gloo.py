@@ -96,3 +96,54 @@ def test_root_parallel_exchange_two_ranks():
     # patience 2: it stops after two non-improving rounds or runs all 4
     stops = [o[0] for o in out0]
     assert stops.count(True) <= 1 and (not any(stops[:-1]))
+
+
+def _eval_worker(rank, world, port, n, q):
+    """eval_sharded's slicing and gather on gloo, with a stand-in evaluator that
+    writes each row's global index into its record (the library needs a GPU)."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_15010_b200 import parallel as P
+        seqs = torch.arange(n * 32, dtype=torch.int16).reshape(n, 32) if n else torch.zeros((0, 32), dtype=torch.int16)
+        seen = []
+
+        def fake(sl, out):
+            seen.append(int(sl.shape[0]))
+            out.view(torch.int64)[:, 0] = sl[:, 0].to(torch.int64) // 32   # the global row index
+            out.view(torch.int64)[:, 1] = rank
+
+        res = P.eval_sharded(None, seqs, _evaluate=fake)
+        q.put((rank, res.view(torch.int64)[:, 0].tolist(), res.view(torch.int64)[:, 1].tolist(), seen))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [0, 7, 101])
+def test_eval_sharded_two_ranks(n):
+    """contiguous per-rank slices (ragged last slice, empty batch),
+    one all-gather, every rank ends with all n records in batch order."""
+    from paper_2508_15010_b200.parallel import shard_range
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_eval_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, rows, owner, seen in res:
+        assert rows == list(range(n))
+        expect = []
+        for r in range(world):
+            lo_r, hi_r = shard_range(n, r, world)
+            expect += [r] * (hi_r - lo_r)
+        assert owner == expect
+        lo, hi = shard_range(n, rank, world)
+        assert seen == ([hi - lo] if hi > lo else [])
