@@ -900,8 +900,13 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     // the same result dim and operand dim (none off the result: no partial sum)
     // has D == U and P empty for every candidate: it never communicates and
     // never grows a temporary, so it is left out of the tables altogether.
+    // So is an edge from a def op no action can shard (D and P empty: at most
+    // free slices, C11 phase 3).
     auto never_communicates = [&](int32_t d, int32_t t, uint32_t um) {
       const uint32_t sd = a->op_sig[d], su = a->op_sig[t];
+      bool any = false;   // a def op no action can shard: D and P are empty, at most free slices
+      for (int r = 0; r < 8; ++r) any |= (a->h_sig_roles[(size_t)sd * 8 + r] & 0x3FF) != NO_ACOLOR;
+      if (!any) return true;
       if ((a->h_sig_mr[sd] & 0xFFFF) != (a->h_sig_mr[su] & 0xFFFF)) return false;
       const uint32_t rd = a->h_sig_resdim[sd];
       for (int r = 0; r < 8; ++r) {
@@ -1194,6 +1199,7 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     auto zero_edge = [&](int32_t t, size_t k) {
       const int32_t d = g->values[g->ops[t].operands[k]].def_op;
       const uint32_t sd = a->op_sig[d], su = a->op_sig[t];
+      if (!shardable_roles(sd)) return true;   // a def no action can shard: at most free slices
       if ((a->h_sig_mr[sd] & 0xFFFF) != (a->h_sig_mr[su] & 0xFFFF)) return false;
       const uint32_t rd = a->h_sig_resdim[sd], um = use_dimof(t, k), sh = shardable_roles(sd);
       for (int r = 0; r < 8; ++r) {
