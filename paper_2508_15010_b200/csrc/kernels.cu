@@ -1195,14 +1195,19 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     T.cp_comm = reinterpret_cast<const KCpComm*>(p);
     if ((st = upload(a, a->h_cp_comp, &p, err))) return st;
     T.cp_comp = reinterpret_cast<const KCpComp*>(p);
-    int max_blocks = 0;
-    for (int i = 0; i < 4; ++i) max_blocks = std::max(max_blocks, std::max(a->occ_eval[i], a->occ_roll[i]));
-    const size_t bytes = (size_t)max_blocks * sms * (size_t)cp_stride(T) * 32 *
-                         sizeof(double);
-    void* d = nullptr;
-    TOAST_CUDA(cudaMalloc(&d, bytes));
-    a->dev_allocs.push_back(d);
-    T.cp_scratch = reinterpret_cast<double*>(d);
+    // Finish-slot scratch is allocated per launch, stream-ordered, from this
+    // analysis' own pool (kept, not released): concurrent calls on different
+    // streams — the host-buffer pipeline's chunks, or a caller's — each get
+    // their own, since blocks index it by blockIdx.
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = a->device;
+    cudaMemPool_t pool = nullptr;
+    TOAST_CUDA(cudaMemPoolCreate(&pool, &props));
+    a->cp_pool = pool;
+    uint64_t keep = UINT64_MAX;
+    TOAST_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   }
   a->warps_per_block = 1;
   a->eval_blocks = sms * a->occ_eval[0];
@@ -1215,6 +1220,11 @@ void free_tables(toast_analysis* a) {
   for (int i = 0; i < PIPE_STREAMS; ++i)
     if (a->pipe_stream[i]) cudaStreamDestroy((cudaStream_t)a->pipe_stream[i]);
   if (a->pipe_event) cudaEventDestroy((cudaEvent_t)a->pipe_event);
+  if (a->cp_pool) {
+    cudaDeviceSynchronize();
+    cudaMemPoolDestroy((cudaMemPool_t)a->cp_pool);
+    a->cp_pool = nullptr;
+  }
   for (int i = 0; i < PIPE_STREAMS; ++i) a->pipe_stream[i] = nullptr;
   a->pipe_event = nullptr;
   if (a->spool.d) cudaFree(a->spool.d);
@@ -1242,6 +1252,12 @@ static inline int pick_k(const toast_analysis* a, int64_t batches, const int32_t
 }
 static inline int kidx(int K) { return K >= 8 ? 3 : K >= 4 ? 2 : K >= 2 ? 1 : 0; }
 
+// the critical-path walk's finish-slot scratch for one launch of `blocks` blocks
+static cudaError_t cp_scratch_alloc(const toast_analysis* a, int64_t blocks, cudaStream_t st, double** out) {
+  const size_t bytes = (size_t)blocks * cp_stride(a->dt) * 32 * sizeof(double);
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(out), bytes, (cudaMemPool_t)a->cp_pool, st);
+}
+
 toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, void* d_out, void* stream,
                          std::string& err, bool compact) {
   if (n <= 0) return TOAST_OK;
@@ -1251,12 +1267,14 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const dim3 g((unsigned)blocks), b(32 * K);
   const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig);
   cudaStream_t st = (cudaStream_t)stream;
-  const DeviceTables& T = a->dt;
+  DeviceTables T = a->dt;
+  if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
     toast_eval_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_seqs, n, d_out, compact);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());
+  if (T.cp_scratch) TOAST_CUDA(cudaFreeAsync(T.cp_scratch, st));
   return TOAST_OK;
 }
 
@@ -1269,12 +1287,14 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const dim3 g((unsigned)blocks), b(32 * K);
   const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig);
   cudaStream_t st = (cudaStream_t)stream;
-  const DeviceTables& T = a->dt;
+  DeviceTables T = a->dt;
+  if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
     toast_rollout_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep, compact);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());
+  if (T.cp_scratch) TOAST_CUDA(cudaFreeAsync(T.cp_scratch, st));
   return TOAST_OK;
 }
 

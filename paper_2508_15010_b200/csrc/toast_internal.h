@@ -208,7 +208,7 @@ struct DeviceTables {
   int32_t n_bundles = 0;
   const KCpComm* cp_comm = nullptr;
   const KCpComp* cp_comp = nullptr;
-  double* cp_scratch = nullptr;  // per resident block: [n_comm + n_comp + n_slots][32] doubles
+  double* cp_scratch = nullptr;  // per launched block: [cp_stride][32] doubles (allocated per launch)
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -301,6 +301,7 @@ struct toast_analysis {
     bool in_use = false;
   } spool;
   void* pipe_event = nullptr;
+  void* cp_pool = nullptr;      // cudaMemPool_t of the critical-path scratch (R22)
 };
 
 namespace toast {

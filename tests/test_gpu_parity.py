@@ -453,3 +453,36 @@ def test_compact_scores_equal_full_records(name):
     assert np.array_equal(h_seq.numpy().view(np.uint16), gs)
     assert (hs["score"].view(np.uint64) == gc["score"].view(np.uint64)).all()
     assert (hs["state_key"] == gc["state_key"]).all()
+
+
+def test_critical_path_concurrent_streams_and_host_pipeline():
+    """R22's per-launch finish-slot scratch: the pinned host-buffer pipeline
+    (chunks on several streams) and two calls racing on two streams give the
+    device path's records bit for bit."""
+    import torch
+    T = _T()
+    a, o = setup_cp("gpt2")
+    m = 3 * a.preferred_batch() + 123
+    pre = np.zeros((m, 32), np.uint16)
+    gs, gc = gpu_rollout(a, pre, 31, 0)
+    h_pre = torch.zeros((m, 32), dtype=torch.int16).pin_memory()
+    h_seq = torch.empty_like(h_pre).pin_memory()
+    h_out = torch.empty((m, 256), dtype=torch.uint8).pin_memory()
+    T.rollout_batch(a, h_pre, 31, 0, h_seq, h_out)
+    assert np.array_equal(h_seq.numpy().view(np.uint16), gs)
+    assert T.as_costs(h_out).tobytes() == gc.tobytes()
+    d_seqs = torch.from_numpy(np.ascontiguousarray(gs).view(np.int16)).cuda()
+    outs = [torch.empty((m, 256), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for s, out in zip(streams, outs):
+            T.eval_batch(a, d_seqs, out, stream=s)
+    torch.cuda.synchronize()
+    for out in outs:
+        assert T.as_costs(out).tobytes() == gc.tobytes()
+    # sampled rows against the oracle
+    for i in np.random.default_rng(5).choice(m, size=16, replace=False):
+        s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=31, id_base=int(i))
+        assert np.array_equal(gs[i], s1[0])
+        assert_same(gc[i:i + 1], c1, f"row {i}")
