@@ -37,6 +37,9 @@
 #ifndef TOAST_CP_MIN_BLOCKS
 #define TOAST_CP_MIN_BLOCKS 2   // critical-path instantiations (register-heavier bundled walk)
 #endif
+#ifndef TOAST_NA3_MIN_BLOCKS
+#define TOAST_NA3_MIN_BLOCKS 2   // 3-4 axis meshes
+#endif
 #ifndef TOAST_MIN_BLOCKS
 #define TOAST_MIN_BLOCKS 3
 #endif
@@ -915,7 +918,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, void* __restrict__ out, bool compact) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
@@ -944,7 +947,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : 2)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
+__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
                                                             void* __restrict__ out, int64_t rep, bool compact) {
