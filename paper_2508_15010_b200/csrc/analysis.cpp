@@ -241,13 +241,22 @@ static void build_contraction_sets(toast_analysis* a, int64_t NL, const std::vec
   }
   DSU cg(NL);
   std::vector<int32_t> stack;
-  auto merge_adj = [&](std::vector<int32_t>& into, std::vector<int32_t>& from, int32_t z) {
-    for (int32_t v : from) into.push_back(v);
+  // adjacency lists are concatenated (the shorter into the longer) and
+  // compacted (roots, no duplicates, no self) only when they have doubled
+  // since their last compaction, so a large node absorbing many small ones
+  // costs amortised linear time
+  std::vector<size_t> compacted(NL, 0), in_compacted(NL, 0);
+  auto merge_adj = [&](std::vector<int32_t>& into, std::vector<int32_t>& from, size_t& cin, size_t cfrom, int32_t z) {
+    if (from.size() > into.size()) { into.swap(from); cin = cfrom; }
+    into.insert(into.end(), from.begin(), from.end());
     std::vector<int32_t>().swap(from);
-    for (int32_t& v : into) v = cg.root(v);
-    std::sort(into.begin(), into.end());
-    into.erase(std::unique(into.begin(), into.end()), into.end());
-    into.erase(std::remove(into.begin(), into.end(), z), into.end());
+    if (into.size() >= 2 * std::max<size_t>(cin, 16)) {
+      for (int32_t& v : into) v = cg.root(v);
+      std::sort(into.begin(), into.end());
+      into.erase(std::unique(into.begin(), into.end()), into.end());
+      into.erase(std::remove(into.begin(), into.end(), z), into.end());
+      cin = into.size();
+    }
   };
   auto push = [&](std::vector<uint64_t>& S, std::vector<uint64_t>* S2, std::vector<std::vector<int32_t>>& adj, int32_t z) {
     const uint64_t* sz = row(S, z);
@@ -285,8 +294,12 @@ static void build_contraction_sets(toast_analysis* a, int64_t NL, const std::vec
       const uint64_t *ao = row(A, o2), *dox = row(D, o2), *po = row(PA, o2);
       for (size_t q = 0; q < W; ++q) { az[q] |= ao[q]; dz[q] |= dox[q]; pz[q] |= po[q]; }
     }
-    merge_adj(gout[z], gout[o2], z);
-    merge_adj(gin[z], gin[o2], z);
+    {
+      std::vector<size_t>& c = compacted;
+      size_t co = c[o2];
+      merge_adj(gout[z], gout[o2], c[z], co, z);
+    }
+    merge_adj(gin[z], gin[o2], in_compacted[z], in_compacted[o2], z);
     push(A, &PA, gout, z);   // descendants are now reached by A(z)
     push(D, nullptr, gin, z);   // ancestors now reach D(z)
   }
