@@ -4,6 +4,7 @@
 // compatibility closure.  Produces the packed device tables of
 // toast_internal.h.  Definitions: SURVEY §8(c) C1-C8 / DESIGN.md.
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cstring>
 #include <map>
@@ -239,6 +240,8 @@ static void build_contraction_sets(toast_analysis* a, int64_t NL, const std::vec
       for (size_t w = 0; w < W; ++w) { al[w] |= ap[w]; pl[w] |= ppa[w]; }
     }
   }
+  const auto t_init = std::chrono::steady_clock::now();
+  int64_t pushed = 0;
   DSU cg(NL);
   std::vector<int32_t> stack;
   // adjacency lists are concatenated (the shorter into the longer) and
@@ -271,6 +274,7 @@ static void build_contraction_sets(toast_analysis* a, int64_t NL, const std::vec
       for (size_t q = 0; q < W && sub; ++q) sub = (sz[q] & ~sw[q]) == 0;
       if (sub) continue;
       for (size_t q = 0; q < W; ++q) sw[q] |= sz[q];
+      ++pushed;
       if (S2) { uint64_t* s2 = row(*S2, w); for (size_t q = 0; q < W; ++q) s2[q] |= sz2[q]; }
       for (int32_t v : adj[w]) stack.push_back(v);
     }
@@ -303,6 +307,9 @@ static void build_contraction_sets(toast_analysis* a, int64_t NL, const std::vec
     push(A, &PA, gout, z);   // descendants are now reached by A(z)
     push(D, nullptr, gin, z);   // ancestors now reach D(z)
   }
+  if (getenv("TOAST_DEBUG"))
+    fprintf(stderr, "[toast] contraction: %zu-word endpoint bitsets, %lld node updates pushed, main loop %.3f s\n", W,
+            (long long)pushed, std::chrono::duration<double>(std::chrono::steady_clock::now() - t_init).count());
   a->cnode.resize(NL);
   for (int64_t l = 0; l < NL; ++l) a->cnode[l] = cg.root((int32_t)l);
   // sets
