@@ -1247,7 +1247,9 @@ static inline int pick_k(const toast_analysis* a, int64_t batches, const int32_t
   if (a->k_force) return a->k_force;
   const char* fk = getenv("TOAST_FORCE_K");
   int K = a->k_throughput;
-  if (!fk && batches < (int64_t)occ[0] * a->n_sms) {
+  // under the critical-path model warp 0 alone walks the op DAG (the longest
+  // phase), so spreading a batch over more warps buys no latency there
+  if (!fk && batches < (int64_t)occ[0] * a->n_sms && a->dt.cost_model != TOAST_COST_CRITICAL_PATH) {
     for (int i = 3; i >= 1; --i)
       if (occ[i] > 0 && batches <= (int64_t)occ[i] * a->n_sms && a->dt.n_ops >= 64 * (1 << i)) { K = 1 << i; break; }
   }
