@@ -195,7 +195,7 @@ class Analysis:
         self.axes = graph_axes
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:   # (module globals are gone at interpreter exit)
             _lib.toast_free_analysis(self._h)
             self._h = None
 
