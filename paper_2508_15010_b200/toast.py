@@ -173,7 +173,7 @@ class Graph:
         self._h = handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.toast_free_graph(self._h)
             self._h = None
 
@@ -398,6 +398,6 @@ class SearchState:
         return res[0]
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.toast_search_end(self._h, None)
             self._h = None
