@@ -75,15 +75,19 @@ __host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes)
 __host__ __device__ inline int smem_acc_bytes(int n_axes, int K) {
   return n_axes * 4 * 32 * (8 + 4) + (K > 1 ? 32 * 5 * 8 : 0);
 }
-__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K) {
-  int b1 = n_ac * 128, b2 = K * smem_acc_bytes(n_axes, K);
+__host__ __device__ constexpr bool acc_shared(int n_axes, bool cp) { return n_axes <= 2 || cp; }
+__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K, bool cp) {
+  // <= 2 axes (and the critical-path kernels): one region the K warps add into
+  // atomically; 3-4 axes: one region per warp, combined by warp 0 (measured
+  // faster there: Llama-80 281 M vs 259 M evals/s; its critical path 9.2 M vs 8.0 M the other way)
+  int b1 = n_ac * 128, b2 = (acc_shared(n_axes, cp) ? 1 : K) * smem_acc_bytes(n_axes, K);
   return r16(b1 > b2 ? b1 : b2);
 }
 __host__ __device__ inline int smem_d_bytes(int n_ftmpl) { return r16(n_ftmpl * 32); }
 // n_ftmpl / n_fsig: the templates / signatures the frontier's terms use
 __host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_ftmpl,
-                                                int n_mc, int n_fsig) {
-  return smem_c_bytes(n_axes) + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K) +
+                                                int n_mc, int n_fsig, bool cp) {
+  return smem_c_bytes(n_axes) + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K, cp) +
          smem_d_bytes(n_ftmpl) + r16(n_fsig * 32) + r16(n_mc * 32 * (n_axes <= 2 ? 1 : 2));
 }
 
@@ -146,7 +150,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   const uint32_t b = a + smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
   s.acol = b;
   s.acc = b;
-  s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K);
+  s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K, T.cost_model == TOAST_COST_CRITICAL_PATH);
   s.pc = s.tb + smem_d_bytes(T.n_ftmpl);
   s.mca = s.pc + r16(T.n_fsig * 32);
   return s;
@@ -521,6 +525,16 @@ __device__ __forceinline__ double cp_sweep(const DeviceTables& T, int lane, cons
   return cp;
 }
 
+// accumulate into the block's shared payload/count slots (atomically when K > 1 warps share them)
+__device__ __forceinline__ void acc_add(int K, unsigned long long* p, unsigned long long v) {
+  if (K == 1) *p += v;
+  else atomicAdd(p, v);
+}
+__device__ __forceinline__ void acc_add(int K, uint32_t* p, uint32_t v) {
+  if (K == 1) *p += v;
+  else atomicAdd(p, v);
+}
+
 // a block of one warp needs only the warp's own ordering
 __device__ __forceinline__ void block_sync(int K) {
   if (K == 1) __syncwarp();
@@ -607,9 +621,14 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         sp<uint8_t>(S.pc)[fslot * 32 + lane] = (uint8_t)dcode<P2>(T, present);
       }
     }
+    if (acc_shared(NA, CP) && K > 1) {   // the shared accumulators (region B held the event lists until H2a ended)
+      uint32_t* z = sp<uint32_t>(S.acc);
+      const int words = smem_acc_bytes(NA, K) / 4;
+      for (int i = warp * 32 + lane; i < words; i += K * 32) z[i] = 0u;
+    }
   }
   block_sync(K);
-  const uint32_t acc = S.acc + (uint32_t)warp * smem_acc_bytes(NA, K);
+  const uint32_t acc = S.acc + (acc_shared(NA, CP) ? 0u : (uint32_t)warp * smem_acc_bytes(NA, K));
   unsigned long long* pay = sp<unsigned long long>(acc);
   uint32_t* cnt = sp<uint32_t>(acc + NA * 4 * 32 * 8);
   unsigned long long* seg = sp<unsigned long long>(acc + NA * 4 * 32 * 12);
@@ -688,7 +707,15 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     if (t2.y != 0xFFFFFFFFu) sp<uint8_t>(S.tb)[t2.y * 32 + lane] = tbv;
   }
 #pragma unroll
-  for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] = rp[q]; cnt[q * 32 + lane] = rc[q]; }
+  for (int q = 0; q < NA * 4; ++q) {
+    if (K == 1 || !acc_shared(NA, CP)) {
+      pay[q * 32 + lane] = rp[q];
+      cnt[q * 32 + lane] = rc[q];
+    } else {   // sums mod 2^64 / 2^32: the order of the warps' adds does not matter
+      if (rp[q]) atomicAdd(&pay[q * 32 + lane], rp[q]);
+      if (rc[q]) atomicAdd(&cnt[q * 32 + lane], rc[q]);
+    }
+  }
   block_sync(K);
 
   // H5 (C12, reading R19): peak = max over the kept ops of the peak-memory
@@ -772,27 +799,27 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
             for (int A = 0; A < NA; ++A) {       // phase 1a: all_gather (reading R20)
               const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
               if (dd == 15 || du != 15) continue;
-              pay[(A * 4 + TOAST_AG) * 32 + lane] += size;
-              cnt[(A * 4 + TOAST_AG) * 32 + lane] += 1u;
+              acc_add(acc_shared(NA, CP) ? K : 1, &pay[(A * 4 + TOAST_AG) * 32 + lane], size);
+              acc_add(acc_shared(NA, CP) ? K : 1, &cnt[(A * 4 + TOAST_AG) * 32 + lane], 1u);
               size *= (uint64_t)T.sizes[A];
             }
 #pragma unroll
             for (int A = 0; A < NA; ++A) {       // phase 1b: all_to_all
               const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
               if (dd == 15 || du == 15 || dd == du) continue;
-              pay[(A * 4 + TOAST_A2A) * 32 + lane] += size;
-              cnt[(A * 4 + TOAST_A2A) * 32 + lane] += 1u;
+              acc_add(acc_shared(NA, CP) ? K : 1, &pay[(A * 4 + TOAST_A2A) * 32 + lane], size);
+              acc_add(acc_shared(NA, CP) ? K : 1, &cnt[(A * 4 + TOAST_A2A) * 32 + lane], 1u);
             }
 #pragma unroll
             for (int A = 0; A < NA; ++A) {
               if (!((P >> A) & 1)) continue;
               if (((dimU >> (4 * A)) & 15) != 15) {
                 size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
-                pay[(A * 4 + TOAST_RS) * 32 + lane] += size;
-                cnt[(A * 4 + TOAST_RS) * 32 + lane] += 1u;
+                acc_add(acc_shared(NA, CP) ? K : 1, &pay[(A * 4 + TOAST_RS) * 32 + lane], size);
+                acc_add(acc_shared(NA, CP) ? K : 1, &cnt[(A * 4 + TOAST_RS) * 32 + lane], 1u);
               } else {
-                pay[(A * 4 + TOAST_AR) * 32 + lane] += size;
-                cnt[(A * 4 + TOAST_AR) * 32 + lane] += 1u;
+                acc_add(acc_shared(NA, CP) ? K : 1, &pay[(A * 4 + TOAST_AR) * 32 + lane], size);
+                acc_add(acc_shared(NA, CP) ? K : 1, &cnt[(A * 4 + TOAST_AR) * 32 + lane], 1u);
               }
             }
             const long long grow = (long long)dv<P2>(T, gb, dcode<P2>(T, presU)) - (long long)dv<P2>(T, gb, dcode<P2>(T, presD));
@@ -807,31 +834,45 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   }
   }
   if (CP) cp_classes<NA, P2>(T, S, K, warp, lane, T.cp_scratch + (size_t)blockIdx.x * cp_stride(T) * 32);
-  if (K > 1) {
+  if (K > 1 && !acc_shared(NA, CP)) {
     seg[0 * 32 + lane] = key;
     seg[1 * 32 + lane] = flo;
     seg[2 * 32 + lane] = fhi;
     seg[3 * 32 + lane] = 0ULL;
     seg[4 * 32 + lane] = peak;
+  } else if (K > 1) {
+    // the K warps' partial state key, 128-bit FLOP total and peak, combined
+    // in shared memory: sums mod 2^64 (the FLOP carry taken against the value
+    // each add lands on) and a max — independent of the warps' order
+    atomicAdd(&seg[0 * 32 + lane], (unsigned long long)key);
+    const unsigned long long lo_old = atomicAdd(&seg[1 * 32 + lane], (unsigned long long)flo);
+    atomicAdd(&seg[2 * 32 + lane], (unsigned long long)(fhi + ((lo_old + flo < lo_old) ? 1 : 0)));
+    atomicMax(&seg[4 * 32 + lane], (unsigned long long)peak);
   }
   block_sync(K);
   if (warp == 0) {
-    // combine the K warps' sums (into warp 0's slots) and peaks
     unsigned long long pk_all = peak;
-    if (K > 1) { key = 0; flo = 0; fhi = 0; pk_all = 0; }
-    for (int w = 0; K > 1 && w < K; ++w) {
-      const uint32_t aw = S.acc + (uint32_t)w * smem_acc_bytes(NA, K);
-      const unsigned long long* sw = sp<const unsigned long long>(aw + NA * 4 * 32 * 12);
-      key += sw[0 * 32 + lane];
-      const uint64_t f = sw[1 * 32 + lane];
-      flo += f;
-      fhi += sw[2 * 32 + lane] + ((flo < f) ? 1 : 0);
-      const unsigned long long segpk = sw[4 * 32 + lane];
-      pk_all = segpk > pk_all ? segpk : pk_all;
-      if (w) {
-        const unsigned long long* pww = sp<const unsigned long long>(aw);
-        const uint32_t* cww = sp<const uint32_t>(aw + NA * 4 * 32 * 8);
-        for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] += pww[q * 32 + lane]; cnt[q * 32 + lane] += cww[q * 32 + lane]; }
+    if (K > 1 && acc_shared(NA, CP)) {
+      key = seg[0 * 32 + lane];
+      flo = seg[1 * 32 + lane];
+      fhi = seg[2 * 32 + lane];
+      pk_all = seg[4 * 32 + lane];
+    } else if (K > 1) {   // combine the K warps' regions into warp 0's
+      key = 0; flo = 0; fhi = 0; pk_all = 0;
+      for (int w = 0; w < K; ++w) {
+        const uint32_t aw = S.acc + (uint32_t)w * smem_acc_bytes(NA, K);
+        const unsigned long long* sw = sp<const unsigned long long>(aw + NA * 4 * 32 * 12);
+        key += sw[0 * 32 + lane];
+        const uint64_t f = sw[1 * 32 + lane];
+        flo += f;
+        fhi += sw[2 * 32 + lane] + ((flo < f) ? 1 : 0);
+        const unsigned long long segpk = sw[4 * 32 + lane];
+        pk_all = segpk > pk_all ? segpk : pk_all;
+        if (w) {
+          const unsigned long long* pww = sp<const unsigned long long>(aw);
+          const uint32_t* cww = sp<const uint32_t>(aw + NA * 4 * 32 * 8);
+          for (int q = 0; q < NA * 4; ++q) { pay[q * 32 + lane] += pww[q * 32 + lane]; cnt[q * 32 + lane] += cww[q * 32 + lane]; }
+        }
       }
     }
     const uint32_t status = sp<uint32_t>(S.status)[lane];
@@ -1154,7 +1195,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_ftmpl, T.n_mc, T.n_fsig) > dev_smem) {
+  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_ftmpl, T.n_mc, T.n_fsig, T.cost_model == TOAST_COST_CRITICAL_PATH) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -1163,7 +1204,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_ftmpl, T.n_mc, T.n_fsig);
+    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_ftmpl, T.n_mc, T.n_fsig, T.cost_model == TOAST_COST_CRITICAL_PATH);
     int be = 0, br = 0;
     if (sm <= dev_smem) {
       cudaError_t e = dispatch(T, [&]<int NA, bool P2, bool CP>() {
@@ -1270,7 +1311,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig, a->dt.cost_model == TOAST_COST_CRITICAL_PATH);
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
@@ -1290,7 +1331,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig);
+  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig, a->dt.cost_model == TOAST_COST_CRITICAL_PATH);
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
