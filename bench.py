@@ -486,6 +486,7 @@ def run_toast(args, cfg, rank, world, local):
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": cfg.name, "cost_model": args.cost_model, "rollouts_per_step_per_gpu": N, "wave": wave,
                        "warps_per_batch": a.kernel_tables().get("warps_per_batch"),
+                       "blocks_per_sm": a.kernel_tables().get("blocks_per_sm"),
                        "mesh": [list(x) for x in cfg.axes],
                        "ops": dump["n_ops"], "loops": dump["n_loops"], "actions": len(dump["actions"]) + 1,
                        "l2": "flushed (256 MiB write) between timed steps", "description": cfg.description},

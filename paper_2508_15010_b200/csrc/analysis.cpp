@@ -1682,7 +1682,8 @@ std::string dump_json(const toast_analysis* a) {
          I((int64_t)a->cp_walked_ops) + ",\"cp_walked_edges\":" + I((int64_t)a->cp_walked_edges) + ",\"cp_bundles\":" + I((int64_t)a->h_cp_bsize.size()) + ",\"n_acolors\":" + I((int64_t)a->dt.n_acolors) +
          ",\"n_words\":" + I((int64_t)a->dt.n_words) + ",\"n_fsig\":" + I((int64_t)a->dt.n_fsig) + ",\"n_ftmpl\":" +
          I((int64_t)a->dt.n_ftmpl) + ",\"warps_per_batch\":" +
-         I((int64_t)a->k_throughput) + ",\"work\":{\"sig_roles\":" + I(a->work_sig_roles) + ",\"n_tmpl\":" +
+         I((int64_t)a->k_throughput) + ",\"blocks_per_sm\":" +
+         I((int64_t)a->occ_roll[a->k_throughput >= 8 ? 3 : a->k_throughput >= 4 ? 2 : a->k_throughput >= 2 ? 1 : 0]) + ",\"work\":{\"sig_roles\":" + I(a->work_sig_roles) + ",\"n_tmpl\":" +
          I(a->work_tmpl) + ",\"n_terms\":" + I(a->work_terms) + "},\"frontier_ops\":[";
     for (size_t q = 0; q < a->point_op.size(); ++q) { if (q) s += ','; s += I(a->point_op[q]); }
     s += "]}";

@@ -76,19 +76,23 @@ __host__ __device__ inline int smem_acc_bytes(int n_axes, int K) {
   return n_axes * 4 * 32 * (8 + 4) + (K > 1 ? 32 * 5 * 8 : 0);
 }
 __host__ __device__ constexpr bool acc_shared(int n_axes, bool cp) { return n_axes <= 2 || cp; }
-__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K, bool cp) {
+__host__ __device__ inline int smem_m_bytes(int n_mc, int n_axes) { return r16(n_mc * 32 * (n_axes <= 2 ? 1 : 2)); }
+__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K, bool cp, int n_mc) {
   // <= 2 axes (and the critical-path kernels): one region the K warps add into
   // atomically; 3-4 axes: one region per warp, combined by warp 0 (measured
-  // faster there: Llama-80 281 M vs 259 M evals/s; its critical path 9.2 M vs 8.0 M the other way)
-  int b1 = n_ac * 128, b2 = (acc_shared(n_axes, cp) ? 1 : K) * smem_acc_bytes(n_axes, K);
+  // faster there: Llama-80 281 M vs 259 M evals/s; its critical path 9.2 M vs 8.0 M the other way).
+  // With one warp (sum model) the accumulators are first written after H4, when
+  // the class maps that follow region B are dead: they may run on over them.
+  const int acc = (acc_shared(n_axes, cp) ? 1 : K) * smem_acc_bytes(n_axes, K);
+  const int b1 = n_ac * 128, b2 = acc - (K == 1 && !cp ? smem_m_bytes(n_mc, n_axes) : 0);
   return r16(b1 > b2 ? b1 : b2);
 }
 __host__ __device__ inline int smem_d_bytes(int n_ftmpl) { return r16(n_ftmpl * 32); }
 // n_ftmpl / n_fsig: the templates / signatures the frontier's terms use
 __host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_ftmpl,
                                                 int n_mc, int n_fsig, bool cp) {
-  return smem_c_bytes(n_axes) + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K, cp) +
-         smem_d_bytes(n_ftmpl) + r16(n_fsig * 32) + r16(n_mc * 32 * (n_axes <= 2 ? 1 : 2));
+  return smem_c_bytes(n_axes) + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K, cp, n_mc) +
+         smem_m_bytes(n_mc, n_axes) + smem_d_bytes(n_ftmpl) + r16(n_fsig * 32);
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -130,7 +134,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t status;          // [32]
   uint32_t axpos;           // [32] 2-bit axis of every sequence position (u64)
   uint32_t axb;             // [4][32] per mesh axis: bitmap of the positions whose action uses it
-  uint32_t acc;             // per warp: pay [NA*4][32] u64, cnt [NA*4][32] u32, seg [5][32] u64
+  uint32_t acc;             // pay [NA*4][32] u64, cnt [NA*4][32] u32 (+ seg [5][32] u64 when K > 1), shared or per warp
   uint32_t tb;              // [n_ftmpl][32] per frontier template: divU | divD << 4 (equal: no temporary)
   uint32_t pc;              // [n_fsig][32] per frontier signature: division code of the result layout
   uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u8 for <= 2 axes, else u16)
@@ -150,9 +154,9 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   const uint32_t b = a + smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
   s.acol = b;
   s.acc = b;
-  s.tb = b + smem_b_bytes(T.n_acolors, T.n_axes, K, T.cost_model == TOAST_COST_CRITICAL_PATH);
+  s.mca = b + smem_b_bytes(T.n_acolors, T.n_axes, K, T.cost_model == TOAST_COST_CRITICAL_PATH, T.n_mc);
+  s.tb = s.mca + smem_m_bytes(T.n_mc, T.n_axes);
   s.pc = s.tb + smem_d_bytes(T.n_ftmpl);
-  s.mca = s.pc + r16(T.n_fsig * 32);
   return s;
 }
 
@@ -1351,6 +1355,15 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
 // on K — only the speed does.  TOAST_FORCE_K overrides.
 toast_status autotune_k(toast_analysis* a, std::string& err) {
   // (the critical-path variant keeps the occupancy heuristic: its walk runs on one warp per block)
+  if (const char* fb = getenv("TOAST_FORCE_BLOCKS")) {   // pin the residency (profiling a measured choice)
+    const int cap = std::max(1, atoi(fb));
+    for (int i = 0; i < 4; ++i) {
+      a->occ_eval[i] = std::min(a->occ_eval[i], cap);
+      a->occ_roll[i] = std::min(a->occ_roll[i], cap);
+    }
+    a->eval_blocks = a->n_sms * a->occ_eval[0];
+    a->rollout_blocks = a->n_sms * a->occ_roll[0];
+  }
   if (getenv("TOAST_FORCE_K") || a->n_sms <= 0 || a->dt.cost_model == TOAST_COST_CRITICAL_PATH) return TOAST_OK;
   // each K runs eight of its own whole waves (no partial tail; about the
   // bench's 2^18 rollouts), compared by candidates per second
@@ -1368,25 +1381,42 @@ toast_status autotune_k(toast_analysis* a, std::string& err) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int keep = a->k_throughput;
-  int best_k = keep;
+  int best_k = keep, best_cap = 0;
   float best_ms = 1e30f;
   toast_status st = TOAST_OK;
+  // per K, also fewer resident blocks than fit: more blocks leave less of the
+  // SM's unified L1 / shared memory to the tables the kernel reads through L1
   for (int i = 0, K = 1; i < 4 && st == TOAST_OK; ++i, K *= 2) {
     if (a->occ_eval[i] < 1 || a->occ_roll[i] < 1) continue;
-    a->k_force = K;
-    const int64_t nk = 8 * (int64_t)std::min(a->occ_eval[i], a->occ_roll[i]) * a->n_sms * 32;
-    float ms = 1e30f;
-    for (int rep = 0; rep < 6 && st == TOAST_OK; ++rep) {
-      cudaEventRecord(e0, 0);
-      st = launch_rollout(a, d_pre, nk, 1, (uint64_t)rep * nk, d_seq, d_out, nullptr, err, 1);
-      cudaEventRecord(e1, 0);
-      cudaEventSynchronize(e1);
-      float t = 0.f;
-      cudaEventElapsedTime(&t, e0, e1);
-      if (rep) ms = std::min(ms, t);   // rep 0 is the warm-up
+    const int occ_e = a->occ_eval[i], occ_r = a->occ_roll[i], occ = std::min(occ_e, occ_r);
+    for (int cap : {occ, occ - 2, occ - 4}) {
+      if (cap < 1 || (cap < occ && occ - cap >= occ / 2)) continue;
+      a->k_force = K;
+      a->occ_eval[i] = std::min(occ_e, cap);
+      a->occ_roll[i] = std::min(occ_r, cap);
+      const int64_t nk = 8 * (int64_t)cap * a->n_sms * 32;
+      float ms = 1e30f;
+      for (int rep = 0; rep < 6 && st == TOAST_OK; ++rep) {
+        cudaEventRecord(e0, 0);
+        st = launch_rollout(a, d_pre, nk, 1, (uint64_t)rep * nk, d_seq, d_out, nullptr, err, 1);
+        cudaEventRecord(e1, 0);
+        cudaEventSynchronize(e1);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        if (rep) ms = std::min(ms, t);   // rep 0 is the warm-up
+      }
+      a->occ_eval[i] = occ_e;
+      a->occ_roll[i] = occ_r;
+      const float per = ms / (float)nk;   // time per candidate
+      if (per < best_ms) { best_ms = per; best_k = K; best_cap = cap; }
     }
-    const float per = ms / (float)nk;   // time per candidate
-    if (per < best_ms) { best_ms = per; best_k = K; }
+  }
+  if (st == TOAST_OK && best_cap > 0) {   // the measured residency of the chosen K
+    const int bi = best_k >= 8 ? 3 : best_k >= 4 ? 2 : best_k >= 2 ? 1 : 0;
+    a->occ_eval[bi] = std::min(a->occ_eval[bi], best_cap);
+    a->occ_roll[bi] = std::min(a->occ_roll[bi], best_cap);
+    a->eval_blocks = a->n_sms * a->occ_eval[0];
+    a->rollout_blocks = a->n_sms * a->occ_roll[0];
   }
   a->k_force = 0;
   a->k_throughput = st == TOAST_OK ? best_k : keep;
