@@ -1,25 +1,28 @@
-// sm_100a kernels of libtoast (DESIGN.md "Kernels").
+// sm_100a kernels of libtoast (DESIGN.md §5-§6, §11).
 //
-// Mapping: one WARP evaluates 32 CANDIDATES, one per lane, and the 32 lanes
-// walk the op stream in lockstep.  Every table read is therefore warp-uniform
-// (a broadcast from L1), there is no divergence by op kind, and the liveness
-// sweep (H5) is a plain per-lane running sum/max.
+// Mapping: one block evaluates 32 CANDIDATES, one per lane, shared by K warps
+// (K measured per analysis); persistent blocks loop over batches.  Every table
+// read is warp-uniform (a broadcast from L1) and per-candidate state lives in
+// shared memory as [x][lane] (conflict-free).
 //
-// Per candidate (per lane):
-//   H1 decode        the 32 action ids -> per-action-color event lists
-//                    (shared memory, [acolor][lane]) and the fixed SetGroup bits;
-//   H2 materialise   once per op SIGNATURE (ops whose loops have the same
-//                    action colors / divisibility / deselection class get the
-//                    same axes): an axis->role map, 16 bits, kept in shared
-//                    memory [sig][lane] (GPT-24: 44 signatures for 6,579 ops);
-//   sweep            per op: state key (C14), local FLOPs (C10), result bytes,
-//                    per use edge the def/use axis->dim maps -> AG/A2A/RS/AR
-//                    payloads and temporaries (C11), dying bytes, and the
-//                    running live/peak bytes (C12);
+// Per candidate (per lane), over tables H0 compiled (never a per-op loop):
+//   H1 decode        the 32 action ids -> per-action-color position bitmaps,
+//                    per-axis position bitmaps, fixed SetGroup bits, status;
+//   H2 materialise   once per materialisation CLASS (GPT-24: 35 for 6,579 ops):
+//                    the axis -> role map (C9 "attempt" semantics), then per
+//                    signature the entry axis -> role | axis -> result dim; the
+//                    class's summed state-key terms (H7) and FLOPs (H3);
+//   H4 collectives   once per edge TEMPLATE (summed bytes): phase 1a AG, 1b A2A,
+//                    2 RS/AR payloads and counts (C11, reading R20), and the
+//                    template's growth code for H5;
+//   H5 peak memory   max of M_t over the peak-memory frontier (reading R19);
 //   H6               the fixed-order double epilogue (explicit _rn intrinsics,
-//                    never contracted) -> bit-identical to the CPU oracle.
+//                    never contracted) -> bit-identical to the CPU oracle; the
+//                    256-B toast_cost or the 16-B toast_score;
+//   R22 (CP = true)  the duration classes per lane, then the bundled max-plus
+//                    walk of the critical path (cp_classes / cp_sweep).
 // K2 (rollouts): per lane, Philox4x32-10 draws over a per-lane legal bitset
-// (shared memory), then the same device path.
+// (shared memory), then the same path.  K3: a search round's per-leaf reduce.
 // No tensor cores: there is no dense contraction on this path.
 #include <cuda_runtime.h>
 
@@ -65,13 +68,14 @@ __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
 //      sequence [16][32] and the rollout legal set [n_words][32] (dead once
 //      the table is written)
 //   B  the per-color event lists [n_acolors][32] (decode/materialise), then,
-//      per warp, the payload/count accumulators and the segment results
+//      the payload/count accumulators and (K > 1) the state key / FLOPs / peak
+//      partials — shared by the warps, or one region per warp (acc_shared)
 __host__ __device__ inline int smem_c_bytes(int n_axes) { return 32 * (8 + 8 + 4 + 8 + 4 * n_axes); }
 __host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes) {
   int a1 = n_sigs * 32 * sig_entry_bytes(n_axes), a2 = 2048 + n_words * 128;
   return r16(a1 > a2 ? a1 : a2);
 }
-// per warp: payload/count accumulators, plus the segment results when K > 1
+// one accumulator region: payload/count accumulators, plus the K > 1 partials
 __host__ __device__ inline int smem_acc_bytes(int n_axes, int K) {
   return n_axes * 4 * 32 * (8 + 4) + (K > 1 ? 32 * 5 * 8 : 0);
 }
