@@ -486,3 +486,26 @@ def test_critical_path_concurrent_streams_and_host_pipeline():
         s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=31, id_base=int(i))
         assert np.array_equal(gs[i], s1[0])
         assert_same(gc[i:i + 1], c1, f"row {i}")
+
+
+@pytest.mark.parametrize("name", ["gpt2", "unet", "gpt2_4ax_np2"])
+def test_results_independent_of_k_and_residency(name):
+    """The measured K and residency (TOAST_FORCE_K / TOAST_FORCE_BLOCKS pin them)
+    change only the schedule: rollouts and records are bit-identical."""
+    import os
+    T = _T()
+    c = configs.get(name)
+    a0, _o = setup(name)
+    n = 3 * a0.preferred_batch() + 17
+    pre = np.zeros((n, 32), np.uint16)
+    s0, c0 = gpu_rollout(a0, pre, 13, 4)
+    for K, B in ((1, 3), (2, 5), (4, 2), (8, 1)):
+        os.environ["TOAST_FORCE_K"], os.environ["TOAST_FORCE_BLOCKS"] = str(K), str(B)
+        try:
+            a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth,
+                                 cuda_device=0)
+        finally:
+            del os.environ["TOAST_FORCE_K"], os.environ["TOAST_FORCE_BLOCKS"]
+        assert a.kernel_tables()["warps_per_batch"] == K
+        s1, c1 = gpu_rollout(a, pre, 13, 4)
+        assert np.array_equal(s1, s0) and c1.tobytes() == c0.tobytes(), (K, B)
