@@ -1358,7 +1358,6 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
 // and the fastest becomes the analysis' k_throughput.  Results never depend
 // on K — only the speed does.  TOAST_FORCE_K overrides.
 toast_status autotune_k(toast_analysis* a, std::string& err) {
-  // (the critical-path variant keeps the occupancy heuristic: its walk runs on one warp per block)
   if (const char* fb = getenv("TOAST_FORCE_BLOCKS")) {   // pin the residency (profiling a measured choice)
     const int cap = std::max(1, atoi(fb));
     for (int i = 0; i < 4; ++i) {
@@ -1368,7 +1367,8 @@ toast_status autotune_k(toast_analysis* a, std::string& err) {
     a->eval_blocks = a->n_sms * a->occ_eval[0];
     a->rollout_blocks = a->n_sms * a->occ_roll[0];
   }
-  if (getenv("TOAST_FORCE_K") || a->n_sms <= 0 || a->dt.cost_model == TOAST_COST_CRITICAL_PATH) return TOAST_OK;
+  if (getenv("TOAST_FORCE_K") || a->n_sms <= 0 || (a->dt.cost_model == TOAST_COST_CRITICAL_PATH && getenv("TOAST_CP_NO_AUTOTUNE")))
+    return TOAST_OK;
   // each K runs eight of its own whole waves (no partial tail; about the
   // bench's 2^18 rollouts), compared by candidates per second
   int occ_max = 0;
