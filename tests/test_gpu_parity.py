@@ -509,3 +509,23 @@ def test_results_independent_of_k_and_residency(name):
         assert a.kernel_tables()["warps_per_batch"] == K
         s1, c1 = gpu_rollout(a, pre, 13, 4)
         assert np.array_equal(s1, s0) and c1.tobytes() == c0.tobytes(), (K, B)
+
+
+def test_cli_partitions_a_program(tmp_path, capsys):
+    """python -m paper_2508_15010_b200: search on cuda:0, then the best state's
+    record and lowered program; on MLP-c the best equals the oracle's
+    exhaustive optimum (C17)."""
+    from paper_2508_15010_b200.__main__ import main
+    a, o = setup("mlp_c")
+    _, _best, bc = o.bruteforce()
+    c = configs.get("mlp_c")
+    f = tmp_path / "mlp_c.ir"
+    f.write_text(c.ir)
+    mesh = ",".join(f"{n}={s}:{bw!r}" for n, s, bw in c.axes)
+    assert main(["--ir", str(f), "--mesh", mesh, "--flops", repr(c.flops_per_sec), "--dm", str(c.dm),
+                 "--min-dims", str(c.min_dims), "--budget", "20000"]) == 0
+    out = capsys.readouterr().out
+    assert f"best score {float(bc['score']):.6g}" in out
+    assert "return" in out and "mesh" in out
+    assert main(["--config", "gpt2", "--cost-model", "cp", "--grouping", "contraction", "--budget", "20000",
+                 "--no-program"]) == 0
