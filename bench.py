@@ -160,8 +160,14 @@ def cpu_baseline(cfg, seconds: float, n_first: int = 64):
         n = int(min(max(n * 2, rate * (seconds - t_used) * 0.9), 1 << 22)) if t_used < seconds else n
         if n <= 0:
             break
+    # single-thread latency per evaluation, on a small sample
+    m = 256
+    t = time.perf_counter()
+    o.rollout(np.zeros((m, 32), np.uint16), seed=9, id_base=1 << 30, threads=1)
+    lat = (time.perf_counter() - t) / m
     return {"value": done / t_used, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{done} rollouts+evals of {cfg.name} from the empty prefix in {t_used:.1f} s"}
+            "sample": f"{done} rollouts+evals of {cfg.name} from the empty prefix in {t_used:.1f} s",
+            "single_thread_us_per_eval": lat * 1e6}
 
 
 def run_reference(args, cfg, rank, world):
@@ -188,7 +194,8 @@ def run_reference(args, cfg, rank, world):
     ms = 1000.0 * statistics.mean(times)
     value = n / (ms / 1000.0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_median": 1000.0 * statistics.median(times),
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": cfg.name, "rollouts_per_step": n, "mesh": [list(a) for a in cfg.axes],
                        "description": cfg.description},
@@ -482,7 +489,8 @@ def run_toast(args, cfg, rank, world, local):
         peak_alu = 148 * 128 * sm_max * 1e6 / 1e9                  # INT32 lanes x clock (Gop/s)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_median": statistics.median(step_ms),   # rank 0 (SURVEY §8(d) median)
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": cfg.name, "cost_model": args.cost_model, "rollouts_per_step_per_gpu": N, "wave": wave,
                        "warps_per_batch": a.kernel_tables().get("warps_per_batch"),
