@@ -37,6 +37,9 @@
 #ifndef TOAST_MAX_THREADS
 #define TOAST_MAX_THREADS 256
 #endif
+#ifndef TOAST_CP_MAX_THREADS
+#define TOAST_CP_MAX_THREADS 256   // critical-path instantiations: block size bound
+#endif
 #ifndef TOAST_CP_MIN_BLOCKS
 #define TOAST_CP_MIN_BLOCKS 2   // critical-path instantiations (register-heavier bundled walk)
 #endif
@@ -967,7 +970,7 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
+__global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS), (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS)) toast_eval_kernel(const DeviceTables T, const uint16_t* __restrict__ seqs,
                                                          int64_t n, void* __restrict__ out, bool compact) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
@@ -996,7 +999,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
 }
 
 template <int NA, bool P2, bool CP>
-__global__ void __launch_bounds__(TOAST_MAX_THREADS, (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
+__global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS), (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
                                                             uint16_t* __restrict__ out_seqs,
                                                             void* __restrict__ out, int64_t rep, bool compact) {
@@ -1214,7 +1217,8 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
     const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_ftmpl, T.n_mc, T.n_fsig, T.cost_model == TOAST_COST_CRITICAL_PATH);
     int be = 0, br = 0;
-    if (sm <= dev_smem) {
+    const int max_threads = T.cost_model == TOAST_COST_CRITICAL_PATH ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS;
+    if (sm <= dev_smem && 32 * K <= max_threads) {
       cudaError_t e = dispatch(T, [&]<int NA, bool P2, bool CP>() {
         cudaError_t e1 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&be, toast_eval_kernel<NA, P2, CP>, 32 * K, sm);
         cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, toast_rollout_kernel<NA, P2, CP>, 32 * K, sm);
