@@ -148,12 +148,23 @@ class Oracle:
         L = lib()
         return L.orc_n_names(self.h), L.orc_n_map(self.h), L.orc_n_identities(self.h)
 
-    def dump(self) -> dict:
+    def _dump_all(self) -> dict:
         L = lib()
         n = L.orc_dump(self.h, None, 0)
         buf = ctypes.create_string_buffer(int(n))
         L.orc_dump(self.h, buf, n)
         return json.loads(buf.value.decode())
+
+    def dump(self) -> dict:
+        """The H0 analysis (the part comparable with the library's dump)."""
+        d = self._dump_all()
+        d.pop("set_graphs", None)
+        return d
+
+    def set_graphs(self) -> list:
+        """Per compatibility set, the labelled graph its C6 signature hashes: nodes
+        [loop, op kind, role, loop type, side mask], directed M edges, conflict edges."""
+        return self._dump_all()["set_graphs"]
 
     def baseline(self):
         t0, p0, f0 = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()

@@ -12,9 +12,10 @@
 //
 // Parity status per part (see DESIGN.md §"Oracle pins"):
 //   C1–C5, C9–C14 pinned by paper worked examples / closed forms / invariants /
-//   brute force; C15 pinned by Philox KAT vectors; C6 (WL signatures), C7
-//   (argument keys) and C8 (action table order) are "parity unpinned" beyond
-//   the structural invariants in tests/test_oracle_pins.py.  The contraction
+//   brute force; C15 pinned by Philox KAT vectors; C6 (WL signatures) pinned by
+//   brute-force isomorphism of the sets' labelled graphs; C7 (argument keys) and
+//   C8 (action table order) are "parity unpinned" beyond the structural
+//   invariants in tests/test_oracle_pins.py.  The contraction
 //   heuristic (reading R23, NEXT-4) is pinned by the paper's box / incompatible
 //   listings, by "all conflicts of the attention layer
 //   compatible" and by brute-force path checks on random programs.
@@ -713,6 +714,8 @@ struct Oracle {
   std::vector<int> conf_set, conf_side0;
   std::vector<int> set_root;                            // smallest conflict per set
   std::vector<u64> set_sig;
+  struct SetGraph { std::map<int, int> side; std::set<std::pair<int, int>> medges, cedges; };
+  std::vector<SetGraph> set_graphs;                     // C6 input per set (dumped for the isomorphism pin)
   std::vector<int> set_group;
   int n_groups = 0;
   std::vector<int> scolor;                              // per loop
@@ -1013,6 +1016,7 @@ struct Oracle {
           if (sidemask.count(e.first) && sidemask.count(e.second) && cnode[e.first] == cnode[e.second])
             m_edges.insert(e);
       }
+      set_graphs.push_back(SetGraph{sidemask, m_edges, conf_edges});
       std::map<int, u64> label;
       for (auto& kv : sidemask) {
         int l = kv.first;
@@ -1695,6 +1699,26 @@ int64_t orc_dump(void* h, char* buf, int64_t cap) {
   for (size_t i = 0; i < O->set_sig.size(); i++) {
     if (i) s += ",";
     char b[32]; snprintf(b, sizeof b, "\"%016llx\"", (unsigned long long)O->set_sig[i]); s += b;
+  }
+  s += "],\"set_graphs\":[";
+  for (size_t i = 0; i < O->set_graphs.size(); i++) {
+    const auto& G = O->set_graphs[i];
+    if (i) s += ",";
+    s += "{\"nodes\":[";
+    bool first = true;
+    for (auto& kv : G.side) {
+      const Loop& L = O->loops[kv.first];
+      if (!first) s += ",";
+      first = false;
+      s += "[" + num(kv.first) + ",\"" + O->M.ops[L.op].kind + "\"," + num(L.role) + "," + num(L.type) + "," + num(kv.second) + "]";
+    }
+    s += "],\"medges\":[";
+    first = true;
+    for (auto& e : G.medges) { if (!first) s += ","; first = false; s += "[" + num(e.first) + "," + num(e.second) + "]"; }
+    s += "],\"cedges\":[";
+    first = true;
+    for (auto& e : G.cedges) { if (!first) s += ","; first = false; s += "[" + num(e.first) + "," + num(e.second) + "]"; }
+    s += "]}";
   }
   s += "],\"n_groups\":" + num(O->n_groups);
   s += ",\"scolors\":[";

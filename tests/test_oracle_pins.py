@@ -496,3 +496,91 @@ def test_parser_errors(src, code):
     with pytest.raises(OracleError) as e:
         Oracle(src, [("a", 2, 1e10)], 1e12, 1 << 40)
     assert e.value.code == code
+
+
+# --------------------------------------------------------------------------- C6 by brute force
+def _iso(g1, g2):
+    """Labelled-graph isomorphism by backtracking: node labels (op kind, role,
+    loop type, side mask), directed M edges, undirected conflict edges."""
+    n1 = {v[0]: tuple(v[1:]) for v in g1["nodes"]}
+    n2 = {v[0]: tuple(v[1:]) for v in g2["nodes"]}
+    if sorted(n1.values()) != sorted(n2.values()) or len(g1["medges"]) != len(g2["medges"]) \
+            or len(g1["cedges"]) != len(g2["cedges"]):
+        return False
+    m1, m2 = {tuple(e) for e in g1["medges"]}, {tuple(e) for e in g2["medges"]}
+    c1 = {frozenset(e) for e in g1["cedges"]}
+    c2 = {frozenset(e) for e in g2["cedges"]}
+    order = sorted(n1, key=lambda v: sum(1 for w in n1 if n1[w] == n1[v]))   # rarest labels first
+    used, mp = set(), {}
+
+    def ok(v, w):
+        for (a, b) in m1:
+            if a == v and b in mp and (w, mp[b]) not in m2:
+                return False
+            if b == v and a in mp and (mp[a], w) not in m2:
+                return False
+        for e in c1:
+            if v in e:
+                (u,) = e - {v} if len(e) == 2 else (v,)
+                if u in mp and frozenset((w, mp[u])) not in c2:
+                    return False
+        return True
+
+    def go(i):
+        if i == len(order):
+            return True
+        v = order[i]
+        for w in n2:
+            if w in used or n2[w] != n1[v] or not ok(v, w):
+                continue
+            mp[v] = w
+            used.add(w)
+            if go(i + 1):
+                return True
+            del mp[v]
+            used.discard(w)
+        return False
+
+    return go(0)
+
+
+F_BLOCKS = """
+  yt1 = transpose[1,0](y1)
+  f1 = matmul(y1, yt1)
+  yt2 = transpose[1,0](y2)
+  f2 = matmul(y2, yt2)
+"""
+
+
+def _attn_and_f(layers=2):
+    ir = models.stacked_attn(layers)
+    head, rest = ir.split(") {", 1)
+    body, ret = rest.rsplit("  return ", 1)
+    return head + ", y1: f32[8,4], y2: f32[16,4]) {" + body + F_BLOCKS + "  return " + ret.replace("\n}", ", f1, f2\n}")
+
+
+def test_setgroups_are_the_isomorphism_classes():
+    """§3.6: sets share a SetGroup iff they are isomorphic.  Checked by
+    brute-force labelled-graph isomorphism of the graphs the C6 hash reads, on
+    two attention layers plus two x·xᵀ blocks (two classes of two sets each)
+    and on random programs with several sets."""
+    cases = [_attn_and_f(2)] + [models.random_program(s, n_ops=24) for s in range(60)]
+    multi = 0
+    for ir in cases:
+        try:
+            o = Oracle(ir, [("a", 2, 1e10), ("b", 4, 1e11)], 1e12, 1 << 40, 100.0, 1)
+        except OracleError:
+            continue
+        d, gs = o.dump(), o.set_graphs()
+        if len(gs) < 2:
+            continue
+        multi += 1
+        grp = d["set_group"]
+        for i in range(len(gs)):
+            for j in range(i + 1, len(gs)):
+                if max(len(gs[i]["nodes"]), len(gs[j]["nodes"])) > 14:
+                    continue
+                assert _iso(gs[i], gs[j]) == (grp[i] == grp[j]), (ir, i, j)
+    assert multi >= 3
+    d = Oracle(_attn_and_f(2), [("s", 2, 1e10)], 1e12, 1 << 40, 100.0, 1).dump()
+    assert len(d["set_group"]) == 4 and d["n_groups"] == 2
