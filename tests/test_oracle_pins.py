@@ -5,6 +5,7 @@ closed form, an invariant, a library known-answer vector, or brute force —
 never from the oracle itself and never from the CUDA path.
 """
 import itertools
+import re
 import json
 import os
 
@@ -584,3 +585,65 @@ def test_setgroups_are_the_isomorphism_classes():
     assert multi >= 3
     d = Oracle(_attn_and_f(2), [("s", 2, 1e10)], 1e12, 1 << 40, 100.0, 1).dump()
     assert len(d["set_group"]) == 4 and d["n_groups"] == 2
+
+
+# --------------------------------------------------------------------------- C7 argument groups
+def _param_partition(ir, names, axes=(("s", 2, 1e10),)):
+    """Partition of the parameters' (name, dim) pairs by super-color."""
+    o = Oracle(ir, list(axes), 1e12, 1 << 40, 100.0, 1)
+    d = o.dump()
+    groups = {}
+    for op, (name, rank) in enumerate(names):
+        for i in range(rank):
+            groups.setdefault(d["loops"][o.def_loop(op, i)][5], set()).add((name, i))
+    return sorted(sorted(g) for g in groups.values()), d
+
+
+def _attn_params(L):
+    return [("x", 2)] + [(f"{w}{l}", 2) for l in range(L) for w in ("wq", "wk", "wv")]
+
+
+def test_argument_groups_mirror_layers():
+    """§4.4: weights of repeated layers are grouped, so every
+    layer's weights share super-colors with layer 0's and the number of
+    super-colors does not grow with the number of layers (from two layers on:
+    chaining layer 0's output into layer 1 already joins the feature dims)."""
+    n_sc = set()
+    for L in (2, 3, 4, 6):
+        part, d = _param_partition(models.stacked_attn(L), _attn_params(L))
+        n_sc.add(len(d["scolors"]))
+        for l in range(1, L):
+            for w in ("wq", "wk", "wv"):
+                for i in range(2):
+                    assert any((f"{w}0", i) in g and (f"{w}{l}", i) in g for g in part), (L, w, l, i)
+    assert len(n_sc) == 1
+
+
+def test_argument_groups_depend_on_uses_only():
+    """Keys are "constructed from all uses": renaming the parameters and
+    permuting their declaration order leaves the grouping unchanged."""
+    import random
+    L = 2
+    ir = models.stacked_attn(L)
+    names = _attn_params(L)
+    base, _ = _param_partition(ir, names)
+    head, rest = ir.split("(", 1)
+    params, body = rest.split(") {", 1)
+    decl = [f"{n}: {t}" for n, t in re.findall(r"(\w+)\s*:\s*(\w+\[[^\]]*\])", params)]
+    assert len(decl) == len(names)
+    rng = random.Random(3)
+    for trial in range(4):
+        perm = list(range(len(decl)))
+        rng.shuffle(perm)
+        ren = {n: f"r{trial}_{k}" for k, (n, _) in enumerate(names)}
+        new_decl = []
+        for k in perm:
+            n, ty = decl[k].split(":", 1)
+            new_decl.append(f"{ren[n.strip()]}:{ty}")
+        new_body = body
+        for n in sorted(ren, key=len, reverse=True):
+            new_body = re.sub(rf"\b{n}\b", ren[n], new_body)
+        ir2 = f"{head}({', '.join(new_decl)}) {{{new_body}"
+        part2, _ = _param_partition(ir2, [(ren[names[k][0]], names[k][1]) for k in perm])
+        inv = {v: k for k, v in ren.items()}
+        assert sorted(sorted((inv[n], i) for n, i in g) for g in part2) == base
