@@ -141,6 +141,13 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(T.ToastError) as e:
         T.eval_batch(a, seqs, out)
     assert e.value.code == "TOAST_E_CUDA"
+    sc = np.zeros(4, dtype=T.SCORE_DTYPE)
+    outs = np.zeros((4, 32), np.uint16)
+    for call in (lambda: T.eval_scores(a, seqs, sc), lambda: T.rollout_scores(a, seqs, 1, 0, outs, sc),
+                 lambda: T.rollout_batch(a, seqs, 1, 0, outs, out)):
+        with pytest.raises(T.ToastError) as e:
+            call()
+        assert e.value.code == "TOAST_E_CUDA"
 
 
 @pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax_np2", "gns16"])
