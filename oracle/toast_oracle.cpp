@@ -12,7 +12,10 @@
 //
 // Parity status per part (see DESIGN.md §"Oracle pins"):
 //   C1–C5, C9–C14 pinned by paper worked examples / closed forms / invariants /
-//   brute force; C15 pinned by Philox KAT vectors; C6 (WL signatures) pinned by
+//   brute force; the C1 rules of the extension ops (dot_general, conv2d and its
+//   adjoints, resample, concat / slice / pad, gather, segment_sum) pinned by
+//   what the lowered programs compute on every device of 2- and 3-axis meshes
+//   (tests/test_lowering.py, the sharded interpreter); C15 pinned by Philox KAT vectors; C6 (WL signatures) pinned by
 //   brute-force isomorphism of the sets' labelled graphs; C7 (argument keys) and
 //   C8 (action table order) are "parity unpinned" beyond the structural
 //   invariants in tests/test_oracle_pins.py.  The contraction

@@ -7,7 +7,9 @@
 // P:796-810):
 //   phase 1  per axis A (mesh order) held on a dim of D that U does not keep
 //            there: first every all_gather (U holds A on no dim), then every
-//            all_to_all (U holds A on another dim) — reading R20
+//            all_to_all (U holds A on another dim), an axis waiting while its
+//            target dim would not divide; moves that block one another run
+//            as one all_to_all listing them all — reading R20
 //   phase 2  per partial axis A: reduce_scatter onto the dim U holds A on,
 //            else all_reduce
 //   phase 3  per axis U holds that the current layout lacks: a local slice
@@ -20,6 +22,7 @@
 //   mesh <name>=<size> ...
 //   %v = <op>[attrs](%a, ...) <dtype> [global dims] local[dims] layout[m0,...] partial[m]
 //   %v.k = all_gather{axis=A,dim=i}(%v) ... bytes=<payload>
+//   %v.k = all_to_all{axis=A,from=i,to=j}+{axis=B,from=j,to=i}(%v) ... bytes=<payload A>+<payload B>
 //   return %a, ...
 // m = bitmask over mesh axes (bit A = axis A of the mesh line).
 #include <cstring>
@@ -106,6 +109,13 @@ toast_status lower_program(const toast_analysis* a, const uint16_t* seq, std::st
       uint64_t size = (uint64_t)val.elem_bytes;
       for (int64_t e : local_shape(val.shape, D)) size *= (uint64_t)e;
       std::string prev = src;
+      auto emit_spec = [&](const std::string& coll, const std::string& bytes) {
+        const std::string name = "%" + val.name + "." + std::to_string(++n_tmp[v]);
+        s += name + " = " + coll + "(" + prev + ") " + kDtypeName[val.dtype_code] + " " + dims_str(val.shape) +
+             " local" + dims_str(local_shape(val.shape, cur)) + " layout" + masks_str(cur) + " partial[" +
+             std::to_string(part) + "] bytes=" + bytes + "\n";
+        prev = name;
+      };
       auto emit = [&](const std::string& coll, uint64_t bytes, bool has_bytes) {
         const std::string name = "%" + val.name + "." + std::to_string(++n_tmp[v]);
         s += name + " = " + coll + "(" + prev + ") " + kDtypeName[val.dtype_code] + " " + dims_str(val.shape) +
@@ -118,27 +128,55 @@ toast_status lower_program(const toast_analysis* a, const uint16_t* seq, std::st
       // phase 1 (reading R20): 1a all_gather the axes U holds on no dim, then
       // 1b all_to_all the axes U holds on another dim (ascending mesh axis,
       // then dim) — every intermediate layout stays divisible
-      for (int pass = 0; pass < 2; ++pass)
-        for (int A = 0; A < n_axes; ++A) {
-          const uint32_t bit = 1u << A;
-          for (int i = 0; i < rank; ++i) {
-            if (!(cur[i] & bit) || (U[i] & bit)) continue;
-            int j_other = -1;
-            for (int j = 0; j < rank; ++j) if (j != i && (U[j] & bit)) j_other = j;
-            if ((j_other >= 0) != (pass == 1)) continue;
-            const uint64_t pay = size;
-            if (j_other >= 0) {
-              cur[i] &= ~bit;
-              cur[j_other] |= bit;
-              emit("all_to_all{axis=" + std::to_string(A) + ",from=" + std::to_string(i) + ",to=" +
-                       std::to_string(j_other) + "}", pay, true);
-            } else {
-              cur[i] &= ~bit;
-              size *= (uint64_t)g.axis_size[A];
-              emit("all_gather{axis=" + std::to_string(A) + ",dim=" + std::to_string(i) + "}", pay, true);
-            }
-          }
+      // 1a: all_gather every axis of D that U holds on no dim
+      struct Move { int A, i, j; };
+      std::vector<Move> moves;
+      for (int A = 0; A < n_axes; ++A) {
+        const uint32_t bit = 1u << A;
+        for (int i = 0; i < rank; ++i) {
+          if (!(cur[i] & bit) || (U[i] & bit)) continue;
+          int j_other = -1;
+          for (int j = 0; j < rank; ++j) if (j != i && (U[j] & bit)) j_other = j;
+          if (j_other >= 0) { moves.push_back({A, i, j_other}); continue; }
+          const uint64_t pay = size;
+          cur[i] &= ~bit;
+          size *= (uint64_t)g.axis_size[A];
+          emit("all_gather{axis=" + std::to_string(A) + ",dim=" + std::to_string(i) + "}", pay, true);
         }
+      }
+      // 1b: all_to_all every axis U holds on another dim.  An all_to_all keeps
+      // the local size, so its payload (and the cost) does not depend on the
+      // order; the moves run in ascending axis order except that an axis waits
+      // while its target dim would not divide (it still holds an axis that is
+      // about to leave), so every intermediate layout stays divisible.  Moves
+      // that block one another (a cycle, e.g. two axes swapping dims whose
+      // extents cannot hold both) run as ONE all_to_all over the product of
+      // their axes: one statement listing every move, each axis charged as
+      // its own all_to_all (reading R20).
+      while (!moves.empty()) {
+        size_t pick = moves.size();
+        for (size_t q = 0; q < moves.size() && pick == moves.size(); ++q) {
+          const Move& m = moves[q];
+          if (val.shape[m.j] % (prod(cur[m.j]) * g.axis_size[m.A]) == 0) pick = q;
+        }
+        std::vector<Move> step;
+        if (pick == moves.size()) {
+          step.swap(moves);
+        } else {
+          step.push_back(moves[pick]);
+          moves.erase(moves.begin() + (long)pick);
+        }
+        std::string spec, bytes;
+        for (const Move& m : step) {
+          const uint32_t bit = 1u << m.A;
+          cur[m.i] &= ~bit;
+          cur[m.j] |= bit;
+          spec += std::string(spec.empty() ? "" : "+") + "{axis=" + std::to_string(m.A) + ",from=" + std::to_string(m.i) +
+                  ",to=" + std::to_string(m.j) + "}";
+          bytes += (bytes.empty() ? "" : "+") + std::to_string(size);
+        }
+        emit_spec("all_to_all" + spec, bytes);
+      }
       // phase 2: reduce_scatter / all_reduce of the partial axes
       for (int A = 0; A < n_axes; ++A) {
         const uint32_t bit = 1u << A;

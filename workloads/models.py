@@ -356,10 +356,14 @@ def unet(B=32, HW=64, C=(320, 640, 1280), heads=32, in_ch=4, temb=320, blocks_do
 # ---------------------------------------------------------------------------
 # small random programs for property tests (seeded)
 # ---------------------------------------------------------------------------
-def random_program(seed: int, n_ops: int = 12, linear: bool = False, max_ext: int = 8) -> str:
+def random_program(seed: int, n_ops: int = 12, linear: bool = False, max_ext: int = 8, ext: bool = False) -> str:
     """A random straight-line program over unary/binary/transpose/reduce/
     broadcast/matmul.  With linear=True every variable is used exactly once
-    (the [comment] linearity theorem)."""
+    (the [comment] linearity theorem).  With ext=True the
+    program also uses every extension op kind of the BASELINE generators
+    (random_program_ext)."""
+    if ext:
+        return random_program_ext(seed, n_ops)
     import random
     rng = random.Random(seed)
     exts = [2, 4, 8][: max(1, [2, 4, 8].index(max_ext) + 1)] if max_ext in (2, 4, 8) else [2, 4]
@@ -442,3 +446,175 @@ def random_program(seed: int, n_ops: int = 12, linear: bool = False, max_ext: in
         b = g.param("pb", "f32", [2, 2])
         rets = rets + [g.matmul(a, b)]
     return g.text(returns=rets)
+
+
+def random_program_ext(seed: int, n_ops: int = 16) -> str:
+    """A random straight-line program over the op kinds the BASELINE
+    generators emit beyond Fig. 3's: dot_general (random batch / contracting
+    dims, including a value contracted with itself), conv2d and its two
+    backward ops (1x1 and 3x3 filters), resample up/down, concat (including a
+    value concatenated with itself), slice, pad, gather and segment_sum (i32
+    index params, shared between ops as in GNS), plus the elementwise /
+    reduce / broadcast / transpose ops that glue them.  Extents are 2, 4, 8 and
+    the odd extents pad creates; the first ops are a conv pair and a
+    dot_general so every program has a contraction."""
+    import random
+    rng = random.Random(seed)
+    g = Builder(f"x{seed}")
+    E = [2, 4, 8]
+    vals = []           # values usable as operands
+    idx_params = {}     # index shape -> i32 param
+    n_p = [0]
+
+    def newp(shape, dt="f32"):
+        n_p[0] += 1
+        return g.param(f"p{n_p[0]}", dt, list(shape))
+
+    def idx(shape):
+        shape = tuple(shape)
+        if shape not in idx_params or rng.random() < 0.3:
+            n_p[0] += 1
+            idx_params[shape] = g.data(f"i{n_p[0]}", "i32", list(shape))
+        return idx_params[shape]
+
+    def rank(r):
+        c = [v for v in vals if len(g.shape[v]) == r]
+        return rng.choice(c) if c else None
+
+    # seed values: an image-like tensor and a couple of matrices / 3-tensors
+    img = newp([rng.choice([2, 4]), 4, 4, rng.choice(E)])
+    vals += [img, newp([rng.choice(E), rng.choice(E)]), newp([rng.choice(E), rng.choice(E), rng.choice(E)])]
+    w0 = newp([3, 3, g.shape[img][3], rng.choice(E)])
+    vals.append(g.conv2d(img, w0))
+    m = vals[1]
+    vals.append(g.dot_general(m, newp([g.shape[m][1], rng.choice(E)]), [], [], [1], [0]))
+
+    kinds = ["dot", "dot", "self_dot", "conv", "conv_bwd", "resample", "concat", "slice", "pad", "gather",
+             "segment_sum", "unary", "binary", "reduce", "broadcast", "transpose"]
+    for _ in range(n_ops):
+        k = rng.choice(kinds)
+        out = None
+        if k == "dot":
+            x = rng.choice(vals)
+            s = g.shape[x]
+            dims = list(range(len(s)))
+            rng.shuffle(dims)
+            nb = rng.randint(0, max(0, len(s) - 1)) if len(s) >= 2 else 0
+            nb = min(nb, 1)
+            lb, lc = dims[:nb], dims[nb:nb + rng.randint(1, max(1, len(s) - nb))]
+            if not lc:
+                continue
+            free = [rng.choice(E) for _ in range(rng.randint(0, 1))]
+            # rhs dims in a random order: batch, contracting, free
+            items = [("b", i) for i in range(len(lb))] + [("c", i) for i in range(len(lc))] + [("f", i) for i in range(len(free))]
+            rng.shuffle(items)
+            shape, rb, rc = [], [0] * len(lb), [0] * len(lc)
+            for pos, (t, i) in enumerate(items):
+                if t == "b":
+                    rb[i] = pos
+                    shape.append(s[lb[i]])
+                elif t == "c":
+                    rc[i] = pos
+                    shape.append(s[lc[i]])
+                else:
+                    shape.append(free[i])
+            y = rank(len(shape)) if rng.random() < 0.3 else None
+            if y is None or list(g.shape[y]) != shape:
+                y = newp(shape)
+            out = g.dot_general(x, y, lb, rb, lc, rc)
+        elif k == "self_dot":      # x . x^T-like: contract one dim of a value with itself (a conflict)
+            x = rng.choice([v for v in vals if len(g.shape[v]) in (2, 3)] or vals)
+            s = g.shape[x]
+            if len(s) < 2:
+                continue
+            c = len(s) - 1
+            b = [0] if len(s) == 3 else []
+            out = g.dot_general(x, x, b, b, [c], [c])
+        elif k == "conv":
+            x = rank(4)
+            if x is None:
+                continue
+            kk = rng.choice([1, 3])
+            out = g.conv2d(x, newp([kk, kk, g.shape[x][3], rng.choice(E)]))
+        elif k == "conv_bwd":
+            x = rank(4)
+            if x is None:
+                continue
+            kk = rng.choice([1, 3])
+            co = rng.choice(E)
+            w = newp([kk, kk, g.shape[x][3], co])
+            y = g.conv2d(x, w)
+            vals.append(y)
+            if rng.random() < 0.5:
+                out = g.conv2d_bwd_input(y, w)
+            else:
+                out = g.conv2d_bwd_filter(x, y, kk, kk)
+        elif k == "resample":
+            x = rank(4)
+            if x is None:
+                continue
+            s = g.shape[x]
+            if s[1] >= 4 and s[1] % 2 == 0 and s[2] % 2 == 0 and rng.random() < 0.5:
+                out = g.resample(x, "down", 2)
+            elif s[1] <= 4:
+                out = g.resample(x, "up", 2)
+            else:
+                continue
+        elif k == "concat":
+            x = rng.choice(vals)
+            d = rng.randrange(len(g.shape[x]))
+            others = [v for v in vals if v != x and len(g.shape[v]) == len(g.shape[x])
+                      and all(g.shape[v][i] == g.shape[x][i] for i in range(len(g.shape[x])) if i != d)]
+            y = rng.choice(others) if others and rng.random() < 0.6 else x   # concat([x, x]): a repeated operand
+            out = g.concat([x, y], d)
+        elif k == "slice":
+            x = rng.choice(vals)
+            d = rng.randrange(len(g.shape[x]))
+            e = g.shape[x][d]
+            if e < 2:
+                continue
+            out = g.slice(x, d, rng.randrange(0, e // 2 + 1), e // 2)
+        elif k == "pad":
+            x = rng.choice(vals)
+            d = rng.randrange(len(g.shape[x]))
+            lo = rng.choice([0, 1, 2])
+            out = g.pad(x, d, lo, 2 - lo if rng.random() < 0.7 else 1 - min(lo, 1))
+        elif k == "gather":
+            t = rank(2)
+            if t is None:
+                continue
+            ishape = [rng.choice(E)] if rng.random() < 0.7 else [rng.choice(E), rng.choice(E)]
+            out = g.gather(t, idx(ishape))
+        elif k == "segment_sum":
+            x = rng.choice([v for v in vals if len(g.shape[v]) in (2, 3)] or vals)
+            s = g.shape[x]
+            if len(s) < 2:
+                continue
+            out = g.segment_sum(x, idx(s[:-1]), rng.choice(E))
+        elif k == "unary":
+            x = rng.choice(vals)
+            out = g.unary(rng.choice(["relu", "exp", "neg", "silu"]), x)
+        elif k == "binary":
+            x = rng.choice(vals)
+            same = [v for v in vals if g.shape[v] == g.shape[x]]
+            out = g.binary(rng.choice(["add", "mul", "sub"]), x, rng.choice(same))
+        elif k == "reduce":
+            x = rng.choice([v for v in vals if len(g.shape[v]) >= 2] or vals)
+            if len(g.shape[x]) < 2:
+                continue
+            out = g.reduce(x, [rng.randrange(len(g.shape[x]))], rng.choice(["add", "add", "max"]))
+        elif k == "broadcast":
+            x = rng.choice([v for v in vals if len(g.shape[v]) <= 3] or vals)
+            if len(g.shape[x]) > 3:
+                continue
+            out = g.broadcast(x, rng.randint(0, len(g.shape[x])), rng.choice(E))
+        elif k == "transpose":
+            x = rng.choice([v for v in vals if len(g.shape[v]) >= 2] or vals)
+            perm = list(range(len(g.shape[x])))
+            if len(perm) < 2:
+                continue
+            rng.shuffle(perm)
+            out = g.transpose(x, perm)
+        if out is not None and out not in vals and len(g.shape[out]) >= 1:
+            vals.append(out)
+    return g.text(returns=[vals[-1], vals[4]] if vals[-1] != vals[4] else [vals[-1]])
