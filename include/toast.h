@@ -198,8 +198,13 @@ toast_status toast_eval_scores(const toast_analysis* a, const uint16_t* seqs, in
 toast_status toast_rollout_scores(const toast_analysis* a, const uint16_t* prefixes, int64_t n, uint64_t seed,
                                   uint64_t id_base, uint16_t* out_seqs, toast_score* out, void* cuda_stream);
 
-/* per-loop axis masks of one sequence (debug / tests; NEXT-1 lowering).
- * masks: uint8[cap]; *n = number of loops. seq is a host pointer. */
+/* per-loop axis masks of one sequence (debug / tests; NEXT-1 lowering) — the
+ * "attempt" materialisation of C9 (reading G1).
+ * masks: uint8[cap]; *n = number of loops. seq is a host pointer.
+ * Errors: TOAST_E_INVALID_ARG for NULL, or (when masks is written) for a
+ * sequence the kernels' decode would flag (any TOAST_ST_* bit: an id >= the
+ * action count, a repeated (super-color, axis), a resolution disagreeing with
+ * an earlier fixed SetGroup bit, a nonzero id after STOP). */
 toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], uint8_t* masks, int64_t cap,
                                int64_t* n);
 
@@ -212,7 +217,8 @@ toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], 
  * Text, one statement per line; format in DESIGN.md "Lowering" and
  * csrc/lower.cpp.  seq: host uint16[32] (0 = STOP).  *needed = bytes incl.
  * NUL; writes only if cap >= *needed.  Host-side (no GPU needed).
- * Errors: TOAST_E_INVALID_ARG (NULL, an id >= the action count). */
+ * Errors: TOAST_E_INVALID_ARG (NULL, or a sequence the kernels' decode would
+ * flag with any TOAST_ST_* bit — see toast_materialize). */
 toast_status toast_lower(const toast_analysis* a, const uint16_t seq[32], char* buf, size_t cap, size_t* needed);
 
 /* ---------------------------------------------------------------------------

@@ -206,8 +206,8 @@ toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], 
   if (!a || !seq || !n) return fail(TOAST_E_INVALID_ARG, "NULL argument");
   *n = a->n_loops;
   if (masks && cap >= a->n_loops) {
-    for (int i = 0; i < 32 && seq[i]; ++i)
-      if (seq[i] >= a->actions.size()) return fail(TOAST_E_INVALID_ARG, "bad action id");
+    if (const uint32_t st = toast::host_validate(a, seq))
+      return fail(TOAST_E_INVALID_ARG, "invalid sequence (TOAST_ST_* bits " + std::to_string(st) + ")");
     toast::host_materialize(a, seq, masks);
   }
   return ret(TOAST_OK, "");
@@ -215,8 +215,8 @@ toast_status toast_materialize(const toast_analysis* a, const uint16_t seq[32], 
 
 toast_status toast_lower(const toast_analysis* a, const uint16_t seq[32], char* buf, size_t cap, size_t* needed) {
   if (!a || !seq || !needed) return fail(TOAST_E_INVALID_ARG, "NULL argument");
-  for (int i = 0; i < 32 && seq[i]; ++i)
-    if (seq[i] >= a->actions.size()) return fail(TOAST_E_INVALID_ARG, "bad action id");
+  if (const uint32_t st = toast::host_validate(a, seq))
+    return fail(TOAST_E_INVALID_ARG, "invalid sequence (TOAST_ST_* bits " + std::to_string(st) + ")");
   std::string s, err;
   toast_status st = toast::lower_program(a, seq, s, err);
   if (st != TOAST_OK) return fail(st, err);

@@ -1605,6 +1605,37 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
 }
 
 // ---------------------------------------------------------------- host materialisation (debug)
+// The decode checks of C9 (the kernels' H1) on the host: 0, or the TOAST_ST_*
+// bits of an invalid sequence (which toast_lower / toast_materialize refuse).
+uint32_t host_validate(const toast_analysis* a, const uint16_t* seq) {
+  const DeviceTables& T = a->dt;
+  uint32_t status = 0;
+  bool stopped = false;
+  uint64_t fixed = 0, ones = 0;
+  std::vector<uint32_t> axes_of(T.n_acolors, 0);   // per action color: the axes its actions used
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t id = seq[j];
+    if (stopped) { if (id) status |= TOAST_ST_NONZERO_AFTER_STOP; continue; }
+    if (id == 0) { stopped = true; continue; }
+    if (id >= a->h_actions.size()) { status |= TOAST_ST_BAD_ACTION_ID; continue; }
+    const uint32_t w = a->h_actions[id];
+    const uint32_t ac = w & 0x3FF, r = (w >> 10) & 0xFF, ax = (w >> 18) & 3;
+    if ((axes_of[ac] >> ax) & 1) status |= TOAST_ST_DUP_COLOR_AXIS;
+    axes_of[ac] |= 1u << ax;
+    const uint64_t gw = a->h_acol_groups[ac];
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t gid = (gw >> (8 * t)) & 0xFF;
+      if (gid == 0xFF) continue;
+      const uint64_t g = 1ULL << gid, bit = (r >> t) & 1;
+      if ((fixed & g) && (((ones >> gid) & 1) != bit)) status |= TOAST_ST_RES_MISMATCH;
+      if (!(fixed & g)) { fixed |= g; if (bit) ones |= g; }
+    }
+  }
+  return status;
+}
+
+// masks of a VALID sequence (host_validate == 0): an action color holds at
+// most one action per mesh axis, so at most 4 events fit its 4 slots
 void host_materialize(const toast_analysis* a, const uint16_t* seq, uint8_t* masks) {
   const DeviceTables& T = a->dt;
   std::vector<uint32_t> lists(T.n_acolors, 0);
@@ -1615,7 +1646,8 @@ void host_materialize(const toast_analysis* a, const uint16_t* seq, uint8_t* mas
     uint32_t w = a->h_actions[seq[j]];
     uint32_t ac = w & 0x3FF, r = (w >> 10) & 0xFF, ax = (w >> 18) & 3;
     int rank = 0;
-    while ((lists[ac] >> (8 * rank)) & 0x80) ++rank;
+    while (rank < 4 && ((lists[ac] >> (8 * rank)) & 0x80)) ++rank;
+    if (rank == 4) continue;   // unreachable for a valid sequence (see host_validate)
     lists[ac] |= (0x80u | (ax << 5) | (uint32_t)j) << (8 * rank);
     uint64_t gw = a->h_acol_groups[ac];
     for (int t = 0; t < 8; ++t) {
@@ -1682,7 +1714,8 @@ std::string dump_json(const toast_analysis* a) {
          I((int64_t)a->cp_walked_ops) + ",\"cp_walked_edges\":" + I((int64_t)a->cp_walked_edges) + ",\"cp_bundles\":" + I((int64_t)a->h_cp_bsize.size()) + ",\"n_acolors\":" + I((int64_t)a->dt.n_acolors) +
          ",\"n_words\":" + I((int64_t)a->dt.n_words) + ",\"n_fsig\":" + I((int64_t)a->dt.n_fsig) + ",\"n_ftmpl\":" +
          I((int64_t)a->dt.n_ftmpl) + ",\"warps_per_batch\":" +
-         I((int64_t)a->k_throughput) + ",\"blocks_per_sm\":" +
+         I((int64_t)a->k_throughput) + ",\"kernel_variant\":[" + I((int64_t)a->dt.n_axes) + "," +
+         I((int64_t)a->dt.pow2) + "," + I((int64_t)a->dt.cost_model) + "],\"blocks_per_sm\":" +
          I((int64_t)a->occ_roll[a->k_throughput >= 8 ? 3 : a->k_throughput >= 4 ? 2 : a->k_throughput >= 2 ? 1 : 0]) + ",\"work\":{\"sig_roles\":" + I(a->work_sig_roles) + ",\"n_tmpl\":" +
          I(a->work_tmpl) + ",\"n_terms\":" + I(a->work_terms) + "},\"frontier_ops\":[";
     for (size_t q = 0; q < a->point_op.size(); ++q) { if (q) s += ','; s += I(a->point_op[q]); }

@@ -310,6 +310,7 @@ toast_status parse_ir(const char* text, size_t len, toast_graph* g, std::string&
 // analysis.cpp
 toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast_analysis* a, std::string& err);
 std::string dump_json(const toast_analysis* a);
+uint32_t host_validate(const toast_analysis* a, const uint16_t* seq);
 void host_materialize(const toast_analysis* a, const uint16_t* seq, uint8_t* masks);
 // lower.cpp: the device-local program of one action sequence (NEXT-1)
 toast_status lower_program(const toast_analysis* a, const uint16_t* seq, std::string& out, std::string& err);

@@ -57,6 +57,14 @@ def search_root_parallel(a: "T.Analysis", opts: "T.SearchOptions", group=None, s
     return st.end()
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def rank_id_base(rank: int, per_rank: int) -> int:
     """Disjoint Philox counter ranges per rank for weak-scaled rollouts."""
     return rank << 40
@@ -87,14 +95,25 @@ def eval_sharded(a: "T.Analysis", seqs, group=None, stream=None, compact: bool =
     rec = 16 if compact else 256
     lo, hi = shard_range(n, rank, world)
     width = shard_range(n, 0, world)[1]            # the largest slice
-    local = torch.zeros((width, rec), dtype=torch.uint8, device=seqs.device)
-    if hi > lo:
-        if _evaluate is not None:
-            _evaluate(seqs[lo:hi], local[: hi - lo])
-        elif compact:
-            T.eval_scores(a, seqs[lo:hi], local[: hi - lo], stream=stream)
-        else:
-            T.eval_batch(a, seqs[lo:hi], local[: hi - lo], stream=stream)
+    cuda = seqs.device.type == "cuda"
+    # everything (the zero fill, the evaluation) runs on `stream`; the current
+    # stream, which the collective is ordered on, waits for it
+    side = stream if (cuda and stream is not None) else None
+    if side is not None and not isinstance(side, torch.cuda.Stream):
+        side = torch.cuda.ExternalStream(int(getattr(side, "cuda_stream", side)))
+    ctx = torch.cuda.stream(side) if side is not None else _nullctx()
+    with ctx:
+        local = torch.zeros((width, rec), dtype=torch.uint8, device=seqs.device)
+        if hi > lo:
+            if _evaluate is not None:
+                _evaluate(seqs[lo:hi], local[: hi - lo])
+            elif compact:
+                T.eval_scores(a, seqs[lo:hi], local[: hi - lo], stream=side)
+            else:
+                T.eval_batch(a, seqs[lo:hi], local[: hi - lo], stream=side)
+    if side is not None:
+        torch.cuda.current_stream().wait_stream(side)
+        local.record_stream(torch.cuda.current_stream())
     gathered = torch.empty((world * width, rec), dtype=torch.uint8, device=seqs.device)
     dist.all_gather_into_tensor(gathered, local, group=group)
     parts = [gathered[r * width: r * width + (shard_range(n, r, world)[1] - shard_range(n, r, world)[0])]

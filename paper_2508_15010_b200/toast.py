@@ -274,6 +274,7 @@ def eval_batch(a: Analysis, seqs, out, stream=None, n: int | None = None):
 def rollout_batch(a: Analysis, prefixes, seed: int, id_base: int, out_seqs, out, stream=None, n: int | None = None):
     """toast_rollout_batch: extend each prefix with Philox draws (H8), then cost it."""
     n = _len(prefixes, 64) if n is None else n
+    assert _len(out, 256) >= n and _len(out_seqs, 64) >= n, "output buffers hold fewer than n rows"
     _check(_lib.toast_rollout_batch(a._h, _ptr(prefixes), int(n), int(seed), int(id_base), _ptr(out_seqs),
                                     _ptr(out), _stream(stream)))
     return out_seqs, out
@@ -290,7 +291,7 @@ def eval_scores(a: Analysis, seqs, out, stream=None, n: int | None = None):
 def rollout_scores(a: Analysis, prefixes, seed: int, id_base: int, out_seqs, out, stream=None, n: int | None = None):
     """toast_rollout_scores: toast_rollout_batch with 16-B toast_score results."""
     n = _len(prefixes, 64) if n is None else n
-    assert _len(out, 16) >= n
+    assert _len(out, 16) >= n and _len(out_seqs, 64) >= n, "output buffers hold fewer than n rows"
     _check(_lib.toast_rollout_scores(a._h, _ptr(prefixes), int(n), int(seed), int(id_base), _ptr(out_seqs),
                                      _ptr(out), _stream(stream)))
     return out_seqs, out

@@ -76,18 +76,24 @@ def assert_same(g: np.ndarray, o: np.ndarray, ctx=""):
         assert len(bad) == 0, (ctx, f, bad[:5], g[f][bad[:5]], o[f][bad[:5]])
 
 
-ALL = ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2", "gpt24", "gns16", "unet"]
+ALL = ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_1ax_np2", "gpt2_3ax", "gpt2_3ax_np2", "gpt2_4ax", "gpt2_4ax_np2",
+       "gpt24", "gns16", "unet", "llama80"]
+# the small configs the oracle evaluates thousands of times in seconds
+SMALL = ("mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_1ax_np2", "gpt2_3ax", "gpt2_3ax_np2", "gpt2_4ax", "gpt2_4ax_np2")
+# one config per kernel instantiation (mesh axes, every axis a power of two)
+VARIANT_CONFIG = {(1, 1): "attn_toy", (1, 0): "gpt2_1ax_np2", (2, 1): "gpt2", (2, 0): "gpt2_np2", (3, 1): "gpt2_3ax",
+                  (3, 0): "gpt2_3ax_np2", (4, 1): "gpt2_4ax", (4, 0): "gpt2_4ax_np2"}
 
 
 @pytest.mark.parametrize("name", ALL)
 def test_eval_parity_on_oracle_rollouts(name):
     a, o = setup(name)
-    n = 3000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2") else 300
+    n = 3000 if name in SMALL else 100 if name == "llama80" else 300
     seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=1234, threads=8)
     assert_same(gpu_eval(a, seqs), oc, name)
 
 
-@pytest.mark.parametrize("name", ["mlp_c", "gpt2", "unet"])
+@pytest.mark.parametrize("name", ["mlp_c", "gpt2", "gpt2_3ax", "gpt2_3ax_np2", "gpt2_4ax_np2", "unet"])
 def test_eval_parity_uniform_ids_and_status(name):
     """Raw random ids: exercises BAD_ACTION_ID, DUP, RES_MISMATCH, NONZERO_AFTER_STOP
     next to valid sequences (ragged lengths 0..30)."""
@@ -130,10 +136,11 @@ def _legal_long(o: Oracle, n: int, seed: int, length: int = 30) -> np.ndarray:
     return out
 
 
-@pytest.mark.parametrize("name", ["unet", "gpt24", "gns16", "mlp_c"])
+@pytest.mark.parametrize("name", ["unet", "gpt24", "gns16", "mlp_c", "gpt2_3ax", "gpt2_3ax_np2", "gpt2_1ax_np2",
+                                  "llama80"])
 def test_eval_parity_worst_case_long_sequences(name):
     a, o = setup(name)
-    seqs = _legal_long(o, 200, seed=3)
+    seqs = _legal_long(o, 60 if name == "llama80" else 200, seed=3)
     oc = o.eval(seqs, threads=8)
     assert (oc["status"] == 0).all()
     assert_same(gpu_eval(a, seqs), oc, name)
@@ -153,12 +160,12 @@ def test_eval_host_pointer_path_and_edges():
     T.eval_batch(a, seqs[:0], one[:0], n=0)
 
 
-@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2", "gpt24", "unet",
-                                  "gns16"])
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_1ax_np2", "gpt2_3ax", "gpt2_3ax_np2",
+                                  "gpt2_4ax", "gpt2_4ax_np2", "gpt24", "unet", "gns16", "llama80"])
 def test_rollout_parity(name):
     """K2 vs C15: same (seed, id) -> same sequence and same cost record."""
     a, o = setup(name)
-    n = 2000 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gpt2_4ax_np2") else 200
+    n = 2000 if name in SMALL else 100 if name == "llama80" else 200
     pre = np.zeros((n, 32), np.uint16)
     # half the rows start from a (legal) prefix drawn by the oracle
     s0, _ = o.rollout(np.zeros((n // 2, 32), np.uint16), seed=77)
@@ -185,7 +192,7 @@ def test_rollout_bad_prefix_is_not_extended():
     assert_same(gc, oc)
 
 
-@pytest.mark.parametrize("name,samples", [("gpt24", 48), ("unet", 24), ("gns16", 24), ("llama80", 6)])
+@pytest.mark.parametrize("name,samples", [("gpt24", 48), ("unet", 24), ("gns16", 24), ("llama80", 200)])
 def test_full_size_bench_launch_sampled(name, samples):
     """Every BASELINE config at full size in bench.py's launch configuration
     (2^18 rollouts rounded down to whole waves, from the empty prefix, bench's
@@ -292,9 +299,12 @@ def test_eval_sharded_nccl_single_rank():
         d = torch.from_numpy(np.ascontiguousarray(seqs).view(np.int16)).cuda()
         full = P.eval_sharded(a, d)
         comp = P.eval_sharded(a, d, compact=True)
+        side = torch.cuda.Stream()              # a caller's stream other than the current one
+        full_side = P.eval_sharded(a, d, stream=side)
     finally:
         dist.destroy_process_group()
     assert T.as_costs(full).tobytes() == oc.tobytes()
+    assert T.as_costs(full_side).tobytes() == oc.tobytes()
     sc = T.as_scores(comp)
     assert (sc["score"].view(np.uint64) == oc["score"].view(np.uint64)).all() and (sc["state_key"] == oc["state_key"]).all()
 
@@ -367,12 +377,13 @@ def setup_cp(name):
     return _cp_cache[name]
 
 
-@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax", "gns16", "unet"])
+@pytest.mark.parametrize("name", ["mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_1ax_np2", "gpt2_3ax", "gpt2_3ax_np2",
+                                  "gpt2_4ax", "gpt2_4ax_np2", "gns16", "unet", "llama80"])
 def test_critical_path_rollout_parity(name):
     """Reading R22: rollouts + evaluation under the critical-path cost model,
     bit-exact to the oracle's critical path (runtime, score and every field)."""
     a, o = setup_cp(name)
-    n = 2048 if name in ("mlp_c", "attn_toy", "gpt2", "gpt2_np2", "gpt2_4ax") else 256
+    n = 2048 if name in SMALL else 48 if name == "llama80" else 256
     pre = np.zeros((n, 32), np.uint16)
     os_, oc = o.rollout(pre, seed=9, id_base=5)
     gs, gc = gpu_rollout(a, pre, 9, 5)
@@ -529,3 +540,39 @@ def test_cli_partitions_a_program(tmp_path, capsys):
     assert "return" in out and "mesh" in out
     assert main(["--config", "gpt2", "--cost-model", "cp", "--grouping", "contraction", "--budget", "20000",
                  "--no-program"]) == 0
+
+
+@pytest.mark.parametrize("cost_model", [0, 1])
+@pytest.mark.parametrize("variant", sorted(VARIANT_CONFIG))
+def test_every_kernel_instantiation_matches_the_oracle(variant, cost_model):
+    """Each of the 32 kernels (toast_eval_kernel / toast_rollout_kernel x mesh
+    axes 1-4 x power-of-two or not x sum / critical-path model) is the one the
+    analysis dispatches (its kernel_variant) and is bit-exact to the oracle on
+    rollouts from the root and from prefixes and on their re-evaluation."""
+    name = VARIANT_CONFIG[variant]
+    a, o = setup_cp(name) if cost_model else setup(name)
+    assert a.kernel_tables()["kernel_variant"] == [variant[0], variant[1], cost_model]
+    n = 1000
+    pre = np.zeros((n, 32), np.uint16)
+    s0, _ = o.rollout(np.zeros((n // 2, 32), np.uint16), seed=31)
+    for i in range(n // 2):
+        pre[i, :i % 3] = s0[i, :i % 3]
+    os_, oc = o.rollout(pre, seed=8, id_base=1 << 40, threads=8)
+    gs, gc = gpu_rollout(a, pre, 8, 1 << 40)
+    assert np.array_equal(gs, os_)
+    assert_same(gc, oc, (name, cost_model))
+    assert_same(gpu_eval(a, os_), oc, (name, cost_model))
+
+
+def test_llama80_worst_case_and_sampled_critical_path():
+    """Llama-80 (the 3-axis BASELINE config) under the critical-path model:
+    maximal-length sequences evaluated, and a bench-sized launch sampled."""
+    a, o = setup_cp("llama80")
+    seqs = _legal_long(o, 24, seed=5)
+    assert_same(gpu_eval(a, seqs), o.eval(seqs, threads=8), "llama80 cp worst case")
+    n = 32 * 148 * 4
+    gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), 77, 0)
+    for i in np.random.default_rng(4).choice(n, size=24, replace=False):
+        s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=77, id_base=int(i))
+        assert np.array_equal(gs[i], s1[0])
+        assert_same(gc[i:i + 1], c1, f"row {i}")

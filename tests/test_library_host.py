@@ -214,3 +214,30 @@ def test_peak_frontier_random_programs():
             prof = o.profile(seq)
             assert prof.max() == prof[front].max(), (ir, list(seq))
     assert ran >= 30
+
+
+def test_lower_and_materialize_refuse_invalid_sequences():
+    """toast_lower / toast_materialize run the decode checks of C9 (the kernels'
+    H1): a repeated (super-color, axis), a resolution that disagrees with a
+    fixed SetGroup bit, a nonzero id after STOP or a bad id is refused with
+    TOAST_E_INVALID_ARG — exactly when the oracle flags the sequence — and a
+    color repeated five times returns at once (it used to hang)."""
+    import ctypes
+    from workloads import candidates
+    T = _lib()
+    a, o, _ = _both("mlp_c")
+    for bad in ([1, 1], [3, 6], [1, 0, 2], [1, 1, 1, 1, 1], [999]):
+        s = np.zeros((1, 32), np.uint16)
+        s[0, :len(bad)] = bad
+        assert int(o.eval(s)[0]["status"]) != 0, bad
+        for f in (T.lower, T.materialize):
+            with pytest.raises(T.ToastError) as e:
+                f(a, bad)
+            assert e.value.code == "TOAST_E_INVALID_ARG"
+    seqs = candidates.uniform(400, o.n_actions + 1, seed=11, bad_frac=0.1)
+    st = o.eval(seqs)["status"]
+    assert (st != 0).sum() > 50 and (st == 0).sum() > 20
+    for s, bits in zip(seqs, st):
+        n = ctypes.c_size_t()
+        rc = T._lib.toast_lower(a.handle, np.ascontiguousarray(s).ctypes.data, None, 0, ctypes.byref(n))
+        assert (rc != 0) == (bits != 0), (s, bits)

@@ -68,6 +68,11 @@ def get(name: str, **kw) -> Config:
         return Config("gpt2_np2", models.gpt(layers=2, B=12, S=48, D=96, H=6, Dh=16, F=384, V=384, name="gpt2np2"),
                       (("data", 3, BW_NIC), ("model", 6, BW_NVLINK)), F_B200, 1 << 22, 100.0, 10,
                       description="2-layer GPT on a non-power-of-two mesh {data:3, model:6}")
+    if name == "gpt2_1ax_np2":
+        # the 2-layer GPT on one non-power-of-two axis (the kernels' NA = 1, P2 = false instantiation)
+        return Config("gpt2_1ax_np2", models.gpt(layers=2, B=12, S=48, D=96, H=6, Dh=16, F=384, V=384, name="gpt2np2"),
+                      (("model", 3, BW_NVLINK),), F_B200, 1 << 22, 100.0, 10,
+                      description="2-layer GPT on a one-axis non-power-of-two mesh {model:3}")
     if name == "gpt2_3ax":
         # the 2-layer GPT on a three-axis mesh (the kernels' NA = 3 instantiation, Llama-80's mesh shape)
         return Config("gpt2_3ax", models.gpt(layers=2, B=8, S=64, D=64, H=4, Dh=16, F=256, V=512, name="gpt2"),
