@@ -115,7 +115,7 @@ typedef struct {
   double score;            /* RT + MP */
   uint64_t peak_bytes;     /* C12: max over program points of live device-local bytes */
   uint64_t flops;          /* C10: low 64 bits of the local matmul-class FLOP total */
-  uint64_t state_key;      /* C14 (R14): sum over sharded ops of mix64(first loop << 16 | axis->role map) */
+  uint64_t state_key;      /* C14 (R14): sum over (op, axis A, role r holding A) of mix64(first loop << 8 | A << 4 | r) */
   uint32_t status;         /* TOAST_ST_* bits; 0 = ok */
   uint32_t n_collectives;  /* total number of collectives (count[][] saturates at 65535) */
   uint64_t payload[4][4];  /* C11 bytes per [axis][AG, RS, AR, A2A] */
@@ -148,20 +148,34 @@ toast_status toast_load_graph(const char* ir_text, size_t len, const toast_axis*
  * `g` stays owned by the caller and may be freed after this call. */
 toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_analysis** out);
 
-/* number of actions including STOP (id 0) */
+/* number of actions including STOP (id 0): the action table of §4.2 (
+ * SURVEY §8(c) C8).  Errors: TOAST_E_INVALID_ARG (NULL). */
 toast_status toast_num_actions(const toast_analysis* a, int32_t* n);
-/* fills up to cap entries (index = action id); *n = number of actions */
+/* the action table (§4.2, C8): per action id (index; id 0 = STOP,
+ * all -1 but n_value_dims 0) the super-color (§4.4), the
+ * resolution bits over its SetGroups (§3.5-3.6), the mesh axis,
+ * and the number of value dims of the super-color ("at least 10 unique
+ * dimensions").  Fills up to cap entries (caller-owned host array); *n = the
+ * number of actions.  Errors: TOAST_E_INVALID_ARG (NULL, or cap > 0 with out NULL). */
 toast_status toast_query_actions(const toast_analysis* a, toast_action_info* out, int32_t cap, int32_t* n);
-/* the empty sequence's record (RT = 1) */
+/* the empty sequence's record — the unsharded module at the root of the tree
+ * (P:1418), whose runtime and peak are the normalisers t0 and peak0 of
+ * RT / MP, so its RT = 1.  out: caller-owned host toast_cost.
+ * Errors: TOAST_E_INVALID_ARG (NULL). */
 toast_status toast_query_baseline(const toast_analysis* a, toast_cost* out);
 /* candidates one full wave of the GPU evaluates at once (resident warps x 32);
- * batch sizes that are multiples of it leave no partially filled last wave. */
+ * batch sizes that are multiples of it leave no partially filled last wave
+ * (the "many trajectories in parallel" of P:1400, sized for this GPU).
+ * Errors: TOAST_E_INVALID_ARG (NULL); TOAST_E_CUDA for a host-only analysis. */
 toast_status toast_preferred_batch(const toast_analysis* a, int64_t* n);
-/* JSON dump of the H0 tables (loops, conflicts, sets, groups, super-colors,
- * actions, baseline) plus "kernel_tables": the sizes of the per-candidate
- * tables the kernels read and the op index of every peak-memory frontier
- * point (reading R19).  *needed = bytes incl. NUL; writes only if
- * cap >= *needed. */
+/* JSON dump of the H0 tables (loops with their Fig. 3 names' classes P:443-558,
+ * conflicts P:743-746, compatibility sets P:924-946, SetGroups P:949-959,
+ * super-colors P:1442-1449, actions P:1407-1417, baseline P:1461-1477) plus
+ * "kernel_tables": the sizes of the per-candidate tables the kernels read,
+ * the dispatched kernel variant [mesh axes, power-of-two, cost model] and the
+ * op index of every peak-memory frontier point (reading R19).
+ * *needed = bytes incl. NUL; writes only if cap >= *needed (caller-owned host
+ * buffer).  Errors: TOAST_E_INVALID_ARG (NULL). */
 toast_status toast_dump_analysis(const toast_analysis* a, char* buf, size_t cap, size_t* needed);
 
 /* toast_eval_batch — H1-H7 for n candidates.  seqs: uint16[n][32] action ids,
