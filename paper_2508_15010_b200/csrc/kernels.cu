@@ -59,47 +59,51 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// per-warp shared memory = region A (the signature table, overlaid with the
-// sequence + rollout legal set, which are dead once the table is written) +
-// region B (per-color event lists during decode/materialise, then the
-// payload/count accumulators during the sweep)
-__host__ __device__ inline int sig_entry_bytes(int n_axes) { return n_axes <= 2 ? 2 : 4; }
 __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
-// Block shared memory for one batch of 32 candidates swept by K warps:
-//   C  per lane: decode status and the fixed SetGroup bits (read by all warps)
-//   A  the per-lane signature table [n_sigs][32], overlaid with the staged
-//      sequence [16][32] and the rollout legal set [n_words][32] (dead once
-//      the table is written)
-//   B  the per-color event lists [n_acolors][32] (decode/materialise), then,
-//      the payload/count accumulators and (K > 1) the state key / FLOPs / peak
-//      partials — shared by the warps, or one region per warp (acc_shared)
-__host__ __device__ inline int smem_c_bytes(int n_axes) { return 32 * (8 + 8 + 4 + 8 + 4 * n_axes); }
-__host__ __device__ inline int smem_a_bytes(int n_sigs, int n_words, int n_axes) {
-  int a1 = n_sigs * 32 * sig_entry_bytes(n_axes), a2 = 2048 + n_words * 128;
-  return r16(a1 > a2 ? a1 : a2);
-}
+// Block shared memory for one batch of 32 candidates swept by K warps
+// (DESIGN.md §5); every per-candidate array is [x][32], one column per lane:
+//   C  (K > 1 only) the decode results every warp reads: status, the fixed
+//      SetGroup bits, the axis of every position, the per-axis position
+//      bitmaps (with K = 1 they stay in registers)
+//   X  the staged sequences [16][32] (+ the rollout legal set [n_words][32]),
+//      dead after decode; then the materialisation classes' axis -> role maps
+//      [n_mc][32]; with K = 1, the sum model and no special edges, also the
+//      payload / count accumulators once H4 is done (the maps are dead then)
+//   Y  the per-color position bitmaps [n_acolors][32] (decode, H2a); then the
+//      frontier's template growth codes [n_ftmpl][32] (H4 -> H5) and
+//      signature division codes [n_fsig][32] (H2b -> H5); then, when not in
+//      X, the accumulators — one region the K warps add into atomically (<= 2
+//      axes, critical path) or one per warp
+// The epilogue stages the 256-B records through whichever of X / Y does not
+// hold the accumulators (2 KB), so they leave as coalesced rows.
+__host__ __device__ inline int smem_c_bytes(int n_axes, int K) { return K > 1 ? 32 * (8 + 8 + 4 + 8 + 4 * n_axes) : 0; }
 // one accumulator region: payload/count accumulators, plus the K > 1 partials
 __host__ __device__ inline int smem_acc_bytes(int n_axes, int K) {
   return n_axes * 4 * 32 * (8 + 4) + (K > 1 ? 32 * 5 * 8 : 0);
 }
 __host__ __device__ constexpr bool acc_shared(int n_axes, bool cp) { return n_axes <= 2 || cp; }
-__host__ __device__ inline int smem_m_bytes(int n_mc, int n_axes) { return r16(n_mc * 32 * (n_axes <= 2 ? 1 : 2)); }
-__host__ __device__ inline int smem_b_bytes(int n_ac, int n_axes, int K, bool cp, int n_mc) {
-  // <= 2 axes (and the critical-path kernels): one region the K warps add into
-  // atomically; 3-4 axes: one region per warp, combined by warp 0 (measured
-  // faster there: Llama-80 281 M vs 259 M evals/s; its critical path 9.2 M vs 8.0 M the other way).
-  // With one warp (sum model) the accumulators are first written after H4, when
-  // the class maps that follow region B are dead: they may run on over them.
-  const int acc = (acc_shared(n_axes, cp) ? 1 : K) * smem_acc_bytes(n_axes, K);
-  const int b1 = n_ac * 128, b2 = acc - (K == 1 && !cp ? smem_m_bytes(n_mc, n_axes) : 0);
-  return r16(b1 > b2 ? b1 : b2);
+__host__ __device__ inline bool acc_in_x(int K, bool cp, int n_spec) { return K == 1 && !cp && n_spec == 0; }
+constexpr int STAGE_BYTES = 2048;   // one quarter of 32 records
+__host__ __device__ inline int smem_mca_bytes(int n_mc, int n_axes) { return n_mc * 32 * (n_axes <= 2 ? 1 : 2); }
+__host__ __device__ inline int smem_x_bytes(int n_words, int n_mc, int n_axes, int K, bool cp, int n_spec) {
+  int x = 2048 + n_words * 128;
+  const int m = smem_mca_bytes(n_mc, n_axes);
+  if (m > x) x = m;
+  const int acc = smem_acc_bytes(n_axes, K);
+  if (acc_in_x(K, cp, n_spec) && acc > x) x = acc;
+  return r16(x);
 }
-__host__ __device__ inline int smem_d_bytes(int n_ftmpl) { return r16(n_ftmpl * 32); }
-// n_ftmpl / n_fsig: the templates / signatures the frontier's terms use
-__host__ __device__ inline int smem_block_bytes(int n_sigs, int n_ac, int n_words, int n_axes, int K, int n_ftmpl,
-                                                int n_mc, int n_fsig, bool cp) {
-  return smem_c_bytes(n_axes) + smem_a_bytes(n_sigs, n_words, n_axes) + smem_b_bytes(n_ac, n_axes, K, cp, n_mc) +
-         smem_m_bytes(n_mc, n_axes) + smem_d_bytes(n_ftmpl) + r16(n_fsig * 32);
+__host__ __device__ inline int smem_y_bytes(int n_ac, int n_ftmpl, int n_fsig, int n_axes, int K, bool cp, int n_spec) {
+  int y = r16(n_ftmpl * 32) + r16(n_fsig * 32);
+  if (!acc_in_x(K, cp, n_spec)) y += (acc_shared(n_axes, cp) ? 1 : K) * smem_acc_bytes(n_axes, K);
+  else if (y < STAGE_BYTES) y = STAGE_BYTES;   // the record staging
+  if (n_ac * 128 > y) y = n_ac * 128;
+  return r16(y);
+}
+__host__ __device__ inline int smem_block_bytes(const DeviceTables& T, int K) {
+  const bool cp = T.cost_model == TOAST_COST_CRITICAL_PATH;
+  return smem_c_bytes(T.n_axes, K) + smem_x_bytes(T.n_words, T.n_mc, T.n_axes, K, cp, T.n_spec) +
+         smem_y_bytes(T.n_acolors, T.n_ftmpl, T.n_fsig, T.n_axes, K, cp, T.n_spec);
 }
 
 // the block's dynamic shared memory; every access indexes this symbol so the
@@ -132,39 +136,42 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   return v;
 }
 struct Smem {               // byte offsets into g_smem
-  uint32_t sig;             // [n_sigs][32] per signature: axis->role | axis->result dim (4 bits per axis each)
-  uint32_t acol;            // [n_acolors][32] up to 4 events (valid | axis << 5 | position) per action color
-  uint32_t seq;             // [16][32] the candidates' 32 ids as 16 words
-  uint32_t legal;           // [n_words][32] rollout legal bitset
-  uint32_t f0;              // [32] SetGroups fixed to 0 (u64)
-  uint32_t on;              // [32] SetGroups fixed to 1 (u64)
-  uint32_t status;          // [32]
-  uint32_t axpos;           // [32] 2-bit axis of every sequence position (u64)
-  uint32_t axb;             // [4][32] per mesh axis: bitmap of the positions whose action uses it
+  uint32_t f0, on, status, axpos, axb;   // C (K > 1): [32] u64 SetGroups fixed to 0 / to 1, [32] status, [32] u64 2-bit axis per position, [NA][32] per-axis position bitmaps
+  uint32_t seq;             // X: [16][32] the candidates' 32 ids as 16 words (swizzled, seq_word)
+  uint32_t legal;           // X: [n_words][32] rollout legal bitset
+  uint32_t mca;             // X: [n_mc][32] per materialisation class: the axis -> role map (u8 for <= 2 axes, else u16)
+  uint32_t acol;            // Y: [n_acolors][32] per action color: bitmap of the positions holding it
+  uint32_t tb;              // Y: [n_ftmpl][32] per frontier template: divU | divD << 4 (equal: no temporary)
+  uint32_t pc;              // Y: [n_fsig][32] per frontier signature: division code of the result layout
   uint32_t acc;             // pay [NA*4][32] u64, cnt [NA*4][32] u32 (+ seg [5][32] u64 when K > 1), shared or per warp
-  uint32_t tb;              // [n_ftmpl][32] per frontier template: divU | divD << 4 (equal: no temporary)
-  uint32_t pc;              // [n_fsig][32] per frontier signature: division code of the result layout
-  uint32_t mca;             // [n_mc][32] per materialisation class: the axis -> role map (u8 for <= 2 axes, else u16)
+  uint32_t stage;           // the record-store staging (2 KB)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   Smem s;
+  const bool cp = T.cost_model == TOAST_COST_CRITICAL_PATH;
   s.f0 = 0;
   s.on = 256;
   s.status = 512;
   s.axpos = 640;
   s.axb = 896;
-  const uint32_t a = smem_c_bytes(T.n_axes);
-  s.sig = a;
-  s.seq = a;
-  s.legal = a + 2048;
-  const uint32_t b = a + smem_a_bytes(T.n_sigs, T.n_words, T.n_axes);
-  s.acol = b;
-  s.acc = b;
-  s.mca = b + smem_b_bytes(T.n_acolors, T.n_axes, K, T.cost_model == TOAST_COST_CRITICAL_PATH, T.n_mc);
-  s.tb = s.mca + smem_m_bytes(T.n_mc, T.n_axes);
-  s.pc = s.tb + smem_d_bytes(T.n_ftmpl);
+  const uint32_t x = smem_c_bytes(T.n_axes, K);
+  const uint32_t y = x + smem_x_bytes(T.n_words, T.n_mc, T.n_axes, K, cp, T.n_spec);
+  s.seq = x;
+  s.legal = x + 2048;
+  s.mca = x;
+  s.acol = y;
+  s.tb = y;
+  s.pc = y + r16(T.n_ftmpl * 32);
+  const bool inx = acc_in_x(K, cp, T.n_spec);
+  s.acc = inx ? x : s.pc + r16(T.n_fsig * 32);
+  s.stage = inx ? y : x;
   return s;
+}
+// the staged sequences: word w (ids 2w, 2w + 1) of lane L at [w][L ^ 8 (w >> 2)]
+// — the swizzle makes the coalesced row loads and stores conflict-free
+__device__ __forceinline__ uint32_t& seq_word(const Smem& S, int w, int lane) {
+  return sp<uint32_t>(S.seq)[w * 32 + (lane ^ ((w >> 2) << 3))];
 }
 
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
@@ -195,18 +202,6 @@ __device__ __forceinline__ unsigned __int128 dv128(const DeviceTables& T, unsign
   return x * (((unsigned __int128)T.inv128_hi[S] << 64) | T.inv128_lo[S]);
 }
 
-// signature entry per lane: bits [0, 4NA) axis->role, [4NA, 8NA) axis->result dim
-template <int NA> struct Ent { typedef uint32_t T; };
-template <> struct Ent<1> { typedef uint16_t T; };
-template <> struct Ent<2> { typedef uint16_t T; };
-template <int NA>
-__device__ __forceinline__ uint32_t ent_load(const Smem& S, uint32_t sig, int lane) {
-  return sp<const typename Ent<NA>::T>(S.sig)[sig * 32 + lane];
-}
-template <int NA>
-__device__ __forceinline__ void ent_store(const Smem& S, uint32_t sig, int lane, uint32_t e) {
-  sp<typename Ent<NA>::T>(S.sig)[sig * 32 + lane] = (typename Ent<NA>::T)e;
-}
 // a materialisation class's axis -> role map per lane: one byte for meshes of
 // <= 2 axes (the nibbles of absent axes read back as 0xF), else 16 bits
 template <int NA>
@@ -219,26 +214,28 @@ __device__ __forceinline__ void mca_store(const Smem& S, uint32_t c, int lane, u
   if (NA <= 2) sp<uint8_t>(S.mca)[c * 32 + lane] = (uint8_t)a2r;
   else sp<uint16_t>(S.mca)[c * 32 + lane] = (uint16_t)a2r;
 }
-// axis A's role / result dim in an entry (15 = none)
-template <int NA> __device__ __forceinline__ uint32_t e_role(uint32_t e, int A) { return (e >> (4 * A)) & 15; }
-template <int NA> __device__ __forceinline__ uint32_t e_dim(uint32_t e, int A) { return (e >> (4 * NA + 4 * A)) & 15; }
-// the 16-bit axis->role map of the state key (axes >= NA read as 0xF)
-template <int NA> __device__ __forceinline__ uint32_t e_a2r16(uint32_t e) {
-  return NA >= 4 ? (e & 0xFFFFu) : ((e & ((1u << (4 * NA)) - 1u)) | (0xFFFFu & ~((1u << (4 * NA)) - 1u)));
+// axis A's result dim under a class's axis -> role map and a signature's
+// role -> result-dim map (15 = the axis shards no result dim)
+__device__ __forceinline__ uint32_t a_dim(uint32_t a2r, uint32_t rdm, int A) {
+  const uint32_t r = (a2r >> (4 * A)) & 15;
+  return r == 15 ? 15u : (rdm >> (4 * r)) & 15;
 }
 
 // ---------------------------------------------------------------- H1 decode (C9)
 // per action color: the bitmap of sequence positions holding an action of that
 // color (S.acol[c][lane]); per lane the 2-bit axis of every position (axpos)
+// and per mesh axis the bitmap of the positions using it (axb, registers)
+template <int NA>
 __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
-                                           uint64_t& ones, uint64_t& axpos) {
+                                           uint64_t& ones, uint64_t& axpos, uint32_t (&axb)[NA]) {
   for (int c = 0; c < T.n_acolors; ++c) sp<uint32_t>(S.acol)[c * 32 + lane] = 0u;
-  for (int A = 0; A < T.n_axes; ++A) sp<uint32_t>(S.axb)[A * 32 + lane] = 0u;
+#pragma unroll
+  for (int A = 0; A < NA; ++A) axb[A] = 0u;
   uint32_t status = 0;
   bool stopped = false;
   uint64_t fx = 0, on = 0, ap = 0;
   for (int j = 0; j < 32; ++j) {
-    uint32_t id = (sp<uint32_t>(S.seq)[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+    uint32_t id = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
     if (stopped) {
       if (id) status |= TOAST_ST_NONZERO_AFTER_STOP;
       continue;
@@ -253,7 +250,8 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
     if (dup) status |= TOAST_ST_DUP_COLOR_AXIS;
     else {
       sp<uint32_t>(S.acol)[ac * 32 + lane] = pm | (1u << j);
-      sp<uint32_t>(S.axb)[ax * 32 + lane] |= 1u << j;
+#pragma unroll
+      for (int A = 0; A < NA; ++A) axb[A] |= ax == (uint32_t)A ? 1u << j : 0u;
       ap |= (uint64_t)ax << (2 * j);
     }
     uint64_t gw = __ldg(T.acol_groups + ac);
@@ -364,13 +362,6 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
   return a2r;
 }
 
-// pack the 16+16-bit (role, dim) maps into an NA-entry
-template <int NA>
-__device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
-  const uint32_t m = NA >= 4 ? 0xFFFFu : ((1u << (4 * NA)) - 1u);
-  return (full & m) | (((full >> 16) & m) << (4 * NA));
-}
-
 // ---------------------------------------------------------------- R22: critical path (NEXT-2)
 // Per candidate: finish(t) = max over operands, in operand order, of
 // (finish(def) + the edge's collective duration) + t's compute time.  Every
@@ -385,21 +376,17 @@ __device__ __forceinline__ uint32_t pack_entry(uint32_t full) {
 template <int NA, bool P2>
 __device__ __forceinline__ void cp_classes(const DeviceTables& T, const Smem& S, int K, int warp, int lane,
                                            double* __restrict__ scr) {
-  const uint32_t sh = smem_base();
-  constexpr uint32_t esz = sizeof(typename Ent<NA>::T);
-  const uint32_t ea = sh + S.sig + (uint32_t)lane * esz;
-  auto ent = [&](uint32_t sg) { return esz == 2 ? lds_u16(ea + sg * 32 * esz) : lds_u32(ea + sg * 32 * esz); };
   for (int c = warp; c < T.n_comm; c += K) {
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(T.cp_comm + c));
-    const uint32_t de = ent(w.x & 0xFFFF);
+    const uint32_t def_rdm = __ldg(&T.cp_comm[c].def_rdm);
+    const uint32_t da2r = mca_load<NA>(S, w.x & 0xFFFF, lane);
     const uint32_t a2r = mca_load<NA>(S, w.x >> 16, lane);
     const uint64_t gb = u64of(w.z, w.w);
     uint32_t dimU = 0, dimD = 0, P = 0, presD = 0;
 #pragma unroll
     for (int A = 0; A < NA; ++A) {
-      const uint32_t ru = (a2r >> (4 * A)) & 15;
-      const uint32_t du = ru == 15 ? 15u : (w.y >> (4 * ru)) & 15;
-      const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+      const uint32_t du = a_dim(a2r, w.y, A);
+      const uint32_t rd = (da2r >> (4 * A)) & 15, dd = a_dim(da2r, def_rdm, A);
       dimU |= du << (4 * A);
       dimD |= dd << (4 * A);
       P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
@@ -450,7 +437,7 @@ __device__ __forceinline__ void cp_classes(const DeviceTables& T, const Smem& S,
   if (warp == 0) scr[(size_t)(T.n_comm + T.n_comp) * 32 + lane] = 0.0;   // the "no class" duration
   for (int c = warp; c < T.n_comp; c += K) {
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(T.cp_comp + c));
-    const uint32_t a2r = e_a2r16<NA>(ent(w.x));
+    const uint32_t a2r = mca_load<NA>(S, w.x, lane);   // the op's class
     uint32_t opmask = 0;
 #pragma unroll
     for (int A = 0; A < NA; ++A) opmask |= (((a2r >> (4 * A)) & 15) != 15 ? 1u : 0u) << A;
@@ -553,90 +540,77 @@ __device__ __forceinline__ void block_sync(int K) {
 }
 
 // ---------------------------------------------------------------- one batch of 32 candidates
-// The K warps of the block share the batch: warp 0 decodes, all warps
-// materialise a share of the signatures, warp w sweeps op segment w (its own
-// payload accumulators and relative liveness), and warp 0 combines the
-// segments (peak = max_w (L before segment w + segment w's relative peak)),
-// scores and writes the records.  S.seq holds the candidates on entry.
+// The K warps of the block share the batch: warp 0 decodes, the warps
+// materialise a share of the classes (H2a), the frontier signatures' codes
+// (H2b), the edge templates (H4) and the frontier groups (H5) each, and warp
+// 0 combines their sums and peaks, scores and writes the records (rows
+// [row0, row0 + rows) of the output).  S.seq holds the candidates on entry.
 template <int NA, bool P2, bool CP>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
-                                           void* __restrict__ out, int64_t idx, bool compact) {
+                                           void* __restrict__ out, int64_t row0, int rows, bool compact) {
   block_sync(K);
-  if (warp == 0) {
-    uint64_t f0, on, ap;
-    sp<uint32_t>(S.status)[lane] = decode(T, S, lane, f0, on, ap);
-    sp<unsigned long long>(S.f0)[lane] = f0;
-    sp<unsigned long long>(S.on)[lane] = on;
-    sp<unsigned long long>(S.axpos)[lane] = ap;
-  }
-  block_sync(K);
-  // H2: materialise this warp's share of the signatures; per signature the
-  // state-key terms (H7, R14) and the local FLOPs (H3) of all its ops at once
-  uint64_t key = 0, flo = 0, fhi = 0;
-  {
-    const uint64_t f0 = sp<unsigned long long>(S.f0)[lane], on = sp<unsigned long long>(S.on)[lane];
-    const uint64_t ap = sp<unsigned long long>(S.axpos)[lane];
-    uint32_t axb[NA];
+  uint64_t f0 = 0, on = 0, ap = 0;
+  uint32_t axb[NA], status = 0;
+  if (warp == 0) status = decode<NA>(T, S, lane, f0, on, ap, axb);
+  if (K > 1) {   // the decode results every warp reads (one warp: they stay in registers)
+    if (warp == 0) {
+      sp<uint32_t>(S.status)[lane] = status;
+      sp<unsigned long long>(S.f0)[lane] = f0;
+      sp<unsigned long long>(S.on)[lane] = on;
+      sp<unsigned long long>(S.axpos)[lane] = ap;
+#pragma unroll
+      for (int A = 0; A < NA; ++A) sp<uint32_t>(S.axb)[A * 32 + lane] = axb[A];
+    }
+    __syncthreads();
+    f0 = sp<unsigned long long>(S.f0)[lane];
+    on = sp<unsigned long long>(S.on)[lane];
+    ap = sp<unsigned long long>(S.axpos)[lane];
 #pragma unroll
     for (int A = 0; A < NA; ++A) axb[A] = sp<uint32_t>(S.axb)[A * 32 + lane];
-    // H2a: one materialisation per class (signatures that differ only in
-    // their result dims share it): the axis -> role map
-    for (int c = warp; c < T.n_mc; c += K) {
-      const uint64_t glo = __ldg(T.mc_flops + 2 * c), ghi = __ldg(T.mc_flops + 2 * c + 1);
-      const uint32_t a2r = materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
-      mca_store<NA>(S, c, lane, a2r);
-      // the class's state-key terms (H7, R14; every axis's load issued at once,
-      // role 15 reads a valid word and is masked out) and local FLOPs (H3)
-      uint64_t kt[NA];
+  } else {
+    __syncwarp();   // the class maps below overwrite other lanes' staged sequences
+  }
+  // H2a: one materialisation per class (signatures that differ only in their
+  // result dims share it): the axis -> role map; per class the state-key
+  // terms (H7, R14) and the local FLOPs (H3) of all its ops at once
+  uint64_t key = 0, flo = 0, fhi = 0;
+  for (int c = warp; c < T.n_mc; c += K) {
+    const uint64_t glo = __ldg(T.mc_flops + 2 * c), ghi = __ldg(T.mc_flops + 2 * c + 1);
+    const uint32_t a2r = materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
+    mca_store<NA>(S, c, lane, a2r);
+    // the class's state-key terms (every axis's load issued at once, role 15
+    // reads a valid word and is masked out) and local FLOPs
+    uint64_t kt[NA];
 #pragma unroll
-      for (int A = 0; A < NA; ++A) kt[A] = __ldg(T.mc_key + (size_t)c * 32 + A * 8 + ((a2r >> (4 * A)) & 7));
-      uint32_t opmask = 0;
+    for (int A = 0; A < NA; ++A) kt[A] = __ldg(T.mc_key + (size_t)c * 32 + A * 8 + ((a2r >> (4 * A)) & 7));
+    uint32_t opmask = 0;
 #pragma unroll
-      for (int A = 0; A < NA; ++A) {
-        const bool on_ = ((a2r >> (4 * A)) & 15) != 15;
-        key += on_ ? kt[A] : 0ULL;
-        opmask |= (on_ ? 1u : 0u) << A;
-      }
-      if (glo | ghi) {
-        const unsigned __int128 f = dv128<P2>(T, ((unsigned __int128)ghi << 64) | glo, opmask);
-        const uint64_t l = (uint64_t)f;
-        flo += l;
-        fhi += (uint64_t)(f >> 64) + ((flo < l) ? 1 : 0);
-      }
+    for (int A = 0; A < NA; ++A) {
+      const bool on_ = ((a2r >> (4 * A)) & 15) != 15;
+      key += on_ ? kt[A] : 0ULL;
+      opmask |= (on_ ? 1u : 0u) << A;
+    }
+    if (glo | ghi) {
+      const unsigned __int128 f = dv128<P2>(T, ((unsigned __int128)ghi << 64) | glo, opmask);
+      const uint64_t l = (uint64_t)f;
+      flo += l;
+      fhi += (uint64_t)(f >> 64) + ((flo < l) ? 1 : 0);
     }
   }
   block_sync(K);
-  {
-    // H2b: per signature the entry (axis -> role | axis -> result dim) and,
-    // for the frontier's signatures, the result layout's division code
-    // (the next signature's table word is loaded one iteration ahead)
-    uint64_t nmr = warp < T.n_sigs ? __ldg(T.sig_mr + warp) : 0;
-    for (int s = warp; s < T.n_sigs; s += K) {
-      const uint64_t mr = nmr;
-      if (s + K < T.n_sigs) nmr = __ldg(T.sig_mr + s + K);
-      const uint32_t a2r = mca_load<NA>(S, (uint32_t)(mr & 0xFFFF), lane);
-      const uint32_t rdm = (uint32_t)(mr >> 32);   // (bits 16-31 of the low word: the frontier slot)
-      uint32_t dims = 0;
+  // H2b: per frontier signature the division code of its result layout
+  for (int f = warp; f < T.n_fsig; f += K) {
+    const uint64_t w = __ldg(T.fsig + f);
+    const uint32_t a2r = mca_load<NA>(S, (uint32_t)(w & 0xFFFF), lane), rdm = (uint32_t)(w >> 32);
+    uint32_t present = 0;
 #pragma unroll
-      for (int A = 0; A < 4; ++A) {
-        const uint32_t r = (a2r >> (4 * A)) & 15;
-        dims |= (r == 15 ? 15u : (rdm >> (4 * r)) & 15) << (4 * A);
-      }
-      const uint32_t e = pack_entry<NA>(a2r | (dims << 16));
-      ent_store<NA>(S, s, lane, e);
-      const uint32_t fslot = (uint32_t)(mr >> 16) & 0xFFFF;
-      if (fslot != 0xFFFF) {
-        uint32_t present = 0;
-#pragma unroll
-        for (int A = 0; A < NA; ++A) present |= (e_dim<NA>(e, A) != 15 ? 1u : 0u) << A;
-        sp<uint8_t>(S.pc)[fslot * 32 + lane] = (uint8_t)dcode<P2>(T, present);
-      }
-    }
-    if (acc_shared(NA, CP) && K > 1) {   // the shared accumulators (region B held the event lists until H2a ended)
-      uint32_t* z = sp<uint32_t>(S.acc);
-      const int words = smem_acc_bytes(NA, K) / 4;
-      for (int i = warp * 32 + lane; i < words; i += K * 32) z[i] = 0u;
-    }
+    for (int A = 0; A < NA; ++A) present |= (a_dim(a2r, rdm, A) != 15 ? 1u : 0u) << A;
+    sp<uint8_t>(S.pc)[f * 32 + lane] = (uint8_t)dcode<P2>(T, present);
+  }
+  if (acc_shared(NA, CP) && K > 1) {   // the shared accumulators (region Y held the event lists until H2a ended)
+    uint32_t* z = sp<uint32_t>(S.acc);
+    const int words = smem_acc_bytes(NA, K) / 4;
+    for (int i = warp * 32 + lane; i < words; i += K * 32) z[i] = 0u;
   }
   block_sync(K);
   const uint32_t acc = S.acc + (acc_shared(NA, CP) ? 0u : (uint32_t)warp * smem_acc_bytes(NA, K));
@@ -646,35 +620,33 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
 
   // H4 per edge template: every use edge of the template communicates the
   // same way, so its payloads are costed once from the template's summed
-  // bytes; the sweep only needs each edge's temporary (presU/presD)
-  // (payloads and counts accumulate in registers, then land in this warp's slots)
+  // bytes; the def layout comes from the def signature's class and result-dim
+  // map, the use layout from the use class and the edge's role -> dim map
+  // (payloads and counts accumulate in registers, then land in the slots)
   unsigned long long rp[NA * 4];
   uint32_t rc[NA * 4];
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { rp[q] = 0ULL; rc[q] = 0u; }
   // the next template's record is loaded one iteration ahead
-  uint2 n0 = make_uint2(0, 0), n1 = n0, n2 = n0;
+  uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
   if (warp < T.n_tmpl) {
-    n0 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + warp));
-    n1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + warp) + 1);
-    n2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + warp) + 2);
+    n0 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + warp));
+    n1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + warp) + 1);
   }
   for (int tix = warp; tix < T.n_tmpl; tix += K) {
-    const uint2 t0 = n0, t1 = n1, t2 = n2;
+    const uint4 t0 = n0, t1 = n1;
     if (tix + K < T.n_tmpl) {
-      n0 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K));
-      n1 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K) + 1);
-      n2 = __ldg(reinterpret_cast<const uint2*>(T.tmpl + tix + K) + 2);
+      n0 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix + K));
+      n1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix + K) + 1);
     }
-    const uint32_t de = ent_load<NA>(S, t0.x & 0xFFFF, lane);
-    const uint32_t ue = mca_load<NA>(S, t0.x >> 16, lane);   // the use class's axis -> role map
-    const uint32_t use_dimof = t0.y;
+    const uint32_t da2r = mca_load<NA>(S, t0.x & 0xFFFF, lane);   // the def signature's class
+    const uint32_t ue = mca_load<NA>(S, t0.x >> 16, lane);        // the use class
+    const uint32_t use_dimof = t0.y, def_rdm = t1.z;
     uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
     for (int A = 0; A < NA; ++A) {
-      const uint32_t ru = e_role<NA>(ue, A);
-      const uint32_t du = ru == 15 ? 15u : (use_dimof >> (4 * ru)) & 15;
-      const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+      const uint32_t du = a_dim(ue, use_dimof, A);
+      const uint32_t rd = (da2r >> (4 * A)) & 15, dd = a_dim(da2r, def_rdm, A);
       dimD |= dd << (4 * A);
       dimU |= du << (4 * A);
       P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
@@ -683,8 +655,8 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     }
     uint8_t tbv = 0;
     if (dimD != dimU || P) {
-      const uint64_t sgb = u64of(t1.x, t1.y);
-      const uint32_t ne = t2.x;
+      const uint64_t sgb = u64of(t0.z, t0.w);
+      const uint32_t ne = t1.x;
       uint64_t size = dv<P2>(T, sgb, dcode<P2>(T, presD));
 #pragma unroll
       for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather (reading R20)
@@ -715,8 +687,10 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       }
       tbv = (uint8_t)(dcode<P2>(T, presU) | (dcode<P2>(T, presD) << 4));
     }
-    if (t2.y != 0xFFFFFFFFu) sp<uint8_t>(S.tb)[t2.y * 32 + lane] = tbv;
+    if (t1.y != 0xFFFFFFFFu) sp<uint8_t>(S.tb)[t1.y * 32 + lane] = tbv;
   }
+  // (with K = 1 the slots may overlay the class maps: every lane's last read first)
+  if (K == 1) __syncwarp();
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) {
     if (K == 1 || !acc_shared(NA, CP)) {
@@ -732,7 +706,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   // H5 (C12, reading R19): peak = max over the kept ops of the peak-memory
   // frontier of M_t = constant + sum_s Live_t[s] / d_s + sum_tm growth_tm(Tmp_t[tm])
   // (+ the special edges of ops that use one value twice); this warp takes
-  // every K-th point
+  // every K-th group of points
   const uint32_t sh = smem_base();
   const uint32_t pc_base = sh + S.pc + lane, tb_base = sh + S.tb + lane;
   unsigned long long peak = 0;
@@ -766,26 +740,23 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     }
     if (n_spec) {
       // a value used more than once by this op: costed per edge, once per distinct layout
-      const uint32_t sig = pw.w >> 16;
-      const KUse* ue = T.spec + pw.z;
-      const uint32_t esz = sizeof(typename Ent<NA>::T);
-      const uint32_t ea = sh + S.sig + (uint32_t)lane * esz;
-      const uint32_t a2r = e_a2r16<NA>(esz == 2 ? lds_u16(ea + sig * 32 * esz) : lds_u32(ea + sig * 32 * esz));
+      const uint32_t a2r = mca_load<NA>(S, pw.w >> 16, lane);   // the op's class
+      const KUseDev* ue = T.spec + pw.z;
       long long temp = 0, gmax = 0;
       uint32_t gq = 0;
 #pragma unroll 1
       for (uint32_t q = 0; q < n_spec; ++q) {
         const uint4 u = __ldg(reinterpret_cast<const uint4*>(ue + q));
+        const uint32_t def_rdm = __ldg(&ue[q].def_rdm);
         const uint64_t gb = u64of(u.z, u.w & 0x00FFFFFFu);
         const uint32_t uflags = u.w >> 24;
         if (uflags & 1) { gmax = 0; gq = q; }
-        const uint32_t de = esz == 2 ? lds_u16(ea + (u.x & 0xFFFF) * 32 * esz) : lds_u32(ea + (u.x & 0xFFFF) * 32 * esz);
+        const uint32_t da2r = mca_load<NA>(S, u.x & 0xFFFF, lane);
         uint32_t dimU = 0, dimD = 0, P = 0, presD = 0, presU = 0;
 #pragma unroll
         for (int A = 0; A < NA; ++A) {
-          const uint32_t ru = (a2r >> (4 * A)) & 15;
-          const uint32_t du = ru == 15 ? 15u : (u.y >> (4 * ru)) & 15;
-          const uint32_t dd = e_dim<NA>(de, A), rd = e_role<NA>(de, A);
+          const uint32_t du = a_dim(a2r, u.y, A);
+          const uint32_t rd = (da2r >> (4 * A)) & 15, dd = a_dim(da2r, def_rdm, A);
           dimU |= du << (4 * A);
           dimD |= dd << (4 * A);
           P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
@@ -798,10 +769,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
             const uint32_t ud2 = __ldg(&ue[q2].use_dimof);
             uint32_t dimU2 = 0;
 #pragma unroll
-            for (int A = 0; A < NA; ++A) {
-              const uint32_t ru = (a2r >> (4 * A)) & 15;
-              dimU2 |= (ru == 15 ? 15u : (ud2 >> (4 * ru)) & 15) << (4 * A);
-            }
+            for (int A = 0; A < NA; ++A) dimU2 |= a_dim(a2r, ud2, A) << (4 * A);
             dup |= dimU2 == dimU;
           }
           if (!dup) {
@@ -886,7 +854,6 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         }
       }
     }
-    const uint32_t status = sp<uint32_t>(S.status)[lane];
     // H6 score (C13): fixed order, explicit round-to-nearest, no FMA
     double tt = __ddiv_rn(__dadd_rn(__dmul_rn(__ull2double_rn(fhi), 18446744073709551616.0), __ull2double_rn(flo)), T.F);
     unsigned long long ncoll = 0;
@@ -909,29 +876,38 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     const uint64_t pk = pk_all;
     const double RT = __ddiv_rn(tt, T.t0);
     const double MP = pk > T.DM ? __ddiv_rn(__dmul_rn(T.C, __ull2double_rn(pk - T.DM)), __ull2double_rn(T.peak0)) : 0.0;
-    if (valid && compact) {
-      // toast_score (include/toast.h): score | state key, or NaN | status
-      const bool ok = status == 0;
+    const bool ok = status == 0;
+    if (compact) {
+      // toast_score (include/toast.h): score | state key, or NaN | status (16 B per lane: already coalesced)
       const unsigned long long w0 = ok ? (unsigned long long)__double_as_longlong(__dadd_rn(RT, MP)) : 0x7FF8000000000000ULL;
       const unsigned long long w1 = ok ? key : (unsigned long long)status;
-      reinterpret_cast<uint4*>(out)[idx] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
-    } else if (valid) {
-      // record layout = toast_cost (include/toast.h), written as 16 x 16 B
-      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<toast_cost*>(out) + idx);
-      const bool ok = status == 0;
+      if (valid)
+        reinterpret_cast<uint4*>(out)[row0 + lane] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+    } else {
+      // record layout = toast_cost (include/toast.h), 16 x 16 B, staged through
+      // shared memory a quarter at a time (4 x 16 B of each of the 32 records)
+      // and written as whole 64-B row segments (every sector fully used)
+      uint4* stage = sp<uint4>(S.stage);
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<toast_cost*>(out) + row0);
+      const uint32_t sw = (lane >> 1) & 3;   // the slot swizzle: conflict-free 16-B accesses
+      auto put = [&](int slot, uint4 v) { stage[lane * 4 + ((slot & 3) ^ sw)] = v; };
+      auto flush = [&](int quarter) {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int u = i * 32 + lane, L = u >> 2, sl = u & 3;
+          if (L < rows) dst[(size_t)L * 16 + quarter * 4 + sl] = stage[L * 4 + (sl ^ ((L >> 1) & 3))];
+        }
+        __syncwarp();
+      };
       auto d2 = [](double x) { return (unsigned long long)__double_as_longlong(x); };
+      auto u4 = [](unsigned long long a, unsigned long long b) {
+        return make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+      };
       const unsigned long long w0 = ok ? d2(tt) : 0ULL, w1 = ok ? d2(__dadd_rn(RT, MP)) : 0ULL;
       const unsigned long long w2 = ok ? pk : 0ULL, w3 = ok ? flo : 0ULL, w4 = ok ? key : 0ULL;
       const unsigned long long w5 = ok ? ((unsigned long long)(uint32_t)ncoll << 32) : (unsigned long long)status;
-      dst[0] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
-      dst[1] = make_uint4((uint32_t)w2, (uint32_t)(w2 >> 32), (uint32_t)w3, (uint32_t)(w3 >> 32));
-      dst[2] = make_uint4((uint32_t)w4, (uint32_t)(w4 >> 32), (uint32_t)w5, (uint32_t)(w5 >> 32));
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        unsigned long long a = 0ULL, b = 0ULL;
-        if (ok && 2 * k < NA * 4) { a = pay[(2 * k) * 32 + lane]; b = pay[(2 * k + 1) * 32 + lane]; }
-        dst[3 + k] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
-      }
+      auto payq = [&](int q) { return (ok && q < NA * 4) ? (unsigned long long)pay[q * 32 + lane] : 0ULL; };
       uint32_t cw[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -943,17 +919,46 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         }
         cw[k] = ok ? (lo | (hi << 16)) : 0u;
       }
-      dst[11] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-      dst[12] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
-      dst[13] = ok ? make_uint4((uint32_t)fhi, (uint32_t)(fhi >> 32), 0, 0) : make_uint4(0, 0, 0, 0);
-      dst[14] = make_uint4(0, 0, 0, 0);
-      dst[15] = make_uint4(0, 0, 0, 0);
+      put(0, u4(w0, w1));
+      put(1, u4(w2, w3));
+      put(2, u4(w4, w5));
+      put(3, u4(payq(0), payq(1)));
+      flush(0);
+#pragma unroll
+      for (int k = 4; k < 8; ++k) put(k, u4(payq(2 * k - 6), payq(2 * k - 5)));
+      flush(1);
+#pragma unroll
+      for (int k = 8; k < 11; ++k) put(k, u4(payq(2 * k - 6), payq(2 * k - 5)));
+      put(11, make_uint4(cw[0], cw[1], cw[2], cw[3]));
+      flush(2);
+      put(12, make_uint4(cw[4], cw[5], cw[6], cw[7]));
+      put(13, ok ? make_uint4((uint32_t)fhi, (uint32_t)(fhi >> 32), 0, 0) : make_uint4(0, 0, 0, 0));
+      put(14, make_uint4(0, 0, 0, 0));
+      put(15, make_uint4(0, 0, 0, 0));
+      flush(3);
     }
   }
   block_sync(K);
 }
 
-__device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restrict__ g, int lane, bool valid) {
+// the batch's rows [row0, row0 + rows) of a contiguous uint16[n][32] array as
+// coalesced 16-B row loads (uint4 u = 4 r + q holds words 4q..4q+3 of row r),
+// zeros past the end
+__device__ __forceinline__ void load_seq_rows(const Smem& S, const uint16_t* __restrict__ g, int rows, int lane) {
+  const uint4* src = reinterpret_cast<const uint4*>(g);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int u = k * 32 + lane, r = u >> 2, q = u & 3;
+    const uint4 w = r < rows ? __ldg(src + u) : make_uint4(0, 0, 0, 0);
+    seq_word(S, 4 * q + 0, r) = w.x;
+    seq_word(S, 4 * q + 1, r) = w.y;
+    seq_word(S, 4 * q + 2, r) = w.z;
+    seq_word(S, 4 * q + 3, r) = w.w;
+  }
+  __syncwarp();
+}
+// one row per lane (rollouts of a search round: rows repeat a leaf's prefix)
+__device__ __forceinline__ void load_seq_lane(const Smem& S, const uint16_t* __restrict__ g, int lane, bool valid) {
   uint4 w[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
   if (valid) {
     const uint4* src = reinterpret_cast<const uint4*>(g);
@@ -962,10 +967,21 @@ __device__ __forceinline__ void load_seq(const Smem& S, const uint16_t* __restri
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    sp<uint32_t>(S.seq)[(4 * k + 0) * 32 + lane] = w[k].x;
-    sp<uint32_t>(S.seq)[(4 * k + 1) * 32 + lane] = w[k].y;
-    sp<uint32_t>(S.seq)[(4 * k + 2) * 32 + lane] = w[k].z;
-    sp<uint32_t>(S.seq)[(4 * k + 3) * 32 + lane] = w[k].w;
+    seq_word(S, 4 * k + 0, lane) = w[k].x;
+    seq_word(S, 4 * k + 1, lane) = w[k].y;
+    seq_word(S, 4 * k + 2, lane) = w[k].z;
+    seq_word(S, 4 * k + 3, lane) = w[k].w;
+  }
+}
+// the batch's sequences out as coalesced 16-B row stores
+__device__ __forceinline__ void store_seq_rows(const Smem& S, uint16_t* __restrict__ g, int rows, int lane) {
+  __syncwarp();
+  uint4* dst = reinterpret_cast<uint4*>(g);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int u = k * 32 + lane, r = u >> 2, q = u & 3;
+    if (r < rows)
+      dst[u] = make_uint4(seq_word(S, 4 * q, r), seq_word(S, 4 * q + 1, r), seq_word(S, 4 * q + 2, r), seq_word(S, 4 * q + 3, r));
   }
 }
 
@@ -976,10 +992,10 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
   const Smem S = block_smem(T, K);
   const int64_t nbatch = (n + 31) / 32;
   for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
-    const int64_t i = b * 32 + lane;
-    const bool valid = i < n;
-    if (warp == 0) load_seq(S, seqs + i * 32, lane, valid);
-    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, i, compact);
+    const int64_t row0 = b * 32;
+    const int rows = (int)(n - row0 < 32 ? n - row0 : 32);
+    if (warp == 0) load_seq_rows(S, seqs + row0 * 32, rows, lane);
+    batch_eval<NA, P2, CP>(T, S, K, warp, lane, lane < rows, out, row0, rows, compact);
   }
 }
 
@@ -1009,15 +1025,17 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
   const uint32_t seed_lo = (uint32_t)seed, seed_hi = (uint32_t)(seed >> 32);
   const int nw = T.n_words;
   for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
-    const int64_t i = b * 32 + lane;
+    const int64_t row0 = b * 32, i = row0 + lane;
+    const int rows = (int)(n - row0 < 32 ? n - row0 : 32);
     const bool valid = i < n;
     if (warp == 0) {
-    load_seq(S, pre + (i / rep) * 32, lane, valid);
+    if (rep == 1) load_seq_rows(S, pre + row0 * 32, rows, lane);
+    else load_seq_lane(S, pre + (i / rep) * 32, lane, valid);
     // validate the prefix: ids < n_actions before the first 0, zeros after it
     int stop = 32;
     bool bad = false;
     for (int j = 0; j < 32; ++j) {
-      const uint32_t id = (sp<uint32_t>(S.seq)[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+      const uint32_t id = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
       if (stop < 32) { bad |= id != 0; continue; }
       if (id == 0) { stop = j; continue; }
       bad |= (int)id >= T.n_actions;
@@ -1031,7 +1049,7 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
         sp<uint32_t>(S.legal)[w * 32 + lane] = v;
       }
       for (int j = 0; j < stop; ++j) {
-        const uint32_t a = (sp<uint32_t>(S.seq)[(j >> 1) * 32 + lane] >> ((j & 1) * 16)) & 0xFFFFu;
+        const uint32_t a = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
         for (int w = 0; w < nw; ++w) sp<uint32_t>(S.legal)[w * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w);
       }
       const uint64_t id = id_base + (uint64_t)i;
@@ -1060,20 +1078,13 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
         c = word & 1u;              if (k >= c) { pos += 1; }
         const uint32_t a = (uint32_t)w * 32 + pos;
         for (int w2 = 0; w2 < nw; ++w2) sp<uint32_t>(S.legal)[w2 * 32 + lane] &= ~__ldg(T.kill + (size_t)a * nw + w2);
-        uint32_t& sw = sp<uint32_t>(S.seq)[(d >> 1) * 32 + lane];
+        uint32_t& sw = seq_word(S, d >> 1, lane);
         sw = (d & 1) ? ((sw & 0xFFFFu) | (a << 16)) : ((sw & 0xFFFF0000u) | a);
       }
     }
-    __syncwarp();
-    if (valid) {
-      uint4* dst = reinterpret_cast<uint4*>(out_seqs + i * 32);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        dst[k] = make_uint4(sp<uint32_t>(S.seq)[(4 * k) * 32 + lane], sp<uint32_t>(S.seq)[(4 * k + 1) * 32 + lane], sp<uint32_t>(S.seq)[(4 * k + 2) * 32 + lane],
-                            sp<uint32_t>(S.seq)[(4 * k + 3) * 32 + lane]);
-    }
+    store_seq_rows(S, out_seqs + row0 * 32, rows, lane);
     }   // warp 0
-    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, i, compact);
+    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, row0, rows, compact);
   }
 }
 
@@ -1178,22 +1189,44 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   toast_status st;
   const void* p;
   // tail: the last window chunk may read W + E words past the end
-  if ((st = upload(a, a->h_points, &p, err))) return st;
+  // device images: signature references resolved to (class, result-dim map)
+  auto sig_mc = [&](uint32_t sig) { return (uint32_t)(a->h_sig_mr[sig] & 0xFFFF); };
+  auto sig_rdm = [&](uint32_t sig) { return (uint32_t)(a->h_sig_mr[sig] >> 32); };
+  std::vector<KPoint> pts = a->h_points;
+  for (KPoint& kp : pts) kp.use_sig = (uint16_t)sig_mc(kp.use_sig);
+  if ((st = upload(a, pts, &p, err))) return st;
   T.points = reinterpret_cast<const KPoint*>(p);
   if ((st = upload(a, a->h_terms, &p, err))) return st;
   T.terms = reinterpret_cast<const uint64_t*>(p);
-  if ((st = upload(a, a->h_spec, &p, err))) return st;
-  T.spec = reinterpret_cast<const KUse*>(p);
+  std::vector<KUseDev> spec(a->h_spec.size());
+  for (size_t q = 0; q < spec.size(); ++q) {
+    const KUse& u = a->h_spec[q];
+    spec[q] = KUseDev{sig_mc(u.def_sig), u.use_dimof, u.gb_flags, sig_rdm(u.def_sig), {0, 0, 0}};
+  }
+  if ((st = upload(a, spec, &p, err))) return st;
+  T.spec = reinterpret_cast<const KUseDev*>(p);
+  T.n_spec = (int32_t)spec.size();
   if ((st = upload(a, a->h_sigs, &p, err))) return st;
   T.sigs = reinterpret_cast<const KSig*>(p);
-  if ((st = upload(a, a->h_sig_mr, &p, err))) return st;
-  T.sig_mr = reinterpret_cast<const uint64_t*>(p);
+  std::vector<uint64_t> fsig((size_t)std::max(T.n_fsig, 0), 0);
+  for (size_t q = 0; q < a->h_sig_mr.size(); ++q) {
+    const uint32_t slot = (uint32_t)(a->h_sig_mr[q] >> 16) & 0xFFFF;
+    if (slot != 0xFFFF && slot < fsig.size()) fsig[slot] = (uint64_t)sig_mc((uint32_t)q) | ((uint64_t)sig_rdm((uint32_t)q) << 32);
+  }
+  if ((st = upload(a, fsig, &p, err))) return st;
+  T.fsig = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_mc_key, &p, err))) return st;
   T.mc_key = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_mc_flops, &p, err))) return st;
   T.mc_flops = reinterpret_cast<const uint64_t*>(p);
-  if ((st = upload(a, a->h_tmpl, &p, err))) return st;
-  T.tmpl = reinterpret_cast<const KTmpl*>(p);
+  std::vector<KTmplDev> tm(a->h_tmpl.size());
+  for (size_t q = 0; q < tm.size(); ++q) {
+    const KTmpl& t = a->h_tmpl[q];
+    tm[q] = KTmplDev{sig_mc(t.def_sig) | ((uint32_t)t.use_sig << 16), t.use_dimof, t.sum_gbytes, t.n_edges, t.fslot,
+                     sig_rdm(t.def_sig), 0};
+  }
+  if ((st = upload(a, tm, &p, err))) return st;
+  T.tmpl = reinterpret_cast<const KTmplDev*>(p);
   if ((st = upload(a, a->h_desel_cls, &p, err))) return st;
   T.desel = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_actions, &p, err))) return st;
@@ -1206,7 +1239,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, 1, T.n_ftmpl, T.n_mc, T.n_fsig, T.cost_model == TOAST_COST_CRITICAL_PATH) > dev_smem) {
+  if (smem_block_bytes(T, 1) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -1215,7 +1248,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T.n_sigs, T.n_acolors, T.n_words, T.n_axes, K, T.n_ftmpl, T.n_mc, T.n_fsig, T.cost_model == TOAST_COST_CRITICAL_PATH);
+    const int sm = smem_block_bytes(T, K);
     int be = 0, br = 0;
     const int max_threads = T.cost_model == TOAST_COST_CRITICAL_PATH ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS;
     if (sm <= dev_smem && 32 * K <= max_threads) {
@@ -1247,9 +1280,16 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     if ((st = upload(a, a->h_cp_bsize, &p, err))) return st;
     T.cp_bsize = reinterpret_cast<const uint32_t*>(p);
     T.n_bundles = (int32_t)a->h_cp_bsize.size();
-    if ((st = upload(a, a->h_cp_comm, &p, err))) return st;
-    T.cp_comm = reinterpret_cast<const KCpComm*>(p);
-    if ((st = upload(a, a->h_cp_comp, &p, err))) return st;
+    std::vector<KCpCommDev> cm(a->h_cp_comm.size());
+    for (size_t q = 0; q < cm.size(); ++q) {
+      const KCpComm& c = a->h_cp_comm[q];
+      cm[q] = KCpCommDev{sig_mc(c.def_sig) | ((uint32_t)c.use_mc << 16), c.use_dimof, c.gb, sig_rdm(c.def_sig), {0, 0, 0}};
+    }
+    if ((st = upload(a, cm, &p, err))) return st;
+    T.cp_comm = reinterpret_cast<const KCpCommDev*>(p);
+    std::vector<KCpComp> cc = a->h_cp_comp;
+    for (KCpComp& c : cc) c.sig = sig_mc(c.sig);   // the op's class
+    if ((st = upload(a, cc, &p, err))) return st;
     T.cp_comp = reinterpret_cast<const KCpComp*>(p);
     // Finish-slot scratch is allocated per launch, stream-ordered, from this
     // analysis' own pool (kept, not released): concurrent calls on different
@@ -1323,7 +1363,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig, a->dt.cost_model == TOAST_COST_CRITICAL_PATH);
+  const size_t sm = (size_t)smem_block_bytes(a->dt, K);
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
@@ -1343,7 +1383,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt.n_sigs, a->dt.n_acolors, a->dt.n_words, a->dt.n_axes, K, a->dt.n_ftmpl, a->dt.n_mc, a->dt.n_fsig, a->dt.cost_model == TOAST_COST_CRITICAL_PATH);
+  const size_t sm = (size_t)smem_block_bytes(a->dt, K);
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));

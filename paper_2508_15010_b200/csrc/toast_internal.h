@@ -169,6 +169,35 @@ constexpr int CP_EMAX = 8;
 constexpr int PIPE_STREAMS = 8;   // host-buffer pipeline streams (at most)
 constexpr int CP_WINDOW = 96;
 static_assert(sizeof(KCpComm) == 16 && sizeof(KCpComp) == 16, "cp records");
+// Device images of the records above (built by upload_tables): every
+// signature reference a kernel resolves per candidate is replaced by the
+// signature's materialisation class (whose axis -> role map the kernels keep
+// per lane) and its role -> result-dim map, so no per-signature entry table
+// is needed on chip.
+struct KTmplDev {        // 32 B (2 x 16-B loads)
+  uint32_t mcs;          // def class | use class << 16
+  uint32_t use_dimof;
+  uint64_t sum_gbytes;
+  uint32_t n_edges;
+  uint32_t fslot;
+  uint32_t def_rdm;      // nibble r: result dim of the def signature's role r (0xF: none)
+  uint32_t pad;
+};
+struct KUseDev {         // 32 B
+  uint32_t def_mc;
+  uint32_t use_dimof;
+  uint64_t gb_flags;
+  uint32_t def_rdm;
+  uint32_t pad[3];
+};
+struct KCpCommDev {      // 32 B
+  uint32_t mcs;          // def class | use class << 16
+  uint32_t use_dimof;
+  uint64_t gb;
+  uint32_t def_rdm;
+  uint32_t pad[3];
+};
+static_assert(sizeof(KTmplDev) == 32 && sizeof(KUseDev) == 32 && sizeof(KCpCommDev) == 32, "device records");
 static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 && sizeof(KTmpl) == 24, "records");
 
 
@@ -184,14 +213,14 @@ struct LeafRed {
 
 // signature role word: acolor [0,10) | div_ok [10,26) | deselection class [26,34)
 struct DeviceTables {
-  const KPoint* points = nullptr;        // [n_points] peak-memory frontier (R19)
+  const KPoint* points = nullptr;        // [n_points] peak-memory frontier (R19); use_sig holds the op's class
   const uint64_t* terms = nullptr;       // per point: constant, then value | feature << 48
-  const KUse* spec = nullptr;            // special edges of the points
+  const KUseDev* spec = nullptr;         // special edges of the points
   const KSig* sigs = nullptr;            // [n_mc] per materialisation class
-  const uint64_t* sig_mr = nullptr;      // [n_sigs] class | frontier slot << 16 (0xFFFF: none) | result dims << 32
+  const uint64_t* fsig = nullptr;        // [n_fsig] per frontier signature slot: class | result dims << 32
   const uint64_t* mc_key = nullptr;      // [n_mc][4 axes][8 roles] summed state-key terms (R14)
   const uint64_t* mc_flops = nullptr;    // [n_mc][2] summed global FLOPs of matmul-class ops (lo, hi)
-  const KTmpl* tmpl = nullptr;           // [n_tmpl]
+  const KTmplDev* tmpl = nullptr;        // [n_tmpl]
   const uint64_t* desel = nullptr;       // [class][2] = need0, need1 (class 0 = none)
   const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
   const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids (0xFF = unused)
@@ -201,13 +230,14 @@ struct DeviceTables {
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
   int32_t n_points, n_mc;
   int32_t n_fsig, n_ftmpl;  // signatures / templates the frontier terms use (their per-lane code tables)
+  int32_t n_spec = 0;       // special edges (a value used twice by one op) of the frontier points
   int32_t cost_model, n_slots;   // R22: critical path; finish-time slots per candidate
   int32_t n_comm, n_comp;        // R22: edge-duration and compute-time classes
   const uint2* cp = nullptr;     // critical-path stream
   const uint32_t* cp_bsize = nullptr;  // per bundle: edges | prefetch slot << 4 | prefetch slot << 18 (0x3FFF: none)
   int32_t n_bundles = 0;
-  const KCpComm* cp_comm = nullptr;
-  const KCpComp* cp_comp = nullptr;
+  const KCpCommDev* cp_comm = nullptr;
+  const KCpComp* cp_comp = nullptr;      // sig holds the op's class
   double* cp_scratch = nullptr;  // per launched block: [cp_stride][32] doubles (allocated per launch)
   int32_t sizes[4];
   double bw[4];
