@@ -72,5 +72,30 @@ def _build(force: bool, verbose: bool, extra) -> str:
     return LIB
 
 
+LIB_CHECKED = os.path.join(HERE, "lib", "libtoast_checked.so")
+
+
+def build_checked(force: bool = False, verbose: bool = False) -> str:
+    """The checked library (kernels.cu TOAST_CHECKED: shared-memory bounds and
+    table-index checks, dead-region poisoning, randomised barrier timing) —
+    test infrastructure for the race / bounds evidence; the
+    product path never loads it."""
+    return build(force=force, verbose=verbose, lib=LIB_CHECKED, obj=os.path.join(HERE, "build", "checked"),
+                 extra=["-DTOAST_CHECKED=1"])
+
+
+LIB_MUTANT = os.path.join(HERE, "lib", "libtoast_checked_mutant.so")
+
+
+def build_checked_mutant(force: bool = False, verbose: bool = False) -> str:
+    """The checked library with one barrier removed (TOAST_CHK_MUTANT: warps
+    read the decode results without waiting for them) — the planted race the
+    checker must catch (tests/test_gpu_parity.py)."""
+    return build(force=force, verbose=verbose, lib=LIB_MUTANT, obj=os.path.join(HERE, "build", "mutant"),
+                 extra=["-DTOAST_CHECKED=1", "-DTOAST_CHK_MUTANT=1"])
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv, verbose=True))

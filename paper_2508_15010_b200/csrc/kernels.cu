@@ -49,6 +49,22 @@
 #ifndef TOAST_MIN_BLOCKS
 #define TOAST_MIN_BLOCKS 3
 #endif
+// TOAST_CHECKED=1 builds the checked library (lib/libtoast_checked.so, DESIGN.md
+// §6 "Race and bounds evidence"): every shared-memory access is bounds-checked
+// against the launch's dynamic shared memory, table indices are checked, every
+// region is poisoned the moment it dies (a stale read returns garbage and
+// breaks bit-exact parity), and warps and lanes sleep pseudo-random times at
+// every barrier and cross-lane exchange (a missing barrier reorders accesses
+// and breaks parity).  A violated check traps.
+#ifndef TOAST_CHECKED
+#define TOAST_CHECKED 0
+#endif
+#ifndef TOAST_CHK_MUTANT
+#define TOAST_CHK_MUTANT 0
+#endif
+#ifndef TOAST_H4_PREFETCH
+#define TOAST_H4_PREFETCH 1   // the next edge template's record loaded one iteration ahead
+#endif
 #ifndef TOAST_MAX_WPB
 #define TOAST_MAX_WPB 8
 #endif
@@ -76,7 +92,7 @@ __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
 //      axes, critical path) or one per warp
 // The epilogue stages the 256-B records through whichever of X / Y does not
 // hold the accumulators (2 KB), so they leave as coalesced rows.
-__host__ __device__ inline int smem_c_bytes(int n_axes, int K) { return K > 1 ? 32 * (8 + 8 + 4 + 8 + 4 * n_axes) : 0; }
+__host__ __device__ inline int smem_c_bytes(int n_axes, int K) { return K > 1 ? 32 * (8 + 8 + 4 + 8 + 4 * n_axes) + 16 : 0; }
 // one accumulator region: payload/count accumulators, plus the K > 1 partials
 __host__ __device__ inline int smem_acc_bytes(int n_axes, int K) {
   return n_axes * 4 * 32 * (8 + 4) + (K > 1 ? 32 * 5 * 8 : 0);
@@ -109,8 +125,30 @@ __host__ __device__ inline int smem_block_bytes(const DeviceTables& T, int K) {
 // the block's dynamic shared memory; every access indexes this symbol so the
 // compiler emits plain LDS/STS (no generic-address conversion)
 extern __shared__ __align__(16) unsigned char g_smem[];
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+#if TOAST_CHECKED
+// a failed check records its line in a mapped host word (readable after the
+// trap kills the context: toast_checked_failure_line), then traps
+__device__ unsigned int* g_chk_host = nullptr;
+#define TOAST_CHK(cond)                                                                \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      if (g_chk_host) { atomicCAS(g_chk_host, 0u, (unsigned)__LINE__); __threadfence_system(); } \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define TOAST_CHK(cond) do { } while (0)
+#endif
 template <typename V>
-__device__ __forceinline__ V* sp(uint32_t off) { return reinterpret_cast<V*>(g_smem + off); }
+__device__ __forceinline__ V* sp(uint32_t off) {
+  TOAST_CHK(off + sizeof(V) <= dyn_smem_bytes() && off % alignof(V) == 0);
+  return reinterpret_cast<V*>(g_smem + off);
+}
 // 32-bit shared-window loads for the sweep's read-only tables (the generic
 // path re-derives the CTA's shared window on every access)
 __device__ __forceinline__ uint32_t smem_base() {
@@ -131,6 +169,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  TOAST_CHK(a - smem_base() < dyn_smem_bytes());
   uint32_t v;
   asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
@@ -145,6 +184,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t pc;              // Y: [n_fsig][32] per frontier signature: division code of the result layout
   uint32_t acc;             // pay [NA*4][32] u64, cnt [NA*4][32] u32 (+ seg [5][32] u64 when K > 1), shared or per warp
   uint32_t stage;           // the record-store staging (2 KB)
+  uint32_t next;            // C (K > 1): the block's next batch (dynamic scheduling)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -155,6 +195,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.status = 512;
   s.axpos = 640;
   s.axb = 896;
+  s.next = 896 + 128 * T.n_axes;
   const uint32_t x = smem_c_bytes(T.n_axes, K);
   const uint32_t y = x + smem_x_bytes(T.n_words, T.n_mc, T.n_axes, K, cp, T.n_spec);
   s.seq = x;
@@ -244,6 +285,7 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
     if ((int)id >= T.n_actions) { status |= TOAST_ST_BAD_ACTION_ID; continue; }
     uint32_t aw = __ldg(T.actions + id);
     uint32_t ac = aw & 0x3FF, rr = (aw >> 10) & 0xFF, ax = (aw >> 18) & 3;
+    TOAST_CHK(ac < (uint32_t)T.n_acolors && ax < (uint32_t)NA);
     uint32_t pm = sp<uint32_t>(S.acol)[ac * 32 + lane];
     bool dup = false;
     for (uint32_t b = pm; b; b &= b - 1) dup |= ((ap >> (2 * (__ffs(b) - 1))) & 3) == ax;
@@ -533,10 +575,96 @@ __device__ __forceinline__ void acc_add(int K, uint32_t* p, uint32_t v) {
   else atomicAdd(p, v);
 }
 
-// a block of one warp needs only the warp's own ordering
+// checked build: pseudo-random sleeps (per warp, and per lane where lanes
+// exchange data) and dead-region poisoning; no code in the product build
+__device__ __forceinline__ void chk_delay(uint32_t phase, bool per_lane) {
+#if TOAST_CHECKED
+  uint32_t h = (blockIdx.x * 0x9E3779B1u) ^ ((threadIdx.x >> (per_lane ? 0 : 5)) * 0x85EBCA77u) ^ (phase * 0xC2B2AE3Du) ^
+               (uint32_t)clock64();
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12;
+  if ((h & 3) == 0) __nanosleep(32 + ((h >> 4) & 2047));
+#else
+  (void)phase; (void)per_lane;
+#endif
+}
+// a block of one warp needs only the warp's own ordering (the checked build
+// sleeps a pseudo-random time per warp on both sides of every barrier)
 __device__ __forceinline__ void block_sync(int K) {
+  chk_delay(1, false);
   if (K == 1) __syncwarp();
   else __syncthreads();
+  chk_delay(2, false);
+}
+
+// checked build: dead-region poisoning (no code in the product build)
+__device__ __forceinline__ void chk_poison(uint32_t off, uint32_t bytes, int K, int warp, int lane) {
+#if TOAST_CHECKED
+  block_sync(K);
+  for (uint32_t i = (uint32_t)(warp * 32 + lane) * 4; i + 4 <= bytes; i += (uint32_t)K * 128)
+    *sp<uint32_t>(off + i) = 0xA5A5A5A5u;
+  block_sync(K);
+#else
+  (void)off; (void)bytes; (void)K; (void)warp; (void)lane;
+#endif
+}
+
+// ---------------------------------------------------------------- H4: one edge template, one lane
+// Per axis A: the def layout's dim (the def signature's class and result-dim
+// map), the use layout's dim (the use class and the edge's role -> dim map),
+// whether the def value is partial over A.  No collective when every axis
+// sits on the same dim on both sides and nothing is partial; otherwise C11's
+// phases (reading R20): 1a all_gather the
+// axes the use holds on no dim (ascending, the size growing by each), 1b
+// all_to_all the axes it holds on another dim, 2 reduce_scatter (the use
+// holds the axis) or all_reduce the partial axes.  Returns the template's
+// growth code for H5 (0: no temporary).  (A branch-free version — every
+// phase as predicated selects — measured 9% slower on GPT-24: it executes every
+// phase for every communicating template.)
+template <int NA, bool P2>
+__device__ __forceinline__ uint8_t h4_template(const DeviceTables& T, uint32_t da2r, uint32_t ue, uint32_t use_dimof,
+                                               uint32_t def_rdm, uint64_t sgb, uint32_t ne,
+                                               unsigned long long (&rp)[NA * 4], uint32_t (&rc)[NA * 4]) {
+  uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {
+    const uint32_t du = a_dim(ue, use_dimof, A);
+    const uint32_t rd = (da2r >> (4 * A)) & 15, dd = a_dim(da2r, def_rdm, A);
+    dimD |= dd << (4 * A);
+    dimU |= du << (4 * A);
+    P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
+    presD |= (dd != 15 ? 1u : 0u) << A;
+    presU |= (du != 15 ? 1u : 0u) << A;
+  }
+  if (dimD == dimU && !P) return 0;
+  uint64_t size = dv<P2>(T, sgb, dcode<P2>(T, presD));
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather
+    const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+    if (dd == 15 || du != 15) continue;
+    rp[A * 4 + TOAST_AG] += size;
+    rc[A * 4 + TOAST_AG] += ne;
+    size *= (uint64_t)T.sizes[A];
+  }
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
+    const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
+    if (dd == 15 || du == 15 || dd == du) continue;
+    rp[A * 4 + TOAST_A2A] += size;
+    rc[A * 4 + TOAST_A2A] += ne;
+  }
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
+    if (!((P >> A) & 1)) continue;
+    if (((dimU >> (4 * A)) & 15) != 15) {
+      size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
+      rp[A * 4 + TOAST_RS] += size;
+      rc[A * 4 + TOAST_RS] += ne;
+    } else {
+      rp[A * 4 + TOAST_AR] += size;
+      rc[A * 4 + TOAST_AR] += ne;
+    }
+  }
+  return (uint8_t)(dcode<P2>(T, presU) | (dcode<P2>(T, presD) << 4));
 }
 
 // ---------------------------------------------------------------- one batch of 32 candidates
@@ -545,9 +673,16 @@ __device__ __forceinline__ void block_sync(int K) {
 // (H2b), the edge templates (H4) and the frontier groups (H5) each, and warp
 // 0 combines their sums and peaks, scores and writes the records (rows
 // [row0, row0 + rows) of the output).  S.seq holds the candidates on entry.
-template <int NA, bool P2, bool CP>
-__device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
-                                           void* __restrict__ out, int64_t row0, int rows, bool compact) {
+// the front half's per-candidate results: the state key (H7), the 128-bit
+// FLOP total (H3) and the decode status (H1); the class maps stay in S.mca
+struct Front {
+  uint64_t key, flo, fhi;
+  uint32_t status;
+};
+
+// front half: decode (H1) and materialise every class (H2a) with its key terms and FLOPs
+template <int NA, bool P2>
+__device__ __forceinline__ Front batch_front(const DeviceTables& T, const Smem& S, int K, int warp, int lane) {
   block_sync(K);
   uint64_t f0 = 0, on = 0, ap = 0;
   uint32_t axb[NA], status = 0;
@@ -561,15 +696,20 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
 #pragma unroll
       for (int A = 0; A < NA; ++A) sp<uint32_t>(S.axb)[A * 32 + lane] = axb[A];
     }
+#if !TOAST_CHK_MUTANT   // (a planted race for the checker's own test: TOAST_CHK_MUTANT=1 drops this barrier)
     __syncthreads();
+#endif
     f0 = sp<unsigned long long>(S.f0)[lane];
     on = sp<unsigned long long>(S.on)[lane];
     ap = sp<unsigned long long>(S.axpos)[lane];
 #pragma unroll
     for (int A = 0; A < NA; ++A) axb[A] = sp<uint32_t>(S.axb)[A * 32 + lane];
   } else {
+    chk_delay(3, true);
     __syncwarp();   // the class maps below overwrite other lanes' staged sequences
   }
+  // (checked build: the staged sequences and legal sets are dead from here on)
+  chk_poison(S.seq, S.acol - S.seq, K, warp, lane);
   // H2a: one materialisation per class (signatures that differ only in their
   // result dims share it): the axis -> role map; per class the state-key
   // terms (H7, R14) and the local FLOPs (H3) of all its ops at once
@@ -597,7 +737,19 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       fhi += (uint64_t)(f >> 64) + ((flo < l) ? 1 : 0);
     }
   }
+  return Front{key, flo, fhi, status};
+}
+
+// back half: H2b, H4, H5 (+ the critical path), H6 and the records of rows
+// [row0, row0 + rows), from the class maps in S.mca and the front's results
+// (with K > 1 warps, warp w's partial key / FLOPs; the status in warp 0)
+template <int NA, bool P2, bool CP>
+__device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
+                                           Front fr, void* __restrict__ out, int64_t row0, int rows, bool compact) {
+  uint64_t key = fr.key, flo = fr.flo, fhi = fr.fhi;
+  const uint32_t status = fr.status;
   block_sync(K);
+  chk_poison(S.acol, (uint32_t)T.n_acolors * 128, K, warp, lane);   // (checked build: the event bitmaps are dead)
   // H2b: per frontier signature the division code of its result layout
   for (int f = warp; f < T.n_fsig; f += K) {
     const uint64_t w = __ldg(T.fsig + f);
@@ -616,7 +768,8 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
   const uint32_t acc = S.acc + (acc_shared(NA, CP) ? 0u : (uint32_t)warp * smem_acc_bytes(NA, K));
   unsigned long long* pay = sp<unsigned long long>(acc);
   uint32_t* cnt = sp<uint32_t>(acc + NA * 4 * 32 * 8);
-  unsigned long long* seg = sp<unsigned long long>(acc + NA * 4 * 32 * 12);
+  // (the K > 1 partials follow the slots; one warp has none)
+  unsigned long long* seg = K > 1 ? sp<unsigned long long>(acc + NA * 4 * 32 * 12) : nullptr;
 
   // H4 per edge template: every use edge of the template communicates the
   // same way, so its payloads are costed once from the template's summed
@@ -634,63 +787,28 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     n1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + warp) + 1);
   }
   for (int tix = warp; tix < T.n_tmpl; tix += K) {
+#if TOAST_H4_PREFETCH
     const uint4 t0 = n0, t1 = n1;
     if (tix + K < T.n_tmpl) {
       n0 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix + K));
       n1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix + K) + 1);
     }
+#else
+    const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix)), t1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix) + 1);
+#endif
+    TOAST_CHK((t0.x & 0xFFFF) < (uint32_t)T.n_mc && (t0.x >> 16) < (uint32_t)T.n_mc &&
+              (t1.y == 0xFFFFFFFFu || t1.y < (uint32_t)T.n_ftmpl));
     const uint32_t da2r = mca_load<NA>(S, t0.x & 0xFFFF, lane);   // the def signature's class
     const uint32_t ue = mca_load<NA>(S, t0.x >> 16, lane);        // the use class
-    const uint32_t use_dimof = t0.y, def_rdm = t1.z;
-    uint32_t dimD = 0, dimU = 0, P = 0, presD = 0, presU = 0;
-#pragma unroll
-    for (int A = 0; A < NA; ++A) {
-      const uint32_t du = a_dim(ue, use_dimof, A);
-      const uint32_t rd = (da2r >> (4 * A)) & 15, dd = a_dim(da2r, def_rdm, A);
-      dimD |= dd << (4 * A);
-      dimU |= du << (4 * A);
-      P |= ((rd != 15 && dd == 15) ? 1u : 0u) << A;
-      presD |= (dd != 15 ? 1u : 0u) << A;
-      presU |= (du != 15 ? 1u : 0u) << A;
-    }
-    uint8_t tbv = 0;
-    if (dimD != dimU || P) {
-      const uint64_t sgb = u64of(t0.z, t0.w);
-      const uint32_t ne = t1.x;
-      uint64_t size = dv<P2>(T, sgb, dcode<P2>(T, presD));
-#pragma unroll
-      for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather (reading R20)
-        const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
-        if (dd == 15 || du != 15) continue;
-        rp[A * 4 + TOAST_AG] += size;
-        rc[A * 4 + TOAST_AG] += ne;
-        size *= (uint64_t)T.sizes[A];
-      }
-#pragma unroll
-      for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
-        const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
-        if (dd == 15 || du == 15 || dd == du) continue;
-        rp[A * 4 + TOAST_A2A] += size;
-        rc[A * 4 + TOAST_A2A] += ne;
-      }
-#pragma unroll
-      for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
-        if (!((P >> A) & 1)) continue;
-        if (((dimU >> (4 * A)) & 15) != 15) {
-          size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
-          rp[A * 4 + TOAST_RS] += size;
-          rc[A * 4 + TOAST_RS] += ne;
-        } else {
-          rp[A * 4 + TOAST_AR] += size;
-          rc[A * 4 + TOAST_AR] += ne;
-        }
-      }
-      tbv = (uint8_t)(dcode<P2>(T, presU) | (dcode<P2>(T, presD) << 4));
-    }
+    const uint8_t tbv = h4_template<NA, P2>(T, da2r, ue, t0.y, t1.z, u64of(t0.z, t0.w), t1.x, rp, rc);
     if (t1.y != 0xFFFFFFFFu) sp<uint8_t>(S.tb)[t1.y * 32 + lane] = tbv;
   }
   // (with K = 1 the slots may overlay the class maps: every lane's last read first)
-  if (K == 1) __syncwarp();
+  if (K == 1) {
+    chk_delay(4, true);
+    __syncwarp();
+    if (acc_in_x(K, CP, T.n_spec)) chk_poison(S.acc, smem_acc_bytes(NA, K), K, warp, lane);   // (checked: the maps are dead)
+  }
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) {
     if (K == 1 || !acc_shared(NA, CP)) {
@@ -723,6 +841,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     for (uint32_t k = 0; k < n_sig; ++k) {
       const uint64_t w = __ldg(tp + k);
       const long long v = (long long)(w << 16) >> 16;    // signed 48-bit value
+      TOAST_CHK((uint32_t)(w >> 48) < (uint32_t)T.n_fsig);
       Ms += dvs<P2>(T, v, lds_u8(pc_base + (uint32_t)(w >> 48) * 32));
     }
     tp += n_sig;
@@ -731,6 +850,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     for (uint32_t k = 0; k < n_tm; ++k) {
       const uint64_t w = __ldg(tp + k);
       const uint64_t v = w & ((1ULL << 48) - 1);
+      TOAST_CHK((uint32_t)(w >> 48) < (uint32_t)T.n_ftmpl);
       const uint32_t b = lds_u8(tb_base + (uint32_t)(w >> 48) * 32);
       const uint32_t cU = b & 15, cD = b >> 4;
       if (cU != cD) {
@@ -892,6 +1012,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
       const uint32_t sw = (lane >> 1) & 3;   // the slot swizzle: conflict-free 16-B accesses
       auto put = [&](int slot, uint4 v) { stage[lane * 4 + ((slot & 3) ^ sw)] = v; };
       auto flush = [&](int quarter) {
+        chk_delay(5, true);
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -900,6 +1021,7 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
         }
         __syncwarp();
       };
+      chk_poison(S.stage, STAGE_BYTES, 1, 0, lane);   // (checked build: the staging holds nothing live)
       auto d2 = [](double x) { return (unsigned long long)__double_as_longlong(x); };
       auto u4 = [](unsigned long long a, unsigned long long b) {
         return make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
@@ -939,6 +1061,31 @@ __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S,
     }
   }
   block_sync(K);
+  // (checked build: everything but the decode results is dead between batches)
+  chk_poison(S.seq, (uint32_t)smem_block_bytes(T, K) - S.seq, K, warp, lane);
+}
+
+template <int NA, bool P2, bool CP>
+__device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
+                                           void* __restrict__ out, int64_t row0, int rows, bool compact) {
+  const Front fr = batch_front<NA, P2>(T, S, K, warp, lane);
+  batch_back<NA, P2, CP>(T, S, K, warp, lane, valid, fr, out, row0, rows, compact);
+}
+
+// the block's next batch: with a ticket (dynamic scheduling) the next unclaimed
+// batch of the launch, so blocks that drew cheap batches take more of them
+// (results never depend on which block evaluates a batch); else a static stride
+__device__ __forceinline__ int64_t next_batch(const DeviceTables& T, const Smem& S, int64_t b, int K) {
+  if (!T.ticket) return b + gridDim.x;
+  if (K == 1) {
+    unsigned int t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(T.ticket, 1u);
+    return (int64_t)gridDim.x + __shfl_sync(0xffffffffu, t, 0);
+  }
+  if (threadIdx.x == 0) sp<unsigned int>(S.next)[0] = atomicAdd(T.ticket, 1u);
+  __syncthreads();
+  const int64_t nb = (int64_t)gridDim.x + sp<unsigned int>(S.next)[0];
+  return nb;
 }
 
 // the batch's rows [row0, row0 + rows) of a contiguous uint16[n][32] array as
@@ -955,6 +1102,7 @@ __device__ __forceinline__ void load_seq_rows(const Smem& S, const uint16_t* __r
     seq_word(S, 4 * q + 2, r) = w.z;
     seq_word(S, 4 * q + 3, r) = w.w;
   }
+  chk_delay(6, true);
   __syncwarp();
 }
 // one row per lane (rollouts of a search round: rows repeat a leaf's prefix)
@@ -975,6 +1123,7 @@ __device__ __forceinline__ void load_seq_lane(const Smem& S, const uint16_t* __r
 }
 // the batch's sequences out as coalesced 16-B row stores
 __device__ __forceinline__ void store_seq_rows(const Smem& S, uint16_t* __restrict__ g, int rows, int lane) {
+  chk_delay(7, true);
   __syncwarp();
   uint4* dst = reinterpret_cast<uint4*>(g);
 #pragma unroll
@@ -991,7 +1140,7 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
   const int64_t nbatch = (n + 31) / 32;
-  for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+  for (int64_t b = blockIdx.x; b < nbatch; b = next_batch(T, S, b, K)) {
     const int64_t row0 = b * 32;
     const int rows = (int)(n - row0 < 32 ? n - row0 : 32);
     if (warp == 0) load_seq_rows(S, seqs + row0 * 32, rows, lane);
@@ -1024,7 +1173,7 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
   const int64_t nbatch = (n + 31) / 32;
   const uint32_t seed_lo = (uint32_t)seed, seed_hi = (uint32_t)(seed >> 32);
   const int nw = T.n_words;
-  for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+  for (int64_t b = blockIdx.x; b < nbatch; b = next_batch(T, S, b, K)) {
     const int64_t row0 = b * 32, i = row0 + lane;
     const int rows = (int)(n - row0 < 32 ? n - row0 : 32);
     const bool valid = i < n;
@@ -1183,8 +1332,23 @@ static toast_status upload(toast_analysis* a, const V& v, const void** dst, std:
   return TOAST_OK;
 }
 
+#if TOAST_CHECKED
+static unsigned int* h_chk_word = nullptr;
+#endif
+
 toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaSetDevice(a->device));
+#if TOAST_CHECKED
+  if (!h_chk_word) {
+    TOAST_CUDA(cudaHostAlloc((void**)&h_chk_word, sizeof(unsigned int), cudaHostAllocMapped | cudaHostAllocPortable));
+    *h_chk_word = 0;
+  }
+  {
+    unsigned int* dptr = nullptr;
+    TOAST_CUDA(cudaHostGetDevicePointer((void**)&dptr, h_chk_word, 0));
+    TOAST_CUDA(cudaMemcpyToSymbol(g_chk_host, &dptr, sizeof(dptr)));
+  }
+#endif
   DeviceTables& T = a->dt;
   toast_status st;
   const void* p;
@@ -1291,10 +1455,12 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     for (KCpComp& c : cc) c.sig = sig_mc(c.sig);   // the op's class
     if ((st = upload(a, cc, &p, err))) return st;
     T.cp_comp = reinterpret_cast<const KCpComp*>(p);
-    // Finish-slot scratch is allocated per launch, stream-ordered, from this
-    // analysis' own pool (kept, not released): concurrent calls on different
-    // streams — the host-buffer pipeline's chunks, or a caller's — each get
-    // their own, since blocks index it by blockIdx.
+  }
+  {
+    // Per-launch scratch (the batch ticket; the critical path's finish slots)
+    // is allocated stream-ordered from this analysis' own pool (kept, not
+    // released): concurrent calls on different streams — the host-buffer
+    // pipeline's chunks, or a caller's — each get their own.
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
@@ -1356,6 +1522,20 @@ static cudaError_t cp_scratch_alloc(const toast_analysis* a, int64_t blocks, cud
   return cudaMallocFromPoolAsync(reinterpret_cast<void**>(out), bytes, (cudaMemPool_t)a->cp_pool, st);
 }
 
+// the dynamic-scheduling ticket of one launch (zeroed), when blocks will take
+// more than one batch — an experiment knob (TOAST_DYNAMIC_SCHED=1): measured
+// ~1% slower than the static stride on all four configs (the bench's whole
+// waves leave little imbalance to recover), so the static stride is the default
+static cudaError_t ticket_alloc(const toast_analysis* a, int64_t batches, int64_t blocks, cudaStream_t st,
+                                unsigned int** out) {
+  *out = nullptr;
+  static const bool dyn = getenv("TOAST_DYNAMIC_SCHED") != nullptr;
+  if (!dyn || batches <= blocks) return cudaSuccess;
+  cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(out), sizeof(unsigned int), (cudaMemPool_t)a->cp_pool, st);
+  if (e != cudaSuccess) return e;
+  return cudaMemsetAsync(*out, 0, sizeof(unsigned int), st);
+}
+
 toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_t n, void* d_out, void* stream,
                          std::string& err, bool compact) {
   if (n <= 0) return TOAST_OK;
@@ -1367,12 +1547,14 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
+  TOAST_CUDA(ticket_alloc(a, batches, blocks, st, &T.ticket));
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
     toast_eval_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_seqs, n, d_out, compact);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());
   if (T.cp_scratch) TOAST_CUDA(cudaFreeAsync(T.cp_scratch, st));
+  if (T.ticket) TOAST_CUDA(cudaFreeAsync(T.ticket, st));
   return TOAST_OK;
 }
 
@@ -1387,12 +1569,14 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
+  TOAST_CUDA(ticket_alloc(a, batches, blocks, st, &T.ticket));
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
     toast_rollout_kernel<NA, P2, CP><<<g, b, sm, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep, compact);
     return 0;
   });
   TOAST_CUDA(cudaGetLastError());
   if (T.cp_scratch) TOAST_CUDA(cudaFreeAsync(T.cp_scratch, st));
+  if (T.ticket) TOAST_CUDA(cudaFreeAsync(T.ticket, st));
   return TOAST_OK;
 }
 
@@ -1562,3 +1746,11 @@ toast_status run_host_buffers(toast_analysis* a, bool rollout, const uint16_t* h
 }
 
 }  // namespace toast
+
+#if TOAST_CHECKED
+// checked build only (not part of include/toast.h): the kernels.cu line of the
+// first failed TOAST_CHK, 0 if none
+extern "C" unsigned int toast_checked_failure_line() {
+  return toast::h_chk_word ? *reinterpret_cast<volatile unsigned int*>(toast::h_chk_word) : 0u;
+}
+#endif

@@ -239,6 +239,7 @@ struct DeviceTables {
   const KCpCommDev* cp_comm = nullptr;
   const KCpComp* cp_comp = nullptr;      // sig holds the op's class
   double* cp_scratch = nullptr;  // per launched block: [cp_stride][32] doubles (allocated per launch)
+  unsigned int* ticket = nullptr; // per launch: the next batch counter (dynamic batch scheduling; null: static)
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -331,7 +332,7 @@ struct toast_analysis {
     bool in_use = false;
   } spool;
   void* pipe_event = nullptr;
-  void* cp_pool = nullptr;      // cudaMemPool_t of the critical-path scratch (R22)
+  void* cp_pool = nullptr;      // cudaMemPool_t of the per-launch scratch (batch ticket; R22 finish slots)
 };
 
 namespace toast {

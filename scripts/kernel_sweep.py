@@ -10,10 +10,12 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2508_15010_b200", "lib", "variants")
 VARIANTS = {
     "b3": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=3"],
-    "b4": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=4"],
-    "b5": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=5"],
-    "b6": ["-DTOAST_MAX_THREADS=256", "-DTOAST_MIN_BLOCKS=6"],
+    "t128b7": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=7"],
+    "t128b8": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=8"],
+    "t128b7np": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=7", "-DTOAST_H4_PREFETCH=0"],
 }
+if os.environ.get("SWEEP_ONLY"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
 KS = [int(k) for k in os.environ.get("SWEEP_KS", "1,2").split(",")]
 
 

@@ -1,7 +1,15 @@
-"""Drive every kernel instantiation the parity suite uses, small, for
-compute-sanitizer (racecheck / synccheck / memcheck / initcheck):
+"""Drive every kernel instantiation the parity suite uses, small, under a
+checking tool:
 
-    compute-sanitizer --tool racecheck --kernel-name kns=toast_ python scripts/sanitize.py
+    TOAST_LIB=paper_2508_15010_b200/lib/libtoast_checked.so python scripts/sanitize.py
+
+The checked library (kernels.cu TOAST_CHECKED) bounds-checks every shared-memory
+access and table index (a violation traps), poisons every region the moment it
+dies and sleeps pseudo-random times at every barrier and cross-lane exchange,
+so a race or a stale read breaks the bit-exact comparison below.  (The same
+driver runs under compute-sanitizer — `compute-sanitizer --tool racecheck
+--kernel-name kns=toast_ python scripts/sanitize.py` — where it is available;
+this pool's GPU boxes refuse it.)
 
 Per config (1-4 axes, power-of-two and not) x cost model (sum, critical path)
 x K in {1, 2, 4, 8} warps per batch (TOAST_FORCE_K, read when the analysis is
@@ -12,6 +20,7 @@ that is hazard-free is also a parity run of every instantiation.
 """
 from __future__ import annotations
 
+import ctypes
 import os
 import sys
 
@@ -47,12 +56,20 @@ def main():
                 pre = torch.zeros((n, 32), dtype=torch.int16, device="cuda")
                 seqs = torch.empty_like(pre)
                 out = torch.empty((n, 256), dtype=torch.uint8, device="cuda")
-                T.rollout_batch(a, pre, 5, 0, seqs, out)
-                out2 = torch.empty_like(out)
-                T.eval_batch(a, seqs, out2)
-                sc = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
-                T.eval_scores(a, seqs, sc)
-                torch.cuda.synchronize()
+                try:
+                    T.rollout_batch(a, pre, 5, 0, seqs, out)
+                    torch.cuda.synchronize()
+                    out2 = torch.empty_like(out)
+                    T.eval_batch(a, seqs, out2)
+                    sc = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
+                    T.eval_scores(a, seqs, sc)
+                    torch.cuda.synchronize()
+                except Exception:
+                    f = getattr(T._lib, "toast_checked_failure_line", None)
+                    if f is not None:
+                        f.restype = ctypes.c_uint
+                        print(f"{name} cost_model={cm} K={K}: CHECK FAILED at kernels.cu:{f()}", flush=True)
+                    raise
                 g_seqs = seqs.cpu().numpy().view(np.uint16)
                 ok = (np.array_equal(g_seqs, o_seqs) and T.as_costs(out).tobytes() == oc.tobytes()
                       and T.as_costs(out2).tobytes() == oc.tobytes())

@@ -576,3 +576,45 @@ def test_llama80_worst_case_and_sampled_critical_path():
         s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=77, id_base=int(i))
         assert np.array_equal(gs[i], s1[0])
         assert_same(gc[i:i + 1], c1, f"row {i}")
+
+
+def test_checked_library_race_and_bounds():
+    """Race / bounds evidence without compute-sanitizer (closed on this pool):
+    the checked library (kernels.cu TOAST_CHECKED, built by build()) traps on
+    any out-of-bounds shared-memory access or table index, poisons every
+    shared-memory region as soon as it dies (the sequence staging after
+    decode, the event bitmaps after H2a, the class maps under the
+    accumulators, the record staging, everything between batches) and sleeps
+    pseudo-random times per warp at every barrier and per lane at every
+    cross-lane exchange.  scripts/sanitize.py runs every kernel instantiation
+    (1-4 mesh axes, power of two or not, sum and critical-path models) at
+    K = 1, 2, 4 and 8 warps per batch on a ragged batch through it: all
+    bit-identical to the oracle."""
+    import os
+    import subprocess
+    import sys
+    from paper_2508_15010_b200 import build as B
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    assert os.path.exists(B.LIB_CHECKED), "build() builds the checked library"
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "sanitize.py")], capture_output=True, text=True,
+                       env=dict(os.environ, TOAST_LIB=B.LIB_CHECKED), timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "all bit-identical to the oracle" in r.stdout
+    assert r.stdout.count(": ok") == 8 * 2 * 4
+
+
+def test_checked_library_catches_a_planted_race():
+    """The checker is not vacuous: the same library with the barrier between
+    warp 0's decode and the other warps' reads of its results removed
+    (TOAST_CHK_MUTANT) fails the K > 1 runs of scripts/sanitize.py."""
+    import os
+    import subprocess
+    import sys
+    from paper_2508_15010_b200 import build as B
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    assert os.path.exists(B.LIB_MUTANT), "build() builds the mutant library"
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "sanitize.py"), "gpt2", "gpt2_3ax"],
+                       capture_output=True, text=True, env=dict(os.environ, TOAST_LIB=B.LIB_MUTANT), timeout=900)
+    assert r.returncode != 0, r.stdout[-2000:]
+    assert "gpt2 cost_model=0 K=1: ok" in r.stdout          # one-warp blocks never needed that barrier
+    assert "gpt2 cost_model=0 K=2: ok" not in r.stdout      # the first multi-warp run is caught
