@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--cost-model", default="sum", choices=["sum", "cp"],
                    help="runtime model of the timed arm: straight-line sum (G14) or critical path (R22)")
     p.add_argument("--no-variants", action="store_true", help="skip the variant measurements (critical path, contraction)")
+    p.add_argument("--dedup", type=int, default=0, choices=[0, 1],
+                   help="1: rollout launches cost each distinct state once (toast_nda_opts.dedup, NEXT-3)")
     return p.parse_args()
 
 
@@ -407,7 +409,7 @@ def run_toast(args, cfg, rank, world, local):
     t = time.perf_counter()
     cm = T.COST_CRITICAL_PATH if args.cost_model == "cp" else T.COST_SUM
     a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
-                         cuda_device=local, cost_model=cm)
+                         cuda_device=local, cost_model=cm, dedup=args.dedup)
     nda_s = time.perf_counter() - t
     dump = a.dump()
     wave = a.preferred_batch()
@@ -492,7 +494,8 @@ def run_toast(args, cfg, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_median": statistics.median(step_ms),   # rank 0 (SURVEY §8(d) median)
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": cfg.name, "cost_model": args.cost_model, "rollouts_per_step_per_gpu": N, "wave": wave,
+            "config": {"workload": cfg.name, "cost_model": args.cost_model, "dedup": args.dedup,
+                       "rollouts_per_step_per_gpu": N, "wave": wave,
                        "warps_per_batch": a.kernel_tables().get("warps_per_batch"),
                        "blocks_per_sm": a.kernel_tables().get("blocks_per_sm"),
                        "mesh": [list(x) for x in cfg.axes],

@@ -96,7 +96,14 @@ typedef struct {
    the [comment] block P:1346-1357, reading R23: eagerly contract
    M edges unless a directed path would join the two endpoints of a
    conflict; conflicts on the same pair of contracted nodes form one set).
-   Any other value: TOAST_E_INVALID_ARG. */
+   dedup ("any action sequence yielding the
+   same sharded model resolves to the same unique state"): 0 = every
+   candidate of a rollout launch is evaluated on its own; 1 = a rollout launch
+   materialises every candidate (H1, H2, H3, H7), then costs each distinct
+   materialised state once (H4-H6, and the critical path) and copies its
+   record to the candidates that reached it — the same bits either way
+   (states are compared exactly: equal state key AND equal per-class axis
+   maps).  Any other value of these three: TOAST_E_INVALID_ARG. */
 enum { TOAST_COST_SUM = 0, TOAST_COST_CRITICAL_PATH = 1 };
 enum { TOAST_GROUP_COMPAT = 0, TOAST_GROUP_CONTRACTION = 1 };
 typedef struct {
@@ -104,6 +111,7 @@ typedef struct {
   int32_t max_depth;
   int32_t cost_model;
   int32_t conflict_grouping;
+  int32_t dedup;
 } toast_nda_opts;
 
 typedef struct toast_graph toast_graph;        /* opaque, library-owned */
@@ -247,7 +255,10 @@ typedef struct {
   int32_t leaves_per_round; /* L */
   int32_t rollouts_per_leaf;/* R */
   int32_t patience;         /* stop after this many non-improving rounds (1) */
-  int32_t pad0;
+  int32_t transpositions;   /* 0 = a tree of action sequences; 1 = each materialised state
+                               once (reading R24): a selected leaf
+                               whose exactly evaluated state another node already holds
+                               (equal state key) leaves the tree after its round */
   double uct_c;             /* UCT exploration constant (sqrt 2) */
   double target_score;      /* stop once best <= target; NaN = disabled */
   void* cuda_stream;

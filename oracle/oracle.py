@@ -84,7 +84,7 @@ def lib():
         L.orc_edges.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         L.orc_search.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_double,
                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
-                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
     return _lib
 
 
@@ -214,12 +214,13 @@ class Oracle:
         return n, best, cost[0]
 
     def search(self, seed=0, max_evals=0, time_limit_s=0.0, L=16, R=16, patience=1, uct_c=2 ** 0.5,
-               target_score=float("nan"), threads=1, trace_cap=4096):
+               target_score=float("nan"), threads=1, trace_cap=4096, transpositions=0):
+        """C16; transpositions=1: each materialised state once in the tree (reading R24)."""
         res = np.zeros(1, dtype=SEARCH_DTYPE)
         trace = np.zeros(trace_cap, dtype=np.float64)
         lib().orc_search(self.h, int(seed), int(max_evals), float(time_limit_s), int(L), int(R), int(patience),
                          float(uct_c), float(target_score), int(threads), res.ctypes.data, trace.ctypes.data,
-                         int(trace_cap))
+                         int(trace_cap), int(transpositions))
         r = res[0]
         return r, trace[:min(int(r["rounds"]), trace_cap)].copy()
 

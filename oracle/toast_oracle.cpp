@@ -1746,7 +1746,8 @@ int64_t orc_dump(void* h, char* buf, int64_t cap) {
 
 // C16 search (single process).  rollout_threads = CPU threads for the batch.
 int orc_search(void* h, uint64_t seed, int64_t max_evals, double time_limit_s, int L, int R, int patience,
-               double uct_c, double target_score, int threads, void* result, double* trace, int trace_cap) {
+               double uct_c, double target_score, int threads, void* result, double* trace, int trace_cap,
+               int transpositions) {
   Oracle* O = (Oracle*)h;
   SearchOut* res = (SearchOut*)result;
   memset(res, 0, sizeof(SearchOut));
@@ -1754,11 +1755,13 @@ int orc_search(void* h, uint64_t seed, int64_t max_evals, double time_limit_s, i
   auto elapsed = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - tstart).count(); };
   Node* root = new Node();
   root->untried = legal_after(*O, root->prefix);
+  std::map<u64, Node*> holder;   // reading R24: which node holds each materialised state (by its key)
   // the root is the unsharded module: it is the first incumbent
   bool have = true;
   Cost best;
   u16 best_seq[32] = {0};
   O->raw_eval(best_seq, best);
+  holder[best.state_key] = root;
   i64 evals = 1, rollouts_done = 0;
   int rounds = 0, nonimprove = 0;
   res->time_to_target_s = -1.0;
@@ -1817,6 +1820,26 @@ int orc_search(void* h, uint64_t seed, int64_t max_evals, double time_limit_s, i
       for (Node* x = leaves[l]; x; x = x->parent) { x->N += R + 1; x->W += sum; }
       consider(lcost[l], &lpre[(size_t)l * 32]);
       for (int j = 0; j < R; j++) consider(costs[(size_t)l * R + j], &outs[((size_t)l * R + j) * 32]);
+    }
+    // reading R24: "any action sequence yielding the same sharded
+    // model resolves to the same unique state, eliminating duplication by
+    // construction" — with transpositions on, a selected leaf whose state (its
+    // exactly evaluated key) another node already holds leaves the tree; leaves
+    // are taken in selection order, so the first to reach a state keeps it
+    if (transpositions) {
+      std::vector<Node*> gone;
+      for (int l = 0; l < L; l++) {
+        if (lcost[l].status != 0) continue;
+        auto it = holder.find(lcost[l].state_key);
+        if (it == holder.end()) holder[lcost[l].state_key] = leaves[l];
+        else if (it->second != leaves[l] && std::find(gone.begin(), gone.end(), leaves[l]) == gone.end())
+          gone.push_back(leaves[l]);
+      }
+      for (Node* g : gone) {
+        std::vector<Node*>& ch = g->parent->children;
+        ch.erase(std::find(ch.begin(), ch.end(), g));
+        delete g;
+      }
     }
     evals += (i64)L * (R + 1);
     if (trace && rounds < trace_cap) trace[rounds] = best.score;

@@ -86,6 +86,7 @@ toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_anal
     return fail(TOAST_E_INVALID_ARG, "cost_model must be TOAST_COST_SUM or TOAST_COST_CRITICAL_PATH");
   if (o->conflict_grouping != TOAST_GROUP_COMPAT && o->conflict_grouping != TOAST_GROUP_CONTRACTION)
     return fail(TOAST_E_INVALID_ARG, "conflict_grouping must be TOAST_GROUP_COMPAT or TOAST_GROUP_CONTRACTION");
+  if (o->dedup != 0 && o->dedup != 1) return fail(TOAST_E_INVALID_ARG, "dedup must be 0 or 1");
   toast_analysis* a = new (std::nothrow) toast_analysis();
   if (!a) return fail(TOAST_E_OOM, "out of host memory");
   std::string err;
@@ -99,6 +100,7 @@ toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_anal
       if (st == TOAST_OK) st = toast::autotune_k(a, err);
       if (st != TOAST_OK) { toast::free_tables(a); delete a; return fail(st, err); }
     }
+    a->dedup = o->dedup;   // (after the autotune, which times the one-kernel path)
   } catch (std::bad_alloc&) {
     delete a;
     return fail(TOAST_E_OOM, "out of host memory");

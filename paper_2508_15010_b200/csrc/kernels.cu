@@ -209,6 +209,12 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   s.stage = inx ? y : x;
   return s;
 }
+// the same layout starting at byte `base` (the dedup back kernel's independent warps)
+__device__ __forceinline__ Smem smem_at(Smem s, uint32_t base) {
+  s.f0 += base; s.on += base; s.status += base; s.axpos += base; s.axb += base; s.seq += base; s.legal += base;
+  s.mca += base; s.acol += base; s.tb += base; s.pc += base; s.acc += base; s.stage += base; s.next += base;
+  return s;
+}
 // the staged sequences: word w (ids 2w, 2w + 1) of lane L at [w][L ^ 8 (w >> 2)]
 // — the swizzle makes the coalesced row loads and stores conflict-free
 __device__ __forceinline__ uint32_t& seq_word(const Smem& S, int w, int lane) {
@@ -745,7 +751,8 @@ __device__ __forceinline__ Front batch_front(const DeviceTables& T, const Smem& 
 // (with K > 1 warps, warp w's partial key / FLOPs; the status in warp 0)
 template <int NA, bool P2, bool CP>
 __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
-                                           Front fr, void* __restrict__ out, int64_t row0, int rows, bool compact) {
+                                           Front fr, void* __restrict__ out, int64_t row0, int rows, bool compact,
+                                           int64_t scr_idx) {
   uint64_t key = fr.key, flo = fr.flo, fhi = fr.fhi;
   const uint32_t status = fr.status;
   block_sync(K);
@@ -932,7 +939,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
     peak = M > peak ? M : peak;
   }
   }
-  if (CP) cp_classes<NA, P2>(T, S, K, warp, lane, T.cp_scratch + (size_t)blockIdx.x * cp_stride(T) * 32);
+  if (CP) cp_classes<NA, P2>(T, S, K, warp, lane, T.cp_scratch + (size_t)scr_idx * cp_stride(T) * 32);
   if (K > 1 && !acc_shared(NA, CP)) {
     seg[0 * 32 + lane] = key;
     seg[1 * 32 + lane] = flo;
@@ -990,7 +997,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
       for (int k = 0; k < 4; ++k) ncoll += cnt[(A * 4 + k) * 32 + lane];
     }
     if (CP) {
-      double* scr = T.cp_scratch + (size_t)blockIdx.x * cp_stride(T) * 32;
+      double* scr = T.cp_scratch + (size_t)scr_idx * cp_stride(T) * 32;
       tt = cp_sweep(T, lane, scr, scr + (size_t)(T.n_comm + T.n_comp + 1) * 32);
     }
     const uint64_t pk = pk_all;
@@ -1062,14 +1069,14 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
   }
   block_sync(K);
   // (checked build: everything but the decode results is dead between batches)
-  chk_poison(S.seq, (uint32_t)smem_block_bytes(T, K) - S.seq, K, warp, lane);
+  chk_poison(S.seq, (uint32_t)(smem_block_bytes(T, K) - smem_c_bytes(T.n_axes, K)), K, warp, lane);
 }
 
 template <int NA, bool P2, bool CP>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
                                            void* __restrict__ out, int64_t row0, int rows, bool compact) {
   const Front fr = batch_front<NA, P2>(T, S, K, warp, lane);
-  batch_back<NA, P2, CP>(T, S, K, warp, lane, valid, fr, out, row0, rows, compact);
+  batch_back<NA, P2, CP>(T, S, K, warp, lane, valid, fr, out, row0, rows, compact, blockIdx.x);
 }
 
 // the block's next batch: with a ticket (dynamic scheduling) the next unclaimed
@@ -1233,7 +1240,175 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
     }
     store_seq_rows(S, out_seqs + row0 * 32, rows, lane);
     }   // warp 0
+    if (T.dd.key) {   // NEXT-3 dedup launch (one warp per block): the front half only
+      const Front fr = batch_front<NA, P2>(T, S, K, warp, lane);
+      dedup_front<NA>(T, S, lane, valid, i, fr);
+      block_sync(K);
+      continue;
+    }
     batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, row0, rows, compact);
+  }
+}
+
+// ---------------------------------------------------------------- NEXT-3: one cost per distinct state
+// "any action sequence yielding the same sharded model resolves
+// to the same unique state".  A dedup rollout launch runs in three kernels:
+//   front    (the rollout kernel with T.dd set, one warp per block): H8, H1,
+//            H2a, H3, H7 per candidate; its class maps (the materialised
+//            state), key, FLOPs and status go to the launch's scratch, and a
+//            lock-free hash set on the key, verified by comparing the class
+//            maps word for word, makes the first candidate of every state its
+//            representative (a 64-bit key collision only costs a duplicate
+//            evaluation, never a wrong record);
+//   back     H2b, H4, H5 (+ the critical path), H6 for the representatives
+//            only, into a compact record list;
+//   scatter  every candidate's record = its representative's (status != 0:
+//            the error record), bit for bit what the one-kernel path writes.
+// word w of a candidate's row of class maps (4 one-byte maps for <= 2 axes, else
+// 2 two-byte maps); entries past the last class are 0 (the row of a state is
+// a function of the state alone)
+template <int NA>
+__device__ __forceinline__ uint32_t mca_word(const DeviceTables& T, const Smem& S, int w, int lane) {
+  uint32_t v = 0;
+  if (NA <= 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * w + k < T.n_mc) v |= (uint32_t)sp<const uint8_t>(S.mca)[(4 * w + k) * 32 + lane] << (8 * k);
+    return v;
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    if (2 * w + k < T.n_mc) v |= (uint32_t)sp<const uint16_t>(S.mca)[(2 * w + k) * 32 + lane] << (16 * k);
+  return v;
+}
+template <int NA>
+__device__ __forceinline__ void dedup_front(const DeviceTables& T, const Smem& S, int lane, bool valid, int64_t i,
+                                            const Front& fr) {
+  const DedupCtx& D = T.dd;
+  const uint32_t rw = D.row_words;
+  const bool live = valid && fr.status == 0;
+  if (valid) {
+    D.key[i] = fr.key;
+    D.flo[i] = fr.flo;
+    D.fhi[i] = fr.fhi;
+    D.status[i] = fr.status;
+    if (!live) D.rep[i] = 0xFFFFFFFFu;
+  }
+  // lanes of this warp with the same key and the same class maps share one
+  // insertion: the lowest such lane (the leader) inserts, the others copy its
+  // answer — a popular state costs one table access per warp, not per lane
+  const unsigned lm = __ballot_sync(FULL, live);
+  const unsigned grp = __match_any_sync(FULL, live ? fr.key : ~0ULL) & lm;
+  const int leader = live ? __ffs(grp) - 1 : lane;
+  bool same_maps = true;
+  for (uint32_t w = 0; w < rw; ++w) {
+    const uint32_t mine = mca_word<NA>(T, S, (int)w, lane);
+    same_maps &= __shfl_sync(FULL, mine, leader) == mine;
+  }
+  const bool follower = live && leader != lane && same_maps;
+  const bool inserter = live && !follower;
+  uint32_t rep = (uint32_t)i;
+  if (inserter) {
+    uint32_t* row = D.rows + (size_t)i * rw;
+    for (uint32_t w = 0; w < rw; ++w) row[w] = mca_word<NA>(T, S, (int)w, lane);
+    __threadfence();   // the row and key are visible before the candidate can be found in the table
+    uint32_t h = (uint32_t)(fr.key ^ (fr.key >> 29) ^ (fr.key >> 47)) & D.cap_mask;
+    for (;;) {
+      uint32_t e = __ldcg(D.table + h);   // a plain read first: most probes find their state already there
+      if (e == 0) e = atomicCAS(D.table + h, 0u, (uint32_t)i + 1u);
+      if (e == 0) {   // the first candidate of its state
+        const uint32_t sl = atomicAdd(D.count, 1u);
+        D.slot[i] = sl;
+        D.rep_of_slot[sl] = (uint32_t)i;
+        break;
+      }
+      const uint32_t r = e - 1u;
+      __threadfence();
+      bool same = __ldcg(D.key + r) == fr.key;
+      for (uint32_t w = 0; w < rw && same; ++w) same = __ldcg(D.rows + (size_t)r * rw + w) == mca_word<NA>(T, S, (int)w, lane);
+      if (same) { rep = r; break; }
+      h = (h + 1u) & D.cap_mask;
+    }
+  }
+  const uint32_t lrep = __shfl_sync(FULL, rep, leader);
+  if (live) D.rep[i] = follower ? lrep : rep;
+}
+
+// a representative's class maps (global rows) into S.mca[c][lane]
+template <int NA>
+__device__ __forceinline__ void load_rep_maps(const DeviceTables& T, const Smem& S, int lane, bool valid, uint32_t i) {
+  const DedupCtx& D = T.dd;
+  const uint32_t rw = D.row_words;
+  for (uint32_t w = 0; w < rw; ++w) {
+    const uint32_t v = valid ? D.rows[(size_t)i * rw + w] : 0xFFFFFFFFu;
+    if (NA <= 2) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((int)(4 * w) + k < T.n_mc) sp<uint8_t>(S.mca)[(4 * w + k) * 32 + lane] = (uint8_t)(v >> (8 * k));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if ((int)(2 * w) + k < T.n_mc) sp<uint16_t>(S.mca)[(2 * w + k) * 32 + lane] = (uint16_t)(v >> (16 * k));
+    }
+  }
+}
+
+// The representatives' back halves.  Their count is known on the device only,
+// so a block of W warps decides at run time: with at least one batch per warp
+// of the grid, its warps run independently (one-warp layout each, one batch
+// each at a time — the throughput mode); with fewer, its W warps share one
+// batch (the latency mode of small launches, as pick_k does for K1/K2).
+template <int NA, bool P2, bool CP>
+__global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS), (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS))
+toast_dedup_back_kernel(const DeviceTables T, void* __restrict__ out, bool compact) {
+  const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const DedupCtx& D = T.dd;
+  const int64_t nrep = (int64_t)*D.count, nb = (nrep + 31) / 32;
+  if (nb >= (int64_t)gridDim.x * W) {   // independent warps, each with its own one-warp layout and scratch
+    const Smem S = smem_at(block_smem(T, 1), (uint32_t)warp * (uint32_t)smem_block_bytes(T, 1));
+    for (int64_t b = (int64_t)blockIdx.x * W + warp; b < nb; b += (int64_t)gridDim.x * W) {
+      const int64_t row0 = b * 32;
+      const int rows = (int)(nrep - row0 < 32 ? nrep - row0 : 32);
+      const bool valid = lane < rows;
+      const uint32_t i = valid ? D.rep_of_slot[row0 + lane] : 0u;
+      block_sync(1);
+      load_rep_maps<NA>(T, S, lane, valid, i);
+      const Front fr{valid ? D.key[i] : 0ULL, valid ? D.flo[i] : 0ULL, valid ? D.fhi[i] : 0ULL, 0u};
+      batch_back<NA, P2, CP>(T, S, 1, 0, lane, valid, fr, out, row0, rows, compact, (int64_t)blockIdx.x * W + warp);
+    }
+  } else {                               // the block's warps share each batch
+    const Smem S = block_smem(T, W);
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+      const int64_t row0 = b * 32;
+      const int rows = (int)(nrep - row0 < 32 ? nrep - row0 : 32);
+      const bool valid = lane < rows;
+      const uint32_t i = valid ? D.rep_of_slot[row0 + lane] : 0u;
+      block_sync(W);
+      if (warp == 0) load_rep_maps<NA>(T, S, lane, valid, i);
+      // warp 0 carries the key / FLOP total (the warps' partials are summed), the others add nothing
+      const Front fr{(valid && warp == 0) ? D.key[i] : 0ULL, (valid && warp == 0) ? D.flo[i] : 0ULL,
+                     (valid && warp == 0) ? D.fhi[i] : 0ULL, 0u};
+      batch_back<NA, P2, CP>(T, S, W, warp, lane, valid, fr, out, row0, rows, compact, (int64_t)blockIdx.x * W);
+    }
+  }
+}
+
+// every candidate's record from its representative's (16-B words, coalesced)
+__global__ void toast_dedup_scatter_kernel(const DedupCtx D, int64_t n, const uint4* __restrict__ recs,
+                                           uint4* __restrict__ out, int words) {
+  const int64_t total = n * words;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / words;
+    const int w = (int)(q - i * words);
+    const uint32_t r = D.rep[i];
+    uint4 v;
+    if (r == 0xFFFFFFFFu) {   // an invalid candidate: NaN | status (16-B score) or status alone (256-B record)
+      const uint32_t st = D.status[i];
+      v = words == 1 ? make_uint4(0u, 0x7FF80000u, st, 0u) : (w == 2 ? make_uint4(0u, 0u, st, 0u) : make_uint4(0u, 0u, 0u, 0u));
+    } else {
+      v = __ldg(recs + (size_t)D.slot[r] * words + w);
+    }
+    out[q] = v;
   }
 }
 
@@ -1267,6 +1442,8 @@ __global__ void toast_round_reduce_kernel(const toast_cost* __restrict__ lcost, 
   }
   out[l].reward_sum = sum;
   out[l].best = best;
+  out[l].leaf_status = lcost[l].status;
+  out[l].leaf_key = lcost[l].state_key;
   if (bc) {
     out[l].cost = *bc;
     for (int i = 0; i < 32; ++i) out[l].seq[i] = bs[i];
@@ -1277,6 +1454,7 @@ template <int NA, bool P2, bool CP>
 void set_smem_attr(int bytes) {
   cudaFuncSetAttribute(toast_eval_kernel<NA, P2, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(toast_rollout_kernel<NA, P2, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(toast_dedup_back_kernel<NA, P2, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 // call f.template operator()<NA, P2, CP>() for the analysis' (axis count,
@@ -1426,6 +1604,21 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     a->occ_eval[i] = be;
     a->occ_roll[i] = br;
   }
+  {   // the dedup back kernel: blocks of the largest W <= 8 warps whose layouts fit
+    a->back_warps = 1;
+    a->occ_back = 1;
+    const int max_threads = T.cost_model == TOAST_COST_CRITICAL_PATH ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS;
+    for (int W = 8; W >= 1; W /= 2) {
+      const int sm = std::max(W * smem_block_bytes(T, 1), smem_block_bytes(T, W));
+      if (sm > dev_smem || 32 * W > max_threads) continue;
+      int bb = 0;
+      cudaError_t e = dispatch(T, [&]<int NA, bool P2, bool CP>() {
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, toast_dedup_back_kernel<NA, P2, CP>, 32 * W, sm);
+      });
+      TOAST_CUDA(e);
+      if (bb >= 1) { a->back_warps = W; a->occ_back = bb; break; }
+    }
+  }
   if (a->occ_eval[0] < 1 || a->occ_roll[0] < 1) { err = "kernels cannot be resident"; return TOAST_E_LIMIT; }
   // throughput K: the most resident warps per SM (sharing one signature table
   // between K warps saves shared memory), ties to the smaller K
@@ -1558,9 +1751,75 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   return TOAST_OK;
 }
 
+// NEXT-3 dedup launch: front (rollout kernel, one warp per block) -> back
+// (representatives only) -> scatter; all scratch stream-ordered from the pool
+static toast_status launch_rollout_dedup(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed,
+                                         uint64_t id_base, uint16_t* d_seqs, void* d_out, cudaStream_t st,
+                                         std::string& err, int64_t rep, bool compact) {
+  const DeviceTables& T0 = a->dt;
+  DeviceTables T = T0;
+  const uint32_t rw = (uint32_t)(T.n_axes <= 2 ? (T.n_mc + 3) / 4 : (T.n_mc + 1) / 2);
+  uint32_t cap = 64;
+  while ((int64_t)cap < 2 * n) cap <<= 1;
+  const size_t rec = compact ? sizeof(toast_score) : sizeof(toast_cost);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t b_u64 = al((size_t)n * 8), b_u32 = al((size_t)n * 4), b_rows = al((size_t)n * rw * 4);
+  const size_t b_tab = al((size_t)cap * 4), b_rec = al((size_t)n * rec);
+  const size_t bytes = 3 * b_u64 + 4 * b_u32 + b_rows + b_tab + 256 + b_rec;
+  char* base = nullptr;
+  TOAST_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&base), bytes, (cudaMemPool_t)a->cp_pool, st));
+  char* q = base;
+  DedupCtx& D = T.dd;
+  D.key = reinterpret_cast<uint64_t*>(q); q += b_u64;
+  D.flo = reinterpret_cast<uint64_t*>(q); q += b_u64;
+  D.fhi = reinterpret_cast<uint64_t*>(q); q += b_u64;
+  D.status = reinterpret_cast<uint32_t*>(q); q += b_u32;
+  D.rep = reinterpret_cast<uint32_t*>(q); q += b_u32;
+  D.slot = reinterpret_cast<uint32_t*>(q); q += b_u32;
+  D.rep_of_slot = reinterpret_cast<uint32_t*>(q); q += b_u32;
+  D.rows = reinterpret_cast<uint32_t*>(q); q += b_rows;
+  D.table = reinterpret_cast<uint32_t*>(q);
+  D.count = reinterpret_cast<unsigned int*>(q + b_tab);
+  void* recs = q + b_tab + 256;
+  D.cap_mask = cap - 1;
+  D.row_words = rw;
+  TOAST_CUDA(cudaMemsetAsync(D.table, 0, b_tab + 256, st));   // the table and the counter
+  // front: the rollout kernel, one warp per block
+  const int64_t batches = (n + 31) / 32;
+  const int64_t fblocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[0] * a->n_sms));
+  const size_t sm1 = (size_t)smem_block_bytes(T0, 1);
+  dispatch(T, [&]<int NA, bool P2, bool CP>() {
+    toast_rollout_kernel<NA, P2, CP><<<dim3((unsigned)fblocks), dim3(32), sm1, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep, compact);
+    return 0;
+  });
+  TOAST_CUDA(cudaGetLastError());
+  // back: the representatives (their count is on the device: a full grid of W-warp blocks)
+  const int W = a->back_warps;
+  const int64_t bblocks = std::max<int64_t>(1, std::min<int64_t>((batches + W - 1) / W, (int64_t)a->occ_back * a->n_sms));
+  DeviceTables TB = T;
+  if (TB.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, bblocks * W, st, &TB.cp_scratch));
+  const size_t smb = (size_t)std::max(W * smem_block_bytes(T0, 1), smem_block_bytes(T0, W));
+  dispatch(TB, [&]<int NA, bool P2, bool CP>() {
+    toast_dedup_back_kernel<NA, P2, CP><<<dim3((unsigned)bblocks), dim3(32 * W), smb, st>>>(TB, recs, compact);
+    return 0;
+  });
+  TOAST_CUDA(cudaGetLastError());
+  if (TB.cp_scratch) TOAST_CUDA(cudaFreeAsync(TB.cp_scratch, st));
+  // scatter
+  const int words = (int)(rec / 16);
+  const int64_t thr = n * words;
+  const int sblocks = (int)std::min<int64_t>((thr + 255) / 256, (int64_t)a->n_sms * 16);
+  toast_dedup_scatter_kernel<<<sblocks, 256, 0, st>>>(D, n, reinterpret_cast<const uint4*>(recs),
+                                                       reinterpret_cast<uint4*>(d_out), words);
+  TOAST_CUDA(cudaGetLastError());
+  TOAST_CUDA(cudaFreeAsync(base, st));
+  return TOAST_OK;
+}
+
 toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
                             uint16_t* d_seqs, void* d_out, void* stream, std::string& err, int64_t rep, bool compact) {
   if (n <= 0) return TOAST_OK;
+  if (a->dedup) return launch_rollout_dedup(a, d_pre, n, seed, id_base, d_seqs, d_out, (cudaStream_t)stream, err, rep, compact);
   const int64_t batches = (n + 31) / 32;
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));

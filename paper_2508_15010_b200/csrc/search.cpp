@@ -9,11 +9,13 @@
 // all-gathers the records (torch.distributed / NCCL) and imports them.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "toast_internal.h"
@@ -40,6 +42,7 @@ struct toast_search_state {
   int32_t rank = 0, world = 1;
   uint64_t seed = 0;
   toast::SNode* root = nullptr;
+  std::unordered_map<uint64_t, toast::SNode*> states;   // transpositions (R24): state key -> the node holding it
   // local incumbent (reset to the global one after each import) and global incumbent
   toast_cost best{};
   uint16_t best_seq[32] = {0};
@@ -116,6 +119,7 @@ toast_status search_begin(const toast_analysis* a, const toast_search_opts* o, i
   s->t_start = std::chrono::steady_clock::now();
   s->root = new SNode();
   s->root->untried = legal_after(a, s->root->prefix);
+  s->states[a->baseline.state_key] = s->root;   // the unsharded module (key 0)
   s->best = a->baseline;              // the unsharded root is the first incumbent
   memset(s->best_seq, 0, sizeof s->best_seq);
   s->gbest = s->best;
@@ -232,6 +236,27 @@ toast_status search_round(toast_search_state* s, void* export_buf, std::string& 
     if (rr.best != -2 && better(rr.cost, rr.seq, s->best, s->best_seq)) {
       s->best = rr.cost;
       memcpy(s->best_seq, rr.seq, 64);
+    }
+  }
+  // reading R24 ("any action sequence yielding the same sharded
+  // model resolves to the same unique state, eliminating duplication by
+  // construction"): with transpositions on, the tree holds each materialised
+  // state once — a selected leaf whose exactly evaluated state another node
+  // already holds leaves the tree (its rewards stay backed up on its path)
+  if (s->o.transpositions) {
+    std::vector<SNode*> gone;
+    for (int l = 0; l < L; ++l) {
+      const LeafRed& rr = s->h_red[l];
+      if (rr.leaf_status != 0) continue;
+      SNode* lf = leaves[l];
+      auto it = s->states.find(rr.leaf_key);
+      if (it == s->states.end()) s->states.emplace(rr.leaf_key, lf);
+      else if (it->second != lf && std::find(gone.begin(), gone.end(), lf) == gone.end()) gone.push_back(lf);
+    }
+    for (SNode* g : gone) {
+      auto& ch = g->parent->children;
+      ch.erase(std::find(ch.begin(), ch.end(), g));
+      delete g;
     }
   }
   s->evals += (int64_t)L * (R + 1);

@@ -205,10 +205,27 @@ static_assert(sizeof(KSig) == 64 && sizeof(KPoint) == 16 && sizeof(KUse) == 16 &
 struct LeafRed {
   double reward_sum;     // sum of the leaf's R+1 rewards (-score), in order (R16)
   int32_t best;          // -1 = the leaf's own state, j = rollout j, -2 = none valid
-  int32_t pad;
-  uint64_t pad2;
+  uint32_t leaf_status;  // the leaf's own state: status and key (transpositions, reading R24)
+  uint64_t leaf_key;
   toast_cost cost;       // the leaf's best record
   uint16_t seq[32];      // and its sequence
+};
+
+// NEXT-3 in-launch dedup (toast_nda_opts.dedup): per launch, scratch for the
+// front kernel's per-candidate results, the hash set of distinct states and
+// the compact list of their representatives (kernels.cu "dedup")
+struct DedupCtx {
+  uint64_t* key = nullptr;        // [n] state key (H7); null: dedup off
+  uint64_t* flo = nullptr;        // [n] FLOP total, low / high word (H3)
+  uint64_t* fhi = nullptr;
+  uint32_t* status = nullptr;     // [n] decode status (H1)
+  uint32_t* rep = nullptr;        // [n] the candidate whose state this is (itself if first), ~0u if invalid
+  uint32_t* slot = nullptr;       // [n] a representative's index in the compact list
+  uint32_t* rep_of_slot = nullptr;// [n] the compact list
+  uint32_t* rows = nullptr;       // [n][row_words] the class maps (the materialised state)
+  uint32_t* table = nullptr;      // [cap] candidate + 1 (0 = empty), open addressing on the key
+  unsigned int* count = nullptr;  // [1] representatives
+  uint32_t cap_mask = 0, row_words = 0;
 };
 
 // signature role word: acolor [0,10) | div_ok [10,26) | deselection class [26,34)
@@ -240,6 +257,7 @@ struct DeviceTables {
   const KCpComp* cp_comp = nullptr;      // sig holds the op's class
   double* cp_scratch = nullptr;  // per launched block: [cp_stride][32] doubles (allocated per launch)
   unsigned int* ticket = nullptr; // per launch: the next batch counter (dynamic batch scheduling; null: static)
+  DedupCtx dd;                    // per launch (dedup launches only)
   int32_t sizes[4];
   double bw[4];
   double F, C, t0;
@@ -320,6 +338,9 @@ struct toast_analysis {
   int32_t occ_eval[4] = {0, 0, 0, 0}, occ_roll[4] = {0, 0, 0, 0};   // blocks per SM for K = 1, 2, 4, 8
   int32_t n_sms = 0, k_throughput = 1;
   int32_t k_force = 0;   // autotune: every launch uses this K (0: pick)
+  int32_t dedup = 0;     // NEXT-3: rollout launches cost each distinct state once
+  int32_t occ_back = 1;  // resident blocks per SM of the dedup back kernel
+  int32_t back_warps = 1;  // ... and its warps per block
   void* pipe_stream[toast::PIPE_STREAMS] = {};      // host-buffer path: chunked H2D / kernel / D2H overlap
   // search buffers, kept between searches (a search that finds them in use allocates its own)
   struct SearchPool {

@@ -58,7 +58,7 @@ class _Machine(ctypes.Structure):
 
 class _NdaOpts(ctypes.Structure):
     _fields_ = [("min_unique_dims", ctypes.c_int32), ("max_depth", ctypes.c_int32), ("cost_model", ctypes.c_int32),
-                ("conflict_grouping", ctypes.c_int32)]
+                ("conflict_grouping", ctypes.c_int32), ("dedup", ctypes.c_int32)]
 
 
 COST_SUM, COST_CRITICAL_PATH = 0, 1
@@ -73,7 +73,7 @@ class _ActionInfo(ctypes.Structure):
 class _SearchOpts(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("max_evals", ctypes.c_int64), ("time_limit_s", ctypes.c_double),
                 ("leaves_per_round", ctypes.c_int32), ("rollouts_per_leaf", ctypes.c_int32),
-                ("patience", ctypes.c_int32), ("pad0", ctypes.c_int32), ("uct_c", ctypes.c_double),
+                ("patience", ctypes.c_int32), ("transpositions", ctypes.c_int32), ("uct_c", ctypes.c_double),
                 ("target_score", ctypes.c_double), ("cuda_stream", ctypes.c_void_p)]
 
 
@@ -246,18 +246,19 @@ class Analysis:
 
 
 def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30, cost_model: int = COST_SUM,
-        grouping: int = GROUP_COMPAT) -> Analysis:
-    """toast_nda (H0).  grouping: GROUP_COMPAT (C4/C5) or GROUP_CONTRACTION (reading R23)."""
-    o = _NdaOpts(int(min_unique_dims), int(max_depth), int(cost_model), int(grouping))
+        grouping: int = GROUP_COMPAT, dedup: int = 0) -> Analysis:
+    """toast_nda (H0).  grouping: GROUP_COMPAT (C4/C5) or GROUP_CONTRACTION (reading R23);
+    dedup: 1 = rollout launches cost each distinct state once (NEXT-3, same results)."""
+    o = _NdaOpts(int(min_unique_dims), int(max_depth), int(cost_model), int(grouping), int(dedup))
     h = _P()
     _check(_lib.toast_nda(graph._h, ctypes.byref(o), ctypes.byref(h)))
     return Analysis(h, None)
 
 
 def build_analysis(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c=100.0, min_unique_dims=10,
-                   max_depth=30, cuda_device=0, cost_model=COST_SUM, grouping=GROUP_COMPAT) -> Analysis:
+                   max_depth=30, cuda_device=0, cost_model=COST_SUM, grouping=GROUP_COMPAT, dedup=0) -> Analysis:
     g = load_graph(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c, cuda_device)
-    a = nda(g, min_unique_dims, max_depth, cost_model, grouping)
+    a = nda(g, min_unique_dims, max_depth, cost_model, grouping, dedup)
     a.axes = list(axes)
     return a
 
@@ -343,10 +344,11 @@ class SearchOptions:
     patience: int = 1
     uct_c: float = math.sqrt(2.0)
     target_score: float = float("nan")
+    transpositions: int = 0   # 1: each materialised state once in the tree (reading R24)
 
     def c(self, stream):
         return _SearchOpts(int(self.seed), int(self.max_evals), float(self.time_limit_s), int(self.leaves_per_round),
-                           int(self.rollouts_per_leaf), int(self.patience), 0, float(self.uct_c),
+                           int(self.rollouts_per_leaf), int(self.patience), int(self.transpositions), float(self.uct_c),
                            float(self.target_score), _stream(stream))
 
 

@@ -78,6 +78,23 @@ def main():
                     sys.exit(1)
                 done += 1
                 del a
+        # the dedup pipeline (front / back / scatter kernels), both cost models
+        for cm in (T.COST_SUM, T.COST_CRITICAL_PATH):
+            os.environ.pop("TOAST_FORCE_K", None)
+            o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cost_model=cm)
+            o_seqs, oc = o.rollout(np.zeros((n, 32), np.uint16), seed=5, id_base=0)
+            a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth,
+                                 cuda_device=0, cost_model=cm, dedup=1)
+            pre = torch.zeros((n, 32), dtype=torch.int16, device="cuda")
+            seqs = torch.empty_like(pre)
+            out = torch.empty((n, 256), dtype=torch.uint8, device="cuda")
+            T.rollout_batch(a, pre, 5, 0, seqs, out)
+            torch.cuda.synchronize()
+            ok = np.array_equal(seqs.cpu().numpy().view(np.uint16), o_seqs) and T.as_costs(out).tobytes() == oc.tobytes()
+            print(f"{name} cost_model={cm} dedup: {'ok' if ok else 'MISMATCH'}", flush=True)
+            if not ok:
+                sys.exit(1)
+            done += 1
     os.environ.pop("TOAST_FORCE_K", None)
     print(f"sanitize driver: {done} (config, cost model, K) runs, all bit-identical to the oracle")
 

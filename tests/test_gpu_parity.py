@@ -232,6 +232,15 @@ def test_search_trace_parity(name, dm):
     same rounds, evaluation count and best state."""
     T = _T()
     a, o = setup(name, dm=dm) if dm else setup(name)
+    for tp in (0, 1):   # a tree of sequences, and with transpositions (reading R24)
+        opts = T.SearchOptions(seed=3, max_evals=3000, leaves_per_round=4, rollouts_per_leaf=8, patience=3,
+                               transpositions=tp)
+        r = T.search(a, opts)
+        ro, _ = o.search(seed=3, max_evals=3000, L=4, R=8, patience=3, transpositions=tp)
+        assert int(r["rounds"]) == int(ro["rounds"]), tp
+        assert int(r["evals"]) == int(ro["evals"]), tp
+        assert np.array_equal(r["best_seq"], ro["best_seq"]), tp
+        assert r["best"]["score"] == ro["best"]["score"], tp
     opts = T.SearchOptions(seed=3, max_evals=3000, leaves_per_round=4, rollouts_per_leaf=8, patience=3)
     r = T.search(a, opts)
     ro, _ = o.search(seed=3, max_evals=3000, L=4, R=8, patience=3)
@@ -600,7 +609,7 @@ def test_checked_library_race_and_bounds():
                        env=dict(os.environ, TOAST_LIB=B.LIB_CHECKED), timeout=1500)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "all bit-identical to the oracle" in r.stdout
-    assert r.stdout.count(": ok") == 8 * 2 * 4
+    assert r.stdout.count(": ok") == 8 * 2 * 4 + 8 * 2
 
 
 def test_checked_library_catches_a_planted_race():
@@ -618,3 +627,76 @@ def test_checked_library_catches_a_planted_race():
     assert r.returncode != 0, r.stdout[-2000:]
     assert "gpt2 cost_model=0 K=1: ok" in r.stdout          # one-warp blocks never needed that barrier
     assert "gpt2 cost_model=0 K=2: ok" not in r.stdout      # the first multi-warp run is caught
+
+
+_dd_cache = {}
+
+
+def setup_dedup(name, cost_model=0):
+    key = (name, cost_model)
+    if key not in _dd_cache:
+        T = _T()
+        c = configs.get(name)
+        a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0,
+                             cost_model=cost_model, dedup=1)
+        o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cost_model=cost_model)
+        _dd_cache[key] = (a, o)
+    return _dd_cache[key]
+
+
+@pytest.mark.parametrize("cost_model", [0, 1])
+@pytest.mark.parametrize("name", ["mlp_c", "gpt2", "gpt2_np2", "gpt2_3ax", "gpt2_3ax_np2", "gpt2_4ax_np2", "gpt2_1ax_np2",
+                                  "unet", "gns16"])
+def test_dedup_rollouts_bit_identical(name, cost_model):
+    """NEXT-3: with dedup on, a rollout launch costs each distinct
+    materialised state once and copies its record to every candidate that
+    reached it — sequences and records bit-identical to the oracle's, with
+    prefixes, a bad prefix (its error record) and a ragged tail, full and
+    compact records, device and pinned-host buffers."""
+    import torch
+    T = _T()
+    a, o = setup_dedup(name, cost_model)
+    n = 3001 if name not in ("unet", "gns16") else 601
+    pre = np.zeros((n, 32), np.uint16)
+    s0, _ = o.rollout(np.zeros((n // 2, 32), np.uint16), seed=41)
+    for i in range(n // 2):
+        pre[i, :i % 3] = s0[i, :i % 3]
+    pre[7, 0] = 60000                     # a bad id: the error record
+    os_, oc = o.rollout(pre, seed=12, id_base=99, threads=8)
+    gs, gc = gpu_rollout(a, pre, 12, 99)
+    assert np.array_equal(gs, os_)
+    assert_same(gc, oc, (name, cost_model, "dedup"))
+    assert len(np.unique(oc["state_key"][oc["status"] == 0])) < n   # there were duplicates to share
+    # compact records through the pinned host pipeline
+    h_pre = torch.from_numpy(pre.view(np.int16)).pin_memory()
+    h_seq = torch.empty_like(h_pre).pin_memory()
+    h_sc = torch.empty((n, 16), dtype=torch.uint8).pin_memory()
+    T.rollout_scores(a, h_pre, 12, 99, h_seq, h_sc)
+    sc = T.as_scores(h_sc)
+    ok = oc["status"] == 0
+    assert np.array_equal(h_seq.numpy().view(np.uint16), os_)
+    assert (sc["score"][ok].view(np.uint64) == oc["score"][ok].view(np.uint64)).all()
+    assert (sc["state_key"][ok] == oc["state_key"][ok]).all()
+    assert np.isnan(sc["score"][~ok]).all() and (sc["state_key"][~ok] == oc["status"][~ok]).all()
+
+
+def test_dedup_full_size_and_search():
+    """GPT-24 at the bench's launch size with dedup: sampled rows equal the
+    oracle's, every row equals the one-kernel path's; a search with dedup on
+    follows the same trajectory as without (same evals, rounds, best)."""
+    T = _T()
+    a, o = setup_dedup("gpt24")
+    a1, _ = setup("gpt24")
+    wave = a1.preferred_batch()
+    n = max(wave, ((1 << 18) // wave) * wave)
+    gs, gc = gpu_rollout(a, np.zeros((n, 32), np.uint16), 2024, 0)
+    gs1, gc1 = gpu_rollout(a1, np.zeros((n, 32), np.uint16), 2024, 0)
+    assert np.array_equal(gs, gs1) and gc.tobytes() == gc1.tobytes()
+    for i in np.random.default_rng(3).choice(n, size=16, replace=False):
+        s1, c1 = o.rollout(np.zeros((1, 32), np.uint16), seed=2024, id_base=int(i))
+        assert np.array_equal(gs[i], s1[0])
+        assert_same(gc[i:i + 1], c1, f"row {i}")
+    opts = T.SearchOptions(seed=1, max_evals=200000, leaves_per_round=16, rollouts_per_leaf=64, patience=3)
+    r, r1 = T.search(a, opts), T.search(a1, opts)
+    assert int(r["evals"]) == int(r1["evals"]) and int(r["rounds"]) == int(r1["rounds"])
+    assert r["best"].tobytes() == r1["best"].tobytes() and np.array_equal(r["best_seq"], r1["best_seq"])

@@ -465,25 +465,65 @@ def test_rollout_depth_and_legality():
 
 
 # --------------------------------------------------------------------------- C16/C17
-def test_search_reaches_bruteforce_optimum_mlp_c():
-    """MCTS best equals the exhaustive optimum at desk scale."""
+@pytest.mark.parametrize("tp", [0, 1])
+def test_search_reaches_bruteforce_optimum_mlp_c(tp):
+    """MCTS best equals the exhaustive optimum at desk scale
+    (as a tree of sequences, and with transpositions, reading R24)."""
     c = configs.get("mlp_c")
     o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims)
     n, best, bc = o.bruteforce()
     assert n > 1000
-    r, trace = o.search(seed=0, max_evals=4000, L=4, R=8, patience=4)
+    r, trace = o.search(seed=0, max_evals=4000, L=4, R=8, patience=4, transpositions=tp)
     assert r["best"]["score"] == bc["score"]
     assert np.all(np.diff(trace) <= 0)
 
 
+@pytest.mark.parametrize("tp", [0, 1])
 @pytest.mark.parametrize("dm", [1 << 40, 700, 400])
-def test_search_reaches_bruteforce_optimum_attn(dm):
+def test_search_reaches_bruteforce_optimum_attn(dm, tp):
     """toy attention with DM below the unsharded peak forces sharding."""
     c = configs.get("attn_toy")
     o = Oracle(c.ir, c.axes, c.flops_per_sec, dm, c.penalty_c, c.min_dims)
     n, best, bc = o.bruteforce()
-    r, _ = o.search(seed=1, max_evals=4000, L=4, R=8, patience=4)
+    r, _ = o.search(seed=1, max_evals=4000, L=4, R=8, patience=4, transpositions=tp)
     assert r["best"]["score"] == bc["score"]
+
+
+def test_transpositions_keep_each_state_once():
+    """Reading R24 ("any action sequence yielding the same sharded
+    model resolves to the same unique state"): on MLP-c, whose 3,849 legal
+    sequences reach far fewer distinct states, a search with transpositions
+    spends its rounds on distinct states — it reaches the exhaustive optimum
+    with no more evaluations than the tree of sequences, and the exhaustive
+    count of distinct states (by state key) is well below the sequence count."""
+    c = configs.get("mlp_c")
+    o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims)
+    n, best, bc = o.bruteforce()
+    # every legal sequence's state key (the exhaustive enumeration of C17 restated as a DFS here)
+    acts = o.dump()["actions"]
+    groups = [sc[2] for sc in o.dump()["scolors"]]
+
+    def kills(x, y):
+        cx, rx, ax = acts[x - 1]
+        cy, ry, ay = acts[y - 1]
+        if cx == cy and ax == ay:
+            return True
+        return any(gx == gy and ((rx >> i) ^ (ry >> j)) & 1 for i, gx in enumerate(groups[cx])
+                   for j, gy in enumerate(groups[cy]))
+    seqs = []
+
+    def dfs(seq, legal):
+        seqs.append(seq)
+        for x in legal:
+            dfs(seq + [x], [y for y in legal if not kills(x, y)])
+    dfs([], list(range(1, len(acts) + 1)))
+    keys = o.eval(Oracle.seqs(seqs))["state_key"]
+    assert len(seqs) == n and len(np.unique(keys)) < len(seqs) // 4
+    r0, _ = o.search(seed=0, max_evals=100000, L=4, R=8, patience=1000, target_score=float(bc["score"]))
+    r1, _ = o.search(seed=0, max_evals=100000, L=4, R=8, patience=1000, target_score=float(bc["score"]),
+                     transpositions=1)
+    assert r1["hit_target"] and r0["hit_target"]
+    assert int(r1["evals"]) <= int(r0["evals"])
 
 
 # --------------------------------------------------------------------------- parser errors
