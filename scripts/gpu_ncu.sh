@@ -2,7 +2,7 @@
 # The throughput K and residency measured by toast_nda are pinned (TOAST_FORCE_K, TOAST_FORCE_BLOCKS) for the profiled runs: under ncu's replay the
 # measurement itself would be distorted.
 C=${1:-gpt24}
-CMD="python bench.py --config $C --steps 3 --warmup 3 --no-search --no-cpu-baseline"
+CMD="python bench.py --config $C --steps 3 --warmup 3 --no-search --no-cpu-baseline --no-variants"
 $CMD > gpurun_out/plain_$C.log 2>&1 && \
 export TOAST_FORCE_K=$(python -c "import json;print(json.loads(open('gpurun_out/plain_$C.log').read().strip().splitlines()[-1])['config']['warps_per_batch'])") && \
 export TOAST_FORCE_BLOCKS=$(python -c "import json;print(json.loads(open('gpurun_out/plain_$C.log').read().strip().splitlines()[-1])['config']['blocks_per_sm'])") && \

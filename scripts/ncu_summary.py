@@ -42,6 +42,13 @@ out.update({
     "warps_active_pct": float(M["sm__warps_active.avg.pct_of_peak_sustained_active"][0]),
     "registers": int(float(M["launch__registers_per_thread"][0])),
     "smem_wavefronts": float(M["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][0].replace(",", "")),
+    "alu_pipe_pct": float(M["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"][0]),
+    "fma_pipe_pct": float(M["sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"][0]),
+    "lsu_pipe_pct": float(M["sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"][0]),
+    "thread_inst_per_inst": float(M["smsp__thread_inst_executed_per_inst_executed.ratio"][0]),
+    "theoretical_occupancy_pct": float(M["sm__maximum_warps_per_active_cycle_pct"][0]),
+    "occupancy_limit_registers": float(M["launch__occupancy_limit_registers"][0]),
+    "occupancy_limit_shared_mem": float(M["launch__occupancy_limit_shared_mem"][0]),
     "report": os.path.basename(rep), "round": tag,
 })
 # evaluations in the captured launch: the bench line of the same run (plain_<cfg>.log)

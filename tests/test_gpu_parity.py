@@ -700,3 +700,67 @@ def test_dedup_full_size_and_search():
     r, r1 = T.search(a, opts), T.search(a1, opts)
     assert int(r["evals"]) == int(r1["evals"]) and int(r["rounds"]) == int(r1["rounds"])
     assert r["best"].tobytes() == r1["best"].tobytes() and np.array_equal(r["best_seq"], r1["best_seq"])
+
+
+def _root_parallel_worker(rank, world, port, out_dir):
+    import json
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_15010_b200 import parallel as P
+        from paper_2508_15010_b200 import toast as T
+        import torch
+        torch.cuda.set_device(0)
+        c = configs.get("gpt2")
+        a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0)
+        opts = T.SearchOptions(seed=11, max_evals=60000, leaves_per_round=8, rollouts_per_leaf=32, patience=4)
+        st = T.SearchState(a, opts, rank, world)
+        own = None
+        rounds = 0
+        while True:                        # the library's own rounds, exchanged over gloo
+            rec = st.round()
+            own = rec.copy()
+            stop = st.import_(P.all_gather_bytes(rec))
+            rounds += 1
+            if stop:
+                break
+        summed = st.root_stats()
+        res = st.end()
+        hdr = P.EXPORT_DTYPE.itemsize
+        own_root = own[hdr:].view(T.ROOT_STAT_DTYPE)
+        json.dump({"best_seq": [int(x) for x in res["best_seq"]], "score": float(res["best"]["score"]),
+                   "best_bytes": res["best"].tobytes().hex(), "evals": int(res["evals"]), "rounds": rounds,
+                   "summed_visits": summed["visits"].tolist(), "summed_values": summed["value_sum"].tolist(),
+                   "own_visits": own_root["visits"].tolist(), "own_values": own_root["value_sum"].tolist()},
+                  open(os.path.join(out_dir, f"rank{rank}.json"), "w"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_root_parallel_search_two_ranks_library_rounds(tmp_path):
+    """Root-parallel search ("many trajectories in
+    parallel") with the library's own rounds on two ranks (two processes on
+    cuda:0, gloo between them; the ranks' kernels never wait on each other):
+    every rank ends with the same global best, the root statistics every rank
+    reports are the sum of the ranks' own, and the best is the oracle's score
+    for its sequence."""
+    import json
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_root_parallel_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r = [json.load(open(tmp_path / f"rank{k}.json")) for k in range(2)]
+    assert r[0]["best_seq"] == r[1]["best_seq"] and r[0]["best_bytes"] == r[1]["best_bytes"]
+    assert r[0]["evals"] == r[1]["evals"] and r[0]["rounds"] == r[1]["rounds"]
+    assert r[0]["summed_visits"] == r[1]["summed_visits"]
+    assert r[0]["summed_visits"] == [x + y for x, y in zip(r[0]["own_visits"], r[1]["own_visits"])]
+    assert r[0]["summed_values"] == [x + y for x, y in zip(r[0]["own_values"], r[1]["own_values"])]
+    assert r[0]["own_values"] != r[1]["own_values"]          # the ranks' rollouts differ (seed + rank)
+    _, o = setup("gpt2")
+    c = o.eval(np.array([r[0]["best_seq"]], np.uint16))[0]
+    assert c["status"] == 0 and float(c["score"]) == r[0]["score"]
