@@ -35,6 +35,8 @@ def main(argv=None) -> int:
     p.add_argument("--min-dims", type=int, default=10, help="P:1417 minimum value dims per super-color")
     p.add_argument("--cost-model", choices=["sum", "cp"], default="sum", help="G14 straight-line sum or R22 critical path")
     p.add_argument("--grouping", choices=["compat", "contraction"], default="compat", help="C4/C5 or R23")
+    p.add_argument("--dedup", action="store_true", help="cost each distinct state of a rollout launch once (NEXT-3)")
+    p.add_argument("--transpositions", action="store_true", help="each materialised state once in the tree (R24)")
     p.add_argument("--budget", type=int, default=2_000_000, help="evaluations")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-program", action="store_true", help="do not print the lowered program")
@@ -53,9 +55,11 @@ def main(argv=None) -> int:
         axes, flops, dm, pen, min_dims = _mesh(args.mesh), args.flops, int(args.dm), args.penalty, args.min_dims
     a = T.build_analysis(ir, axes, flops, int(dm), pen, min_dims, 30, cuda_device=0,
                          cost_model=T.COST_CRITICAL_PATH if args.cost_model == "cp" else T.COST_SUM,
-                         grouping=T.GROUP_CONTRACTION if args.grouping == "contraction" else T.GROUP_COMPAT)
+                         grouping=T.GROUP_CONTRACTION if args.grouping == "contraction" else T.GROUP_COMPAT,
+                         dedup=int(args.dedup))
     acts = a.actions()
-    r = T.search(a, T.SearchOptions(seed=args.seed, max_evals=args.budget, patience=1 << 30))
+    r = T.search(a, T.SearchOptions(seed=args.seed, max_evals=args.budget, patience=1 << 30,
+                                    transpositions=int(args.transpositions)))
     best = r["best"]
     seq = [int(x) for x in r["best_seq"] if x]
     print(f"evaluations {int(r['evals'])} in {int(r['rounds'])} rounds, {float(r['wall_s']) * 1e3:.2f} ms")
