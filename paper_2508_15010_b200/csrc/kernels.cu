@@ -233,6 +233,13 @@ __device__ __forceinline__ uint32_t dcode(const DeviceTables& T, uint32_t S) {
   // kernel-parameter array would serialise across lanes)
   return P2 ? (uint32_t)(T.shift_pack >> (4 * S)) & 15u : S;
 }
+// the same for a mesh of NA axes: the subsets of up to 3 axes fit the word's
+// low 32 bits (a 32-bit shift)
+template <bool P2, int NA>
+__device__ __forceinline__ uint32_t dcode_na(const DeviceTables& T, uint32_t S) {
+  if (P2 && NA <= 3) return ((uint32_t)T.shift_pack >> (4 * S)) & 15u;
+  return dcode<P2>(T, S);
+}
 template <bool P2>
 __device__ __forceinline__ uint64_t dv(const DeviceTables& T, uint64_t x, uint32_t code) {
   return P2 ? (x >> code) : (x >> T.shift[code]) * T.inv[code];
@@ -264,8 +271,10 @@ __device__ __forceinline__ void mca_store(const Smem& S, uint32_t c, int lane, u
 // axis A's result dim under a class's axis -> role map and a signature's
 // role -> result-dim map (15 = the axis shards no result dim)
 __device__ __forceinline__ uint32_t a_dim(uint32_t a2r, uint32_t rdm, int A) {
-  const uint32_t r = (a2r >> (4 * A)) & 15;
-  return r == 15 ? 15u : (rdm >> (4 * r)) & 15;
+  // the map extended to 16 nibbles with 0xF above role 7: role 15 ("none")
+  // reads 0xF without a compare (one funnel shift and a mask)
+  const uint32_t r4 = ((a2r >> (4 * A)) & 15) << 2;
+  return (uint32_t)((((uint64_t)0xFFFFFFFFu << 32) | rdm) >> r4) & 15u;
 }
 
 // ---------------------------------------------------------------- H1 decode (C9)
@@ -642,7 +651,7 @@ __device__ __forceinline__ uint8_t h4_template(const DeviceTables& T, uint32_t d
     presU |= (du != 15 ? 1u : 0u) << A;
   }
   if (dimD == dimU && !P) return 0;
-  uint64_t size = dv<P2>(T, sgb, dcode<P2>(T, presD));
+  uint64_t size = dv<P2>(T, sgb, dcode_na<P2, NA>(T, presD));
 #pragma unroll
   for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather
     const uint32_t dd = (dimD >> (4 * A)) & 15, du = (dimU >> (4 * A)) & 15;
@@ -662,7 +671,7 @@ __device__ __forceinline__ uint8_t h4_template(const DeviceTables& T, uint32_t d
   for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
     if (!((P >> A) & 1)) continue;
     if (((dimU >> (4 * A)) & 15) != 15) {
-      size = dv<P2>(T, size, dcode<P2>(T, 1u << A));
+      size = dv<P2>(T, size, dcode_na<P2, NA>(T, 1u << A));
       rp[A * 4 + TOAST_RS] += size;
       rc[A * 4 + TOAST_RS] += ne;
     } else {
@@ -670,7 +679,7 @@ __device__ __forceinline__ uint8_t h4_template(const DeviceTables& T, uint32_t d
       rc[A * 4 + TOAST_AR] += ne;
     }
   }
-  return (uint8_t)(dcode<P2>(T, presU) | (dcode<P2>(T, presD) << 4));
+  return (uint8_t)(dcode_na<P2, NA>(T, presU) | (dcode_na<P2, NA>(T, presD) << 4));
 }
 
 // ---------------------------------------------------------------- one batch of 32 candidates
@@ -764,7 +773,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
     uint32_t present = 0;
 #pragma unroll
     for (int A = 0; A < NA; ++A) present |= (a_dim(a2r, rdm, A) != 15 ? 1u : 0u) << A;
-    sp<uint8_t>(S.pc)[f * 32 + lane] = (uint8_t)dcode<P2>(T, present);
+    sp<uint8_t>(S.pc)[f * 32 + lane] = (uint8_t)dcode_na<P2, NA>(T, present);
   }
   if (acc_shared(NA, CP) && K > 1) {   // the shared accumulators (region Y held the event lists until H2a ended)
     uint32_t* z = sp<uint32_t>(S.acc);
@@ -1899,7 +1908,9 @@ toast_status autotune_k(toast_analysis* a, std::string& err) {
       a->occ_eval[i] = occ_e;
       a->occ_roll[i] = occ_r;
       const float per = ms / (float)nk;   // time per candidate
-      if (per < best_ms) { best_ms = per; best_k = K; best_cap = cap; }
+      // a later (less resident / wider) choice must win by 2%: the first —
+      // K = 1 at full residency — is kept through measurement noise
+      if (per < (best_ms < 1e29f ? 0.98f * best_ms : best_ms)) { best_ms = per; best_k = K; best_cap = cap; }
     }
   }
   if (st == TOAST_OK && best_cap > 0) {   // the measured residency of the chosen K

@@ -13,6 +13,8 @@ VARIANTS = {
     "t128b7": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=7"],
     "t128b8": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=8"],
     "t128b7np": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=7", "-DTOAST_H4_PREFETCH=0"],
+    "na3b3": ["-DTOAST_NA3_MIN_BLOCKS=3"],
+    "na3b4": ["-DTOAST_NA3_MIN_BLOCKS=4"],
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
