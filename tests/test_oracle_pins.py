@@ -607,6 +607,7 @@ def test_setgroups_are_the_isomorphism_classes():
     and on random programs with several sets."""
     cases = [_attn_and_f(2)] + [models.random_program(s, n_ops=24) for s in range(60)]
     multi = 0
+    pairs = {True: 0, False: 0}
     for ir in cases:
         try:
             o = Oracle(ir, [("a", 2, 1e10), ("b", 4, 1e11)], 1e12, 1 << 40, 100.0, 1)
@@ -621,8 +622,11 @@ def test_setgroups_are_the_isomorphism_classes():
             for j in range(i + 1, len(gs)):
                 if max(len(gs[i]["nodes"]), len(gs[j]["nodes"])) > 14:
                     continue
-                assert _iso(gs[i], gs[j]) == (grp[i] == grp[j]), (ir, i, j)
+                iso = _iso(gs[i], gs[j])
+                assert iso == (grp[i] == grp[j]), (ir, i, j)
+                pairs[iso] += 1
     assert multi >= 3
+    assert pairs[True] >= 100 and pairs[False] >= 500, pairs   # comparisons made, not just programs seen
     d = Oracle(_attn_and_f(2), [("s", 2, 1e10)], 1e12, 1 << 40, 100.0, 1).dump()
     assert len(d["set_group"]) == 4 and d["n_groups"] == 2
 
@@ -687,3 +691,30 @@ def test_argument_groups_depend_on_uses_only():
         part2, _ = _param_partition(ir2, [(ren[names[k][0]], names[k][1]) for k in perm])
         inv = {v: k for k, v in ren.items()}
         assert sorted(sorted((inv[n], i) for n, i in g) for g in part2) == base
+
+
+def test_set_graphs_rebuilt_by_hand():
+    """The labelled graphs C6 hashes, rebuilt by hand from the paper's
+    attention layer (Fig. 5; the five conflicts of P:891 at the
+    score matmul, the reduce, the broadcast, the div and the output matmul,
+    joined by the M edges of the score's uses) and from the x·xᵀ block
+    (the matmul's (i, j) and the returned value's two dims): the
+    oracle's graphs are isomorphic to these, label for label (op kind, role,
+    loop type P=0 / R=1, side 1 / 2)."""
+    def graph(nodes, medges, cedges):
+        return {"nodes": [[k] + list(v) for k, v in nodes.items()], "medges": medges, "cedges": cedges}
+    attn = graph({"a0": ("matmul", 0, 0, 1), "a1": ("matmul", 1, 0, 2),          # a = matmul(k, qt): i, j
+                  "r0": ("reduce", 0, 1, 1), "r1": ("reduce", 1, 0, 2),          # b = reduce[0](a): dim 0 reduced
+                  "b0": ("broadcast", 0, 0, 1), "b1": ("broadcast", 1, 0, 2),    # c = broadcast[0](b)
+                  "d0": ("div", 0, 0, 1), "d1": ("div", 1, 0, 2),                # d = div(a, c)
+                  "z0": ("matmul", 0, 0, 1), "zk": ("matmul", 2, 1, 2)},         # z = matmul(d, v): i, k
+                 [["a0", "r0"], ["a0", "d0"], ["a1", "r1"], ["a1", "d1"], ["b0", "d0"], ["b1", "d1"],
+                  ["d0", "z0"], ["d1", "zk"]],
+                 [["a0", "a1"], ["r0", "r1"], ["b0", "b1"], ["d0", "d1"], ["z0", "zk"]])
+    xxt = graph({"i": ("matmul", 0, 0, 1), "j": ("matmul", 1, 0, 2), "s0": ("ret", 0, 0, 1), "s1": ("ret", 1, 0, 2)},
+                [["i", "s0"], ["j", "s1"]], [["i", "j"], ["s0", "s1"]])
+    o = Oracle(_attn_and_f(2), [("s", 2, 1e10)], 1e12, 1 << 40, 100.0, 1)
+    gs = o.set_graphs()
+    assert len(gs) == 4
+    assert [_iso(g, attn) for g in gs] == [True, True, False, False]
+    assert [_iso(g, xxt) for g in gs] == [False, False, True, True]
