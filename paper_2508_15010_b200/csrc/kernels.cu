@@ -288,18 +288,14 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
 #pragma unroll
   for (int A = 0; A < NA; ++A) axb[A] = 0u;
   uint32_t status = 0;
-  bool stopped = false;
   uint64_t fx = 0, on = 0, ap = 0;
-  for (int j = 0; j < 32; ++j) {
-    uint32_t id = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
-    if (stopped) {
-      if (id) status |= TOAST_ST_NONZERO_AFTER_STOP;
-      continue;
-    }
-    if (id == 0) { stopped = true; continue; }
+  int j = 0;
+  for (; j < 32; ++j) {
+    const uint32_t id = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
+    if (id == 0) break;   // STOP
     if ((int)id >= T.n_actions) { status |= TOAST_ST_BAD_ACTION_ID; continue; }
     uint32_t aw = __ldg(T.actions + id);
-    uint32_t ac = aw & 0x3FF, rr = (aw >> 10) & 0xFF, ax = (aw >> 18) & 3;
+    uint32_t ac = aw & 0x3FF, ax = (aw >> 18) & 3;
     TOAST_CHK(ac < (uint32_t)T.n_acolors && ax < (uint32_t)NA);
     uint32_t pm = sp<uint32_t>(S.acol)[ac * 32 + lane];
     bool dup = false;
@@ -311,16 +307,17 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
       for (int A = 0; A < NA; ++A) axb[A] |= ax == (uint32_t)A ? 1u << j : 0u;
       ap |= (uint64_t)ax << (2 * j);
     }
-    uint64_t gw = __ldg(T.acol_groups + ac);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      uint32_t gid = (uint32_t)(gw >> (8 * t)) & 0xFF;
-      if (gid == 0xFF) continue;
-      uint64_t g = 1ULL << gid;
-      uint64_t bit = (rr >> t) & 1;
-      if ((fx & g) && (((on >> gid) & 1) != bit)) status |= TOAST_ST_RES_MISMATCH;
-      if (!(fx & g)) { fx |= g; if (bit) on |= g; }
-    }
+    // the SetGroups the action fixes (gm) and those it fixes to 1 (om): a group
+    // already fixed the other way is a resolution mismatch
+    const uint64_t gm = __ldg(T.action_grp + 2 * id), om = __ldg(T.action_grp + 2 * id + 1);
+    if (fx & gm & (on ^ om)) status |= TOAST_ST_RES_MISMATCH;
+    on |= om & gm & ~fx;
+    fx |= gm;
+  }
+  if (j < 32) {   // the ids after STOP must all be 0
+    uint32_t after = (j & 1) ? 0u : seq_word(S, j >> 1, lane) >> 16;
+    for (int w = (j >> 1) + 1; w < 16; ++w) after |= seq_word(S, w, lane);
+    if (after) status |= TOAST_ST_NONZERO_AFTER_STOP;
   }
   fixed0 = fx & ~on;
   ones = on;
@@ -364,7 +361,7 @@ __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const
     return a2r;
   }
   uint32_t a2r = 0xFFFFu, masks = 0, opmask = 0;
-  while (bits) {
+  while (bits && opmask != (1u << NA) - 1) {   // (every axis placed: the later events change nothing)
     const uint32_t j = __ffs(bits) - 1;
     bits &= bits - 1;
     const uint32_t A = (uint32_t)(axpos >> (2 * j)) & 3;
@@ -390,7 +387,8 @@ __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const
 
 template <int NA>
 __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, int s,
-                                                    uint64_t fixed0, uint64_t ones, uint64_t axpos, const uint32_t* axb) {
+                                                    uint64_t fixed0, uint64_t ones, uint64_t dsel, uint64_t axpos,
+                                                    const uint32_t* axb) {
   const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
   // all four 16-B words of the record in flight at once
   const uint4 mt = __ldg(kp + 3), c0 = __ldg(kp + 1), c1 = __ldg(kp + 2), dw = __ldg(kp);
@@ -402,8 +400,12 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
   for (uint32_t b = dr; b; b &= b - 1) {
     const uint32_t r = __ffs(b) - 1;
     const uint32_t cls = (uint32_t)(u64of(mt.z, mt.w) >> (8 * r)) & 0xFF;
-    const uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
-    if ((fixed0 & n0) | (ones & n1)) dmask |= 1u << r;
+    if (T.n_desel <= 64) {   // the candidate's active deselection classes, computed once per batch
+      dmask |= (uint32_t)((dsel >> cls) & 1) << r;
+    } else {
+      const uint64_t n0 = __ldg(T.desel + 2 * cls), n1 = __ldg(T.desel + 2 * cls + 1);
+      if ((fixed0 & n0) | (ones & n1)) dmask |= 1u << r;
+    }
   }
   uint32_t a2r;
   switch (m) {   // warp-uniform: the merge is unrolled over the signature's color count
@@ -729,9 +731,16 @@ __device__ __forceinline__ Front batch_front(const DeviceTables& T, const Smem& 
   // result dims share it): the axis -> role map; per class the state-key
   // terms (H7, R14) and the local FLOPs (H3) of all its ops at once
   uint64_t key = 0, flo = 0, fhi = 0;
+  // bit c: deselection class c is active (an endpoint its fixed SetGroup bits deselect)
+  uint64_t dsel = 0;
+  if (T.n_desel <= 64)
+    for (int c = 1; c < T.n_desel; ++c) {
+      const uint64_t n0 = __ldg(T.desel + 2 * c), n1 = __ldg(T.desel + 2 * c + 1);
+      dsel |= ((f0 & n0) | (on & n1)) ? 1ULL << c : 0ULL;
+    }
   for (int c = warp; c < T.n_mc; c += K) {
     const uint64_t glo = __ldg(T.mc_flops + 2 * c), ghi = __ldg(T.mc_flops + 2 * c + 1);
-    const uint32_t a2r = materialize_sig<NA>(T, S, lane, c, f0, on, ap, axb);
+    const uint32_t a2r = materialize_sig<NA>(T, S, lane, c, f0, on, dsel, ap, axb);
     mca_store<NA>(S, c, lane, a2r);
     // the class's state-key terms (every axis's load issued at once, role 15
     // reads a valid word and is masked out) and local FLOPs
@@ -1586,6 +1595,22 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   T.acol_groups = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_kill, &p, err))) return st;
   T.kill = reinterpret_cast<const uint32_t*>(p);
+  {   // per action: the SetGroups it fixes and those it fixes to 1 (its color's groups, its resolution bits)
+    std::vector<uint64_t> grp(2 * a->h_actions.size(), 0);
+    for (size_t id = 1; id < a->h_actions.size(); ++id) {
+      const uint32_t w = a->h_actions[id], ac = w & 0x3FF, rr = (w >> 10) & 0xFF;
+      const uint64_t gw = a->h_acol_groups[ac];
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t gid = (uint32_t)(gw >> (8 * t)) & 0xFF;
+        if (gid == 0xFF) continue;
+        grp[2 * id] |= 1ULL << gid;
+        if ((rr >> t) & 1) grp[2 * id + 1] |= 1ULL << gid;
+      }
+    }
+    if ((st = upload(a, grp, &p, err))) return st;
+    T.action_grp = reinterpret_cast<const uint64_t*>(p);
+    T.n_desel = (int32_t)(a->h_desel_cls.size() / 2);
+  }
 
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));

@@ -242,6 +242,8 @@ struct DeviceTables {
   const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
   const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids (0xFF = unused)
   const uint32_t* kill = nullptr;        // [n_actions][n_words]
+  const uint64_t* action_grp = nullptr;  // [n_actions][2]: the SetGroups an action fixes, and those it fixes to 1
+  int32_t n_desel = 0;                   // deselection classes (class 0 = none)
   // constants
   int32_t n_ops, n_loops, n_actions, n_acolors, n_words, n_axes, max_depth, n_sigs;
   int32_t n_tmpl, pow2;  // pow2: every axis size is a power of two (exact division = shift)
