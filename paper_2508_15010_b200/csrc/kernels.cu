@@ -62,6 +62,9 @@
 #ifndef TOAST_CHK_MUTANT
 #define TOAST_CHK_MUTANT 0
 #endif
+#ifndef TOAST_SIG_PREFETCH
+#define TOAST_SIG_PREFETCH 0   // the next class's record loaded one iteration ahead (measured: see DESIGN §6)
+#endif
 #ifndef TOAST_H4_PREFETCH
 #define TOAST_H4_PREFETCH 1   // the next edge template's record loaded one iteration ahead
 #endif
@@ -257,10 +260,10 @@ __device__ __forceinline__ unsigned __int128 dv128(const DeviceTables& T, unsign
 }
 
 // a materialisation class's axis -> role map per lane: one byte for meshes of
-// <= 2 axes (the nibbles of absent axes read back as 0xF), else 16 bits
+// <= 2 axes, else 16 bits (every reader looks at the nibbles of axes < NA only)
 template <int NA>
 __device__ __forceinline__ uint32_t mca_load(const Smem& S, uint32_t c, int lane) {
-  if (NA <= 2) return 0xFF00u | sp<const uint8_t>(S.mca)[c * 32 + lane];
+  if (NA <= 2) return sp<const uint8_t>(S.mca)[c * 32 + lane];   // (callers read nibbles A < NA only)
   return sp<const uint16_t>(S.mca)[c * 32 + lane];
 }
 template <int NA>
@@ -385,13 +388,20 @@ __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const
   return a2r;
 }
 
+// a materialisation class's 64-B record (KSig) as four 16-B words
+struct SigRec {
+  uint4 dw, c0, c1, mt;
+};
+__device__ __forceinline__ SigRec sig_load(const DeviceTables& T, int s) {
+  const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
+  return SigRec{__ldg(kp), __ldg(kp + 1), __ldg(kp + 2), __ldg(kp + 3)};
+}
+
 template <int NA>
-__device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, int s,
+__device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const Smem& S, int lane, const SigRec& R,
                                                     uint64_t fixed0, uint64_t ones, uint64_t dsel, uint64_t axpos,
                                                     const uint32_t* axb) {
-  const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
-  // all four 16-B words of the record in flight at once
-  const uint4 mt = __ldg(kp + 3), c0 = __ldg(kp + 1), c1 = __ldg(kp + 2), dw = __ldg(kp);
+  const uint4 mt = R.mt, c0 = R.c0, c1 = R.c1, dw = R.dw;
   const uint32_t m = mt.y & 0xFF, dr = (mt.y >> 8) & 0xFF;
   const bool alldiv = (mt.y >> 24) & 1;
   if (m == 0) return 0xFFFFu;
@@ -738,9 +748,20 @@ __device__ __forceinline__ Front batch_front(const DeviceTables& T, const Smem& 
       const uint64_t n0 = __ldg(T.desel + 2 * c), n1 = __ldg(T.desel + 2 * c + 1);
       dsel |= ((f0 & n0) | (on & n1)) ? 1ULL << c : 0ULL;
     }
+#if TOAST_SIG_PREFETCH
+  // the next class's record is loaded one iteration ahead
+  SigRec nrec{};
+  if (warp < T.n_mc) nrec = sig_load(T, warp);
+#endif
   for (int c = warp; c < T.n_mc; c += K) {
+#if TOAST_SIG_PREFETCH
+    const SigRec rec = nrec;
+    if (c + K < T.n_mc) nrec = sig_load(T, c + K);
+#else
+    const SigRec rec = sig_load(T, c);
+#endif
     const uint64_t glo = __ldg(T.mc_flops + 2 * c), ghi = __ldg(T.mc_flops + 2 * c + 1);
-    const uint32_t a2r = materialize_sig<NA>(T, S, lane, c, f0, on, dsel, ap, axb);
+    const uint32_t a2r = materialize_sig<NA>(T, S, lane, rec, f0, on, dsel, ap, axb);
     mca_store<NA>(S, c, lane, a2r);
     // the class's state-key terms (every axis's load issued at once, role 15
     // reads a valid word and is masked out) and local FLOPs
@@ -857,8 +878,10 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
   for (int gi = warp; gi < n_groups; gi += K) {
   long long Ms = 0;   // the group's running constant + signature part
   const int p_end = min(T.n_points, (gi + 1) * FRONTIER_GROUP);
+  uint4 npw = __ldg(reinterpret_cast<const uint4*>(T.points) + gi * FRONTIER_GROUP);
   for (int pi = gi * FRONTIER_GROUP; pi < p_end; ++pi) {
-    const uint4 pw = __ldg(reinterpret_cast<const uint4*>(T.points) + pi);
+    const uint4 pw = npw;   // (the next point's record is loaded one point ahead)
+    if (pi + 1 < p_end) npw = __ldg(reinterpret_cast<const uint4*>(T.points) + pi + 1);
     const uint32_t n_sig = pw.y & 0xFFFF, n_tm = pw.y >> 16, n_spec = pw.w & 0xFFFF;
     const uint64_t* tp = T.terms + pw.x;
     Ms += (long long)__ldg(tp++);
