@@ -670,7 +670,7 @@ __device__ __forceinline__ uint8_t h4_template(const DeviceTables& T, uint32_t d
     if (dd == 15 || du != 15) continue;
     rp[A * 4 + TOAST_AG] += size;
     rc[A * 4 + TOAST_AG] += ne;
-    size *= (uint64_t)T.sizes[A];
+    size = P2 ? size << T.shift[1u << A] : size * (uint64_t)T.sizes[A];
   }
 #pragma unroll
   for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
@@ -1229,15 +1229,45 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
     if (rep == 1) load_seq_rows(S, pre + row0 * 32, rows, lane);
     else load_seq_lane(S, pre + (i / rep) * 32, lane, valid);
     // validate the prefix: ids < n_actions before the first 0, zeros after it
-    int stop = 32;
+    int stop = 0;
     bool bad = false;
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t id = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
-      if (stop < 32) { bad |= id != 0; continue; }
-      if (id == 0) { stop = j; continue; }
+    for (; stop < 32; ++stop) {
+      const uint32_t id = (seq_word(S, stop >> 1, lane) >> ((stop & 1) * 16)) & 0xFFFFu;
+      if (id == 0) break;
       bad |= (int)id >= T.n_actions;
     }
-    if (valid && !bad) {
+    if (stop < 32) {   // the ids after the prefix's STOP must all be 0
+      uint32_t after = (stop & 1) ? 0u : seq_word(S, stop >> 1, lane) >> 16;
+      for (int w = (stop >> 1) + 1; w < 16; ++w) after |= seq_word(S, w, lane);
+      bad |= after != 0;
+    }
+    if (valid && !bad && nw == 1) {
+      // <= 31 actions (GPT-24, GNS-16, Llama-80): the legal set lives in one
+      // register — the same draws, kills and choices as the general path below
+      uint32_t legal = (T.n_actions >= 32 ? FULL : ((1u << T.n_actions) - 1u)) & ~1u;
+      for (int j = 0; j < stop; ++j) {
+        const uint32_t a = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
+        legal &= ~__ldg(T.kill + a);
+      }
+      const uint64_t id = id_base + (uint64_t)i;
+      for (int d = stop; d < T.max_depth; ++d) {
+        uint32_t r0, r1;
+        philox4x32_10((uint32_t)id, (uint32_t)(id >> 32), (uint32_t)d, 0u, seed_lo, seed_hi, r0, r1);
+        if ((uint64_t)r0 * (uint64_t)T.max_depth < ((uint64_t)d << 32)) break;   // p_stop = d / max_depth
+        const uint32_t total = __popc(legal);
+        if (total == 0) break;
+        uint32_t k = (uint32_t)(((uint64_t)r1 * total) >> 32);
+        uint32_t word = legal, pos = 0, c;
+        c = __popc(word & 0xFFFFu); if (k >= c) { k -= c; word >>= 16; pos += 16; }
+        c = __popc(word & 0xFFu);   if (k >= c) { k -= c; word >>= 8; pos += 8; }
+        c = __popc(word & 0xFu);    if (k >= c) { k -= c; word >>= 4; pos += 4; }
+        c = __popc(word & 0x3u);    if (k >= c) { k -= c; word >>= 2; pos += 2; }
+        c = word & 1u;              if (k >= c) { pos += 1; }
+        legal &= ~__ldg(T.kill + pos);
+        uint32_t& sw = seq_word(S, d >> 1, lane);
+        sw = (d & 1) ? ((sw & 0xFFFFu) | (pos << 16)) : ((sw & 0xFFFF0000u) | pos);
+      }
+    } else if (valid && !bad) {
       for (int w = 0; w < nw; ++w) {
         uint32_t v = FULL;
         const int hi = T.n_actions - w * 32;   // ids >= n_actions are not actions
