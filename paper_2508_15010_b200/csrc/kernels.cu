@@ -62,6 +62,9 @@
 #ifndef TOAST_CHK_MUTANT
 #define TOAST_CHK_MUTANT 0
 #endif
+#ifndef TOAST_SMEM_TABLES
+#define TOAST_SMEM_TABLES 0   // stage the uniform tables (class records, templates, frontier) in shared memory by TMA
+#endif
 #ifndef TOAST_SIG_PREFETCH
 #define TOAST_SIG_PREFETCH 0   // the next class's record loaded one iteration ahead (measured: see DESIGN §6)
 #endif
@@ -125,6 +128,14 @@ __host__ __device__ inline int smem_block_bytes(const DeviceTables& T, int K) {
          smem_y_bytes(T.n_acolors, T.n_ftmpl, T.n_fsig, T.n_axes, K, cp, T.n_spec);
 }
 
+// TOAST_SMEM_TABLES: the block's copy of the uniform tables sits at the end of
+// its dynamic shared memory (one copy shared by every warp of the block):
+// [mbarrier 16 B][class records n_mc x 64][templates n_tmpl x 32][points n_points x 16][terms n_terms x 8, to 16]
+__host__ __device__ inline uint32_t smem_table_bytes(const DeviceTables& T) {
+  if (!TOAST_SMEM_TABLES) return 0;
+  return 16u + (uint32_t)T.n_mc * 64u + (uint32_t)T.n_tmpl * 32u + (uint32_t)T.n_points * 16u +
+         (uint32_t)r16(T.n_terms * 8);
+}
 // the block's dynamic shared memory; every access indexes this symbol so the
 // compiler emits plain LDS/STS (no generic-address conversion)
 extern __shared__ __align__(16) unsigned char g_smem[];
@@ -188,6 +199,7 @@ struct Smem {               // byte offsets into g_smem
   uint32_t acc;             // pay [NA*4][32] u64, cnt [NA*4][32] u32 (+ seg [5][32] u64 when K > 1), shared or per warp
   uint32_t stage;           // the record-store staging (2 KB)
   uint32_t next;            // C (K > 1): the block's next batch (dynamic scheduling)
+  uint32_t tab;             // TOAST_SMEM_TABLES: the block's table copy (0: the tables are read from global memory)
 };
 
 __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
@@ -210,6 +222,7 @@ __device__ __forceinline__ Smem block_smem(const DeviceTables& T, int K) {
   const bool inx = acc_in_x(K, cp, T.n_spec);
   s.acc = inx ? x : s.pc + r16(T.n_fsig * 32);
   s.stage = inx ? y : x;
+  s.tab = TOAST_SMEM_TABLES ? dyn_smem_bytes() - smem_table_bytes(T) : 0u;
   return s;
 }
 // the same layout starting at byte `base` (the dedup back kernel's independent warps)
@@ -225,6 +238,67 @@ __device__ __forceinline__ uint32_t& seq_word(const Smem& S, int w, int lane) {
 }
 
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+// ---------------------------------------------------------------- uniform tables (global, or staged by TMA)
+__device__ __forceinline__ void stage_tables(const DeviceTables& T, const Smem& S) {
+#if TOAST_SMEM_TABLES
+  const uint32_t mbar = smem_base() + S.tab;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t nb[4] = {(uint32_t)T.n_mc * 64u, (uint32_t)T.n_tmpl * 32u, (uint32_t)T.n_points * 16u,
+                            (uint32_t)r16(T.n_terms * 8)};
+    const void* src[4] = {T.sigs, T.tmpl, T.points, T.terms};
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(nb[0] + nb[1] + nb[2] + nb[3])
+                 : "memory");
+    uint32_t dst = mbar + 16;
+    for (int q = 0; q < 4; ++q) {   // one TMA bulk copy per table, completing on the mbarrier
+      if (nb[q])
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(src[q]), "r"(nb[q]), "r"(mbar) : "memory");
+      dst += nb[q];
+    }
+  }
+  asm volatile("{\n .reg .pred P;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n @!P bra WAIT%=;\n}"
+               ::"r"(mbar) : "memory");
+#else
+  (void)T; (void)S;
+#endif
+}
+__device__ __forceinline__ uint32_t tab_off(const DeviceTables& T, int which) {   // byte offset of a table in the copy
+  uint32_t o = 16;
+  if (which > 0) o += (uint32_t)T.n_mc * 64u;
+  if (which > 1) o += (uint32_t)T.n_tmpl * 32u;
+  if (which > 2) o += (uint32_t)T.n_points * 16u;
+  return o;
+}
+__device__ __forceinline__ uint4 tmpl_word(const DeviceTables& T, const Smem& S, int t, int half) {
+#if TOAST_SMEM_TABLES
+  return sp<const uint4>(S.tab + tab_off(T, 1))[2 * t + half];
+#else
+  (void)S;
+  return __ldg(reinterpret_cast<const uint4*>(T.tmpl + t) + half);
+#endif
+}
+__device__ __forceinline__ uint4 point_word(const DeviceTables& T, const Smem& S, int pi) {
+#if TOAST_SMEM_TABLES
+  return sp<const uint4>(S.tab + tab_off(T, 2))[pi];
+#else
+  (void)S;
+  return __ldg(reinterpret_cast<const uint4*>(T.points) + pi);
+#endif
+}
+__device__ __forceinline__ uint64_t term_word(const DeviceTables& T, const Smem& S, uint32_t k) {
+#if TOAST_SMEM_TABLES
+  return sp<const unsigned long long>(S.tab + tab_off(T, 3))[k];
+#else
+  (void)S;
+  return __ldg(T.terms + k);
+#endif
+}
 
 // "division codes": for power-of-two meshes (P2) the code of an axis subset is
 // log2 of its size product and exact division is a shift; otherwise the code
@@ -392,9 +466,15 @@ __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const
 struct SigRec {
   uint4 dw, c0, c1, mt;
 };
-__device__ __forceinline__ SigRec sig_load(const DeviceTables& T, int s) {
+__device__ __forceinline__ SigRec sig_load(const DeviceTables& T, const Smem& S, int s) {
+#if TOAST_SMEM_TABLES
+  const uint4* kp = sp<const uint4>(S.tab + 16) + 4 * s;
+  return SigRec{kp[0], kp[1], kp[2], kp[3]};
+#else
+  (void)S;
   const uint4* kp = reinterpret_cast<const uint4*>(T.sigs + s);
   return SigRec{__ldg(kp), __ldg(kp + 1), __ldg(kp + 2), __ldg(kp + 3)};
+#endif
 }
 
 template <int NA>
@@ -752,14 +832,14 @@ __device__ __forceinline__ Front batch_front(const DeviceTables& T, const Smem& 
 #if TOAST_SIG_PREFETCH
   // the next class's record is loaded one iteration ahead
   SigRec nrec{};
-  if (warp < T.n_mc) nrec = sig_load(T, warp);
+  if (warp < T.n_mc) nrec = sig_load(T, S, warp);
 #endif
   for (int c = warp; c < T.n_mc; c += K) {
 #if TOAST_SIG_PREFETCH
     const SigRec rec = nrec;
-    if (c + K < T.n_mc) nrec = sig_load(T, c + K);
+    if (c + K < T.n_mc) nrec = sig_load(T, S, c + K);
 #else
-    const SigRec rec = sig_load(T, c);
+    const SigRec rec = sig_load(T, S, c);
 #endif
     const uint64_t glo = __ldg(T.mc_flops + 2 * c), ghi = __ldg(T.mc_flops + 2 * c + 1);
     const uint32_t a2r = materialize_sig<NA>(T, S, lane, rec, f0, on, dsel, ap, axb);
@@ -830,18 +910,18 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
   // the next template's record is loaded one iteration ahead
   uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
   if (warp < T.n_tmpl) {
-    n0 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + warp));
-    n1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + warp) + 1);
+    n0 = tmpl_word(T, S, warp, 0);
+    n1 = tmpl_word(T, S, warp, 1);
   }
   for (int tix = warp; tix < T.n_tmpl; tix += K) {
 #if TOAST_H4_PREFETCH
     const uint4 t0 = n0, t1 = n1;
     if (tix + K < T.n_tmpl) {
-      n0 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix + K));
-      n1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix + K) + 1);
+      n0 = tmpl_word(T, S, tix + K, 0);
+      n1 = tmpl_word(T, S, tix + K, 1);
     }
 #else
-    const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix)), t1 = __ldg(reinterpret_cast<const uint4*>(T.tmpl + tix) + 1);
+    const uint4 t0 = tmpl_word(T, S, tix, 0), t1 = tmpl_word(T, S, tix, 1);
 #endif
     TOAST_CHK((t0.x & 0xFFFF) < (uint32_t)T.n_mc && (t0.x >> 16) < (uint32_t)T.n_mc &&
               (t1.y == 0xFFFFFFFFu || t1.y < (uint32_t)T.n_ftmpl));
@@ -879,16 +959,16 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
   for (int gi = warp; gi < n_groups; gi += K) {
   long long Ms = 0;   // the group's running constant + signature part
   const int p_end = min(T.n_points, (gi + 1) * FRONTIER_GROUP);
-  uint4 npw = __ldg(reinterpret_cast<const uint4*>(T.points) + gi * FRONTIER_GROUP);
+  uint4 npw = point_word(T, S, gi * FRONTIER_GROUP);
   for (int pi = gi * FRONTIER_GROUP; pi < p_end; ++pi) {
     const uint4 pw = npw;   // (the next point's record is loaded one point ahead)
-    if (pi + 1 < p_end) npw = __ldg(reinterpret_cast<const uint4*>(T.points) + pi + 1);
+    if (pi + 1 < p_end) npw = point_word(T, S, pi + 1);
     const uint32_t n_sig = pw.y & 0xFFFF, n_tm = pw.y >> 16, n_spec = pw.w & 0xFFFF;
-    const uint64_t* tp = T.terms + pw.x;
-    Ms += (long long)__ldg(tp++);
+    uint32_t tp = pw.x;
+    Ms += (long long)term_word(T, S, tp++);
 #pragma unroll 4
     for (uint32_t k = 0; k < n_sig; ++k) {
-      const uint64_t w = __ldg(tp + k);
+      const uint64_t w = term_word(T, S, tp + k);
       const long long v = (long long)(w << 16) >> 16;    // signed 48-bit value
       TOAST_CHK((uint32_t)(w >> 48) < (uint32_t)T.n_fsig);
       Ms += dvs<P2>(T, v, lds_u8(pc_base + (uint32_t)(w >> 48) * 32));
@@ -897,7 +977,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
     uint64_t M = (uint64_t)Ms;
 #pragma unroll 2
     for (uint32_t k = 0; k < n_tm; ++k) {
-      const uint64_t w = __ldg(tp + k);
+      const uint64_t w = term_word(T, S, tp + k);
       const uint64_t v = w & ((1ULL << 48) - 1);
       TOAST_CHK((uint32_t)(w >> 48) < (uint32_t)T.n_ftmpl);
       const uint32_t b = lds_u8(tb_base + (uint32_t)(w >> 48) * 32);
@@ -1188,6 +1268,7 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
                                                          int64_t n, void* __restrict__ out, bool compact) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
+  stage_tables(T, S);
   const int64_t nbatch = (n + 31) / 32;
   for (int64_t b = blockIdx.x; b < nbatch; b = next_batch(T, S, b, K)) {
     const int64_t row0 = b * 32;
@@ -1219,6 +1300,7 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
                                                             void* __restrict__ out, int64_t rep, bool compact) {
   const int K = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Smem S = block_smem(T, K);
+  stage_tables(T, S);
   const int64_t nbatch = (n + 31) / 32;
   const uint32_t seed_lo = (uint32_t)seed, seed_hi = (uint32_t)(seed >> 32);
   const int nw = T.n_words;
@@ -1434,6 +1516,7 @@ template <int NA, bool P2, bool CP>
 __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS), (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS))
 toast_dedup_back_kernel(const DeviceTables T, void* __restrict__ out, bool compact) {
   const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  stage_tables(T, block_smem(T, 1));
   const DedupCtx& D = T.dd;
   const int64_t nrep = (int64_t)*D.count, nb = (nrep + 31) / 32;
   if (nb >= (int64_t)gridDim.x * W) {   // independent warps, each with its own one-warp layout and scratch
@@ -1610,8 +1693,13 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   for (KPoint& kp : pts) kp.use_sig = (uint16_t)sig_mc(kp.use_sig);
   if ((st = upload(a, pts, &p, err))) return st;
   T.points = reinterpret_cast<const KPoint*>(p);
-  if ((st = upload(a, a->h_terms, &p, err))) return st;
+  {   // (padded to whole 16-B words: the staged copy reads them so)
+    std::vector<uint64_t> terms = a->h_terms;
+    if (terms.size() & 1) terms.push_back(0);
+    if ((st = upload(a, terms, &p, err))) return st;
+  }
   T.terms = reinterpret_cast<const uint64_t*>(p);
+  T.n_terms = (int32_t)a->h_terms.size();
   std::vector<KUseDev> spec(a->h_spec.size());
   for (size_t q = 0; q < spec.size(); ++q) {
     const KUse& u = a->h_spec[q];
@@ -1669,7 +1757,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   int dev_smem = 0, sms = 0;
   TOAST_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, a->device));
   TOAST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, a->device));
-  if (smem_block_bytes(T, 1) > dev_smem) {
+  if (smem_block_bytes(T, 1) + (int)smem_table_bytes(T) > dev_smem) {
     err = "op-signature tables do not fit in shared memory";
     return TOAST_E_LIMIT;
   }
@@ -1678,7 +1766,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   TOAST_CUDA(cudaGetLastError());
   a->n_sms = sms;
   for (int i = 0, K = 1; i < 4; ++i, K *= 2) {
-    const int sm = smem_block_bytes(T, K);
+    const int sm = smem_block_bytes(T, K) + (int)smem_table_bytes(T);
     int be = 0, br = 0;
     const int max_threads = T.cost_model == TOAST_COST_CRITICAL_PATH ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS;
     if (sm <= dev_smem && 32 * K <= max_threads) {
@@ -1697,7 +1785,7 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
     a->occ_back = 1;
     const int max_threads = T.cost_model == TOAST_COST_CRITICAL_PATH ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS;
     for (int W = 8; W >= 1; W /= 2) {
-      const int sm = std::max(W * smem_block_bytes(T, 1), smem_block_bytes(T, W));
+      const int sm = std::max(W * smem_block_bytes(T, 1), smem_block_bytes(T, W)) + (int)smem_table_bytes(T);
       if (sm > dev_smem || 32 * W > max_threads) continue;
       int bb = 0;
       cudaError_t e = dispatch(T, [&]<int NA, bool P2, bool CP>() {
@@ -1824,7 +1912,7 @@ toast_status launch_eval(const toast_analysis* a, const uint16_t* d_seqs, int64_
   const int K = pick_k(a, batches, a->occ_eval);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_eval[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt, K);
+  const size_t sm = (size_t)smem_block_bytes(a->dt, K) + smem_table_bytes(a->dt);
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));
@@ -1875,7 +1963,7 @@ static toast_status launch_rollout_dedup(const toast_analysis* a, const uint16_t
   // front: the rollout kernel, one warp per block
   const int64_t batches = (n + 31) / 32;
   const int64_t fblocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[0] * a->n_sms));
-  const size_t sm1 = (size_t)smem_block_bytes(T0, 1);
+  const size_t sm1 = (size_t)smem_block_bytes(T0, 1) + smem_table_bytes(T0);
   dispatch(T, [&]<int NA, bool P2, bool CP>() {
     toast_rollout_kernel<NA, P2, CP><<<dim3((unsigned)fblocks), dim3(32), sm1, st>>>(T, d_pre, n, seed, id_base, d_seqs, d_out, rep, compact);
     return 0;
@@ -1886,7 +1974,7 @@ static toast_status launch_rollout_dedup(const toast_analysis* a, const uint16_t
   const int64_t bblocks = std::max<int64_t>(1, std::min<int64_t>((batches + W - 1) / W, (int64_t)a->occ_back * a->n_sms));
   DeviceTables TB = T;
   if (TB.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, bblocks * W, st, &TB.cp_scratch));
-  const size_t smb = (size_t)std::max(W * smem_block_bytes(T0, 1), smem_block_bytes(T0, W));
+  const size_t smb = (size_t)std::max(W * smem_block_bytes(T0, 1), smem_block_bytes(T0, W)) + smem_table_bytes(T0);
   dispatch(TB, [&]<int NA, bool P2, bool CP>() {
     toast_dedup_back_kernel<NA, P2, CP><<<dim3((unsigned)bblocks), dim3(32 * W), smb, st>>>(TB, recs, compact);
     return 0;
@@ -1912,7 +2000,7 @@ toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int6
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
   const dim3 g((unsigned)blocks), b(32 * K);
-  const size_t sm = (size_t)smem_block_bytes(a->dt, K);
+  const size_t sm = (size_t)smem_block_bytes(a->dt, K) + smem_table_bytes(a->dt);
   cudaStream_t st = (cudaStream_t)stream;
   DeviceTables T = a->dt;
   if (T.cost_model == TOAST_COST_CRITICAL_PATH) TOAST_CUDA(cp_scratch_alloc(a, blocks, st, &T.cp_scratch));

@@ -250,6 +250,7 @@ struct DeviceTables {
   int32_t n_points, n_mc;
   int32_t n_fsig, n_ftmpl;  // signatures / templates the frontier terms use (their per-lane code tables)
   int32_t n_spec = 0;       // special edges (a value used twice by one op) of the frontier points
+  int32_t n_terms = 0;      // frontier terms (the TOAST_SMEM_TABLES copy)
   int32_t cost_model, n_slots;   // R22: critical path; finish-time slots per candidate
   int32_t n_comm, n_comp;        // R22: edge-duration and compute-time classes
   const uint2* cp = nullptr;     // critical-path stream
