@@ -309,6 +309,15 @@ toast_status toast_search_begin(const toast_analysis* a, const toast_search_opts
 toast_status toast_search_round(toast_search_state* s, void* export_buf);
 /* imports world records ([world][export_bytes], host memory); *stop = 1 when all ranks must stop */
 toast_status toast_search_import(toast_search_state* s, const void* gathered, int32_t* stop);
+/* the same with the exchange in device memory: the round's
+   record is copied to `export_dev` (device, toast_search_export_bytes()
+   bytes) on `cuda_stream`, so an NCCL all-gather enqueued on that stream
+   after the call reads it without a host round trip; `gathered_dev` (device,
+   [world][export_bytes]) is read back on `cuda_stream` and imported.  Both
+   return once their copy is complete.  Errors: TOAST_E_INVALID_ARG (NULL, a
+   host pointer), TOAST_E_CUDA. */
+toast_status toast_search_round_dev(toast_search_state* s, void* export_dev, void* cuda_stream);
+toast_status toast_search_import_dev(toast_search_state* s, const void* gathered_dev, int32_t* stop, void* cuda_stream);
 toast_status toast_search_end(toast_search_state* s, toast_search_result* out);
 /* root-child statistics summed over the ranks at the last import (index =
    action id; visits 0 = the child is not expanded on any rank).  out: cap

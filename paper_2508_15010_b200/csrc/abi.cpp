@@ -17,6 +17,9 @@ toast_status search_begin(const toast_analysis* a, const toast_search_opts* o, i
                           toast_search_state** out, std::string& err);
 toast_status search_round(toast_search_state* s, void* export_buf, std::string& err);
 toast_status search_import(toast_search_state* s, const void* gathered, int32_t* stop, std::string& err);
+toast_status search_round_dev(toast_search_state* s, void* export_dev, void* stream, std::string& err);
+toast_status search_import_dev(toast_search_state* s, const void* gathered_dev, int32_t* stop, void* stream,
+                               std::string& err);
 void search_result(const toast_search_state* s, toast_search_result* out);
 size_t search_export_bytes(const toast_analysis* a);
 int32_t search_root_stats(const toast_search_state* s, toast_root_stat* out, int32_t cap);
@@ -255,6 +258,20 @@ toast_status toast_search_import(toast_search_state* s, const void* gathered, in
   if (!s || !gathered || !stop) return fail(TOAST_E_INVALID_ARG, "NULL argument");
   std::string err;
   return ret(toast::search_import(s, gathered, stop, err), err);
+}
+
+toast_status toast_search_round_dev(toast_search_state* s, void* export_dev, void* cuda_stream) {
+  if (!s || !export_dev) return fail(TOAST_E_INVALID_ARG, "NULL argument");
+  if (!toast::is_device_pointer(export_dev)) return fail(TOAST_E_INVALID_ARG, "export_dev is not device memory");
+  std::string err;
+  return ret(toast::search_round_dev(s, export_dev, cuda_stream, err), err);
+}
+
+toast_status toast_search_import_dev(toast_search_state* s, const void* gathered_dev, int32_t* stop, void* cuda_stream) {
+  if (!s || !gathered_dev || !stop) return fail(TOAST_E_INVALID_ARG, "NULL argument");
+  if (!toast::is_device_pointer(gathered_dev)) return fail(TOAST_E_INVALID_ARG, "gathered_dev is not device memory");
+  std::string err;
+  return ret(toast::search_import_dev(s, gathered_dev, stop, cuda_stream, err), err);
 }
 
 toast_status toast_search_end(toast_search_state* s, toast_search_result* out) {

@@ -324,6 +324,27 @@ toast_status search_import(toast_search_state* s, const void* gathered, int32_t*
   return TOAST_OK;
 }
 
+// the same round / import with the exchange buffers in device memory, ordered
+// on the caller's stream (the NCCL all-gather runs between them on that stream)
+toast_status search_round_dev(toast_search_state* s, void* export_dev, void* stream, std::string& err) {
+  std::vector<char> buf(search_export_bytes(s->a));
+  toast_status st = search_round(s, buf.data(), err);
+  if (st) return st;
+  cudaError_t e = cudaMemcpyAsync(export_dev, buf.data(), buf.size(), cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);   // the host record dies with this call
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_CUDA; }
+  return TOAST_OK;
+}
+
+toast_status search_import_dev(toast_search_state* s, const void* gathered_dev, int32_t* stop, void* stream,
+                               std::string& err) {
+  std::vector<char> buf(search_export_bytes(s->a) * (size_t)s->world);
+  cudaError_t e = cudaMemcpyAsync(buf.data(), gathered_dev, buf.size(), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return TOAST_E_CUDA; }
+  return search_import(s, buf.data(), stop, err);
+}
+
 void search_result(const toast_search_state* s, toast_search_result* out) {
   memset(out, 0, sizeof(*out));
   memcpy(out->best_seq, s->best_seq, 64);

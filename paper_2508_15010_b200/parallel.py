@@ -40,13 +40,26 @@ def search_root_parallel(a: "T.Analysis", opts: "T.SearchOptions", group=None, s
     and root visit statistics) and every rank imports the same bytes, so the
     global best, the summed root statistics and the stop decision agree.
     root_stats: optional list that receives the final summed root statistics."""
+    import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     st = T.SearchState(a, opts, rank, world, stream=stream)
+    nccl = dist.get_backend(group) == "nccl"
+    if nccl:   # the exchange stays in device memory (toast_search_round_dev / _import_dev)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        rec_d = torch.empty(st.export_bytes, dtype=torch.uint8, device=dev)
+        all_d = torch.empty(world * st.export_bytes, dtype=torch.uint8, device=dev)
+        cur = torch.cuda.current_stream(dev)
     while True:
-        rec = st.round()
-        gathered = all_gather_bytes(rec, group)
-        stop = st.import_(gathered)
+        if nccl:
+            st.round_dev(rec_d, stream=cur)
+            dist.all_gather_into_tensor(all_d, rec_d, group=group)
+            stop = st.import_dev(all_d, stream=cur)
+            gathered = all_d.cpu().numpy() if trace is not None else None
+        else:
+            rec = st.round()
+            gathered = all_gather_bytes(rec, group)
+            stop = st.import_(gathered)
         if trace is not None:
             g = gathered.reshape(world, -1)[:, :EXPORT_DTYPE.itemsize].copy().view(EXPORT_DTYPE)
             trace.append(float(g["best_score"].min()))

@@ -108,6 +108,8 @@ _sigs = {
     "toast_search_begin": [_P, ctypes.POINTER(_SearchOpts), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_P)],
     "toast_search_round": [_P, _P],
     "toast_search_import": [_P, _P, ctypes.POINTER(ctypes.c_int32)],
+    "toast_search_round_dev": [_P, _P, _P],
+    "toast_search_import_dev": [_P, _P, ctypes.POINTER(ctypes.c_int32), _P],
     "toast_search_end": [_P, _P],
 }
 for _n, _a in _sigs.items():
@@ -379,6 +381,18 @@ class SearchState:
         buf = np.zeros(self.export_bytes, dtype=np.uint8)
         _check(_lib.toast_search_round(self._h, buf.ctypes.data))
         return buf
+
+    def round_dev(self, export_dev, stream=None):
+        """toast_search_round_dev: the round's record into a device tensor (uint8[export_bytes])."""
+        assert _len(export_dev, 1) >= self.export_bytes
+        _check(_lib.toast_search_round_dev(self._h, _ptr(export_dev), _stream(stream)))
+        return export_dev
+
+    def import_dev(self, gathered_dev, stream=None) -> bool:
+        """toast_search_import_dev: the all-gathered records ([world][export_bytes], device)."""
+        stop = ctypes.c_int32()
+        _check(_lib.toast_search_import_dev(self._h, _ptr(gathered_dev), ctypes.byref(stop), _stream(stream)))
+        return bool(stop.value)
 
     def import_(self, gathered: np.ndarray) -> bool:
         g = np.ascontiguousarray(gathered, dtype=np.uint8)

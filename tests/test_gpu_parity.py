@@ -259,8 +259,9 @@ def test_search_mlp_c_finds_bruteforce_optimum():
 
 
 def test_root_parallel_search_nccl_single_rank():
-    """The multi-GPU search driver (NCCL all-gather + import) at world size 1
-    reproduces toast_search exactly (same seed, same trajectory)."""
+    """The multi-GPU search driver at world size 1 over NCCL — the exchange in
+    device memory (toast_search_round_dev / toast_search_import_dev, SURVEY
+    §8(b)) — reproduces toast_search exactly (same seed, same trajectory)."""
     import os
     import socket
 
