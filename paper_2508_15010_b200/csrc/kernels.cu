@@ -1995,7 +1995,9 @@ static toast_status launch_rollout_dedup(const toast_analysis* a, const uint16_t
 toast_status launch_rollout(const toast_analysis* a, const uint16_t* d_pre, int64_t n, uint64_t seed, uint64_t id_base,
                             uint16_t* d_seqs, void* d_out, void* stream, std::string& err, int64_t rep, bool compact) {
   if (n <= 0) return TOAST_OK;
-  if (a->dedup) return launch_rollout_dedup(a, d_pre, n, seed, id_base, d_seqs, d_out, (cudaStream_t)stream, err, rep, compact);
+  // (dedup indexes candidates with 32 bits: larger launches take the one-kernel path, the same records)
+  if (a->dedup && n < (int64_t)0x7FFFFFFF)
+    return launch_rollout_dedup(a, d_pre, n, seed, id_base, d_seqs, d_out, (cudaStream_t)stream, err, rep, compact);
   const int64_t batches = (n + 31) / 32;
   const int K = pick_k(a, batches, a->occ_roll);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(batches, (int64_t)a->occ_roll[kidx(K)] * a->n_sms));
