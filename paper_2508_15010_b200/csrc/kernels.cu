@@ -775,6 +775,63 @@ __device__ __forceinline__ uint8_t h4_template(const DeviceTables& T, uint32_t d
   return (uint8_t)(dcode_na<P2, NA>(T, presU) | (dcode_na<P2, NA>(T, presD) << 4));
 }
 
+// The same from byte maps: one byte permute per side gives every axis's dim at
+// once (a role selector of 15 replicates the 0xFF of byte 7), and the template
+// does not communicate iff the two results agree (a partial axis reads 0xFE on
+// the def side, which no use dim equals).
+__device__ __forceinline__ uint32_t prmt(uint32_t lo, uint32_t hi, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(sel));
+  return r;
+}
+template <int NA, bool P2>
+__device__ __forceinline__ uint8_t h4_template_b(const DeviceTables& T, uint32_t da2r, uint32_t ue, const uint4& m,
+                                                 uint64_t sgb, uint32_t ne,
+                                                 unsigned long long (&rp)[NA * 4], uint32_t (&rc)[NA * 4]) {
+  constexpr uint32_t BM = NA >= 4 ? 0xFFFFFFFFu : (1u << (8 * NA)) - 1u;
+  const uint32_t Db = prmt(m.z, m.w | 0xFF000000u, da2r) & BM;
+  const uint32_t Ub = prmt(m.x, m.y | 0xFF000000u, ue) & BM;
+  if (Db == Ub) return 0;
+  uint32_t P = 0, presD = 0, presU = 0, a2a = 0;
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {
+    const uint32_t dd = (Db >> (8 * A)) & 0xFF, du = (Ub >> (8 * A)) & 0xFF;
+    const bool hd = dd < 0x80, hu = du < 0x80;
+    P |= (dd == 0xFE ? 1u : 0u) << A;
+    presD |= (hd ? 1u : 0u) << A;
+    presU |= (hu ? 1u : 0u) << A;
+    a2a |= ((hd && hu && dd != du) ? 1u : 0u) << A;
+  }
+  const uint32_t ag = presD & ~presU;
+  uint64_t size = dv<P2>(T, sgb, dcode_na<P2, NA>(T, presD));
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {          // phase 1a: all_gather
+    if (!((ag >> A) & 1)) continue;
+    rp[A * 4 + TOAST_AG] += size;
+    rc[A * 4 + TOAST_AG] += ne;
+    size = P2 ? size << T.shift[1u << A] : size * (uint64_t)T.sizes[A];
+  }
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {          // phase 1b: all_to_all
+    if (!((a2a >> A) & 1)) continue;
+    rp[A * 4 + TOAST_A2A] += size;
+    rc[A * 4 + TOAST_A2A] += ne;
+  }
+#pragma unroll
+  for (int A = 0; A < NA; ++A) {          // phase 2: reduce_scatter / all_reduce
+    if (!((P >> A) & 1)) continue;
+    if ((presU >> A) & 1) {
+      size = dv<P2>(T, size, dcode_na<P2, NA>(T, 1u << A));
+      rp[A * 4 + TOAST_RS] += size;
+      rc[A * 4 + TOAST_RS] += ne;
+    } else {
+      rp[A * 4 + TOAST_AR] += size;
+      rc[A * 4 + TOAST_AR] += ne;
+    }
+  }
+  return (uint8_t)(dcode_na<P2, NA>(T, presU) | (dcode_na<P2, NA>(T, presD) << 4));
+}
+
 // ---------------------------------------------------------------- one batch of 32 candidates
 // The K warps of the block share the batch: warp 0 decodes, the warps
 // materialise a share of the classes (H2a), the frontier signatures' codes
@@ -907,6 +964,21 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
   uint32_t rc[NA * 4];
 #pragma unroll
   for (int q = 0; q < NA * 4; ++q) { rp[q] = 0ULL; rc[q] = 0u; }
+  if (T.tmpl_bytes && !TOAST_SMEM_TABLES) {
+    // byte-map templates (every op has <= 7 roles); the next record is loaded one iteration ahead
+    uint4 b0 = make_uint4(0, 0, 0, 0), b1 = b0;
+    if (warp < T.n_tmpl) { b0 = __ldg(T.tmpl_b + 2 * warp); b1 = __ldg(T.tmpl_b + 2 * warp + 1); }
+    for (int tix = warp; tix < T.n_tmpl; tix += K) {
+      const uint4 t0 = b0, t1 = b1;
+      if (tix + K < T.n_tmpl) { b0 = __ldg(T.tmpl_b + 2 * (tix + K)); b1 = __ldg(T.tmpl_b + 2 * (tix + K) + 1); }
+      TOAST_CHK((t0.x & 0xFFFF) < (uint32_t)T.n_mc && (t0.x >> 16) < (uint32_t)T.n_mc);
+      const uint32_t da2r = mca_load<NA>(S, t0.x & 0xFFFF, lane), ue = mca_load<NA>(S, t0.x >> 16, lane);
+      const uint8_t tbv = h4_template_b<NA, P2>(T, da2r, ue, t1, u64of(t0.z, t0.w), t0.y, rp, rc);
+      const uint32_t fs = (t1.y >> 24) | ((t1.w >> 24) << 8);
+      TOAST_CHK(fs == 0xFFFFu || fs < (uint32_t)T.n_ftmpl);
+      if (fs != 0xFFFFu) sp<uint8_t>(S.tb)[fs * 32 + lane] = tbv;
+    }
+  } else {
   // the next template's record is loaded one iteration ahead
   uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
   if (warp < T.n_tmpl) {
@@ -929,6 +1001,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
     const uint32_t ue = mca_load<NA>(S, t0.x >> 16, lane);        // the use class
     const uint8_t tbv = h4_template<NA, P2>(T, da2r, ue, t0.y, t1.z, u64of(t0.z, t0.w), t1.x, rp, rc);
     if (t1.y != 0xFFFFFFFFu) sp<uint8_t>(S.tb)[t1.y * 32 + lane] = tbv;
+  }
   }
   // (with K = 1 the slots may overlay the class maps: every lane's last read first)
   if (K == 1) {
@@ -1729,6 +1802,33 @@ toast_status upload_tables(toast_analysis* a, std::string& err) {
   }
   if ((st = upload(a, tm, &p, err))) return st;
   T.tmpl = reinterpret_cast<const KTmplDev*>(p);
+  {   // byte-map templates: byte r = the dim of role r (def: 0xFE when role r holds no result dim;
+      // use: 0xFF when it holds no operand dim); byte 7 carries half of the frontier slot, the
+      // kernel reads it as 0xFF — so every op must have <= 7 roles
+    int max_roles = 0;
+    for (uint8_t nr : a->h_sig_nroles) max_roles = std::max<int>(max_roles, nr);
+    T.tmpl_bytes = max_roles <= 7 && !getenv("TOAST_TMPL_NIBBLES") ? 1 : 0;   // (knob: the nibble-map path, for A/B)
+    std::vector<uint4> tb(2 * a->h_tmpl.size());
+    auto bmap = [](uint32_t nib, uint32_t none, uint32_t top) {
+      uint64_t m = 0;
+      for (int r = 0; r < 7; ++r) {
+        const uint32_t v = (nib >> (4 * r)) & 15;
+        m |= (uint64_t)(v == 15 ? none : v) << (8 * r);
+      }
+      return m | ((uint64_t)(top & 0xFF) << 56);
+    };
+    for (size_t q = 0; q < a->h_tmpl.size(); ++q) {
+      const KTmpl& t = a->h_tmpl[q];
+      const uint32_t fs = t.fslot == 0xFFFFFFFFu ? 0xFFFFu : t.fslot;
+      const uint64_t um = bmap(t.use_dimof, 0xFF, fs), dm = bmap(sig_rdm(t.def_sig), 0xFE, fs >> 8);
+      tb[2 * q] = make_uint4(sig_mc(t.def_sig) | ((uint32_t)t.use_sig << 16), t.n_edges, (uint32_t)t.sum_gbytes,
+                             (uint32_t)(t.sum_gbytes >> 32));
+      tb[2 * q + 1] = make_uint4((uint32_t)um, (uint32_t)(um >> 32), (uint32_t)dm, (uint32_t)(dm >> 32));
+      if (t.fslot != 0xFFFFFFFFu && t.fslot >= 0xFFFFu) T.tmpl_bytes = 0;
+    }
+    if ((st = upload(a, tb, &p, err))) return st;
+    T.tmpl_b = reinterpret_cast<const uint4*>(p);
+  }
   if ((st = upload(a, a->h_desel_cls, &p, err))) return st;
   T.desel = reinterpret_cast<const uint64_t*>(p);
   if ((st = upload(a, a->h_actions, &p, err))) return st;

@@ -238,6 +238,8 @@ struct DeviceTables {
   const uint64_t* mc_key = nullptr;      // [n_mc][4 axes][8 roles] summed state-key terms (R14)
   const uint64_t* mc_flops = nullptr;    // [n_mc][2] summed global FLOPs of matmul-class ops (lo, hi)
   const KTmplDev* tmpl = nullptr;        // [n_tmpl]
+  const uint4* tmpl_b = nullptr;         // [n_tmpl][2] the same with byte maps (prmt lookups), when tmpl_bytes
+  int32_t tmpl_bytes = 0;                // every op has <= 7 roles: H4 reads the byte-map templates
   const uint64_t* desel = nullptr;       // [class][2] = need0, need1 (class 0 = none)
   const uint32_t* actions = nullptr;     // acolor | r << 10 | axis << 18
   const uint64_t* acol_groups = nullptr; // 8 x 8-bit group ids (0xFF = unused)
