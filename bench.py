@@ -58,8 +58,9 @@ def parse():
     p.add_argument("--ttb-configs", default="unet,llama80",
                    help="extra configs whose time-to-best is measured beside the main one ('' = none)")
     p.add_argument("--ttb-cpu-seconds", type=float, default=20.0, help="CPU oracle search limit of the extra configs")
-    p.add_argument("--dedup", type=int, default=0, choices=[0, 1],
-                   help="1: rollout launches cost each distinct state once (toast_nda_opts.dedup, NEXT-3)")
+    p.add_argument("--dedup", type=int, default=2, choices=[0, 1, 2],
+                   help="rollout launches cost each distinct state once (toast_nda_opts.dedup, NEXT-3): "
+                        "0 off, 1 on, 2 auto = on under the critical-path model only")
     return p.parse_args()
 
 
@@ -371,9 +372,10 @@ def variant_cp(args, cfg, local, stream, flush):
     model (reading R22), timed the same way on this GPU (10 steps)."""
     from paper_2508_15010_b200 import toast as T
     a = T.build_analysis(cfg.ir, cfg.axes, cfg.flops_per_sec, cfg.dm, cfg.penalty_c, cfg.min_dims, cfg.max_depth,
-                         cuda_device=local, cost_model=T.COST_CRITICAL_PATH)
+                         cuda_device=local, cost_model=T.COST_CRITICAL_PATH)   # (dedup auto: on)
     r = _variant_rate(args, a, local, stream, flush)
-    r.update({"cost_model": "critical path (DESIGN.md reading R22)", "finish_slots": a.kernel_tables().get("n_slots")})
+    r.update({"cost_model": "critical path (DESIGN.md reading R22)", "finish_slots": a.kernel_tables().get("n_slots"),
+              "dedup": "auto (on under the critical path; variants.dedup has it off and on)"})
     return r
 
 

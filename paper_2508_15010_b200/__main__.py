@@ -56,7 +56,7 @@ def main(argv=None) -> int:
     a = T.build_analysis(ir, axes, flops, int(dm), pen, min_dims, 30, cuda_device=0,
                          cost_model=T.COST_CRITICAL_PATH if args.cost_model == "cp" else T.COST_SUM,
                          grouping=T.GROUP_CONTRACTION if args.grouping == "contraction" else T.GROUP_COMPAT,
-                         dedup=int(args.dedup))
+                         dedup=T.DEDUP_ON if args.dedup else T.DEDUP_AUTO)
     acts = a.actions()
     r = T.search(a, T.SearchOptions(seed=args.seed, max_evals=args.budget, patience=1 << 30,
                                     transpositions=int(args.transpositions)))

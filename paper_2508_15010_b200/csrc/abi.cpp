@@ -89,7 +89,7 @@ toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_anal
     return fail(TOAST_E_INVALID_ARG, "cost_model must be TOAST_COST_SUM or TOAST_COST_CRITICAL_PATH");
   if (o->conflict_grouping != TOAST_GROUP_COMPAT && o->conflict_grouping != TOAST_GROUP_CONTRACTION)
     return fail(TOAST_E_INVALID_ARG, "conflict_grouping must be TOAST_GROUP_COMPAT or TOAST_GROUP_CONTRACTION");
-  if (o->dedup != 0 && o->dedup != 1) return fail(TOAST_E_INVALID_ARG, "dedup must be 0 or 1");
+  if (o->dedup < 0 || o->dedup > 2) return fail(TOAST_E_INVALID_ARG, "dedup must be 0, 1 or 2");
   toast_analysis* a = new (std::nothrow) toast_analysis();
   if (!a) return fail(TOAST_E_OOM, "out of host memory");
   std::string err;
@@ -103,7 +103,8 @@ toast_status toast_nda(const toast_graph* g, const toast_nda_opts* o, toast_anal
       if (st == TOAST_OK) st = toast::autotune_k(a, err);
       if (st != TOAST_OK) { toast::free_tables(a); delete a; return fail(st, err); }
     }
-    a->dedup = o->dedup;   // (after the autotune, which times the one-kernel path)
+    // (after the autotune, which times the one-kernel path); 2 = on for the critical path only
+    a->dedup = o->dedup == 2 ? (o->cost_model == TOAST_COST_CRITICAL_PATH ? 1 : 0) : o->dedup;
   } catch (std::bad_alloc&) {
     delete a;
     return fail(TOAST_E_OOM, "out of host memory");

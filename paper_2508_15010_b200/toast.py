@@ -247,10 +247,14 @@ class Analysis:
         return self._dump_all()["kernel_tables"]
 
 
+DEDUP_OFF, DEDUP_ON, DEDUP_AUTO = 0, 1, 2
+
+
 def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30, cost_model: int = COST_SUM,
-        grouping: int = GROUP_COMPAT, dedup: int = 0) -> Analysis:
+        grouping: int = GROUP_COMPAT, dedup: int = DEDUP_AUTO) -> Analysis:
     """toast_nda (H0).  grouping: GROUP_COMPAT (C4/C5) or GROUP_CONTRACTION (reading R23);
-    dedup: 1 = rollout launches cost each distinct state once (NEXT-3, same results)."""
+    dedup: rollout launches cost each distinct state once (NEXT-3, same results) —
+    DEDUP_ON, DEDUP_OFF, or DEDUP_AUTO (on under the critical-path model only)."""
     o = _NdaOpts(int(min_unique_dims), int(max_depth), int(cost_model), int(grouping), int(dedup))
     h = _P()
     _check(_lib.toast_nda(graph._h, ctypes.byref(o), ctypes.byref(h)))
@@ -258,7 +262,7 @@ def nda(graph: Graph, min_unique_dims: int = 10, max_depth: int = 30, cost_model
 
 
 def build_analysis(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c=100.0, min_unique_dims=10,
-                   max_depth=30, cuda_device=0, cost_model=COST_SUM, grouping=GROUP_COMPAT, dedup=0) -> Analysis:
+                   max_depth=30, cuda_device=0, cost_model=COST_SUM, grouping=GROUP_COMPAT, dedup=DEDUP_AUTO) -> Analysis:
     g = load_graph(ir_text, axes, flops_per_sec, device_memory_bytes, penalty_c, cuda_device)
     a = nda(g, min_unique_dims, max_depth, cost_model, grouping, dedup)
     a.axes = list(axes)

@@ -52,7 +52,7 @@ def main():
             for K in ks:
                 os.environ["TOAST_FORCE_K"] = str(K)
                 a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth,
-                                     cuda_device=0, cost_model=cm)
+                                     cuda_device=0, cost_model=cm, dedup=T.DEDUP_OFF)
                 pre = torch.zeros((n, 32), dtype=torch.int16, device="cuda")
                 seqs = torch.empty_like(pre)
                 out = torch.empty((n, 256), dtype=torch.uint8, device="cuda")

@@ -269,7 +269,7 @@ def test_gpu_critical_path_under_contraction():
     T = _T()
     c = configs.get("gpt2")
     a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0,
-                         cost_model=T.COST_CRITICAL_PATH, grouping=T.GROUP_CONTRACTION)
+                         cost_model=T.COST_CRITICAL_PATH, grouping=T.GROUP_CONTRACTION, dedup=T.DEDUP_OFF)
     o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cost_model=1,
                grouping=CONTRACTION)
     n = 2048

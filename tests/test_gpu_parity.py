@@ -381,7 +381,7 @@ def setup_cp(name):
         T = _T()
         c = configs.get(name)
         a = T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=0,
-                             cost_model=T.COST_CRITICAL_PATH)
+                             cost_model=T.COST_CRITICAL_PATH, dedup=T.DEDUP_OFF)   # the one-kernel path
         o = Oracle(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cost_model=1)
         _cp_cache[name] = (a, o)
     return _cp_cache[name]
@@ -428,6 +428,7 @@ def test_critical_path_random_programs(grouping):
         axes = [("a", 2, 1e10), ("b", 3, 1e11)] if seed % 2 else [("a", 2, 1e10), ("b", 4, 1e11)]
         try:
             a = T.build_analysis(ir, axes, 1e12, 1 << 40, 100.0, 1, 30, cuda_device=0, cost_model=T.COST_CRITICAL_PATH,
+                                 dedup=T.DEDUP_OFF if seed % 2 else T.DEDUP_ON,
                                  grouping=grouping)
         except T.ToastError:
             continue

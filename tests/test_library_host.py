@@ -241,3 +241,18 @@ def test_lower_and_materialize_refuse_invalid_sequences():
         n = ctypes.c_size_t()
         rc = T._lib.toast_lower(a.handle, np.ascontiguousarray(s).ctypes.data, None, 0, ctypes.byref(n))
         assert (rc != 0) == (bits != 0), (s, bits)
+
+
+def test_nda_dedup_option_values():
+    """toast_nda_opts.dedup: 0 off, 1 on, 2 auto (on under the critical-path
+    model); anything else is TOAST_E_INVALID_ARG."""
+    T = _lib()
+    c = configs.get("mlp_c")
+    for d in (0, 1, 2):
+        T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth, cuda_device=-1,
+                         dedup=d)
+    for d in (-1, 3):
+        with pytest.raises(T.ToastError) as e:
+            T.build_analysis(c.ir, c.axes, c.flops_per_sec, c.dm, c.penalty_c, c.min_dims, c.max_depth,
+                             cuda_device=-1, dedup=d)
+        assert e.value.code == "TOAST_E_INVALID_ARG"
