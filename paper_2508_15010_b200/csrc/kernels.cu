@@ -1366,6 +1366,55 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
   o1 = c1;
 }
 
+// H8 for one lane with the legal set in NW registers: from depth `stop`, Philox
+// draws decide stop (p = depth / max_depth) or the k-th legal action, whose
+// kills leave the set; the ids land in the staged sequence
+template <int NW>
+__device__ __forceinline__ void rollout_extend(const DeviceTables& T, const Smem& S, int lane, int stop, uint64_t id,
+                                               uint32_t seed_lo, uint32_t seed_hi) {
+  uint32_t legal[NW];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int hi = T.n_actions - w * 32;   // ids >= n_actions are not actions
+    legal[w] = hi >= 32 ? FULL : (hi <= 0 ? 0u : ((1u << hi) - 1u));
+  }
+  legal[0] &= ~1u;                         // STOP is not in the legal set
+  for (int j = 0; j < stop; ++j) {
+    const uint32_t a = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) legal[w] &= ~__ldg(T.kill + (size_t)a * NW + w);
+  }
+  for (int d = stop; d < T.max_depth; ++d) {
+    uint32_t r0, r1;
+    philox4x32_10((uint32_t)id, (uint32_t)(id >> 32), (uint32_t)d, 0u, seed_lo, seed_hi, r0, r1);
+    if ((uint64_t)r0 * (uint64_t)T.max_depth < ((uint64_t)d << 32)) break;   // p_stop = d / max_depth
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) total += __popc(legal[w]);
+    if (total == 0) break;
+    uint32_t k = (uint32_t)(((uint64_t)r1 * total) >> 32);
+    // the word holding the k-th (0-based) legal action, then its bit by a binary search on popcounts
+    uint32_t word = legal[0], base = 0;
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      const uint32_t c0 = __popc(word);
+      const bool later = k >= c0 && base == (uint32_t)(w - 1) * 32;
+      if (later) { k -= c0; word = legal[w]; base = (uint32_t)w * 32; }
+    }
+    uint32_t pos = 0, c;
+    c = __popc(word & 0xFFFFu); if (k >= c) { k -= c; word >>= 16; pos += 16; }
+    c = __popc(word & 0xFFu);   if (k >= c) { k -= c; word >>= 8; pos += 8; }
+    c = __popc(word & 0xFu);    if (k >= c) { k -= c; word >>= 4; pos += 4; }
+    c = __popc(word & 0x3u);    if (k >= c) { k -= c; word >>= 2; pos += 2; }
+    c = word & 1u;              if (k >= c) { pos += 1; }
+    const uint32_t a = base + pos;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) legal[w] &= ~__ldg(T.kill + (size_t)a * NW + w);
+    uint32_t& sw = seq_word(S, d >> 1, lane);
+    sw = (d & 1) ? ((sw & 0xFFFFu) | (a << 16)) : ((sw & 0xFFFF0000u) | a);
+  }
+}
+
 template <int NA, bool P2, bool CP>
 __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS), (CP ? TOAST_CP_MIN_BLOCKS : NA <= 2 ? TOAST_MIN_BLOCKS : TOAST_NA3_MIN_BLOCKS)) toast_rollout_kernel(const DeviceTables T, const uint16_t* __restrict__ pre,
                                                             int64_t n, uint64_t seed, uint64_t id_base,
@@ -1397,31 +1446,15 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
       for (int w = (stop >> 1) + 1; w < 16; ++w) after |= seq_word(S, w, lane);
       bad |= after != 0;
     }
-    if (valid && !bad && nw == 1) {
-      // <= 31 actions (GPT-24, GNS-16, Llama-80): the legal set lives in one
-      // register — the same draws, kills and choices as the general path below
-      uint32_t legal = (T.n_actions >= 32 ? FULL : ((1u << T.n_actions) - 1u)) & ~1u;
-      for (int j = 0; j < stop; ++j) {
-        const uint32_t a = (seq_word(S, j >> 1, lane) >> ((j & 1) * 16)) & 0xFFFFu;
-        legal &= ~__ldg(T.kill + a);
-      }
+    if (valid && !bad && nw <= 4) {
+      // <= 127 actions (every BASELINE config): the legal set lives in registers
+      // — the same draws, kills and choices as the general path below
       const uint64_t id = id_base + (uint64_t)i;
-      for (int d = stop; d < T.max_depth; ++d) {
-        uint32_t r0, r1;
-        philox4x32_10((uint32_t)id, (uint32_t)(id >> 32), (uint32_t)d, 0u, seed_lo, seed_hi, r0, r1);
-        if ((uint64_t)r0 * (uint64_t)T.max_depth < ((uint64_t)d << 32)) break;   // p_stop = d / max_depth
-        const uint32_t total = __popc(legal);
-        if (total == 0) break;
-        uint32_t k = (uint32_t)(((uint64_t)r1 * total) >> 32);
-        uint32_t word = legal, pos = 0, c;
-        c = __popc(word & 0xFFFFu); if (k >= c) { k -= c; word >>= 16; pos += 16; }
-        c = __popc(word & 0xFFu);   if (k >= c) { k -= c; word >>= 8; pos += 8; }
-        c = __popc(word & 0xFu);    if (k >= c) { k -= c; word >>= 4; pos += 4; }
-        c = __popc(word & 0x3u);    if (k >= c) { k -= c; word >>= 2; pos += 2; }
-        c = word & 1u;              if (k >= c) { pos += 1; }
-        legal &= ~__ldg(T.kill + pos);
-        uint32_t& sw = seq_word(S, d >> 1, lane);
-        sw = (d & 1) ? ((sw & 0xFFFFu) | (pos << 16)) : ((sw & 0xFFFF0000u) | pos);
+      switch (nw) {   // warp-uniform
+        case 1: rollout_extend<1>(T, S, lane, stop, id, seed_lo, seed_hi); break;
+        case 2: rollout_extend<2>(T, S, lane, stop, id, seed_lo, seed_hi); break;
+        case 3: rollout_extend<3>(T, S, lane, stop, id, seed_lo, seed_hi); break;
+        default: rollout_extend<4>(T, S, lane, stop, id, seed_lo, seed_hi); break;
       }
     } else if (valid && !bad) {
       for (int w = 0; w < nw; ++w) {
