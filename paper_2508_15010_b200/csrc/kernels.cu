@@ -65,6 +65,9 @@
 #ifndef TOAST_SMEM_TABLES
 #define TOAST_SMEM_TABLES 0   // stage the uniform tables (class records, templates, frontier) in shared memory by TMA
 #endif
+#ifndef TOAST_STREAM_STORES
+#define TOAST_STREAM_STORES 0   // results written with st.global.cs (evict-first) instead of the default policy
+#endif
 #ifndef TOAST_SIG_PREFETCH
 #define TOAST_SIG_PREFETCH 0   // the next class's record loaded one iteration ahead (measured: see DESIGN §6)
 #endif
@@ -238,6 +241,14 @@ __device__ __forceinline__ uint32_t& seq_word(const Smem& S, int w, int lane) {
 }
 
 __device__ __forceinline__ uint64_t u64of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+// a 16-B result store (records, scores, sequences)
+__device__ __forceinline__ void out_store(uint4* p, uint4 v) {
+#if TOAST_STREAM_STORES
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
 
 // ---------------------------------------------------------------- uniform tables (global, or staged by TMA)
 __device__ __forceinline__ void stage_tables(const DeviceTables& T, const Smem& S) {
@@ -1204,7 +1215,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
       const unsigned long long w0 = ok ? (unsigned long long)__double_as_longlong(__dadd_rn(RT, MP)) : 0x7FF8000000000000ULL;
       const unsigned long long w1 = ok ? key : (unsigned long long)status;
       if (valid)
-        reinterpret_cast<uint4*>(out)[row0 + lane] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
+        out_store(reinterpret_cast<uint4*>(out) + row0 + lane, make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32)));
     } else {
       // record layout = toast_cost (include/toast.h), 16 x 16 B, staged through
       // shared memory a quarter at a time (4 x 16 B of each of the 32 records)
@@ -1219,7 +1230,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int u = i * 32 + lane, L = u >> 2, sl = u & 3;
-          if (L < rows) dst[(size_t)L * 16 + quarter * 4 + sl] = stage[L * 4 + (sl ^ ((L >> 1) & 3))];
+          if (L < rows) out_store(dst + (size_t)L * 16 + quarter * 4 + sl, stage[L * 4 + (sl ^ ((L >> 1) & 3))]);
         }
         __syncwarp();
       };
@@ -1332,7 +1343,7 @@ __device__ __forceinline__ void store_seq_rows(const Smem& S, uint16_t* __restri
   for (int k = 0; k < 4; ++k) {
     const int u = k * 32 + lane, r = u >> 2, q = u & 3;
     if (r < rows)
-      dst[u] = make_uint4(seq_word(S, 4 * q, r), seq_word(S, 4 * q + 1, r), seq_word(S, 4 * q + 2, r), seq_word(S, 4 * q + 3, r));
+      out_store(dst + u, make_uint4(seq_word(S, 4 * q, r), seq_word(S, 4 * q + 1, r), seq_word(S, 4 * q + 2, r), seq_word(S, 4 * q + 3, r)));
   }
 }
 

@@ -15,6 +15,7 @@ VARIANTS = {
     "t128b7np": ["-DTOAST_MAX_THREADS=128", "-DTOAST_MIN_BLOCKS=7", "-DTOAST_H4_PREFETCH=0"],
     "sigpf": ["-DTOAST_SIG_PREFETCH=1"],
     "smemtab": ["-DTOAST_SMEM_TABLES=1"],
+    "stcs": ["-DTOAST_STREAM_STORES=1"],
     "na3b3": ["-DTOAST_NA3_MIN_BLOCKS=3"],
     "na3b4": ["-DTOAST_NA3_MIN_BLOCKS=4"],
 }
