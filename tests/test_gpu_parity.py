@@ -551,6 +551,33 @@ def test_cli_partitions_a_program(tmp_path, capsys):
     assert "return" in out and "mesh" in out
     assert main(["--config", "gpt2", "--cost-model", "cp", "--grouping", "contraction", "--budget", "20000",
                  "--no-program"]) == 0
+    assert main(["--ir", str(f), "--mesh", mesh, "--flops", repr(c.flops_per_sec), "--dm", str(c.dm),
+                 "--min-dims", str(c.min_dims), "--budget", "20000", "--dedup", "--transpositions"]) == 0
+    assert f"best score {float(bc['score']):.6g}" in capsys.readouterr().out
+
+
+def test_search_device_exchange_refuses_host_buffers():
+    """toast_search_round_dev / toast_search_import_dev take device memory only
+    (TOAST_E_INVALID_ARG for a host buffer), and a device round's record equals
+    the host round's of the same search state."""
+    import torch
+    T = _T()
+    a, _ = setup("gpt2")
+    opts = T.SearchOptions(seed=2, max_evals=5000, leaves_per_round=4, rollouts_per_leaf=8)
+    st_h, st_d = T.SearchState(a, opts, 0, 1), T.SearchState(a, opts, 0, 1)
+    with pytest.raises(T.ToastError) as e:
+        st_d.round_dev(np.zeros(st_d.export_bytes, np.uint8))
+    assert e.value.code == "TOAST_E_INVALID_ARG"
+    rec_h = st_h.round()
+    dev = torch.empty(st_d.export_bytes, dtype=torch.uint8, device="cuda")
+    st_d.round_dev(dev)
+    rec_d = dev.cpu().numpy()
+    hdr = 8 + 8 + 64 + 8   # best score, key, sequence, evals (elapsed_s and after differ by the clock)
+    assert rec_h[:hdr].tobytes() == rec_d[:hdr].tobytes()
+    assert rec_h[hdr + 8 + 8:].tobytes() == rec_d[hdr + 8 + 8:].tobytes()
+    assert st_h.import_(rec_h) == st_d.import_dev(dev)
+    st_h.end()
+    st_d.end()
 
 
 @pytest.mark.parametrize("cost_model", [0, 1])
