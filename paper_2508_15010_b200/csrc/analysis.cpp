@@ -862,13 +862,14 @@ toast_status build_analysis(const toast_graph* g, const toast_nda_opts* o, toast
     for (size_t mcq = 0; mcq < mc_rep.size(); ++mcq) {
       const size_t q = mc_rep[mcq];
       KSig& k = a->h_sigs[mcq];
-      k.resdim = sig_rd[q];   // (unused by the kernels: result dims are per signature, h_sig_mr)
       k.nr = (uint8_t)sig_words[q].size();
       for (size_t r = 0; r < sig_words[q].size(); ++r) {
         const uint64_t w = sig_words[q][r];
         const uint32_t ac = (uint32_t)(w & 0x3FF);
         if (ac == NO_ACOLOR) continue;
         k.div[r >> 1] |= (uint32_t)((w >> 10) & 0xFFFF) << (16 * (r & 1));
+        for (int A = 0; A < n_axes; ++A)
+          if ((w >> (10 + (1u << A))) & 1) k.div1 |= 1u << (8 * A + r);
         const uint32_t cls = (uint32_t)(w >> 26) & 0xFF;
         if (cls) { k.dsel_roles |= (uint8_t)(1u << r); k.cls |= (uint64_t)cls << (8 * r); }
         int kk = 0;

@@ -420,8 +420,8 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
 // bitmaps, walked in ascending order.
 template <int M, int NA>
 __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const uint4& c0, const uint4& c1,
-                                                  uint32_t dmask, const uint4& dw, uint64_t axpos, const uint32_t* axb,
-                                                  bool alldiv) {
+                                                  uint32_t dmask, const uint4& dw, uint32_t div1, uint64_t axpos,
+                                                  const uint32_t* axb, bool alldiv) {
   const uint32_t col[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
   uint32_t pm[M], rm[M], bits = 0;
 #pragma unroll
@@ -448,26 +448,30 @@ __device__ __forceinline__ uint32_t materialize_m(const Smem& S, int lane, const
     }
     return a2r;
   }
-  uint32_t a2r = 0xFFFFu, masks = 0, opmask = 0;
-  while (bits && opmask != (1u << NA) - 1) {   // (every axis placed: the later events change nothing)
+  // the walk: events in position order; a role holding no axis yet takes axis
+  // A iff A alone divides it (div1's byte A), a role already holding axes iff
+  // their union with A does; the first such role in role order wins, and a
+  // placed axis's later events are dropped from the walk
+  uint32_t a2r = 0xFFFFu, masks = 0, occ = 0;
+  while (bits) {
     const uint32_t j = __ffs(bits) - 1;
     bits &= bits - 1;
     const uint32_t A = (uint32_t)(axpos >> (2 * j)) & 3;
-    if ((opmask >> A) & 1) continue;
     uint32_t roles = 0;
 #pragma unroll
     for (int k = 0; k < M; ++k) roles |= ((pm[k] >> j) & 1) ? rm[k] : 0u;
-    while (roles) {
-      const uint32_t r = __ffs(roles) - 1;
-      roles &= roles - 1;
+    uint32_t ok = roles & (div1 >> (8 * A)) & ~occ;
+    for (uint32_t ro = roles & occ; ro; ro &= ro - 1) {
+      const uint32_t r = __ffs(ro) - 1;
       const uint32_t d = (uint32_t)(((r & 4) ? dhi : dlo) >> (16 * (r & 3))) & 0xFFFF;
-      const uint32_t cur = (masks >> (4 * r)) & 15;
-      if ((d >> (cur | (1u << A))) & 1) {
-        masks |= (1u << A) << (4 * r);
-        opmask |= 1u << A;
-        a2r = (a2r & ~(0xFu << (4 * A))) | (r << (4 * A));
-        break;
-      }
+      if ((d >> (((masks >> (4 * r)) & 15) | (1u << A))) & 1) ok |= 1u << r;
+    }
+    if (ok) {
+      const uint32_t r = __ffs(ok) - 1;
+      masks |= (1u << A) << (4 * r);
+      occ |= 1u << r;
+      a2r = (a2r & ~(0xFu << (4 * A))) | (r << (4 * A));
+      bits &= ~axb[A];
     }
   }
   return a2r;
@@ -510,14 +514,14 @@ __device__ __forceinline__ uint32_t materialize_sig(const DeviceTables& T, const
   }
   uint32_t a2r;
   switch (m) {   // warp-uniform: the merge is unrolled over the signature's color count
-    case 1: a2r = materialize_m<1, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
-    case 2: a2r = materialize_m<2, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
-    case 3: a2r = materialize_m<3, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
-    case 4: a2r = materialize_m<4, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
-    case 5: a2r = materialize_m<5, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
-    case 6: a2r = materialize_m<6, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
-    case 7: a2r = materialize_m<7, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
-    default: a2r = materialize_m<8, NA>(S, lane, c0, c1, dmask, dw, axpos, axb, alldiv); break;
+    case 1: a2r = materialize_m<1, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
+    case 2: a2r = materialize_m<2, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
+    case 3: a2r = materialize_m<3, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
+    case 4: a2r = materialize_m<4, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
+    case 5: a2r = materialize_m<5, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
+    case 6: a2r = materialize_m<6, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
+    case 7: a2r = materialize_m<7, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
+    default: a2r = materialize_m<8, NA>(S, lane, c0, c1, dmask, dw, mt.x, axpos, axb, alldiv); break;
   }
   return a2r;
 }

@@ -135,7 +135,7 @@ struct KTmpl {           // 24 B
 struct KSig {
   uint32_t div[4];       // role r: div_ok (bit S <=> extent divisible by prod(axis subset S)) = div[r >> 1] >> 16 * (r & 1)
   uint32_t col[8];       // k < m: acolor | role mask << 10
-  uint32_t resdim;       // nibble r: result dim of role r (0xF: none)
+  uint32_t div1;         // byte A: the roles (with a color) whose extent axis A alone divides (the walk's test for a role holding no axis yet)
   uint8_t m;             // distinct action colors among the roles
   uint8_t dsel_roles;    // roles with a deselection class
   uint8_t nr;
