@@ -10,7 +10,8 @@ done
 if [ -z "$NO_CP" ]; then
   bash scripts/gpu_ncu_cp.sh gpt24
   python scripts/ncu_summary.py gpt24_cp gpurun_out/prof_cp_gpt24.ncu-rep r02 > /dev/null 2>&1; echo "summary cp rc=$?"
-  rm -f gpurun_out/prof_cp_gpt24.ncu-rep
+  python scripts/ncu_summary.py gpt24_cp_dedup_back gpurun_out/prof_cpdd_gpt24.ncu-rep r02 > /dev/null 2>&1; echo "summary cp dedup rc=$?"
+  rm -f gpurun_out/prof_cp_gpt24.ncu-rep gpurun_out/prof_cpdd_gpt24.ncu-rep
 fi
-cp profiles/r02_* profiles/ncu_summary.json gpurun_out/profiles_r02/ 2>/dev/null
+cp profiles/r02_ncu_* profiles/ncu_summary.json gpurun_out/profiles_r02/ 2>/dev/null   # (the launch lists were copied above)
 ls -la gpurun_out/profiles_r02
