@@ -386,7 +386,7 @@ __device__ __forceinline__ uint32_t a_dim(uint32_t a2r, uint32_t rdm, int A) {
 // color (S.acol[c][lane]); per lane the 2-bit axis of every position (axpos)
 // and per mesh axis the bitmap of the positions using it (axb, registers)
 template <int NA>
-__device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, uint64_t& fixed0,
+__device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S, int lane, bool clean, uint64_t& fixed0,
                                            uint64_t& ones, uint64_t& axpos, uint32_t (&axb)[NA]) {
   for (int c = 0; c < T.n_acolors; ++c) sp<uint32_t>(S.acol)[c * 32 + lane] = 0u;
 #pragma unroll
@@ -418,7 +418,7 @@ __device__ __forceinline__ uint32_t decode(const DeviceTables& T, const Smem& S,
     on |= om & gm & ~fx;
     fx |= gm;
   }
-  if (j < 32) {   // the ids after STOP must all be 0
+  if (j < 32 && !clean) {   // the ids after STOP must all be 0 (clean: a rollout's own extension of a valid prefix)
     uint32_t after = (j & 1) ? 0u : seq_word(S, j >> 1, lane) >> 16;
     for (int w = (j >> 1) + 1; w < 16; ++w) after |= seq_word(S, w, lane);
     if (after) status |= TOAST_ST_NONZERO_AFTER_STOP;
@@ -878,11 +878,12 @@ struct Front {
 
 // front half: decode (H1) and materialise every class (H2a) with its key terms and FLOPs
 template <int NA, bool P2>
-__device__ __forceinline__ Front batch_front(const DeviceTables& T, const Smem& S, int K, int warp, int lane) {
+__device__ __forceinline__ Front batch_front(const DeviceTables& T, const Smem& S, int K, int warp, int lane,
+                                             bool clean = false) {
   block_sync(K);
   uint64_t f0 = 0, on = 0, ap = 0;
   uint32_t axb[NA], status = 0;
-  if (warp == 0) status = decode<NA>(T, S, lane, f0, on, ap, axb);
+  if (warp == 0) status = decode<NA>(T, S, lane, clean, f0, on, ap, axb);
   if (K > 1) {   // the decode results every warp reads (one warp: they stay in registers)
     if (warp == 0) {
       sp<uint32_t>(S.status)[lane] = status;
@@ -1304,8 +1305,9 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
 
 template <int NA, bool P2, bool CP>
 __device__ __forceinline__ void batch_eval(const DeviceTables& T, const Smem& S, int K, int warp, int lane, bool valid,
-                                           void* __restrict__ out, int64_t row0, int rows, bool compact) {
-  const Front fr = batch_front<NA, P2>(T, S, K, warp, lane);
+                                           void* __restrict__ out, int64_t row0, int rows, bool compact,
+                                           bool clean = false) {
+  const Front fr = batch_front<NA, P2>(T, S, K, warp, lane, clean);
   batch_back<NA, P2, CP>(T, S, K, warp, lane, valid, fr, out, row0, rows, compact, blockIdx.x);
 }
 
@@ -1465,6 +1467,7 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
     const int64_t row0 = b * 32, i = row0 + lane;
     const int rows = (int)(n - row0 < 32 ? n - row0 : 32);
     const bool valid = i < n;
+    bool clean = false;   // (warp 0) the lane's sequence is a valid prefix + this kernel's extension: zeros after STOP
     if (warp == 0) {
     if (rep == 1) load_seq_rows(S, pre + row0 * 32, rows, lane);
     else load_seq_lane(S, pre + (i / rep) * 32, lane, valid);
@@ -1481,6 +1484,7 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
       for (int w = (stop >> 1) + 1; w < 16; ++w) after |= seq_word(S, w, lane);
       bad |= after != 0;
     }
+    clean = valid && !bad;
     if (valid && !bad && nw <= 4) {
       // <= 127 actions (every BASELINE config): the legal set lives in registers
       // — the same draws, kills and choices as the general path below
@@ -1536,12 +1540,12 @@ __global__ void __launch_bounds__((CP ? TOAST_CP_MAX_THREADS : TOAST_MAX_THREADS
     store_seq_rows(S, out_seqs + row0 * 32, rows, lane);
     }   // warp 0
     if (T.dd.key) {   // NEXT-3 dedup launch (one warp per block): the front half only
-      const Front fr = batch_front<NA, P2>(T, S, K, warp, lane);
+      const Front fr = batch_front<NA, P2>(T, S, K, warp, lane, clean);
       dedup_front<NA>(T, S, lane, valid, i, fr);
       block_sync(K);
       continue;
     }
-    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, row0, rows, compact);
+    batch_eval<NA, P2, CP>(T, S, K, warp, lane, valid, out, row0, rows, compact, clean);
   }
 }
 
