@@ -1075,7 +1075,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
     const uint32_t n_sig = pw.y & 0xFFFF, n_tm = pw.y >> 16, n_spec = pw.w & 0xFFFF;
     uint32_t tp = pw.x;
     Ms += (long long)term_word(T, S, tp++);
-#pragma unroll 4
+#pragma unroll(NA <= 2 ? 8 : 4)   // (8 on NA = 3: 1% slower on Llama-80)
     for (uint32_t k = 0; k < n_sig; ++k) {
       const uint64_t w = term_word(T, S, tp + k);
       const long long v = (long long)(w << 16) >> 16;    // signed 48-bit value
