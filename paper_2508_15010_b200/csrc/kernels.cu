@@ -38,6 +38,14 @@
 #ifndef TOAST_MAX_THREADS
 #define TOAST_MAX_THREADS 256
 #endif
+// H5's unroll depths on <= 2-axis meshes (experiment knobs; the 3-axis kernels keep 4 / 2)
+#ifndef TOAST_H5_SIG_UNROLL
+#define TOAST_H5_SIG_UNROLL 8
+#endif
+#ifndef TOAST_H5_TM_UNROLL
+#define TOAST_H5_TM_UNROLL 2
+#endif
+constexpr int H5_SIG_UNROLL = TOAST_H5_SIG_UNROLL, H5_TM_UNROLL = TOAST_H5_TM_UNROLL;   // (pragma arguments are not macro-expanded)
 #ifndef TOAST_CP_MAX_THREADS
 #define TOAST_CP_MAX_THREADS 256   // critical-path instantiations: block size bound
 #endif
@@ -1075,7 +1083,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
     const uint32_t n_sig = pw.y & 0xFFFF, n_tm = pw.y >> 16, n_spec = pw.w & 0xFFFF;
     uint32_t tp = pw.x;
     Ms += (long long)term_word(T, S, tp++);
-#pragma unroll(NA <= 2 ? 8 : 4)   // (8 on NA = 3: 1% slower on Llama-80)
+#pragma unroll(NA <= 2 ? H5_SIG_UNROLL : 4)   // (8 on NA = 3: 1% slower on Llama-80)
     for (uint32_t k = 0; k < n_sig; ++k) {
       const uint64_t w = term_word(T, S, tp + k);
       const long long v = (long long)(w << 16) >> 16;    // signed 48-bit value
@@ -1084,7 +1092,7 @@ __device__ __forceinline__ void batch_back(const DeviceTables& T, const Smem& S,
     }
     tp += n_sig;
     uint64_t M = (uint64_t)Ms;
-#pragma unroll 2
+#pragma unroll(NA <= 2 ? H5_TM_UNROLL : 2)
     for (uint32_t k = 0; k < n_tm; ++k) {
       const uint64_t w = term_word(T, S, tp + k);
       const uint64_t v = w & ((1ULL << 48) - 1);
